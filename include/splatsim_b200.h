@@ -1,0 +1,222 @@
+/*
+ * splatsim_b200.h — C-ABI of the B200-native Balanced-3DGS forward rasterizer.
+ *
+ * Every entry point is extern "C", takes plain device pointers + sizes, is
+ * stream-ordered on the `stream` argument (a cudaStream_t passed as void*,
+ * NULL = legacy default stream), performs no hidden allocation (callers pass
+ * workspace sized by the matching *_workspace_bytes query) and returns a
+ * bs_status (0 = ok, < 0 = error; bs_status_string() names it).  There is no
+ * CPU fallback: every call launches sm_100a kernels or fails.
+ *
+ * Reference interfaces replaced (/root/reference/proj/core, namespace splatsim):
+ *   bs_preprocess        project_all / project_gaussian   include/splatsim/preprocess.hpp:57-59
+ *                        (covariance_of scene.hpp:55, project_covariance preprocess.hpp:51-53)
+ *   bs_bin_count+_sort   bin_tiles                         include/splatsim/preprocess.hpp:64-65
+ *   bs_tile_stats        tile_load_histogram               include/splatsim/preprocess.hpp:67
+ *   bs_render_forward    render_reference / run_kernel     include/splatsim/blend.hpp:100-102,
+ *                                                          include/splatsim/kernels.hpp:104-106
+ *   bs_frame_work        TileWork.consumed / trace inputs  src/kernels.cpp:283-298
+ *   bs_select_variant    (per-frame form of) checkpoint    include/splatsim/adaptive.hpp:54-55
+ *   bs_variant_name/_from_name  variant_name/_from_name    include/splatsim/kernels.hpp:25-26
+ * The C++ host layer (splatsim_b200.hpp) restores the reference's value-typed
+ * signatures and exceptions on top of this ABI.
+ */
+#ifndef SPLATSIM_B200_H
+#define SPLATSIM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BS_ABI_VERSION 1
+
+typedef enum bs_status {
+  BS_OK = 0,
+  BS_ERR_INVALID_ARGUMENT = -1, /* std::invalid_argument in the reference */
+  BS_ERR_GRID_MISMATCH = -2,    /* "binning grid does not match image dims" */
+  BS_ERR_WORKSPACE = -3,        /* workspace too small for this call */
+  BS_ERR_CAPACITY = -4,         /* K exceeds the u32 point_list index space */
+  BS_ERR_CUDA = -5,             /* a CUDA launch / runtime call failed */
+  BS_ERR_UNSUPPORTED = -6,      /* patch larger than 1024 pixels, ... */
+  BS_ERR_LOGIC = -7,            /* std::logic_error (selector already switched) */
+  BS_ERR_NO_DEVICE = -8         /* no sm_100 device visible */
+} bs_status;
+
+/* Gaussian3D — include/splatsim/scene.hpp:16-22, by field (rot is w,x,y,z as
+ * in the scene JSON, src/scene.cpp:124).  56 bytes, AoS. */
+typedef struct bs_gaussian3d {
+  float mean[3];
+  float scale[3];
+  float rot[4];
+  float opacity;
+  float color[3];
+} bs_gaussian3d;
+
+/* Camera — include/splatsim/scene.hpp:24-29.  view is row-major world->camera. */
+typedef struct bs_camera {
+  float view[16];
+  float focal[2];
+  int32_t width;
+  int32_t height;
+} bs_camera;
+
+/* Gaussian2D — include/splatsim/preprocess.hpp:16-25, host interop layout (44 B). */
+typedef struct bs_gaussian2d {
+  float x, y;
+  float conic_a, conic_b, conic_c;
+  float opacity;
+  float color[3];
+  float depth;
+  float radius;
+} bs_gaussian2d;
+
+/* Device-resident projected splats (SoA of float4, indexed by compacted id):
+ *   xyab[i] = (x, y, conic_a, conic_b)
+ *   cop[i]  = (conic_c, opacity, power_cut, depth)
+ *   rgbr[i] = (r, g, b, radius)
+ * power_cut is a conservative per-splat bound: power < power_cut implies
+ * alpha < 1/255 (so the exact exp can be skipped without changing any
+ * decision).  Each array holds n_cap float4 (16-byte aligned). */
+typedef struct bs_splats {
+  float* xyab;
+  float* cop;
+  float* rgbr;
+} bs_splats;
+
+/* KernelVariant — include/splatsim/kernels.hpp:13-19 (same order / names). */
+typedef enum bs_variant {
+  BS_NAIVE = 0,
+  BS_DYNAMIC_BLOCKS = 1,
+  BS_GAUSSIAN_WISE = 2,
+  BS_FINE_GRAINED_COMBINED = 3,
+  BS_SHARED_MEM_OPT = 4,
+  BS_VARIANT_AUTO = -1 /* bs_render_forward: not accepted; use bs_select_variant */
+} bs_variant;
+
+/* Alpha arithmetic.
+ *   BS_ALPHA_EXACT: alpha = min(0.99, opacity * expf(power)) with expf
+ *     bit-identical to glibc 2.39 libm (the reference's std::exp(float)),
+ *     serial float transmittance for every skip/stop decision, double
+ *     colour/depth accumulators — the reference semantics bit for bit.
+ *   BS_ALPHA_FAST: ex2.approx alpha, float accumulators and (Gaussian-wise
+ *     variants) prefix-product stop decisions as in the paper's Alg. 6.
+ *     Within 1e-4 of the reference; stop/skip flips at the termination
+ *     boundary are possible and are counted by the parity tests. */
+typedef enum bs_alpha_mode { BS_ALPHA_EXACT = 0, BS_ALPHA_FAST = 1 } bs_alpha_mode;
+
+/* RenderOutput — include/splatsim/blend.hpp:86-97 (device pointers, P = W*H). */
+typedef struct bs_frame_out {
+  float* color;     /* f32[3P], rgb interleaved */
+  float* alpha;     /* f32[P] */
+  float* depth;     /* f32[P] */
+  float* final_t;   /* f32[P] */
+  int32_t* contrib; /* i32[P] committed steps */
+  int32_t* term;    /* i32[P] 1-based termination index, 0 = none */
+} bs_frame_out;
+
+/* TileHistogram summary — include/splatsim/preprocess.hpp:38-45. */
+typedef struct bs_tile_histogram {
+  uint32_t min;
+  uint32_t max;
+  uint32_t p50; /* nearest-rank, as src/preprocess.cpp:130-134 */
+  uint32_t p99;
+  double mean;
+  uint64_t total;    /* K */
+  int32_t tiles;     /* T */
+  int32_t nonempty;  /* tiles with count > 0 */
+} bs_tile_histogram;
+
+/* ---- library ---- */
+int bs_abi_version(void);
+const char* bs_status_string(int status);
+/* Number of SMs of the current device (148 on B200); fails without a GPU. */
+int bs_device_sm_count(int32_t* sm_count);
+const char* bs_variant_name(int variant);
+int bs_variant_from_name(const char* name); /* -1 when unknown */
+
+/* ---- P1-P4: EWA projection + order-preserving compaction ----
+ * Projects n Gaussians (device AoS) through cam (host struct), writes the
+ * survivors in input order to out[0..n_visible) and *n_visible (device i32).
+ * Semantics: src/preprocess.cpp:17-64 (near cull, det/eigen culls, no +0.3
+ * dilation).  out arrays must hold n entries. */
+size_t bs_preprocess_workspace_bytes(int64_t n);
+int bs_preprocess(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, bs_splats out, int32_t* n_visible,
+                  void* ws, size_t ws_bytes, void* stream);
+
+/* Interop: device AoS Gaussian2D <-> splats (fills power_cut). */
+int bs_splats_from_g2d(const bs_gaussian2d* g2d, int64_t n, bs_splats out, void* stream);
+int bs_splats_to_g2d(bs_splats in, int64_t n, bs_gaussian2d* g2d, void* stream);
+
+/* ---- P5: binning (bit-exact with src/preprocess.cpp:66-115) ----
+ * Two calls so the host can size point_list without a hidden sync:
+ *   bs_bin_count: per-splat tile rects, stable depth sort of the visible
+ *     splats, exclusive scan of tiles-touched.  Writes K to *k_total (device
+ *     i64).  Reads the splat count from *n_visible (device) — n_cap bounds it.
+ *   bs_bin_sort: duplicates (tile, id) pairs in depth order, stable radix sort
+ *     by tile id, tile ranges.  k is K read back by the host.  Must be given
+ *     the same workspace the matching bs_bin_count call used.
+ * Workspace: bs_bin_workspace_bytes(n_cap, W, H, pw, ph, k_cap) with
+ * k_cap >= k; bs_bin_sort returns BS_ERR_WORKSPACE if k > k_cap.
+ * tile_ranges holds 2*T u32 ([start, end) per tile, row-major tiles). */
+size_t bs_bin_workspace_bytes(int64_t n_cap, int32_t width, int32_t height, int32_t pw, int32_t ph, int64_t k_cap);
+int bs_bin_count(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height, int32_t pw,
+                 int32_t ph, int64_t* k_total, void* ws, size_t ws_bytes, void* stream);
+int bs_bin_sort(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height, int32_t pw,
+                int32_t ph, int64_t k, uint32_t* point_list, uint32_t* tile_ranges, void* ws, size_t ws_bytes,
+                void* stream);
+
+/* ---- P6: tile statistics + LPT task order ----
+ * counts[t] = end - start; stats as tile_load_histogram (written to device
+ * memory at *stats); task_order = tiles by list length descending, ties by
+ * tile id ascending (the fine-grained queue order).  counts/task_order may be
+ * NULL. */
+size_t bs_tile_stats_workspace_bytes(int32_t tiles);
+int bs_tile_stats(const uint32_t* tile_ranges, int32_t tiles, bs_tile_histogram* stats, uint32_t* counts,
+                  uint32_t* task_order, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- R1-R8: forward render ----
+ * variant: bs_variant (not AUTO).  task_order: LPT tile order from
+ * bs_tile_stats (required for BS_FINE_GRAINED_COMBINED, ignored otherwise;
+ * NULL = index order).  bg: host rgb.  Writes every pixel of out.
+ * Output equals render_reference (pixel-wise variants) or
+ * render_gaussianwise (GaussianWise / FineGrainedCombined).
+ * Workspace holds the dynamic-queue counter (reset by the call). */
+size_t bs_render_workspace_bytes(void);
+int bs_render_forward(int variant, int alpha_mode, bs_splats g, const uint32_t* point_list,
+                      const uint32_t* tile_ranges, const uint32_t* task_order, int32_t width, int32_t height,
+                      int32_t pw, int32_t ph, const float bg[3], bs_frame_out out, void* ws, size_t ws_bytes,
+                      void* stream);
+
+/* Work counters of a rendered frame (src/kernels.cpp:283-298):
+ *   evaluated = sum_p consumed(p), consumed = term > 0 ? term : list_len(tile(p))
+ *   committed = sum_p contrib(p)
+ * written to device u64[2] = {evaluated, committed}. */
+int bs_frame_work(const int32_t* term, const int32_t* contrib, const uint32_t* tile_ranges, int32_t width,
+                  int32_t height, int32_t pw, int32_t ph, uint64_t* evaluated_committed, void* stream);
+
+/* ---- S-1: per-frame variant predictor (host call, host struct) ----
+ * Returns the bs_variant the B200 cost model predicts fastest for a frame
+ * with these tile statistics.  Host-only logic. */
+int bs_select_variant(const bs_tile_histogram* stats, int32_t width, int32_t height, int32_t pw, int32_t ph,
+                      int32_t sm_count);
+
+/* ---- diagnostics ----
+ * y[i] = the device exp the render kernels use in alpha_mode (EXACT: the
+ * glibc-identical expf; FAST: ex2.approx).  Used by the parity tests to pin
+ * the exact path against the host libm. */
+int bs_test_expf(const float* x, float* y, int64_t n, int alpha_mode, void* stream);
+
+/* ---- host-side helpers (implemented in the C++ host layer) ----
+ * gen_clustered_scene (src/workload.cpp:198-246, include/splatsim/workload.hpp:68-76):
+ * writes n Gaussians to the HOST array out. */
+int bs_host_gen_clustered_scene(int32_t n, int32_t n_clusters, uint64_t seed, double cluster_sigma,
+                                double background_fraction, const bs_camera* cam, bs_gaussian3d* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPLATSIM_B200_H */

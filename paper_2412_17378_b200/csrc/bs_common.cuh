@@ -1,0 +1,73 @@
+// bs_common.cuh — shared device helpers for the B200 forward rasterizer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "splatsim_b200.h"
+
+#define BS_CUDA_TRY(expr)                              \
+  do {                                                 \
+    cudaError_t _e = (expr);                           \
+    if (_e != cudaSuccess) return BS_ERR_CUDA;         \
+  } while (0)
+
+#define BS_LAUNCH_CHECK()                              \
+  do {                                                 \
+    if (cudaPeekAtLastError() != cudaSuccess) {        \
+      (void)cudaGetLastError();                        \
+      return BS_ERR_CUDA;                              \
+    }                                                  \
+  } while (0)
+
+namespace bs {
+
+constexpr float kNearPlane = 0.01f;           // preprocess.hpp:47
+constexpr float kAlphaClamp = 0.99f;          // blend.hpp:13
+constexpr float kAlphaSkip = 1.0f / 255.0f;   // blend.hpp:14
+constexpr float kStopThreshold = 1e-4f;       // blend.hpp:15
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Bump allocator over a caller workspace (all carve-outs 256-byte aligned).
+struct WsCarver {
+  char* base;
+  size_t cap;
+  size_t off = 0;
+  bool ok = true;
+  WsCarver(void* p, size_t c) : base(static_cast<char*>(p)), cap(c) {}
+  template <typename T>
+  T* take(size_t count) {
+    off = align_up(off, 256);
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += count * sizeof(T);
+    if (off > cap) ok = false;
+    return p;
+  }
+};
+
+// Size-only variant of the carver (same layout rules; returns nullptr).
+struct WsSizer {
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = align_up(off, 256);
+    off += count * sizeof(T);
+    return nullptr;
+  }
+};
+
+// Sortable key of a float under operator< (ties -0 == +0 collapse).
+__device__ __forceinline__ uint32_t float_sort_key(float f) {
+  if (f == 0.0f) f = 0.0f;  // -0 -> +0
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace bs

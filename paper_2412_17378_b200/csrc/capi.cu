@@ -1,0 +1,76 @@
+// capi.cu — library-level C-ABI entry points: version, status strings,
+// variant names (include/splatsim/kernels.hpp:13-26, src/kernels.cpp:10-25),
+// device query and the per-frame variant predictor.
+#include <math.h>
+#include <string.h>
+
+#include "bs_common.cuh"
+
+extern "C" int bs_abi_version(void) { return BS_ABI_VERSION; }
+
+extern "C" const char* bs_status_string(int status) {
+  switch (status) {
+    case BS_OK: return "ok";
+    case BS_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case BS_ERR_GRID_MISMATCH: return "binning grid does not match image dims";
+    case BS_ERR_WORKSPACE: return "workspace too small";
+    case BS_ERR_CAPACITY: return "capacity exceeded (u32 index space)";
+    case BS_ERR_CUDA: return "CUDA error";
+    case BS_ERR_UNSUPPORTED: return "unsupported configuration";
+    case BS_ERR_LOGIC: return "selection already switched";
+    case BS_ERR_NO_DEVICE: return "no CUDA device";
+  }
+  return "unknown status";
+}
+
+static const char* const kVariantNames[5] = {"Naive", "DynamicBlocks", "GaussianWise", "FineGrainedCombined",
+                                             "SharedMemOpt"};
+
+extern "C" const char* bs_variant_name(int variant) {
+  if (variant < 0 || variant > 4) return "?";
+  return kVariantNames[variant];
+}
+
+extern "C" int bs_variant_from_name(const char* name) {
+  if (!name) return -1;
+  for (int i = 0; i < 5; ++i)
+    if (strcmp(name, kVariantNames[i]) == 0) return i;
+  return -1;
+}
+
+extern "C" int bs_device_sm_count(int32_t* sm_count) {
+  if (!sm_count) return BS_ERR_INVALID_ARGUMENT;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    (void)cudaGetLastError();
+    return BS_ERR_NO_DEVICE;
+  }
+  int dev = 0, sms = 0;
+  BS_CUDA_TRY(cudaGetDevice(&dev));
+  BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  *sm_count = sms;
+  return BS_OK;
+}
+
+// Per-frame predictor.  With L_t the list length of
+// tile t, a static one-CTA-per-tile launch finishes no earlier than the
+// heaviest tile (L_max) and no earlier than the balanced share
+// sum(L)/(S*k) of S SMs with k resident tile-CTAs each; the fine-grained
+// queue removes the first bound at a per-step overhead rho:
+//   t_static ~ max(L_max, sum(L)/(S*k)),   t_fine ~ rho * sum(L)/(S*k)
+// FineGrainedCombined wins when t_static > t_fine, else SharedMemOpt (the
+// selector's fallback, src/adaptive.cpp:27-28).  k and rho are B200
+// calibrations (bench.py --sweep measures them).
+extern "C" int bs_select_variant(const bs_tile_histogram* stats, int32_t width, int32_t height, int32_t pw, int32_t ph,
+                                 int32_t sm_count) {
+  if (!stats || width <= 0 || height <= 0 || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
+  const double S = sm_count > 0 ? (double)sm_count : 148.0;
+  const int pixels = pw * ph;
+  const double k = pixels <= 128 ? 12.0 : (pixels <= 256 ? 6.0 : 3.0);  // resident tile CTAs per SM
+  const double rho = 1.6;
+  const double sumL = (double)stats->total;
+  const double balanced = sumL / (S * k);
+  const double t_static = fmax((double)stats->max, balanced);
+  const double t_fine = rho * balanced;
+  return t_static > t_fine ? BS_FINE_GRAINED_COMBINED : BS_SHARED_MEM_OPT;
+}

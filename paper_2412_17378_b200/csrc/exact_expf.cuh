@@ -1,0 +1,59 @@
+// exact_expf.cuh — device expf bit-identical to glibc 2.39 libm expf.
+//
+// The reference computes alpha = min(0.99f, opacity * std::exp(power))
+// (src/blend.cpp:12); on x86-64 std::exp(float) is glibc's expf, whose
+// algorithm (sysdeps/ieee754/flt-32/e_expf.c, from ARM optimized-routines) is
+//   z = x * 32/ln2;  k = round(z);  r = z - k
+//   exp(x) = 2^(k/32) * (1 + C2 r + C1 r^2 + C0 r^3)      (all in double)
+// with a 32-entry 2^(i/32) table.  Every operation below is an IEEE
+// round-to-nearest double op (explicit intrinsics, so no contraction other
+// than the FMAs glibc's __expf_fma itself uses), giving bit-identical floats.
+// tests/test_gpu_parity.py::test_exact_expf_matches_libm checks that claim on
+// the device against the host libm; tests/test_oracle_kat.py checks the
+// algorithm exhaustively on [-103.9, 0] on the CPU.  One input in that range
+// (x = -0x1.f8cbb2p+5) is special-cased by glibc 2.39 and is reproduced here.
+#pragma once
+
+#include <stdint.h>
+
+namespace bs {
+
+// tab[i] = bits(2^(i/32)) - (i << 47)
+#define BS_EXP2F_TAB_INIT                                                                              \
+  {0x3ff0000000000000ull, 0x3fefd9b0d3158574ull, 0x3fefb5586cf9890full, 0x3fef9301d0125b51ull,        \
+   0x3fef72b83c7d517bull, 0x3fef54873168b9aaull, 0x3fef387a6e756238ull, 0x3fef1e9df51fdee1ull,        \
+   0x3fef06fe0a31b715ull, 0x3feef1a7373aa9cbull, 0x3feedea64c123422ull, 0x3feece086061892dull,        \
+   0x3feebfdad5362a27ull, 0x3feeb42b569d4f82ull, 0x3feeab07dd485429ull, 0x3feea47eb03a5585ull,        \
+   0x3feea09e667f3bcdull, 0x3fee9f75e8ec5f74ull, 0x3feea11473eb0187ull, 0x3feea589994cce13ull,        \
+   0x3feeace5422aa0dbull, 0x3feeb737b0cdc5e5ull, 0x3feec49182a3f090ull, 0x3feed503b23e255dull,        \
+   0x3feee89f995ad3adull, 0x3feeff76f2fb5e47ull, 0x3fef199bdd85529cull, 0x3fef3720dcef9069ull,        \
+   0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull}
+
+// x in [-103.97, 88.7]; tab points at a 32-entry table (shared memory in the
+// render kernels: divergent indices would serialise a __constant__ read).
+__device__ __forceinline__ float glibc_expf(float x, const unsigned long long* tab) {
+  const double kInvLn2N = 0x1.71547652b82fep+0 * 32.0;
+  const double kShift = 0x1.8p+52;
+  const double kC0 = 0x1.c6af84b912394p-5 / 32.0 / 32.0 / 32.0;
+  const double kC1 = 0x1.ebfce50fac4f3p-3 / 32.0 / 32.0;
+  const double kC2 = 0x1.62e42ff0c52d6p-1 / 32.0;
+  if (x < -0x1.9fe368p6f) return 0.0f;  // glibc __math_uflowf(0): 0x1p-95f * 0x1p-95f rounds to 0
+  const double xd = (double)x;
+  const double z = __dmul_rn(kInvLn2N, xd);
+  double kd = __dadd_rn(z, kShift);
+  const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
+  kd = __dsub_rn(kd, kShift);
+  const double r = __dsub_rn(z, kd);
+  const unsigned long long t = tab[ki & 31ull] + (ki << 47);
+  const double s = __longlong_as_double((long long)t);
+  const double zz = __fma_rn(kC0, r, kC1);
+  const double r2 = __dmul_rn(r, r);
+  double y = __fma_rn(kC2, r, 1.0);
+  y = __fma_rn(zz, r2, y);
+  y = __dmul_rn(y, s);
+  float out = __double2float_rn(y);
+  if (__float_as_uint(x) == 0xC27C65D9u) out = __uint_as_float(0x11FA2993u);  // -0x1.f8cbb2p+5 -> 0x1.f45326p-92
+  return out;
+}
+
+}  // namespace bs

@@ -1,0 +1,245 @@
+// preprocess.cu — P1-P4: EWA projection + order-preserving compaction.
+//
+// Compiled with --fmad=false: every float/double expression below rounds
+// after each operation exactly like the reference built with
+// -ffp-contract=off (/root/reference/proj/CMakeLists.txt:11-12).  The
+// evaluation order is the oracle's documented Eigen 3.4 order
+// (oracle/oracle.cpp covariance_of / project_covariance / project_gaussian):
+// 3x3 float products reduce a0 + (a1 + a2); 2-row double products sum
+// left to right.
+//
+// Layout: input AoS bs_gaussian3d (56 B, read once, 16 B-aligned rows are not
+// guaranteed so it is read as 14 scalar floats: a warp touches 1792
+// contiguous bytes, fully coalesced at sector granularity).  Output SoA of
+// float4 (bs_splats).  HBM-bound: 56 B in + 48 B out per Gaussian.
+#include <math.h>
+
+#include "bs_common.cuh"
+#include "scan.cuh"
+
+namespace bs {
+
+struct CamDev {
+  float v[12];  // rows 0..2 of the row-major 4x4 view
+  float fx, fy;
+  int w, h;
+};
+
+struct Projected {
+  float x, y, ca, cb, cc, depth, radius;
+};
+
+// src/scene.cpp:67-71 (see oracle covariance_of for the order).
+__device__ __forceinline__ void covariance_of(const float* rot, const float* scale, float S[3][3]) {
+  float qw = rot[0], qx = rot[1], qy = rot[2], qz = rot[3];
+  const float n2 = (qx * qx + qz * qz) + (qy * qy + qw * qw);
+  if (n2 > 0.0f) {
+    const float n = __fsqrt_rn(n2);
+    qx = __fdiv_rn(qx, n); qy = __fdiv_rn(qy, n); qz = __fdiv_rn(qz, n); qw = __fdiv_rn(qw, n);
+  }
+  const float tx = 2.0f * qx, ty = 2.0f * qy, tz = 2.0f * qz;
+  const float twx = tx * qw, twy = ty * qw, twz = tz * qw;
+  const float txx = tx * qx, txy = ty * qx, txz = tz * qx;
+  const float tyy = ty * qy, tyz = tz * qy, tzz = tz * qz;
+  float r[3][3];
+  r[0][0] = 1.0f - (tyy + tzz); r[0][1] = txy - twz;          r[0][2] = txz + twy;
+  r[1][0] = txy + twz;          r[1][1] = 1.0f - (txx + tzz); r[1][2] = tyz - twx;
+  r[2][0] = txz - twy;          r[2][1] = tyz + twx;          r[2][2] = 1.0f - (txx + tyy);
+  float m[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) m[i][j] = r[i][j] * scale[j];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) S[i][j] = m[i][0] * m[j][0] + (m[i][1] * m[j][1] + m[i][2] * m[j][2]);
+}
+
+// src/preprocess.cpp:17-55.  Returns false when culled.
+__device__ __forceinline__ bool project_one(const bs_gaussian3d& g, const CamDev& cam, Projected& o) {
+  const float* V = cam.v;
+  float p[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    p[i] = (V[i * 4 + 0] * g.mean[0] + (V[i * 4 + 1] * g.mean[1] + V[i * 4 + 2] * g.mean[2])) + V[i * 4 + 3];
+  if (!(p[2] > kNearPlane)) return false;
+
+  const double x = p[0], y = p[1], z = p[2];
+  const double fx = cam.fx, fy = cam.fy;
+  const double zz = z * z;
+  const double jac[2][3] = {{fx / z, 0.0, -fx * x / zz}, {0.0, fy / z, -fy * y / zz}};
+  float Sf[3][3];
+  covariance_of(g.rot, g.scale, Sf);
+  double t[2][3], u[2][3], c[2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      t[i][j] = (jac[i][0] * (double)V[0 * 4 + j] + jac[i][1] * (double)V[1 * 4 + j]) + jac[i][2] * (double)V[2 * 4 + j];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      u[i][j] = (t[i][0] * (double)Sf[0][j] + t[i][1] * (double)Sf[1][j]) + t[i][2] * (double)Sf[2][j];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) c[i][j] = (u[i][0] * t[j][0] + u[i][1] * t[j][1]) + u[i][2] * t[j][2];
+
+  const double det = c[0][0] * c[1][1] - c[0][1] * c[1][0];
+  if (!(det > 0.0) || !isfinite(det)) return false;
+  const double mid = 0.5 * (c[0][0] + c[1][1]);
+  const double lambda_max = mid + sqrt(fmax(0.0, mid * mid - det));
+  if (!(lambda_max > 0.0)) return false;
+
+  o.x = (float)(fx * x / z) + 0.5f * (float)cam.w;
+  o.y = (float)(fy * y / z) + 0.5f * (float)cam.h;
+  o.ca = (float)(c[1][1] / det);
+  o.cb = (float)(-c[0][1] / det);
+  o.cc = (float)(c[0][0] / det);
+  o.depth = (float)z;
+  o.radius = (float)(3.0 * sqrt(lambda_max));
+  if (!isfinite(o.ca) || !isfinite(o.cb) || !isfinite(o.cc) || !isfinite(o.radius)) return false;
+  return true;
+}
+
+// power < cut  =>  opacity * expf(power) < 1/255 (1% margin in the exponent,
+// far above every rounding error), so the exact exp can be skipped without
+// changing a single decision.  opacity <= 0 -> everything skips.
+__device__ __forceinline__ float power_cut_of(float opacity) {
+  if (!(opacity > 0.0f)) return INFINITY;
+  return logf(1.0f / (255.0f * opacity)) - 0.01f;
+}
+
+__device__ __forceinline__ void load_g3d(const bs_gaussian3d* __restrict__ src, int64_t i, bs_gaussian3d& g) {
+  const float* s = reinterpret_cast<const float*>(src + i);
+  float* d = reinterpret_cast<float*>(&g);
+#pragma unroll
+  for (int k = 0; k < 14; ++k) d[k] = __ldg(s + k);
+}
+
+__global__ void __launch_bounds__(256) k_project_flags(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam,
+                                                       uint32_t* __restrict__ block_counts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool vis = false;
+  if (i < n) {
+    bs_gaussian3d g;
+    load_g3d(g3d, i, g);
+    Projected o;
+    vis = project_one(g, cam, o);
+  }
+  const int cnt = __syncthreads_count(vis);
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = (uint32_t)cnt;
+}
+
+__global__ void __launch_bounds__(256) k_project_write(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam,
+                                                       const uint32_t* __restrict__ block_offsets, float4* __restrict__ xyab,
+                                                       float4* __restrict__ cop, float4* __restrict__ rgbr) {
+  __shared__ uint32_t warp_counts[8];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bs_gaussian3d g;
+  Projected o;
+  bool vis = false;
+  if (i < n) {
+    load_g3d(g3d, i, g);
+    vis = project_one(g, cam, o);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t ballot = __ballot_sync(0xffffffffu, vis);
+  if (lane == 0) warp_counts[warp] = __popc(ballot);
+  __syncthreads();
+  uint32_t before = 0;
+  for (int w = 0; w < warp; ++w) before += warp_counts[w];
+  if (vis) {
+    const uint32_t dst = block_offsets[blockIdx.x] + before + __popc(ballot & lanemask_lt());
+    xyab[dst] = make_float4(o.x, o.y, o.ca, o.cb);
+    cop[dst] = make_float4(o.cc, g.opacity, power_cut_of(g.opacity), o.depth);
+    rgbr[dst] = make_float4(g.color[0], g.color[1], g.color[2], o.radius);
+  }
+}
+
+__global__ void k_splats_from_g2d(const bs_gaussian2d* __restrict__ g2d, int64_t n, float4* __restrict__ xyab,
+                                  float4* __restrict__ cop, float4* __restrict__ rgbr) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bs_gaussian2d g = g2d[i];
+  xyab[i] = make_float4(g.x, g.y, g.conic_a, g.conic_b);
+  cop[i] = make_float4(g.conic_c, g.opacity, power_cut_of(g.opacity), g.depth);
+  rgbr[i] = make_float4(g.color[0], g.color[1], g.color[2], g.radius);
+}
+
+__global__ void k_splats_to_g2d(const float4* __restrict__ xyab, const float4* __restrict__ cop,
+                                const float4* __restrict__ rgbr, int64_t n, bs_gaussian2d* __restrict__ g2d) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 a = xyab[i], b = cop[i], c = rgbr[i];
+  bs_gaussian2d g;
+  g.x = a.x; g.y = a.y; g.conic_a = a.z; g.conic_b = a.w;
+  g.conic_c = b.x; g.opacity = b.y; g.depth = b.w;
+  g.color[0] = c.x; g.color[1] = c.y; g.color[2] = c.z; g.radius = c.w;
+  g2d[i] = g;
+}
+
+}  // namespace bs
+
+using namespace bs;
+
+extern "C" size_t bs_preprocess_workspace_bytes(int64_t n) {
+  const int64_t nb = (n + 255) / 256;
+  WsSizer s;
+  s.take<uint32_t>((size_t)nb);                   // block counts -> offsets
+  s.take<uint32_t>((size_t)scan_num_blocks(nb));  // scan partials
+  return s.off + 256;
+}
+
+extern "C" int bs_preprocess(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, bs_splats out,
+                             int32_t* n_visible, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || !cam || !n_visible || (n > 0 && (!g3d || !out.xyab || !out.cop || !out.rgbr))) return BS_ERR_INVALID_ARGUMENT;
+  if (n >= (int64_t)0x7fffffff) return BS_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) {
+    BS_CUDA_TRY(cudaMemsetAsync(n_visible, 0, sizeof(int32_t), st));
+    return BS_OK;
+  }
+  CamDev c;
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 4; ++k) c.v[r * 4 + k] = cam->view[r * 4 + k];
+  c.fx = cam->focal[0];
+  c.fy = cam->focal[1];
+  c.w = cam->width;
+  c.h = cam->height;
+  const int64_t nb = (n + 255) / 256;
+  WsCarver wc(ws, ws_bytes);
+  uint32_t* counts = wc.take<uint32_t>((size_t)nb);
+  uint32_t* partials = wc.take<uint32_t>((size_t)scan_num_blocks(nb));
+  if (!wc.ok || !ws) return BS_ERR_WORKSPACE;
+  k_project_flags<<<(unsigned)nb, 256, 0, st>>>(g3d, n, c, counts);
+  BS_LAUNCH_CHECK();
+  // exclusive scan of block counts in place; grand total -> n_visible (u32 == i32 bits for n < 2^31)
+  BS_CUDA_TRY((exclusive_scan<uint32_t, uint32_t>(counts, counts, nb, nullptr, partials,
+                                                 reinterpret_cast<uint32_t*>(n_visible), st)));
+  k_project_write<<<(unsigned)nb, 256, 0, st>>>(g3d, n, c, counts, reinterpret_cast<float4*>(out.xyab),
+                                                reinterpret_cast<float4*>(out.cop), reinterpret_cast<float4*>(out.rgbr));
+  BS_LAUNCH_CHECK();
+  return BS_OK;
+}
+
+extern "C" int bs_splats_from_g2d(const bs_gaussian2d* g2d, int64_t n, bs_splats out, void* stream) {
+  if (n < 0 || (n > 0 && (!g2d || !out.xyab || !out.cop || !out.rgbr))) return BS_ERR_INVALID_ARGUMENT;
+  if (n == 0) return BS_OK;
+  k_splats_from_g2d<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      g2d, n, reinterpret_cast<float4*>(out.xyab), reinterpret_cast<float4*>(out.cop), reinterpret_cast<float4*>(out.rgbr));
+  BS_LAUNCH_CHECK();
+  return BS_OK;
+}
+
+extern "C" int bs_splats_to_g2d(bs_splats in, int64_t n, bs_gaussian2d* g2d, void* stream) {
+  if (n < 0 || (n > 0 && (!g2d || !in.xyab || !in.cop || !in.rgbr))) return BS_ERR_INVALID_ARGUMENT;
+  if (n == 0) return BS_OK;
+  k_splats_to_g2d<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(in.xyab), reinterpret_cast<const float4*>(in.cop),
+      reinterpret_cast<const float4*>(in.rgbr), n, g2d);
+  BS_LAUNCH_CHECK();
+  return BS_OK;
+}

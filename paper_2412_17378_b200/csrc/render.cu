@@ -1,0 +1,541 @@
+// render.cu — R1-R8: the forward alpha-blend, five variants.
+//
+//   Naive              pixel-wise, static grid (one CTA per tile, thread = pixel),
+//                      xy/conic/opacity staged in smem per 1-CTA-wide chunk,
+//                      colour fetched from L2 on commit        (paper Alg. 4/5)
+//   SharedMemOpt       Naive + colour/depth staged too           (paper §5.2.2)
+//   DynamicBlocks      pixel-wise, persistent CTAs claim tiles from an
+//                      atomicAdd queue in tile order               (paper Alg. 1)
+//   GaussianWise       static grid, CTA = tile, 4 warps; each warp blends one
+//                      pixel with its 32 lanes on 32 consecutive list entries,
+//                      prefix product of (1-alpha) by shfl_up doubling, lane-31
+//                      carry                                  (paper Alg. 2/6)
+//   FineGrainedCombined persistent CTAs (4 warps = 4 pixels) claim 4-pixel
+//                      sub-tile tasks from an atomicAdd queue ordered by tile
+//                      list length, longest first (LPT)          (paper Alg. 3)
+//
+// Semantics: pixel-wise variants == render_reference
+// (src/blend.cpp:55-107); Gaussian-wise variants == render_gaussianwise
+// (src/kernels.cpp:57-155).  In BS_ALPHA_EXACT mode every float op that the
+// reference performs is reproduced with explicit _rn intrinsics (no FMA
+// contraction), expf is glibc-exact, transmittance decisions follow the serial
+// float recurrence and colour/depth accumulate in double — so pixel-wise
+// output is bit-identical to the oracle and Gaussian-wise contrib/term/T/alpha
+// are bit-identical (colour/depth differ only by double-sum association).
+// BS_ALPHA_FAST trades that for ex2.approx + float accumulators.
+//
+// No tensor-core path: blending is a dependent scan, not a contraction.  The
+// kernel is bound by FP32/MUFU/FP64 issue for long lists and by L2 for short
+// ones.
+#include <math.h>
+
+#include "bs_common.cuh"
+#include "exact_expf.cuh"
+
+namespace bs {
+
+__constant__ unsigned long long c_exp2f_tab[32] = BS_EXP2F_TAB_INIT;
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kFgWarps = 4;             // paper Alg. 3: 4 warps <-> 4 pixels per task
+constexpr int kFgThreads = kFgWarps * 32;
+
+struct RArgs {
+  const float4* __restrict__ xyab;
+  const float4* __restrict__ cop;
+  const float4* __restrict__ rgbr;
+  const uint32_t* __restrict__ point_list;
+  const uint32_t* __restrict__ ranges;
+  const uint32_t* __restrict__ task_order;
+  int W, H, pw, ph, cols, T;
+  float bg0, bg1, bg2;
+  float* __restrict__ color;
+  float* __restrict__ alpha;
+  float* __restrict__ depth;
+  float* __restrict__ final_t;
+  int32_t* __restrict__ contrib;
+  int32_t* __restrict__ term;
+  unsigned int* queue;
+};
+
+// R1 eval_alpha + the power>0 arm + skip rule (src/blend.cpp:8-21, 90).
+// Returns true when the step is NOT skipped; alpha is the reference's alpha.
+template <int MODE>
+__device__ __forceinline__ bool eval_step(const float4 a, const float4 c, float sx, float sy,
+                                          const unsigned long long* tab, float& alpha) {
+  const float dx = __fsub_rn(sx, a.x);
+  const float dy = __fsub_rn(sy, a.y);
+  const float q = __fadd_rn(__fmul_rn(__fmul_rn(a.z, dx), dx), __fmul_rn(__fmul_rn(c.x, dy), dy));
+  const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(a.w, dx), dy));
+  if (power < c.z) return false;    // certain skip (see power_cut_of)
+  if (power > 0.0f) return false;   // alpha forced to 0 -> skipped
+  float e;
+  if (MODE == BS_ALPHA_EXACT) {
+    e = glibc_expf(power, tab);
+  } else {
+    float p2 = power * 1.4426950408889634f;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(p2));
+  }
+  const float a0 = __fmul_rn(c.y, e);
+  alpha = (a0 < kAlphaClamp) ? a0 : kAlphaClamp;  // std::min(0.99f, a0)
+  return !(alpha < kAlphaSkip);
+}
+
+template <int MODE>
+struct Accum;
+
+template <>
+struct Accum<BS_ALPHA_EXACT> {
+  double r = 0, g = 0, b = 0, d = 0;
+  __device__ __forceinline__ void add(float alpha, float t, float4 col, float dep) {
+    const double w = __dmul_rn((double)alpha, (double)t);
+    r = __dadd_rn(r, __dmul_rn((double)col.x, w));
+    g = __dadd_rn(g, __dmul_rn((double)col.y, w));
+    b = __dadd_rn(b, __dmul_rn((double)col.z, w));
+    d = __dadd_rn(d, __dmul_rn((double)dep, w));
+  }
+  __device__ __forceinline__ void warp_sum() {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r += __shfl_xor_sync(kFull, r, o);
+      g += __shfl_xor_sync(kFull, g, o);
+      b += __shfl_xor_sync(kFull, b, o);
+      d += __shfl_xor_sync(kFull, d, o);
+    }
+  }
+  __device__ __forceinline__ void finish(const RArgs& A, size_t p, float t, int contrib, int term) const {
+    A.color[3 * p + 0] = __double2float_rn(__dadd_rn(r, __dmul_rn((double)A.bg0, (double)t)));
+    A.color[3 * p + 1] = __double2float_rn(__dadd_rn(g, __dmul_rn((double)A.bg1, (double)t)));
+    A.color[3 * p + 2] = __double2float_rn(__dadd_rn(b, __dmul_rn((double)A.bg2, (double)t)));
+    A.alpha[p] = __fsub_rn(1.0f, t);
+    A.depth[p] = __double2float_rn(d);
+    A.final_t[p] = t;
+    A.contrib[p] = contrib;
+    A.term[p] = term;
+  }
+};
+
+template <>
+struct Accum<BS_ALPHA_FAST> {
+  float r = 0, g = 0, b = 0, d = 0;
+  __device__ __forceinline__ void add(float alpha, float t, float4 col, float dep) {
+    const float w = alpha * t;
+    r = fmaf(col.x, w, r);
+    g = fmaf(col.y, w, g);
+    b = fmaf(col.z, w, b);
+    d = fmaf(dep, w, d);
+  }
+  __device__ __forceinline__ void warp_sum() {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r += __shfl_xor_sync(kFull, r, o);
+      g += __shfl_xor_sync(kFull, g, o);
+      b += __shfl_xor_sync(kFull, b, o);
+      d += __shfl_xor_sync(kFull, d, o);
+    }
+  }
+  __device__ __forceinline__ void finish(const RArgs& A, size_t p, float t, int contrib, int term) const {
+    A.color[3 * p + 0] = fmaf(A.bg0, t, r);
+    A.color[3 * p + 1] = fmaf(A.bg1, t, g);
+    A.color[3 * p + 2] = fmaf(A.bg2, t, b);
+    A.alpha[p] = 1.0f - t;
+    A.depth[p] = d;
+    A.final_t[p] = t;
+    A.contrib[p] = contrib;
+    A.term[p] = term;
+  }
+};
+
+__device__ __forceinline__ void load_tab(unsigned long long* s_tab) {
+  if (threadIdx.x < 32) s_tab[threadIdx.x] = c_exp2f_tab[threadIdx.x];
+}
+
+// ---------------------------------------------------------------------------
+// Pixel-wise tile (Naive / SharedMemOpt / DynamicBlocks).  BLOCK threads, one
+// per pixel slot of the pw x ph patch (BLOCK >= pw*ph).  The CTA stages the
+// tile list in BLOCK-wide chunks; a chunk is skipped once every pixel stopped
+// (__syncthreads_count, as Inria's renderCUDA does).
+template <int MODE, bool STAGE_COLOR, int BLOCK>
+struct PwChunk {
+  // 1024-thread CTAs staging colour too would exceed 48 KB of static smem
+  static constexpr int value = (STAGE_COLOR && BLOCK > 512) ? 512 : BLOCK;
+};
+
+template <int MODE, bool STAGE_COLOR, int BLOCK>
+__device__ __forceinline__ void pixelwise_tile(const RArgs& A, int tile, float4* s_xyab, float4* s_cop,
+                                               float4* s_rgb, uint32_t* s_id, const unsigned long long* s_tab) {
+  const int tid = threadIdx.x;
+  const int tx = tile % A.cols, ty = tile / A.cols;
+  const int lx = tid % A.pw, ly = tid / A.pw;
+  const int px = tx * A.pw + lx, py = ty * A.ph + ly;
+  const bool inside = tid < A.pw * A.ph && px < A.W && py < A.H;
+  const float sx = __fadd_rn((float)px, 0.5f), sy = __fadd_rn((float)py, 0.5f);
+  const uint32_t start = A.ranges[2 * tile], end = A.ranges[2 * tile + 1];
+
+  bool done = !inside;
+  float t = 1.0f;
+  int contrib = 0, term = 0;
+  Accum<MODE> acc;
+
+  constexpr int CHUNK = PwChunk<MODE, STAGE_COLOR, BLOCK>::value;
+  for (uint32_t base = start; base < end; base += CHUNK) {
+    if (__syncthreads_count(!done) == 0) break;
+    const uint32_t k = base + tid;
+    if (tid < CHUNK && k < end) {
+      const uint32_t id = __ldg(A.point_list + k);
+      s_xyab[tid] = __ldg(A.xyab + id);
+      s_cop[tid] = __ldg(A.cop + id);
+      if (STAGE_COLOR) s_rgb[tid] = __ldg(A.rgbr + id);
+      else s_id[tid] = id;
+    }
+    __syncthreads();
+    if (!done) {
+      const int cnt = (int)min((uint32_t)CHUNK, end - base);
+      for (int j = 0; j < cnt; ++j) {
+        float alpha;
+        const float4 c = s_cop[j];
+        if (!eval_step<MODE>(s_xyab[j], c, sx, sy, s_tab, alpha)) continue;
+        const float tmp = __fmul_rn(t, __fsub_rn(1.0f, alpha));
+        if (tmp < kStopThreshold) {
+          done = true;
+          term = (int)(base - start) + j + 1;
+          break;
+        }
+        const float4 col = STAGE_COLOR ? s_rgb[j] : __ldg(A.rgbr + s_id[j]);
+        acc.add(alpha, t, col, c.w);
+        t = tmp;
+        ++contrib;
+      }
+    }
+  }
+  if (inside) acc.finish(A, (size_t)py * A.W + px, t, contrib, term);
+}
+
+template <int MODE, bool STAGE_COLOR, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_render_pixelwise(RArgs A) {
+  constexpr int CHUNK = PwChunk<MODE, STAGE_COLOR, BLOCK>::value;
+  __shared__ float4 s_xyab[CHUNK];
+  __shared__ float4 s_cop[CHUNK];
+  __shared__ float4 s_rgb[STAGE_COLOR ? CHUNK : 1];
+  __shared__ uint32_t s_id[STAGE_COLOR ? 1 : CHUNK];
+  __shared__ unsigned long long s_tab[32];
+  load_tab(s_tab);
+  __syncthreads();
+  pixelwise_tile<MODE, STAGE_COLOR, BLOCK>(A, blockIdx.x, s_xyab, s_cop, s_rgb, s_id, s_tab);
+}
+
+// Paper Alg. 1 (with the exit test fixed to >=).
+template <int MODE, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_render_dynamic(RArgs A) {
+  __shared__ float4 s_xyab[BLOCK];
+  __shared__ float4 s_cop[BLOCK];
+  __shared__ uint32_t s_id[BLOCK];
+  __shared__ unsigned long long s_tab[32];
+  __shared__ int s_tile;
+  load_tab(s_tab);
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(A.queue, 1u);
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile >= A.T) return;
+    pixelwise_tile<MODE, false, BLOCK>(A, tile, s_xyab, s_cop, nullptr, s_id, s_tab);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Gaussian-wise: kFgWarps warps, warp w blends pixel `pix[w]` of `tile`; the
+// CTA stages the list in 128-entry chunks shared by the 4 warps; each warp
+// walks a chunk in 32-wide groups.
+template <int MODE>
+__device__ __forceinline__ void gaussianwise_task(const RArgs& A, int tile, int sub, float4* s_xyab, float4* s_cop,
+                                                  float4* s_rgb, const unsigned long long* s_tab) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tx = tile % A.cols, ty = tile / A.cols;
+  const int local = sub * kFgWarps + warp;
+  const int lx = local % A.pw, ly = local / A.pw;
+  const int px = tx * A.pw + lx, py = ty * A.ph + ly;
+  const bool inside = local < A.pw * A.ph && px < A.W && py < A.H;
+  const float sx = __fadd_rn((float)px, 0.5f), sy = __fadd_rn((float)py, 0.5f);
+  const uint32_t start = A.ranges[2 * tile], end = A.ranges[2 * tile + 1];
+
+  bool done = !inside;  // warp-uniform
+  float t = 1.0f;       // warp-uniform (serial carry)
+  int contrib = 0, term = 0;
+  Accum<MODE> acc;
+
+  for (uint32_t base = start; base < end; base += kFgThreads) {
+    if (__syncthreads_count(!done) == 0) break;
+    const uint32_t k = base + tid;
+    if (k < end) {
+      const uint32_t id = __ldg(A.point_list + k);
+      s_xyab[tid] = __ldg(A.xyab + id);
+      s_cop[tid] = __ldg(A.cop + id);
+      s_rgb[tid] = __ldg(A.rgbr + id);
+    }
+    __syncthreads();
+    if (done) continue;
+    const uint32_t cnt = min((uint32_t)kFgThreads, end - base);
+    for (uint32_t g0 = 0; g0 < cnt; g0 += 32) {
+      const uint32_t j = g0 + lane;
+      const bool active = j < cnt;
+      float alpha = 0.0f;
+      bool ns = false;
+      float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (active) {
+        c = s_cop[j];
+        ns = eval_step<MODE>(s_xyab[j], c, sx, sy, s_tab, alpha);
+      }
+      const float f = ns ? __fsub_rn(1.0f, alpha) : 1.0f;
+      // R5 warp_prefix_product: inclusive doubling prefix (offsets 1..16)
+      float pre = f;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const float v = __shfl_up_sync(kFull, pre, off);
+        if (lane >= off) pre = __fmul_rn(pre, v);
+      }
+      const float per_lane = __fmul_rn(t, pre);
+      float t_before = __shfl_up_sync(kFull, per_lane, 1);
+      if (lane == 0) t_before = t;
+
+      const unsigned nsmask = __ballot_sync(kFull, ns);
+      int stop = 32;
+      float t_next;
+      if (MODE == BS_ALPHA_EXACT) {
+        // serial float recurrence over the non-skipped lanes (src/kernels.cpp:79-89)
+        float ts = t;
+        unsigned m = nsmask;
+        while (m) {
+          const int jl = __ffs(m) - 1;
+          const float fj = __shfl_sync(kFull, f, jl);
+          const float tmp = __fmul_rn(ts, fj);
+          if (tmp < kStopThreshold) {
+            stop = jl;
+            break;
+          }
+          ts = tmp;
+          m &= m - 1;
+        }
+        t_next = ts;
+      } else {
+        // paper Alg. 6: stop on the prefix product (commit nothing for the
+        // terminating Gaussian, SPEC blend-core decision)
+        const unsigned sm = __ballot_sync(kFull, ns && per_lane < kStopThreshold);
+        if (sm) {
+          stop = __ffs(sm) - 1;
+          t_next = __shfl_sync(kFull, t_before, stop);
+        } else {
+          t_next = __shfl_sync(kFull, per_lane, 31);
+        }
+      }
+      const bool com = ns && lane < stop;
+      if (com) acc.add(alpha, t_before, s_rgb[j], c.w);
+      contrib += __popc(nsmask & ((stop >= 32) ? kFull : ((1u << stop) - 1u)));
+      t = t_next;
+      if (stop < 32) {
+        term = (int)(base - start + g0) + stop + 1;
+        done = true;
+        break;
+      }
+    }
+  }
+  if (inside) {
+    acc.warp_sum();
+    if (lane == 0) acc.finish(A, (size_t)py * A.W + px, t, contrib, term);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kFgThreads) k_render_gaussianwise(RArgs A) {
+  __shared__ float4 s_xyab[kFgThreads];
+  __shared__ float4 s_cop[kFgThreads];
+  __shared__ float4 s_rgb[kFgThreads];
+  __shared__ unsigned long long s_tab[32];
+  load_tab(s_tab);
+  const int tile = blockIdx.x;
+  const int subs = (A.pw * A.ph + kFgWarps - 1) / kFgWarps;
+  for (int s = 0; s < subs; ++s) {
+    __syncthreads();
+    gaussianwise_task<MODE>(A, tile, s, s_xyab, s_cop, s_rgb, s_tab);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kFgThreads) k_render_fine(RArgs A, int subs, int total_tasks) {
+  __shared__ float4 s_xyab[kFgThreads];
+  __shared__ float4 s_cop[kFgThreads];
+  __shared__ float4 s_rgb[kFgThreads];
+  __shared__ unsigned long long s_tab[32];
+  __shared__ int s_task;
+  load_tab(s_tab);
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_task = (int)atomicAdd(A.queue, 1u);
+    __syncthreads();
+    const int task = s_task;
+    if (task >= total_tasks) return;
+    const int q = task / subs;
+    const int tile = A.task_order ? (int)A.task_order[q] : q;
+    gaussianwise_task<MODE>(A, tile, task - q * subs, s_xyab, s_cop, s_rgb, s_tab);
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_frame_work(const int32_t* __restrict__ term, const int32_t* __restrict__ contrib,
+                             const uint32_t* __restrict__ ranges, int W, int H, int pw, int ph, int cols,
+                             unsigned long long* __restrict__ out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long e = 0, c = 0;
+  if (p < (int64_t)W * H) {
+    const int px = (int)(p % W), py = (int)(p / W);
+    const int tile = (py / ph) * cols + (px / pw);
+    const int32_t tm = term[p];
+    e = tm > 0 ? (unsigned long long)tm : (unsigned long long)(ranges[2 * tile + 1] - ranges[2 * tile]);
+    c = (unsigned long long)contrib[p];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    e += __shfl_xor_sync(kFull, e, o);
+    c += __shfl_xor_sync(kFull, c, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out + 0, e);
+    atomicAdd(out + 1, c);
+  }
+}
+
+template <int MODE>
+static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStream_t st) {
+  const int T = A.T;
+  switch (variant) {
+    case BS_NAIVE:
+    case BS_SHARED_MEM_OPT: {
+      const bool smem = variant == BS_SHARED_MEM_OPT;
+#define BS_PW_CASE(B)                                                                   \
+  if (block_pixels <= B) {                                                              \
+    if (smem) k_render_pixelwise<MODE, true, B><<<T, B, 0, st>>>(A);                    \
+    else k_render_pixelwise<MODE, false, B><<<T, B, 0, st>>>(A);                        \
+    break;                                                                              \
+  }
+      BS_PW_CASE(64) BS_PW_CASE(128) BS_PW_CASE(256) BS_PW_CASE(512) BS_PW_CASE(1024)
+#undef BS_PW_CASE
+      return BS_ERR_UNSUPPORTED;
+    }
+    case BS_DYNAMIC_BLOCKS: {
+      int dev = 0, sms = 0;
+      BS_CUDA_TRY(cudaGetDevice(&dev));
+      BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+#define BS_DYN_CASE(B)                                                                                   \
+  if (block_pixels <= B) {                                                                               \
+    int per_sm = 0;                                                                                      \
+    BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_dynamic<MODE, B>, B, 0)); \
+    const int grid = max(1, min(T, sms * max(1, per_sm)));                                               \
+    k_render_dynamic<MODE, B><<<grid, B, 0, st>>>(A);                                                    \
+    break;                                                                                               \
+  }
+      BS_DYN_CASE(64) BS_DYN_CASE(128) BS_DYN_CASE(256) BS_DYN_CASE(512) BS_DYN_CASE(1024)
+#undef BS_DYN_CASE
+      return BS_ERR_UNSUPPORTED;
+    }
+    case BS_GAUSSIAN_WISE:
+      k_render_gaussianwise<MODE><<<T, kFgThreads, 0, st>>>(A);
+      break;
+    case BS_FINE_GRAINED_COMBINED: {
+      int dev = 0, sms = 0, per_sm = 0;
+      BS_CUDA_TRY(cudaGetDevice(&dev));
+      BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_fine<MODE>, kFgThreads, 0));
+      const int subs = (A.pw * A.ph + kFgWarps - 1) / kFgWarps;
+      const int64_t total = (int64_t)T * subs;
+      if (total > 0x7fffffff) return BS_ERR_UNSUPPORTED;
+      const int grid = (int)max((int64_t)1, min(total, (int64_t)sms * max(1, per_sm)));
+      k_render_fine<MODE><<<grid, kFgThreads, 0, st>>>(A, subs, (int)total);
+      break;
+    }
+    default:
+      return BS_ERR_INVALID_ARGUMENT;
+  }
+  BS_LAUNCH_CHECK();
+  return BS_OK;
+}
+
+}  // namespace bs
+
+using namespace bs;
+
+extern "C" size_t bs_render_workspace_bytes(void) { return 256; }
+
+extern "C" int bs_render_forward(int variant, int alpha_mode, bs_splats g, const uint32_t* point_list,
+                                 const uint32_t* tile_ranges, const uint32_t* task_order, int32_t width,
+                                 int32_t height, int32_t pw, int32_t ph, const float bg[3], bs_frame_out out,
+                                 void* ws, size_t ws_bytes, void* stream) {
+  if (width <= 0 || height <= 0 || pw <= 0 || ph <= 0 || !bg || !tile_ranges) return BS_ERR_INVALID_ARGUMENT;
+  if (variant < 0 || variant > 4) return BS_ERR_INVALID_ARGUMENT;
+  if (alpha_mode != BS_ALPHA_EXACT && alpha_mode != BS_ALPHA_FAST) return BS_ERR_INVALID_ARGUMENT;
+  if (!out.color || !out.alpha || !out.depth || !out.final_t || !out.contrib || !out.term) return BS_ERR_INVALID_ARGUMENT;
+  if ((int64_t)pw * ph > 1024) return BS_ERR_UNSUPPORTED;
+  if (!ws || ws_bytes < bs_render_workspace_bytes()) return BS_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  RArgs A;
+  A.xyab = reinterpret_cast<const float4*>(g.xyab);
+  A.cop = reinterpret_cast<const float4*>(g.cop);
+  A.rgbr = reinterpret_cast<const float4*>(g.rgbr);
+  A.point_list = point_list;
+  A.ranges = tile_ranges;
+  A.task_order = task_order;
+  A.W = width; A.H = height; A.pw = pw; A.ph = ph;
+  A.cols = (width + pw - 1) / pw;
+  const int64_t T = (int64_t)A.cols * ((height + ph - 1) / ph);
+  if (T > 0x7fffffff) return BS_ERR_UNSUPPORTED;
+  A.T = (int)T;
+  A.bg0 = bg[0]; A.bg1 = bg[1]; A.bg2 = bg[2];
+  A.color = out.color; A.alpha = out.alpha; A.depth = out.depth; A.final_t = out.final_t;
+  A.contrib = out.contrib; A.term = out.term;
+  A.queue = reinterpret_cast<unsigned int*>(ws);
+  if (variant == BS_DYNAMIC_BLOCKS || variant == BS_FINE_GRAINED_COMBINED)
+    BS_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(unsigned int), st));
+  const int block_pixels = pw * ph;
+  return alpha_mode == BS_ALPHA_EXACT ? launch_variant<BS_ALPHA_EXACT>(variant, A, block_pixels, st)
+                                      : launch_variant<BS_ALPHA_FAST>(variant, A, block_pixels, st);
+}
+
+namespace bs {
+__global__ void k_test_expf(const float* __restrict__ x, float* __restrict__ y, int64_t n, int mode) {
+  __shared__ unsigned long long s_tab[32];
+  load_tab(s_tab);
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float e;
+    if (mode == BS_ALPHA_EXACT) {
+      e = glibc_expf(x[i], s_tab);
+    } else {
+      const float p2 = x[i] * 1.4426950408889634f;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(p2));
+    }
+    y[i] = e;
+  }
+}
+}  // namespace bs
+
+extern "C" int bs_test_expf(const float* x, float* y, int64_t n, int alpha_mode, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !y))) return BS_ERR_INVALID_ARGUMENT;
+  if (n == 0) return BS_OK;
+  const int64_t blocks = min((n + 255) / 256, (int64_t)148 * 16);
+  k_test_expf<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, y, n, alpha_mode);
+  BS_LAUNCH_CHECK();
+  return BS_OK;
+}
+
+extern "C" int bs_frame_work(const int32_t* term, const int32_t* contrib, const uint32_t* tile_ranges, int32_t width,
+                             int32_t height, int32_t pw, int32_t ph, uint64_t* evaluated_committed, void* stream) {
+  if (width <= 0 || height <= 0 || pw <= 0 || ph <= 0 || !term || !contrib || !tile_ranges || !evaluated_committed)
+    return BS_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = (cudaStream_t)stream;
+  BS_CUDA_TRY(cudaMemsetAsync(evaluated_committed, 0, 2 * sizeof(uint64_t), st));
+  const int64_t P = (int64_t)width * height;
+  k_frame_work<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(term, contrib, tile_ranges, width, height, pw, ph,
+                                                            (width + pw - 1) / pw,
+                                                            reinterpret_cast<unsigned long long*>(evaluated_committed));
+  BS_LAUNCH_CHECK();
+  return BS_OK;
+}

@@ -1,0 +1,143 @@
+// scan.cuh — device-wide exclusive prefix sum (reduce-then-scan, 3 kernels).
+// Used for compaction offsets, tiles-touched offsets, radix-sort digit
+// offsets and tile ranges.  Items at index >= *d_count (when d_count is given)
+// count as zero, so counts that live on the device need no host sync.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bs {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;  // 2048
+
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the block total
+// in *total.  blockDim.x must be a multiple of 32, <= 1024.
+template <typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* total) {
+  __shared__ T warp_sums[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  T inc = warp_inclusive_scan(v);
+  if (lane == 31) warp_sums[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T s = lane < nwarps ? warp_sums[lane] : T(0);
+    s = warp_inclusive_scan(s);
+    warp_sums[lane] = s;
+  }
+  __syncthreads();
+  const T warp_prefix = warp == 0 ? T(0) : warp_sums[warp - 1];
+  *total = warp_sums[nwarps - 1];
+  __syncthreads();
+  return warp_prefix + inc - v;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_reduce_sum(T v) {
+  __shared__ T red[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  T s = T(0);
+  if (threadIdx.x == 0)
+    for (int w = 0; w < nwarps; ++w) s += red[w];
+  __syncthreads();
+  return s;  // valid in thread 0
+}
+
+template <typename TIn, typename TOut>
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const TIn* __restrict__ in, int64_t n_cap,
+                                                              const int32_t* __restrict__ d_count,
+                                                              TOut* __restrict__ partials) {
+  const int64_t n = d_count ? (int64_t)*d_count : n_cap;
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  TOut s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int64_t k = base + (int64_t)i * kScanThreads + threadIdx.x;
+    if (k < n) s += (TOut)in[k];
+  }
+  s = block_reduce_sum(s);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+// Single block: exclusive scan of partials in place, writes grand total.
+template <typename TOut>
+__global__ void __launch_bounds__(1024) k_scan_partials(TOut* __restrict__ partials, int64_t nb,
+                                                        TOut* __restrict__ total_out) {
+  __shared__ TOut carry_s;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nb; base += blockDim.x) {
+    const int64_t k = base + threadIdx.x;
+    TOut v = k < nb ? partials[k] : TOut(0);
+    TOut tot;
+    TOut ex = block_exclusive_scan(v, &tot);
+    const TOut carry = carry_s;
+    if (k < nb) partials[k] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s = carry + tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total_out) *total_out = carry_s;
+}
+
+template <typename TIn, typename TOut>
+__global__ void __launch_bounds__(kScanThreads) k_scan_downsweep(const TIn* __restrict__ in, int64_t n_cap,
+                                                                 const int32_t* __restrict__ d_count,
+                                                                 const TOut* __restrict__ partials,
+                                                                 TOut* __restrict__ out) {
+  const int64_t n = d_count ? (int64_t)*d_count : n_cap;
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  // blocked arrangement: thread t owns items [t*8, t*8+8) of the tile
+  TOut v[kScanItems];
+  TOut local = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int64_t k = base + (int64_t)threadIdx.x * kScanItems + i;
+    v[i] = k < n ? (TOut)in[k] : TOut(0);
+    local += v[i];
+  }
+  TOut tot;
+  TOut run = block_exclusive_scan(local, &tot) + partials[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int64_t k = base + (int64_t)threadIdx.x * kScanItems + i;
+    if (k < n_cap) out[k] = run;
+    run += v[i];
+  }
+}
+
+inline int64_t scan_num_blocks(int64_t n_cap) { return (n_cap + kScanTile - 1) / kScanTile; }
+
+// Workspace: partials[nb].  total (device) may be null.  out may alias in.
+template <typename TIn, typename TOut>
+inline cudaError_t exclusive_scan(const TIn* in, TOut* out, int64_t n_cap, const int32_t* d_count, TOut* partials,
+                                  TOut* total, cudaStream_t st) {
+  const int64_t nb = scan_num_blocks(n_cap);
+  if (nb == 0) {
+    if (total) return cudaMemsetAsync(total, 0, sizeof(TOut), st);
+    return cudaSuccess;
+  }
+  k_scan_reduce<TIn, TOut><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_cap, d_count, partials);
+  k_scan_partials<TOut><<<1, 1024, 0, st>>>(partials, nb, total);
+  k_scan_downsweep<TIn, TOut><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_cap, d_count, partials, out);
+  return cudaPeekAtLastError();
+}
+
+}  // namespace bs

@@ -1,0 +1,235 @@
+"""GPU parity: every CUDA stage vs the CPU oracle, through the C-ABI.
+
+Bars (SURVEY §8.0 / BASELINE north star):
+  * preprocess, binning, tile stats: bit-exact;
+  * BS_ALPHA_EXACT render: pixel-wise variants bit-exact on every plane;
+    Gaussian-wise variants bit-exact on alpha / final_t / contrib / term and
+    colour/depth within 1e-6 abs (double-sum association only);
+  * BS_ALPHA_FAST render: RGB and T within 1e-4 abs on pixels whose
+    contrib/term match; mismatching pixels are counted and must stay rare.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from paper_2412_17378_b200 import _native as N  # noqa: E402
+from paper_2412_17378_b200 import api  # noqa: E402
+
+DEV = "cuda"
+PLANES_F = ("color", "alpha", "depth", "final_t")
+
+
+def ncam(o_cam: O.Camera) -> N.Camera:
+    return N.Camera.from_buffer_copy(bytes(o_cam))
+
+
+def scene(n, W, H, f, bgfrac=0.12, seed=42, sigma=0.035):
+    cam = O.make_camera(focal=(f, f), width=W, height=H)
+    return O.gen_clustered_scene(n, cam, seed=seed, sigma=sigma, bgfrac=bgfrac), cam
+
+
+def to_dev_splats(g2d: np.ndarray) -> api.DeviceSplats:
+    return api.splats_from_g2d(g2d, DEV)
+
+
+# ---------------------------------------------------------------------------
+def test_library_loads_and_device():
+    assert N.lib().bs_abi_version() == 1
+    assert api.sm_count() >= 1
+
+
+def test_exact_expf_matches_libm():
+    # every float in [-6, 0] at stride 7 (~1.5e8 values), plus the glibc special case
+    lo = np.float32(-6.0).view(np.uint32)
+    bits = np.arange(0x80000000, int(lo) + 1, 7, dtype=np.uint64).astype(np.uint32)
+    x = np.concatenate([bits.view(np.float32), np.array([-0x1.f8cbb2p+5, -50.0, -103.0, -104.5], np.float32)])
+    xd = torch.from_numpy(x).to(DEV)
+    yd = torch.empty_like(xd)
+    N.call("bs_test_expf", xd.data_ptr(), yd.data_ptr(), x.size, N.ALPHA_EXACT, api._stream(DEV))
+    y = yd.cpu().numpy()
+    bad = O.lib().orc_expf_compare_batch(O.p(x), O.p(y), x.size)
+    assert bad == 0
+
+
+def test_preprocess_bit_exact():
+    g3d, cam = scene(20000, 256, 256, 256.0, bgfrac=0.5)
+    ref = O.project_all(g3d, cam)
+    d = api.g3d_to_device(g3d)
+    s = api.project_all(d, len(g3d), ncam(cam))
+    got = api.splats_to_g2d(s)
+    assert len(got) == len(ref)
+    assert got.tobytes() == ref.tobytes()
+
+
+def test_preprocess_culls_and_empty():
+    cam = O.make_camera(focal=(100, 100), width=64, height=64)
+    g = np.zeros(3, dtype=O.G3D_DTYPE)
+    g["scale"] = 1.0
+    g["rot"][:, 0] = 1.0
+    g["opacity"] = 0.5
+    g["mean"][0] = (0, 0, 0.005)   # behind the near plane
+    g["mean"][1] = (0, 0, 10.0)
+    g["mean"][2] = (1, -1, 5.0)
+    ref = O.project_all(g, cam)
+    s = api.project_all(api.g3d_to_device(g), 3, ncam(cam))
+    got = api.splats_to_g2d(s)
+    assert got.tobytes() == ref.tobytes() and len(got) == 2
+    s0 = api.project_all(torch.empty(56, dtype=torch.uint8, device=DEV), 0, ncam(cam))
+    assert int(s0.n_visible.item()) == 0
+
+
+@pytest.mark.parametrize("W,H,pw,ph,n", [(256, 256, 16, 16, 10000), (250, 130, 16, 8, 4000), (960, 540, 16, 8, 30000),
+                                         (64, 64, 16, 16, 1), (100, 60, 32, 32, 3000)])
+def test_binning_bit_exact(W, H, pw, ph, n):
+    g3d, cam = scene(n, W, H, float(W), bgfrac=0.3)
+    g2d = O.project_all(g3d, cam)
+    pl_ref, rg_ref = O.bin_tiles(g2d, W, H, pw, ph)
+    s = to_dev_splats(g2d)
+    b = api.bin_tiles(s, W, H, pw, ph)
+    assert b.k == len(pl_ref)
+    assert np.array_equal(b.tile_ranges.cpu().numpy().view(np.uint32), rg_ref)
+    assert np.array_equal(b.point_list.cpu().numpy().view(np.uint32), pl_ref)
+
+
+def test_binning_depth_ties_and_empty():
+    # many equal depths: ties must resolve by compacted index
+    g2d = np.zeros(500, dtype=O.G2D_DTYPE)
+    rng = np.random.default_rng(3)
+    g2d["x"] = rng.uniform(-20, 84, 500)
+    g2d["y"] = rng.uniform(-20, 84, 500)
+    g2d["radius"] = rng.uniform(0, 30, 500)
+    g2d["depth"] = rng.choice([1.0, 2.0, 2.5], 500)
+    g2d["conic_a"] = g2d["conic_c"] = 1.0
+    g2d["opacity"] = 0.5
+    pl_ref, rg_ref = O.bin_tiles(g2d, 64, 64, 16, 16)
+    b = api.bin_tiles(to_dev_splats(g2d), 64, 64, 16, 16)
+    assert np.array_equal(b.point_list.cpu().numpy().view(np.uint32), pl_ref)
+    assert np.array_equal(b.tile_ranges.cpu().numpy().view(np.uint32), rg_ref)
+    e = api.bin_tiles(to_dev_splats(np.zeros(0, dtype=O.G2D_DTYPE)), 64, 64, 16, 16)
+    assert e.k == 0 and not e.tile_ranges.cpu().numpy().any()
+
+
+def test_tile_stats_match_oracle():
+    g3d, cam = scene(30000, 960, 540, 960.0)
+    g2d = O.project_all(g3d, cam)
+    pl, rg = O.bin_tiles(g2d, 960, 540, 16, 8)
+    ref = O.tile_load_histogram(rg, 60, 68)
+    b = api.bin_tiles(to_dev_splats(g2d), 960, 540, 16, 8)
+    st = api.tile_load_histogram(b)
+    s = st.summary()
+    for k in ("min", "max", "p50", "p99"):
+        assert s[k] == ref[k], k
+    assert s["mean"] == ref["mean"]
+    assert s["tiles"] == 4080
+    counts = st.counts.cpu().numpy().view(np.uint32)[:4080]
+    assert np.array_equal(counts, ref["counts"])
+    order = st.task_order.cpu().numpy()[:4080]
+    exp = np.lexsort((np.arange(4080), -ref["counts"].astype(np.int64)))
+    assert np.array_equal(order, exp)
+
+
+def _gpu_render(variant, g2d, W, H, pw, ph, bg, mode):
+    s = to_dev_splats(g2d)
+    b = api.bin_tiles(s, W, H, pw, ph)
+    st = api.tile_load_histogram(b)
+    f = api.render_forward(variant, s, b, W, H, pw, ph, bg, mode, st.task_order)
+    torch.cuda.synchronize()
+    return f.to_numpy(), b
+
+
+def _oracle_render(variant, g2d, W, H, pw, ph, bg):
+    pl, rg = O.bin_tiles(g2d, W, H, pw, ph)
+    return O.render(variant, pl, rg, g2d, W, H, pw, ph, bg, lazy=True, threads=0)
+
+
+CASES = [(256, 256, 16, 16, 10000, 1.0), (192, 128, 16, 8, 6000, 0.12), (250, 130, 16, 16, 5000, 0.3)]
+
+
+@pytest.mark.parametrize("W,H,pw,ph,n,bgfrac", CASES)
+@pytest.mark.parametrize("variant", range(5))
+def test_render_exact(variant, W, H, pw, ph, n, bgfrac):
+    g3d, cam = scene(n, W, H, float(W), bgfrac=bgfrac)
+    g2d = O.project_all(g3d, cam)
+    bg = (0.1, 0.2, 0.3)
+    ref = _oracle_render(variant, g2d, W, H, pw, ph, bg)
+    got, _ = _gpu_render(variant, g2d, W, H, pw, ph, bg, N.ALPHA_EXACT)
+    assert np.array_equal(got["contrib"], ref["contrib"])
+    assert np.array_equal(got["term"], ref["term"])
+    assert np.array_equal(got["final_t"].view(np.uint32), ref["final_t"].view(np.uint32))
+    assert np.array_equal(got["alpha"].view(np.uint32), ref["alpha"].view(np.uint32))
+    if variant in (0, 1, 4):  # pixel-wise: bit-exact colour/depth too
+        assert np.array_equal(got["color"].view(np.uint32), ref["color"].view(np.uint32))
+        assert np.array_equal(got["depth"].view(np.uint32), ref["depth"].view(np.uint32))
+    else:
+        assert np.max(np.abs(got["color"] - ref["color"])) <= 1e-6
+        assert np.max(np.abs(got["depth"] - ref["depth"]) / np.maximum(1, np.abs(ref["depth"]))) <= 1e-6
+
+
+@pytest.mark.parametrize("variant", range(5))
+def test_render_fast_tolerance(variant):
+    W, H, pw, ph = 256, 256, 16, 16
+    g3d, cam = scene(20000, W, H, 256.0, bgfrac=0.12)
+    g2d = O.project_all(g3d, cam)
+    bg = (0.1, 0.2, 0.3)
+    ref = _oracle_render(variant, g2d, W, H, pw, ph, bg)
+    got, _ = _gpu_render(variant, g2d, W, H, pw, ph, bg, N.ALPHA_FAST)
+    match = (got["contrib"] == ref["contrib"]) & (got["term"] == ref["term"])
+    frac_mismatch = 1.0 - match.mean()
+    assert frac_mismatch < 2e-3, frac_mismatch
+    col_err = np.abs(got["color"] - ref["color"]).reshape(-1, 3).max(axis=1)
+    assert col_err[match].max() <= 1e-4
+    assert np.abs(got["final_t"] - ref["final_t"])[match].max() <= 1e-4
+
+
+def test_render_empty_scene_is_background():
+    W, H = 64, 48
+    g2d = np.zeros(0, dtype=O.G2D_DTYPE)
+    for v in range(5):
+        got, _ = _gpu_render(v, g2d, W, H, 16, 16, (0.25, 0.5, 0.75), N.ALPHA_EXACT)
+        assert np.allclose(got["color"].reshape(-1, 3), [0.25, 0.5, 0.75])
+        assert (got["final_t"] == 1).all() and (got["contrib"] == 0).all() and (got["term"] == 0).all()
+
+
+def test_frame_work_counts():
+    W, H, pw, ph = 256, 256, 16, 16
+    g3d, cam = scene(10000, W, H, 256.0, bgfrac=0.5)
+    g2d = O.project_all(g3d, cam)
+    got, b = _gpu_render(0, g2d, W, H, pw, ph, (0, 0, 0), N.ALPHA_EXACT)
+    f = api.DeviceFrame.empty(W, H, DEV)
+    f.term.copy_(torch.from_numpy(got["term"]))
+    f.contrib.copy_(torch.from_numpy(got["contrib"]))
+    e, c = api.frame_work(f, b, pw, ph)
+    rg = b.tile_ranges.cpu().numpy().view(np.uint32)
+    lens = (rg[1::2] - rg[0::2]).astype(np.int64)
+    py, px = np.divmod(np.arange(W * H), W)
+    tile = (py // ph) * (W // pw) + px // pw
+    cons = np.where(got["term"] > 0, got["term"], lens[tile])
+    assert e == int(cons.sum()) and c == int(got["contrib"].sum())
+
+
+def test_pipeline_end_to_end_matches_oracle():
+    W, H, pw, ph = 320, 192, 16, 16
+    g3d, cam = scene(15000, W, H, 320.0)
+    ref_g2d = O.project_all(g3d, cam)
+    ref = _oracle_render(3, ref_g2d, W, H, pw, ph, (0, 0, 0))
+    pipe = api.Pipeline(W, H, pw, ph, DEV, N.ALPHA_EXACT)
+    frame, v = pipe.forward(api.g3d_to_device(g3d), len(g3d), ncam(cam), variant="FineGrainedCombined")
+    got = frame.to_numpy()
+    assert np.array_equal(got["contrib"], ref["contrib"]) and np.array_equal(got["term"], ref["term"])
+    assert np.max(np.abs(got["color"] - ref["color"])) <= 1e-6
+
+
+def test_generator_matches_oracle():
+    cam = O.make_camera(focal=(1000, 1000), width=1920, height=1080)
+    ref = O.gen_clustered_scene(5000, cam)
+    got = api.gen_clustered_scene(5000, ncam(cam))
+    assert got.tobytes() == ref.tobytes()
