@@ -51,7 +51,7 @@ def test_exact_expf_matches_libm():
     # every float in [-6, 0] at stride 7 (~1.5e8 values), plus the glibc special case
     lo = np.float32(-6.0).view(np.uint32)
     bits = np.arange(0x80000000, int(lo) + 1, 7, dtype=np.uint64).astype(np.uint32)
-    x = np.concatenate([bits.view(np.float32), np.array([-0x1.f8cbb2p+5, -50.0, -103.0, -104.5], np.float32)])
+    x = np.concatenate([bits.view(np.float32), np.array([float.fromhex("-0x1.f8cbb2p+5"), -50.0, -103.0, -104.5], np.float32)])
     xd = torch.from_numpy(x).to(DEV)
     yd = torch.empty_like(xd)
     N.call("bs_test_expf", xd.data_ptr(), yd.data_ptr(), x.size, N.ALPHA_EXACT, api._stream(DEV))
