@@ -1,0 +1,434 @@
+#!/usr/bin/env python
+"""bench.py — B200 Balanced-3DGS forward render benchmark (driver contract).
+
+Metric (BASELINE.json): fwd render ms/frame + blends/s (1080p, 1M Gaussians);
+views/s at 1/2/4/8 GPU.  One step = one full forward of one 1920x1080 view of
+the 1M-Gaussian clustered scene (preprocess -> bin -> tile stats -> per-frame
+variant selection -> render) on each GPU.  Views come from a 64-view orbit
+(yaw -15..+15 deg about the scene pivot), rank r renders views r, r+N, ...:
+weak scaling, no collective on the data path (the only collectives are the
+timing barrier / max-over-ranks).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+NCU_TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+CONFIGS = {
+    # name: (W, H, focal, N gaussians, bg fraction, cluster sigma)
+    "c2": (1920, 1080, 1000.0, 1_000_000, 0.12, 0.035),
+    "c1": (256, 256, 256.0, 10_000, 1.0, 0.035),
+    "c4": (3840, 2160, 2000.0, 3_000_000, 0.12, 0.035),
+}
+N_VIEWS = 64
+PIVOT_Z = 5.5
+
+
+def orbit_view(k: int, n_views: int = N_VIEWS) -> np.ndarray:
+    """World->camera of view k: yaw about the y axis through (0, 0, PIVOT_Z)."""
+    yaw = math.radians(-15.0 + 30.0 * k / max(1, n_views - 1))
+    c, s = math.cos(yaw), math.sin(yaw)
+    R = np.array([[c, 0.0, s], [0.0, 1.0, 0.0], [-s, 0.0, c]])
+    piv = np.array([0.0, 0.0, PIVOT_Z])
+    t = piv - R @ piv
+    V = np.eye(4)
+    V[:3, :3] = R
+    V[:3, 3] = t
+    return V.astype(np.float32)
+
+
+def load_peaks() -> dict:
+    try:
+        with open(PEAKS_PATH) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_sample_estimate(g3d, cam_o, g2d, pl, ranges, W, H, pw, ph, threads: int, budget_s: float, seed: int = 0):
+    """Time the CPU oracle (the reference's algorithm, restated) on bounded
+    samples of one frame and extrapolate to the full frame:
+      project_all on 1/8 of the Gaussians      x8 (linear)
+      bin_tiles on 1/8 of the projected splats  x K log K ratio
+      render_reference (faithful: evaluates the whole tile list per pixel,
+        src/blend.cpp:85-92) on random tiles   x (sum pixels*len) ratio
+    Returns seconds for one full frame + a description."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+
+    rng = np.random.default_rng(seed)
+    n = len(g3d)
+    sub = np.sort(rng.choice(n, size=max(1, n // 8), replace=False))
+    g3s = np.ascontiguousarray(g3d[sub])
+    t0 = time.perf_counter()
+    O.project_all(g3s, cam_o)
+    t_proj = (time.perf_counter() - t0) * (n / len(sub))
+
+    m = len(g2d)
+    sub2 = np.sort(rng.choice(m, size=max(1, m // 8), replace=False))
+    g2s = np.ascontiguousarray(g2d[sub2])
+    t0 = time.perf_counter()
+    pl_s, _ = O.bin_tiles(g2s, W, H, pw, ph)
+    t_bin_s = time.perf_counter() - t0
+    K, Ks = max(len(pl), 2), max(len(pl_s), 2)
+    t_bin = t_bin_s * (K * math.log(K)) / (Ks * math.log(Ks))
+
+    cols, rows = (W + pw - 1) // pw, (H + ph - 1) // ph
+    lens = (ranges[1::2].astype(np.int64) - ranges[0::2].astype(np.int64))
+    tx, ty = np.arange(cols * rows) % cols, np.arange(cols * rows) // cols
+    pix = (np.minimum(W, (tx + 1) * pw) - tx * pw) * (np.minimum(H, (ty + 1) * ph) - ty * ph)
+    work = pix * lens
+    total_work = int(work.sum())
+    # ~8 ns per evaluated pair per thread (measured order of magnitude); fill the budget
+    target = budget_s / 8e-9 * max(1, threads)
+    order = rng.permutation(cols * rows)
+    csum = np.cumsum(work[order])
+    cut = int(np.searchsorted(csum, min(target, total_work))) + 1
+    tiles = np.sort(order[:cut]).astype(np.int32)
+    t0 = time.perf_counter()
+    O.render(0, pl, ranges, g2d, W, H, pw, ph, (0, 0, 0), lazy=False, threads=threads, tiles=tiles)
+    t_r_s = time.perf_counter() - t0
+    sw = max(1, int(work[tiles].sum()))
+    t_render = t_r_s * total_work / sw
+    desc = (f"project_all on {len(sub)}/{n} Gaussians (x{n / len(sub):.1f}); bin_tiles on {len(sub2)}/{m} splats "
+            f"(x K log K); render_reference faithful on {len(tiles)}/{cols * rows} random tiles "
+            f"({sw / total_work * 100:.2f}% of pixel*list work, extrapolated); threads={threads}")
+    return t_proj + t_bin + t_render, {"project_s": t_proj, "bin_s": t_bin, "render_s": t_render}, desc
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args) -> None:
+    """--impl reference: the reference's CPU implementation (oracle port —
+    the reference itself is unbuildable here) on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+
+    W, H, f, n, bgf, sig = CONFIGS[args.config]
+    pw = ph = 16
+    threads = os.cpu_count() or 1
+    cam = O.make_camera(orbit_view(0), (f, f), W, H)
+    g3d = O.gen_clustered_scene(n, cam, sigma=sig, bgfrac=bgf)
+    g2d = O.project_all(g3d, cam)
+    pl, ranges = O.bin_tiles(g2d, W, H, pw, ph)
+    budget = max(1.0, 150.0 / max(1, args.steps + args.warmup))
+    times = []
+    desc = ""
+    for i in range(args.warmup + args.steps):
+        t, parts, desc = cpu_sample_estimate(g3d, cam, g2d, pl, ranges, W, H, pw, ph, threads, budget, seed=i)
+        if i >= args.warmup:
+            times.append(t)
+    t = float(np.mean(times))
+    value = 1.0 / t
+    out = {"impl": "reference", "metric": metric_name(args.config), "value": value, "unit": "views/s",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulators)",
+           "data": "synthetic: gen_clustered_scene seed 42",
+           "config": config_desc(args.config, W, H, n, pw, ph),
+           "cpu_baseline": {"value": value, "unit": "views/s", "cores": threads, "kind": "port",
+                            "sample": desc, "stage_s": parts},
+           "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def metric_name(cfg: str) -> str:
+    return "fwd render views/s (1080p, 1M Gaussians; full forward per view)" if cfg == "c2" else \
+        f"fwd render views/s ({cfg})"
+
+
+def config_desc(cfg, W, H, n, pw, ph) -> dict:
+    return {"workload": f"{cfg.upper()}: {W}x{H}, {n} clustered Gaussians (4 clusters, sigma 0.035, 12% background), "
+                        f"{pw}x{ph} tiles, views from a 64-view +-15 deg yaw orbit",
+            "global_batch": None, "seq_len": None}
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--alpha", default="exact", choices=["exact", "fast"])
+    ap.add_argument("--variant", default="auto")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip per-variant sweep / e2e / cpu baseline")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_17378_b200 import _native as N
+    from paper_2412_17378_b200 import api
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(dev))
+
+    W, H, f, n, bgf, sig = CONFIGS[args.config]
+    pw = ph = 16
+    mode = N.ALPHA_EXACT if args.alpha == "exact" else N.ALPHA_FAST
+    variant = args.variant if args.variant == "auto" else api.variant_from_name(args.variant)
+
+    cam0 = api.camera(orbit_view(0), (f, f), W, H)
+    g3d = api.gen_clustered_scene(n, cam0, cluster_sigma=sig, background_fraction=bgf)
+    g3d_dev = api.g3d_to_device(g3d, dev)  # scene replica, uploaded once (outside timing)
+    cams = [api.camera(orbit_view(k), (f, f), W, H) for k in range(N_VIEWS)]
+    pipe = api.Pipeline(W, H, pw, ph, dev, mode)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step(i):
+        v = (rank + world * i) % N_VIEWS
+        return pipe.forward(g3d_dev, n, cams[v], variant=variant)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    used = {}
+    clk = ClockSampler(local)
+    clk.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = N.lib().bs_kernel_launches()
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (untimed)
+        starts[i].record()
+        _, v = step(args.warmup + i)
+        ends[i].record()
+        used[v] = used.get(v, 0) + 1
+    torch.cuda.synchronize()
+    launches = int(N.lib().bs_kernel_launches() - launches0)
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = world * args.steps / (max_ms / 1e3)
+
+    extras = {}
+    if rank == 0 and not args.no_extras:
+        extras = rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, pipe, W, H, pw, ph, n, mode, dev, world)
+
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    out = {
+        "metric": metric_name(args.config),
+        "value": value,
+        "unit": "views/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": max_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32 alpha/T, f64 colour+depth accumulators (exact mode)" if mode == N.ALPHA_EXACT else "f32",
+        "data": "synthetic: gen_clustered_scene seed 42 (no dataset)",
+        "config": dict(config_desc(args.config, W, H, n, pw, ph), alpha_mode=args.alpha, variant=args.variant,
+                       variants_used={api.variant_name(k): c for k, c in used.items()},
+                       parallelism=f"view-sharded x{world} (scene replicated, no data-path collective)",
+                       l2="flushed between timed steps (256 MiB write, untimed)"),
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    out.update(extras)
+    print(json.dumps(out), flush=True)
+
+
+def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, pipe, W, H, pw, ph, n, mode, dev, world) -> dict:
+    res = {}
+    peaks = load_peaks()
+    cam_id = api.camera(np.eye(4, dtype=np.float32), cams[0].focal, W, H)  # C2 identity view
+    frame, v_auto = pipe.forward(g3d_dev, n, cam_id, variant="auto")
+    s, b, st = pipe.splats, pipe.last_binning, pipe.last_stats
+    summ = st.summary()
+    stream = torch.cuda.current_stream()
+
+    def time_render(variant, m, reps=5):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        api.render_forward(variant, s, b, W, H, pw, ph, (0, 0, 0), m, st.task_order, frame)
+        for a, e in ev:
+            a.record(stream)
+            api.render_forward(variant, s, b, W, H, pw, ph, (0, 0, 0), m, st.task_order, frame)
+            e.record(stream)
+        torch.cuda.synchronize()
+        return float(np.mean([a.elapsed_time(e) for a, e in ev]))
+
+    per_variant = {}
+    for m, mname in ((N.ALPHA_EXACT, "exact"), (N.ALPHA_FAST, "fast")):
+        per_variant[mname] = {api.variant_name(v): round(time_render(v, m), 4) for v in range(5)}
+    mname = "exact" if mode == N.ALPHA_EXACT else "fast"
+    vsel = v_auto if args.variant == "auto" else api.variant_from_name(args.variant)
+    t_render = time_render(vsel, mode, reps=10)
+    api.render_forward(vsel, s, b, W, H, pw, ph, (0, 0, 0), mode, st.task_order, frame)
+    E, Cc = api.frame_work(frame, b, pw, ph)
+    K, P = b.k, W * H
+    ops = 16 * E + 8 * Cc
+    fp32_peak = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    mufu_peak = 148 * 16 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    hbm_peak = float(peaks.get("hbm_gbs", 6548.2)) * 1e9
+    bytes_alg = 44 * K + 32 * P
+    t_s = t_render / 1e3
+    t_roof = max(ops / fp32_peak, E / mufu_peak, bytes_alg / hbm_peak)
+    traffic = None
+    try:
+        with open(NCU_TRAFFIC_PATH) as fh:
+            traffic = json.load(fh).get(f"{api.variant_name(vsel)}_{mname}")
+    except Exception:
+        pass
+    res["fwd_render_ms_per_frame"] = t_render
+    res["blends_per_s"] = E / t_s
+    res["frame_work"] = {"evaluated_pairs_E": E, "committed_pairs_C": Cc, "tile_instances_K": K, "pixels": P,
+                         "tile_stats": summ, "variant": api.variant_name(vsel)}
+    res["render_ms_by_variant"] = per_variant
+    naive = per_variant[mname]["Naive"]
+    res["speedup_vs_naive"] = {k: round(naive / v, 3) for k, v in per_variant[mname].items()}
+    res["roofline"] = {
+        "bound": "fp32-issue", "kernel": f"render {api.variant_name(vsel)} ({mname})",
+        "achieved": ops / t_s / 1e9, "peak": fp32_peak / 1e9, "unit": "Ginstr/s (FP32 pipe, algorithmic 16E+8C)",
+        "frac": (ops / t_s) / fp32_peak, "t_roof_ms": t_roof * 1e3, "t_roof_frac": t_roof / t_s,
+        "traffic": traffic, "algorithmic_bytes": bytes_alg,
+        "hbm_view": {"achieved_gbs": bytes_alg / t_s / 1e9, "peak_gbs": hbm_peak / 1e9,
+                     "frac": bytes_alg / t_s / hbm_peak},
+        "peak_source": "MEASURED_PEAKS.json sm_max_mhz x 148 SMs x 128 lanes (FP32), hbm_gbs (HBM)"}
+
+    # e2e: host buffers through the C-ABI host frame API (H2D scene + D2H frame in the timed region)
+    ctx = C.c_void_p()
+    N.call("bs_context_create", C.byref(ctx), int(mode))
+    host_g3d = torch.from_numpy(np.ascontiguousarray(g3d).view(np.uint8).reshape(-1).copy()).pin_memory()
+    P3 = P * 3
+    outs = [torch.empty(P3, dtype=torch.float32).pin_memory()] + \
+        [torch.empty(P, dtype=torch.float32).pin_memory() for _ in range(3)] + \
+        [torch.empty(P, dtype=torch.int32).pin_memory() for _ in range(2)]
+    bgc = (C.c_float * 3)(0.0, 0.0, 0.0)
+    vv = -1 if args.variant == "auto" else int(vsel)
+
+    def e2e_step(k):
+        N.call("bs_render_frame_host", ctx, host_g3d.data_ptr(), n, C.byref(cams[k % N_VIEWS]), pw, ph, vv, bgc,
+               *[o.data_ptr() for o in outs], None)
+
+    for k in range(3):
+        e2e_step(k)
+    ne = min(args.steps, 10)
+    t0 = time.perf_counter()
+    for k in range(ne):
+        e2e_step(k)
+    e2e_s = (time.perf_counter() - t0) / ne
+    N.call("bs_context_destroy", ctx)
+    res["e2e"] = {"value": 1.0 / e2e_s, "unit": "views/s", "h2d_bytes_per_step": int(n * 56),
+                  "d2h_bytes_per_step": int(P * 32), "ms_per_step": e2e_s * 1e3,
+                  "path": "bs_render_frame_host (C-ABI, pinned host buffers, wall clock incl. sync)"}
+
+    if world == 1 and not args.no_cpu_baseline:
+        g2d = api.splats_to_g2d(s)
+        pl = b.point_list.cpu().numpy().view(np.uint32)
+        ranges = b.tile_ranges.cpu().numpy().view(np.uint32)
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle_lib as O
+        ocam = O.Camera.from_buffer_copy(bytes(cam_id))
+        tcpu, parts, desc = cpu_sample_estimate(g3d.view(O.G3D_DTYPE), ocam, g2d.view(O.G2D_DTYPE), pl, ranges, W, H,
+                                                pw, ph, 1, args.cpu_budget)
+        res["cpu_baseline"] = {"value": 1.0 / tcpu, "unit": "views/s", "cores": 1, "kind": "port", "sample": desc,
+                               "stage_s": parts, "host_cpu": os.cpu_count()}
+    return res
+
+
+if __name__ == "__main__":
+    main()

@@ -215,6 +215,36 @@ int bs_test_expf(const float* x, float* y, int64_t n, int alpha_mode, void* stre
 int bs_host_gen_clustered_scene(int32_t n, int32_t n_clusters, uint64_t seed, double cluster_sigma,
                                 double background_fraction, const bs_camera* cam, bs_gaussian3d* out);
 
+/* ---- host-buffer frame API (the drop-in for project_all -> bin_tiles ->
+ * run_kernel on HOST data) ----
+ * A context owns a CUDA stream and device buffers that grow on demand.
+ * bs_render_frame_host copies the Gaussians host->device, runs the whole
+ * forward on the device, and copies the RenderOutput planes device->host
+ * (each output pointer may be NULL to skip that plane).  variant = -1 picks
+ * the variant per frame with bs_select_variant. */
+typedef struct bs_context bs_context;
+
+typedef struct bs_frame_info {
+  int32_t variant;          /* variant actually rendered */
+  int32_t n_visible;
+  int64_t k;                /* tile instances */
+  bs_tile_histogram stats;  /* tile_load_histogram of the frame */
+  uint64_t evaluated;       /* sum consumed (pairs blended under serial semantics) */
+  uint64_t committed;       /* sum contrib */
+} bs_frame_info;
+
+int bs_context_create(bs_context** out, int alpha_mode);
+int bs_context_destroy(bs_context* ctx);
+/* cudaStream_t of the context (as void*) */
+void* bs_context_stream(bs_context* ctx);
+int bs_render_frame_host(bs_context* ctx, const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, int32_t pw,
+                         int32_t ph, int32_t variant, const float bg[3], float* color, float* alpha, float* depth,
+                         float* final_t, int32_t* contrib, int32_t* term, bs_frame_info* info);
+
+/* Number of kernel launches issued by this library since load (evidence
+ * counter for bench.py's gpu_launches). */
+uint64_t bs_kernel_launches(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -35,6 +35,11 @@ class TileHistogram(C.Structure):
                 ("mean", C.c_double), ("total", C.c_uint64), ("tiles", C.c_int32), ("nonempty", C.c_int32)]
 
 
+class FrameInfo(C.Structure):
+    _fields_ = [("variant", C.c_int32), ("n_visible", C.c_int32), ("k", C.c_int64), ("stats", TileHistogram),
+                ("evaluated", C.c_uint64), ("committed", C.c_uint64)]
+
+
 G3D_DTYPE = np.dtype([("mean", "<f4", 3), ("scale", "<f4", 3), ("rot", "<f4", 4), ("opacity", "<f4"),
                       ("color", "<f4", 3)])
 G2D_DTYPE = np.dtype([("x", "<f4"), ("y", "<f4"), ("conic_a", "<f4"), ("conic_b", "<f4"), ("conic_c", "<f4"),
@@ -68,6 +73,12 @@ SIGNATURES = {
     "bs_frame_work": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "bs_select_variant": (C.c_int, [C.POINTER(TileHistogram), _i32, _i32, _i32, _i32, _i32]),
     "bs_test_expf": (C.c_int, [_vp, _vp, _i64, C.c_int, _vp]),
+    "bs_context_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
+    "bs_context_destroy": (C.c_int, [_vp]),
+    "bs_context_stream": (_vp, [_vp]),
+    "bs_render_frame_host": (C.c_int, [_vp, _vp, _i64, C.POINTER(Camera), _i32, _i32, _i32, _f32p, _vp, _vp, _vp,
+                                       _vp, _vp, _vp, _vp]),
+    "bs_kernel_launches": (_u64, []),
     "bs_host_gen_clustered_scene": (C.c_int, [_i32, _i32, _u64, C.c_double, C.c_double, C.POINTER(Camera), _vp]),
 }
 

@@ -14,6 +14,7 @@
 
 #define BS_LAUNCH_CHECK()                              \
   do {                                                 \
+    bs::count_launches(1);                             \
     if (cudaPeekAtLastError() != cudaSuccess) {        \
       (void)cudaGetLastError();                        \
       return BS_ERR_CUDA;                              \
@@ -21,6 +22,9 @@
   } while (0)
 
 namespace bs {
+
+// Library-wide kernel launch counter (bs_kernel_launches()).
+void count_launches(unsigned long long n);
 
 constexpr float kNearPlane = 0.01f;           // preprocess.hpp:47
 constexpr float kAlphaClamp = 0.99f;          // blend.hpp:13

@@ -6,6 +6,15 @@
 
 #include "bs_common.cuh"
 
+#include <atomic>
+
+namespace bs {
+static std::atomic<unsigned long long> g_launches{0};
+void count_launches(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace bs
+
+extern "C" uint64_t bs_kernel_launches(void) { return bs::g_launches.load(); }
+
 extern "C" int bs_abi_version(void) { return BS_ABI_VERSION; }
 
 extern "C" const char* bs_status_string(int status) {

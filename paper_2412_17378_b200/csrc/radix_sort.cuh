@@ -156,6 +156,7 @@ inline cudaError_t radix_sort_pairs(uint32_t* k0, uint32_t* v0, uint32_t* k1, ui
     cudaError_t e = exclusive_scan<uint32_t, uint32_t>(w.hist, w.hist, 256 * nb, nullptr, w.partials, nullptr, st);
     if (e != cudaSuccess) return e;
     k_radix_scatter<<<(unsigned)nb, kSortThreads, 0, st>>>(ki, vi, ko, vo, n_cap, d_count, shift, nb, w.hist);
+    count_launches(2);
     uint32_t* t;
     t = ki; ki = ko; ko = t;
     t = vi; vi = vo; vo = t;

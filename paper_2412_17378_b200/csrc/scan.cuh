@@ -137,6 +137,7 @@ inline cudaError_t exclusive_scan(const TIn* in, TOut* out, int64_t n_cap, const
   k_scan_reduce<TIn, TOut><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_cap, d_count, partials);
   k_scan_partials<TOut><<<1, 1024, 0, st>>>(partials, nb, total);
   k_scan_downsweep<TIn, TOut><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_cap, d_count, partials, out);
+  count_launches(3);
   return cudaPeekAtLastError();
 }
 

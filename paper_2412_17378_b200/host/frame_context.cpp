@@ -1,0 +1,256 @@
+// frame_context.cpp — host-buffer forward pipeline over the C-ABI.
+//
+// The drop-in for the reference's host call chain
+//   project_all (src/preprocess.cpp:57) -> bin_tiles (:66) ->
+//   tile_load_histogram (:117) -> run_kernel (src/kernels.cpp:268)
+// on HOST data: one H2D copy of the Gaussians, the whole pipeline on the
+// device (one stream, buffers that persist and grow), one D2H copy per
+// requested output plane.  The only mid-frame sync is the 8-byte K readback
+// needed to size point_list (the reference pipeline has the same data
+// dependency).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+
+#include "splatsim_b200.h"
+
+struct bs_context {
+  int alpha_mode = BS_ALPHA_EXACT;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  // device buffers
+  void* g3d = nullptr;
+  size_t g3d_bytes = 0;
+  float4* splat[3] = {nullptr, nullptr, nullptr};
+  int64_t splat_cap = 0;
+  int32_t* n_visible = nullptr;
+  int64_t* k_dev = nullptr;
+  int64_t* k_host = nullptr;  // pinned
+  void* pre_ws = nullptr;
+  size_t pre_ws_bytes = 0;
+  void* bin_ws = nullptr;
+  size_t bin_ws_bytes = 0;
+  int64_t bin_n = -1, bin_k = -1;
+  int bin_key[4] = {0, 0, 0, 0};
+  uint32_t* point_list = nullptr;
+  int64_t pl_cap = 0;
+  uint32_t* ranges = nullptr;
+  int64_t ranges_cap = 0;
+  void* stats_ws = nullptr;
+  size_t stats_ws_bytes = 0;
+  uint32_t* order = nullptr;
+  int64_t order_cap = 0;
+  bs_tile_histogram* stats_dev = nullptr;
+  bs_tile_histogram* stats_host = nullptr;  // pinned
+  void* render_ws = nullptr;
+  float* planes[4] = {nullptr, nullptr, nullptr, nullptr};
+  int32_t* iplanes[2] = {nullptr, nullptr};
+  int64_t pixel_cap = 0;
+  uint64_t* work_dev = nullptr;
+  uint64_t* work_host = nullptr;  // pinned
+};
+
+namespace {
+
+int grow(void** p, size_t* cap, size_t need) {
+  if (*p && *cap >= need) return BS_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  need = std::max<size_t>(need, 256);
+  if (cudaMalloc(p, need) != cudaSuccess) {
+    (void)cudaGetLastError();
+    *cap = 0;
+    return BS_ERR_CUDA;
+  }
+  *cap = need;
+  return BS_OK;
+}
+
+template <typename T>
+int grow_n(T** p, int64_t* cap, int64_t need, double slack = 1.0) {
+  if (*p && *cap >= need) return BS_OK;
+  const int64_t n = std::max<int64_t>(int64_t(double(need) * slack), 1);
+  size_t bytes = 0;
+  void* v = *p;
+  size_t c = 0;
+  int s = grow(&v, &c, size_t(n) * sizeof(T));
+  (void)bytes;
+  *p = static_cast<T*>(v);
+  *cap = s == BS_OK ? n : 0;
+  return s;
+}
+
+#define TRY(x)                 \
+  do {                         \
+    int _s = (x);              \
+    if (_s != BS_OK) return _s; \
+  } while (0)
+#define CUTRY(x)                                        \
+  do {                                                  \
+    if ((x) != cudaSuccess) {                           \
+      (void)cudaGetLastError();                         \
+      return BS_ERR_CUDA;                               \
+    }                                                   \
+  } while (0)
+
+}  // namespace
+
+extern "C" int bs_context_create(bs_context** out, int alpha_mode) {
+  if (!out || (alpha_mode != BS_ALPHA_EXACT && alpha_mode != BS_ALPHA_FAST)) return BS_ERR_INVALID_ARGUMENT;
+  int32_t sms = 0;
+  int s = bs_device_sm_count(&sms);
+  if (s != BS_OK) return s;
+  bs_context* c = new (std::nothrow) bs_context();
+  if (!c) return BS_ERR_INVALID_ARGUMENT;
+  c->alpha_mode = alpha_mode;
+  c->sm_count = sms;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(reinterpret_cast<void**>(&c->n_visible), 256) != cudaSuccess ||
+      cudaMalloc(reinterpret_cast<void**>(&c->k_dev), 256) != cudaSuccess ||
+      cudaMalloc(reinterpret_cast<void**>(&c->stats_dev), sizeof(bs_tile_histogram) + 256) != cudaSuccess ||
+      cudaMalloc(reinterpret_cast<void**>(&c->work_dev), 256) != cudaSuccess ||
+      cudaMalloc(&c->render_ws, bs_render_workspace_bytes()) != cudaSuccess ||
+      cudaMallocHost(reinterpret_cast<void**>(&c->k_host), 256) != cudaSuccess ||
+      cudaMallocHost(reinterpret_cast<void**>(&c->stats_host), sizeof(bs_tile_histogram) + 256) != cudaSuccess ||
+      cudaMallocHost(reinterpret_cast<void**>(&c->work_host), 256) != cudaSuccess) {
+    (void)cudaGetLastError();
+    bs_context_destroy(c);
+    return BS_ERR_CUDA;
+  }
+  *out = c;
+  return BS_OK;
+}
+
+extern "C" int bs_context_destroy(bs_context* c) {
+  if (!c) return BS_OK;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  void* dev[] = {c->g3d, c->splat[0], c->splat[1], c->splat[2], c->n_visible, c->k_dev, c->pre_ws, c->bin_ws,
+                 c->point_list, c->ranges, c->stats_ws, c->order, c->stats_dev, c->render_ws, c->planes[0],
+                 c->planes[1], c->planes[2], c->planes[3], c->iplanes[0], c->iplanes[1], c->work_dev};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (c->k_host) cudaFreeHost(c->k_host);
+  if (c->stats_host) cudaFreeHost(c->stats_host);
+  if (c->work_host) cudaFreeHost(c->work_host);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return BS_OK;
+}
+
+extern "C" void* bs_context_stream(bs_context* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+extern "C" int bs_render_frame_host(bs_context* c, const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam,
+                                    int32_t pw, int32_t ph, int32_t variant, const float bg[3], float* color,
+                                    float* alpha, float* depth, float* final_t, int32_t* contrib, int32_t* term,
+                                    bs_frame_info* info) {
+  if (!c || !cam || !bg || n < 0 || (n > 0 && !g3d) || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
+  if (variant < -1 || variant > 4) return BS_ERR_INVALID_ARGUMENT;
+  const int32_t W = cam->width, H = cam->height;
+  if (W <= 0 || H <= 0) return BS_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = c->stream;
+  const int64_t cols = (W + pw - 1) / pw, rows = (H + ph - 1) / ph, T = cols * rows;
+  const int64_t P = int64_t(W) * H;
+
+  // P1-P4
+  TRY(grow(&c->g3d, &c->g3d_bytes, size_t(std::max<int64_t>(n, 1)) * sizeof(bs_gaussian3d)));
+  if (n > c->splat_cap) {
+    for (auto& p : c->splat) {
+      if (p) cudaFree(p);
+      p = nullptr;
+    }
+    for (auto& p : c->splat) CUTRY(cudaMalloc(reinterpret_cast<void**>(&p), size_t(n) * sizeof(float4)));
+    c->splat_cap = n;
+  }
+  if (n > 0) CUTRY(cudaMemcpyAsync(c->g3d, g3d, size_t(n) * sizeof(bs_gaussian3d), cudaMemcpyHostToDevice, st));
+  bs_splats sp{reinterpret_cast<float*>(c->splat[0]), reinterpret_cast<float*>(c->splat[1]),
+               reinterpret_cast<float*>(c->splat[2])};
+  TRY(grow(&c->pre_ws, &c->pre_ws_bytes, bs_preprocess_workspace_bytes(n)));
+  TRY(bs_preprocess(static_cast<const bs_gaussian3d*>(c->g3d), n, cam, sp, c->n_visible, c->pre_ws, c->pre_ws_bytes, st));
+
+  // P5 count (workspace keyed on n and the tile grid; k part grown below)
+  const int key[4] = {W, H, pw, ph};
+  const bool same_grid = std::equal(key, key + 4, c->bin_key);
+  if (!same_grid || n > c->bin_n || !c->bin_ws) {
+    c->bin_n = std::max<int64_t>(n, c->bin_n);
+    c->bin_k = std::max<int64_t>(c->bin_k, 0);
+    std::copy(key, key + 4, c->bin_key);
+    TRY(grow(&c->bin_ws, &c->bin_ws_bytes, bs_bin_workspace_bytes(c->bin_n, W, H, pw, ph, c->bin_k)));
+  }
+  TRY(bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, st));
+  CUTRY(cudaMemcpyAsync(c->k_host, c->k_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CUTRY(cudaStreamSynchronize(st));
+  const int64_t k = *c->k_host;
+  if (k > c->bin_k) {
+    // the count state lives in the workspace: grow, then count again
+    c->bin_k = int64_t(double(k) * 1.25) + 1024;
+    void* fresh = nullptr;
+    size_t fresh_bytes = 0;
+    TRY(grow(&fresh, &fresh_bytes, bs_bin_workspace_bytes(c->bin_n, W, H, pw, ph, c->bin_k)));
+    if (c->bin_ws) cudaFree(c->bin_ws);
+    c->bin_ws = fresh;
+    c->bin_ws_bytes = fresh_bytes;
+    TRY(bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, st));
+  }
+  TRY(grow_n(&c->point_list, &c->pl_cap, std::max<int64_t>(k, 1), 1.25));
+  TRY(grow_n(&c->ranges, &c->ranges_cap, 2 * T));
+  TRY(bs_bin_sort(sp, n, c->n_visible, W, H, pw, ph, k, c->point_list, c->ranges, c->bin_ws, c->bin_ws_bytes, st));
+
+  // P6
+  TRY(grow(&c->stats_ws, &c->stats_ws_bytes, bs_tile_stats_workspace_bytes(int32_t(T))));
+  TRY(grow_n(&c->order, &c->order_cap, T));
+  TRY(bs_tile_stats(c->ranges, int32_t(T), c->stats_dev, nullptr, c->order, c->stats_ws, c->stats_ws_bytes, st));
+  int v = variant;
+  if (v < 0) {
+    CUTRY(cudaMemcpyAsync(c->stats_host, c->stats_dev, sizeof(bs_tile_histogram), cudaMemcpyDeviceToHost, st));
+    CUTRY(cudaStreamSynchronize(st));
+    v = bs_select_variant(c->stats_host, W, H, pw, ph, c->sm_count);
+    if (v < 0) return v;
+  }
+
+  // R: render into device planes
+  if (P > c->pixel_cap) {
+    for (auto& p : c->planes) {
+      if (p) cudaFree(p);
+      p = nullptr;
+    }
+    for (auto& p : c->iplanes) {
+      if (p) cudaFree(p);
+      p = nullptr;
+    }
+    CUTRY(cudaMalloc(reinterpret_cast<void**>(&c->planes[0]), size_t(P) * 3 * sizeof(float)));
+    for (int i = 1; i < 4; ++i) CUTRY(cudaMalloc(reinterpret_cast<void**>(&c->planes[i]), size_t(P) * sizeof(float)));
+    for (auto& p : c->iplanes) CUTRY(cudaMalloc(reinterpret_cast<void**>(&p), size_t(P) * sizeof(int32_t)));
+    c->pixel_cap = P;
+  }
+  bs_frame_out fo{c->planes[0], c->planes[1], c->planes[2], c->planes[3], c->iplanes[0], c->iplanes[1]};
+  TRY(bs_render_forward(v, c->alpha_mode, sp, c->point_list, c->ranges, c->order, W, H, pw, ph, bg, fo, c->render_ws,
+                        bs_render_workspace_bytes(), st));
+  if (info) TRY(bs_frame_work(c->iplanes[1], c->iplanes[0], c->ranges, W, H, pw, ph, c->work_dev, st));
+
+  // D2H
+  const size_t pb = size_t(P) * sizeof(float);
+  if (color) CUTRY(cudaMemcpyAsync(color, c->planes[0], pb * 3, cudaMemcpyDeviceToHost, st));
+  if (alpha) CUTRY(cudaMemcpyAsync(alpha, c->planes[1], pb, cudaMemcpyDeviceToHost, st));
+  if (depth) CUTRY(cudaMemcpyAsync(depth, c->planes[2], pb, cudaMemcpyDeviceToHost, st));
+  if (final_t) CUTRY(cudaMemcpyAsync(final_t, c->planes[3], pb, cudaMemcpyDeviceToHost, st));
+  if (contrib) CUTRY(cudaMemcpyAsync(contrib, c->iplanes[0], pb, cudaMemcpyDeviceToHost, st));
+  if (term) CUTRY(cudaMemcpyAsync(term, c->iplanes[1], pb, cudaMemcpyDeviceToHost, st));
+  if (info) {
+    CUTRY(cudaMemcpyAsync(c->stats_host, c->stats_dev, sizeof(bs_tile_histogram), cudaMemcpyDeviceToHost, st));
+    CUTRY(cudaMemcpyAsync(c->work_host, c->work_dev, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  }
+  CUTRY(cudaStreamSynchronize(st));
+  if (info) {
+    int32_t nv = 0;
+    CUTRY(cudaMemcpy(&nv, c->n_visible, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    info->variant = v;
+    info->n_visible = nv;
+    info->k = k;
+    info->stats = *c->stats_host;
+    info->evaluated = c->work_host[0];
+    info->committed = c->work_host[1];
+  }
+  return BS_OK;
+}
