@@ -94,6 +94,12 @@ struct Accum<BS_ALPHA_EXACT> {
     b = __dadd_rn(b, __dmul_rn((double)col.z, w));
     d = __dadd_rn(d, __dmul_rn((double)dep, w));
   }
+  __device__ __forceinline__ void merge(const Accum& o) {
+    r = __dadd_rn(r, o.r);
+    g = __dadd_rn(g, o.g);
+    b = __dadd_rn(b, o.b);
+    d = __dadd_rn(d, o.d);
+  }
   __device__ __forceinline__ void warp_sum() {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -124,6 +130,12 @@ struct Accum<BS_ALPHA_FAST> {
     g = fmaf(col.y, w, g);
     b = fmaf(col.z, w, b);
     d = fmaf(dep, w, d);
+  }
+  __device__ __forceinline__ void merge(const Accum& o) {
+    r += o.r;
+    g += o.g;
+    b += o.b;
+    d += o.d;
   }
   __device__ __forceinline__ void warp_sum() {
 #pragma unroll
@@ -244,6 +256,70 @@ __global__ void __launch_bounds__(BLOCK) k_render_dynamic(RArgs A) {
 }
 
 // ---------------------------------------------------------------------------
+// One 32-wide Gaussian-wise group of one pixel (paper Alg. 6 / R6): lane l
+// holds list entry g0+l.  t (warp-uniform) and contrib are updated; each lane
+// accumulates its own committed entry into acc.  Returns the stop lane (32 =
+// no stop).  All-skipped groups return at once (Alg. 6's __all_sync skip).
+//   EXACT: skip/stop decisions and the carried t follow the serial float
+//     recurrence (src/kernels.cpp:79-89).  Colour weights: SERIAL_W ? the
+//     serial t before each entry (render_reference weights) : the doubling
+//     prefix product (render_gaussianwise weights, inc/blend.hpp:69-83).
+//   FAST: decisions and weights from the prefix product (paper Alg. 6), the
+//     terminating entry committing nothing (SPEC blend-core decision).
+template <int MODE, bool SERIAL_W>
+__device__ __forceinline__ int gw_group(bool ns, float alpha, float4 col, float dep, float& t, int& contrib,
+                                        Accum<MODE>& acc, int lane) {
+  const unsigned nsmask = __ballot_sync(kFull, ns);
+  if (nsmask == 0) return 32;
+  const float f = ns ? __fsub_rn(1.0f, alpha) : 1.0f;
+  int stop = 32;
+  float t_next, tb = t;
+  bool need_prefix = !(MODE == BS_ALPHA_EXACT && SERIAL_W);
+  if (MODE == BS_ALPHA_EXACT) {
+    float ts = t;
+    unsigned m = nsmask;
+    while (m) {
+      const int jl = __ffs(m) - 1;
+      const float fj = __shfl_sync(kFull, f, jl);
+      if (lane == jl) tb = ts;
+      const float tmp = __fmul_rn(ts, fj);
+      if (tmp < kStopThreshold) {
+        stop = jl;
+        break;
+      }
+      ts = tmp;
+      m &= m - 1;
+    }
+    t_next = ts;
+  }
+  if (need_prefix) {
+    float pre = f;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const float v = __shfl_up_sync(kFull, pre, off);
+      if (lane >= off) pre = __fmul_rn(pre, v);
+    }
+    const float per_lane = __fmul_rn(t, pre);
+    float t_before = __shfl_up_sync(kFull, per_lane, 1);
+    if (lane == 0) t_before = t;
+    tb = t_before;
+    if (MODE != BS_ALPHA_EXACT) {
+      const unsigned sm = __ballot_sync(kFull, ns && per_lane < kStopThreshold);
+      if (sm) {
+        stop = __ffs(sm) - 1;
+        t_next = __shfl_sync(kFull, t_before, stop);
+      } else {
+        t_next = __shfl_sync(kFull, per_lane, 31);
+      }
+    }
+  }
+  if (ns && lane < stop) acc.add(alpha, tb, col, dep);
+  contrib += __popc(nsmask & ((stop >= 32) ? kFull : ((1u << stop) - 1u)));
+  t = t_next;
+  return stop;
+}
+
+// ---------------------------------------------------------------------------
 // Gaussian-wise: kFgWarps warps, warp w blends pixel `pix[w]` of `tile`; the
 // CTA stages the list in 128-entry chunks shared by the 4 warps; each warp
 // walks a chunk in 32-wide groups.
@@ -286,52 +362,8 @@ __device__ __forceinline__ void gaussianwise_task(const RArgs& A, int tile, int 
         c = s_cop[j];
         ns = eval_step<MODE>(s_xyab[j], c, sx, sy, s_tab, alpha);
       }
-      const float f = ns ? __fsub_rn(1.0f, alpha) : 1.0f;
-      // R5 warp_prefix_product: inclusive doubling prefix (offsets 1..16)
-      float pre = f;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const float v = __shfl_up_sync(kFull, pre, off);
-        if (lane >= off) pre = __fmul_rn(pre, v);
-      }
-      const float per_lane = __fmul_rn(t, pre);
-      float t_before = __shfl_up_sync(kFull, per_lane, 1);
-      if (lane == 0) t_before = t;
-
-      const unsigned nsmask = __ballot_sync(kFull, ns);
-      int stop = 32;
-      float t_next;
-      if (MODE == BS_ALPHA_EXACT) {
-        // serial float recurrence over the non-skipped lanes (src/kernels.cpp:79-89)
-        float ts = t;
-        unsigned m = nsmask;
-        while (m) {
-          const int jl = __ffs(m) - 1;
-          const float fj = __shfl_sync(kFull, f, jl);
-          const float tmp = __fmul_rn(ts, fj);
-          if (tmp < kStopThreshold) {
-            stop = jl;
-            break;
-          }
-          ts = tmp;
-          m &= m - 1;
-        }
-        t_next = ts;
-      } else {
-        // paper Alg. 6: stop on the prefix product (commit nothing for the
-        // terminating Gaussian, SPEC blend-core decision)
-        const unsigned sm = __ballot_sync(kFull, ns && per_lane < kStopThreshold);
-        if (sm) {
-          stop = __ffs(sm) - 1;
-          t_next = __shfl_sync(kFull, t_before, stop);
-        } else {
-          t_next = __shfl_sync(kFull, per_lane, 31);
-        }
-      }
-      const bool com = ns && lane < stop;
-      if (com) acc.add(alpha, t_before, s_rgb[j], c.w);
-      contrib += __popc(nsmask & ((stop >= 32) ? kFull : ((1u << stop) - 1u)));
-      t = t_next;
+      const float4 col = ns ? s_rgb[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const int stop = gw_group<MODE, false>(ns, alpha, col, c.w, t, contrib, acc, lane);
       if (stop < 32) {
         term = (int)(base - start + g0) + stop + 1;
         done = true;
@@ -360,23 +392,162 @@ __global__ void __launch_bounds__(kFgThreads) k_render_gaussianwise(RArgs A) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// FineGrainedCombined, B200 form (paper Alg. 3 re-cut for 148 SMs):
+//   * persistent CTAs of kFineWarps warps; every WARP claims tasks on its own
+//     from the global atomicAdd queue (no CTA barriers in the loop);
+//   * a task is a 32-pixel sub-tile (lane = pixel) of a tile; tasks are queued
+//     tile by tile in LPT order (longest list first, bs_tile_stats);
+//   * while most of the 32 pixels are live the warp blends pixel-wise over
+//     32-entry batches of the list (staged in per-warp smem, next batch
+//     prefetched into registers); once at most kStragglers pixels remain the
+//     survivors are finished one at a time Gaussian-wise (32 lanes on 32
+//     consecutive entries, gw_group) — the divergence tail that pixel-wise
+//     SIMT would otherwise pay for with 31 idle lanes.
+// EXACT output == render_reference on contrib/term/T/alpha bit for bit, colour
+// and depth to double-sum association (serial weights in the straggler path).
+constexpr int kFineWarps = 8;
+constexpr int kFineThreads = kFineWarps * 32;
+constexpr int kStragglers = 8;
+constexpr int kStragglerMinRemain = 64;
+
+__device__ __forceinline__ void load_rec(const RArgs& A, uint32_t k, float4& a, float4& c, float4& r) {
+  const uint32_t id = __ldg(A.point_list + k);
+  a = __ldg(A.xyab + id);
+  c = __ldg(A.cop + id);
+  r = __ldg(A.rgbr + id);
+}
+
+// Conservative sub-tile cull: true only if alpha < 1/255 at every pixel centre
+// of [rx0,rx1]x[ry0,ry1].  alpha >= 1/255 needs power >= cut, i.e.
+// d^T Q d <= -2 cut (Q = conic); that ellipse lies inside centre +-
+// (sqrt(r2 c/D), sqrt(r2 a/D)), D = ac - b^2.  r2 carries a 1% margin, far above
+// the float rounding of power/extents, so no entry that could pass the skip
+// test is ever dropped (NaN / non-PD conics are never culled).
+__device__ __forceinline__ bool cull_subtile(const float4 a, const float4 c, float rx0, float rx1, float ry0,
+                                             float ry1) {
+  const float cut = c.z;
+  if (cut > 0.0f) return true;  // opacity so small that alpha < 1/255 everywhere
+  const float D = a.z * c.x - a.w * a.w;
+  if (!(D > 0.0f)) return false;
+  const float r2 = -2.02f * cut;
+  const float ex = sqrtf(r2 * c.x / D), ey = sqrtf(r2 * a.z / D);
+  return (a.x + ex < rx0) || (a.x - ex > rx1) || (a.y + ey < ry0) || (a.y - ey > ry1);
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(kFgThreads) k_render_fine(RArgs A, int subs, int total_tasks) {
-  __shared__ float4 s_xyab[kFgThreads];
-  __shared__ float4 s_cop[kFgThreads];
-  __shared__ float4 s_rgb[kFgThreads];
+__device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, float4 (*s)[32], int* s_k,
+                                          const unsigned long long* s_tab) {
+  const int lane = threadIdx.x & 31;
+  const int tx = tile % A.cols, ty = tile / A.cols;
+  // 8x4-pixel sub-tiles tile the pw x ph patch row-major
+  const int nsx = (A.pw + 7) >> 3;
+  const int ox = tx * A.pw + (sub % nsx) * 8, oy = ty * A.ph + (sub / nsx) * 4;
+  const int lx = (sub % nsx) * 8 + (lane & 7), ly = (sub / nsx) * 4 + (lane >> 3);
+  const int px = ox + (lane & 7), py = oy + (lane >> 3);
+  const bool inside = lx < A.pw && ly < A.ph && px < A.W && py < A.H;
+  const float sx = __fadd_rn((float)px, 0.5f), sy = __fadd_rn((float)py, 0.5f);
+  const float rx0 = (float)ox + 0.5f, rx1 = (float)ox + 7.5f, ry0 = (float)oy + 0.5f, ry1 = (float)oy + 3.5f;
+  const uint32_t start = A.ranges[2 * tile], end = A.ranges[2 * tile + 1];
+
+  bool done = !inside;
+  float t = 1.0f;
+  int contrib = 0, term = 0;
+  Accum<MODE> acc;
+
+  uint32_t base = start;
+  float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pc = pa, pr = pa;
+  if (base + lane < end) load_rec(A, base + lane, pa, pc, pr);
+  while (base < end) {
+    const unsigned live = __ballot_sync(kFull, !done);
+    if (!live) break;
+    if (__popc(live) <= kStragglers && end - base >= (uint32_t)kStragglerMinRemain) {
+      // ---- straggler mode: finish each live pixel Gaussian-wise from `base`
+      unsigned rem = live;
+      while (rem) {
+        const int p = __ffs(rem) - 1;
+        rem &= rem - 1;
+        const float psx = __shfl_sync(kFull, sx, p), psy = __shfl_sync(kFull, sy, p);
+        float pt = __shfl_sync(kFull, t, p);
+        int pcnt = 0, ptrm = 0;
+        Accum<MODE> part;
+        float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nc = na, nr = na;
+        if (base + lane < end) load_rec(A, base + lane, na, nc, nr);
+        for (uint32_t g = base; g < end; g += 32) {
+          const bool active = g + lane < end;
+          const float4 a = na, c = nc, r = nr;
+          if (g + 32 + lane < end) load_rec(A, g + 32 + lane, na, nc, nr);  // prefetch next group
+          float alpha = 0.0f;
+          const bool ns = active && eval_step<MODE>(a, c, psx, psy, s_tab, alpha);
+          const int stop = gw_group<MODE, true>(ns, alpha, r, c.w, pt, pcnt, part, lane);
+          if (stop < 32) {
+            ptrm = (int)(g - start) + stop + 1;
+            break;
+          }
+        }
+        part.warp_sum();
+        if (lane == p) {
+          acc.merge(part);
+          t = pt;
+          contrib += pcnt;
+          term = ptrm;
+          done = true;
+        }
+      }
+      break;
+    }
+    // ---- pixel-wise batch of 32 entries: cull against the sub-tile, compact
+    const bool keep = base + lane < end && !cull_subtile(pa, pc, rx0, rx1, ry0, ry1);
+    const unsigned km = __ballot_sync(kFull, keep);
+    if (keep) {
+      const int pos = __popc(km & lanemask_lt());
+      s[0][pos] = pa;
+      s[1][pos] = pc;
+      s[2][pos] = pr;
+      s_k[pos] = (int)(base - start) + lane + 1;  // 1-based list position (term)
+    }
+    __syncwarp();
+    const uint32_t nb = base + 32;
+    if (nb + lane < end) load_rec(A, nb + lane, pa, pc, pr);
+    const int cnt = __popc(km);
+#pragma unroll 2
+    for (int j = 0; j < cnt; ++j) {
+      if (done) continue;
+      float alpha;
+      const float4 c = s[1][j];
+      if (!eval_step<MODE>(s[0][j], c, sx, sy, s_tab, alpha)) continue;
+      const float tmp = __fmul_rn(t, __fsub_rn(1.0f, alpha));
+      if (tmp < kStopThreshold) {
+        done = true;
+        term = s_k[j];
+        continue;
+      }
+      acc.add(alpha, t, s[2][j], c.w);
+      t = tmp;
+      ++contrib;
+    }
+    __syncwarp();
+    base = nb;
+  }
+  if (inside) acc.finish(A, (size_t)py * A.W + px, t, contrib, term);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kFineThreads) k_render_fine(RArgs A, int subs, int total_tasks) {
+  __shared__ float4 s_rec[kFineWarps][3][32];
+  __shared__ int s_k[kFineWarps][32];
   __shared__ unsigned long long s_tab[32];
-  __shared__ int s_task;
   load_tab(s_tab);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_task = (int)atomicAdd(A.queue, 1u);
-    __syncthreads();
-    const int task = s_task;
+    int task = 0;
+    if (lane == 0) task = (int)atomicAdd(A.queue, 1u);
+    task = __shfl_sync(kFull, task, 0);
     if (task >= total_tasks) return;
     const int q = task / subs;
     const int tile = A.task_order ? (int)A.task_order[q] : q;
-    gaussianwise_task<MODE>(A, tile, task - q * subs, s_xyab, s_cop, s_rgb, s_tab);
+    warp_task<MODE>(A, tile, task - q * subs, s_rec[warp], s_k[warp], s_tab);
   }
 }
 
@@ -444,12 +615,13 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
       int dev = 0, sms = 0, per_sm = 0;
       BS_CUDA_TRY(cudaGetDevice(&dev));
       BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_fine<MODE>, kFgThreads, 0));
-      const int subs = (A.pw * A.ph + kFgWarps - 1) / kFgWarps;
+      BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_fine<MODE>, kFineThreads, 0));
+      const int subs = ((A.pw + 7) / 8) * ((A.ph + 3) / 4);  // 8x4 sub-tiles per tile
       const int64_t total = (int64_t)T * subs;
       if (total > 0x7fffffff) return BS_ERR_UNSUPPORTED;
-      const int grid = (int)max((int64_t)1, min(total, (int64_t)sms * max(1, per_sm)));
-      k_render_fine<MODE><<<grid, kFgThreads, 0, st>>>(A, subs, (int)total);
+      const int64_t ctas = (total + kFineWarps - 1) / kFineWarps;
+      const int grid = (int)max((int64_t)1, min(ctas, (int64_t)sms * max(1, per_sm)));
+      k_render_fine<MODE><<<grid, kFineThreads, 0, st>>>(A, subs, (int)total);
       break;
     }
     default:

@@ -151,7 +151,8 @@ def _oracle_render(variant, g2d, W, H, pw, ph, bg):
     return O.render(variant, pl, rg, g2d, W, H, pw, ph, bg, lazy=True, threads=0)
 
 
-CASES = [(256, 256, 16, 16, 10000, 1.0), (192, 128, 16, 8, 6000, 0.12), (250, 130, 16, 16, 5000, 0.3)]
+CASES = [(256, 256, 16, 16, 10000, 1.0), (192, 128, 16, 8, 6000, 0.12), (250, 130, 16, 16, 5000, 0.3),
+         (100, 60, 32, 32, 3000, 0.3), (90, 70, 8, 8, 2000, 0.3)]
 
 
 @pytest.mark.parametrize("W,H,pw,ph,n,bgfrac", CASES)
@@ -172,6 +173,14 @@ def test_render_exact(variant, W, H, pw, ph, n, bgfrac):
     else:
         assert np.max(np.abs(got["color"] - ref["color"])) <= 1e-6
         assert np.max(np.abs(got["depth"] - ref["depth"]) / np.maximum(1, np.abs(ref["depth"]))) <= 1e-6
+    if variant == 3:
+        # the B200 FineGrainedCombined blends with serial weights: it equals
+        # render_reference (not only render_gaussianwise) to double-sum order
+        ref0 = _oracle_render(0, g2d, W, H, pw, ph, bg)
+        assert np.array_equal(got["contrib"], ref0["contrib"]) and np.array_equal(got["term"], ref0["term"])
+        assert np.max(np.abs(got["color"] - ref0["color"])) <= 1e-6
+        same = np.mean(got["color"].view(np.uint32) == ref0["color"].view(np.uint32))
+        assert same > 0.99, same
 
 
 @pytest.mark.parametrize("variant", range(5))

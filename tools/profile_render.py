@@ -1,0 +1,43 @@
+"""Render one C2 frame with a chosen variant/mode (for ncu captures).
+
+  python tools/profile_render.py --variant Naive --alpha exact [--opacity-scale 0.1 --sigma 0.015] [--reps 2]
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2412_17378_b200 import api  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--variant", default="Naive")
+    ap.add_argument("--alpha", default="exact")
+    ap.add_argument("--opacity-scale", type=float, default=1.0)
+    ap.add_argument("--sigma", type=float, default=0.035)
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--W", type=int, default=1920)
+    ap.add_argument("--H", type=int, default=1080)
+    ap.add_argument("--f", type=float, default=1000.0)
+    ap.add_argument("--reps", type=int, default=2)
+    a = ap.parse_args()
+    cam = api.camera(None, (a.f, a.f), a.W, a.H)
+    g3d = api.gen_clustered_scene(a.n, cam, cluster_sigma=a.sigma)
+    g3d["opacity"] *= a.opacity_scale
+    mode = 0 if a.alpha == "exact" else 1
+    pipe = api.Pipeline(a.W, a.H, 16, 16, "cuda", mode)
+    d = api.g3d_to_device(g3d)
+    v = api.variant_from_name(a.variant)
+    for _ in range(a.reps):
+        pipe.forward(d, a.n, cam, variant=v)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()
