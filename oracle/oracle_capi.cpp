@@ -1,9 +1,11 @@
 // oracle/oracle_capi.cpp — extern "C" surface of the CPU oracle for ctypes.
 // TEST INFRASTRUCTURE ONLY: loaded by tests/, __graft_entry__.smoke() and the
 // cpu_baseline / --impl reference legs of bench.py.  Never by the product.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <thread>
+#include <vector>
 
 #include "oracle.hpp"
 
@@ -238,12 +240,35 @@ int64_t orc_expf_exhaustive_check(float lo, float hi, float* bad_x, int max_bad)
   // patterns grow as the value decreases.
   if (!(lo <= hi && hi <= 0.0f && lo < 0.0f)) return -1;
   const uint32_t ustart = (hi == 0.0f) ? 0x80000000u : uhi;
-  for (uint32_t u = ustart;; ++u) {
-    float x;
-    std::memcpy(&x, &u, 4);
-    check(x);
-    if (u == ulo) break;
+  // split the bit-pattern range over the host threads; collect per thread
+  const unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+  const uint64_t span = uint64_t(ulo) - ustart + 1;
+  std::vector<std::vector<float>> hits(nt);
+  std::vector<int64_t> counts(nt, 0);
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < nt; ++t) {
+    pool.emplace_back([&, t]() {
+      const uint64_t b = ustart + span * t / nt, e = ustart + span * (t + 1) / nt;
+      for (uint64_t u = b; u < e; ++u) {
+        float x;
+        const uint32_t u32 = uint32_t(u);
+        std::memcpy(&x, &u32, 4);
+        const float a = std::exp(x), r = restated_expf(x);
+        if (std::memcmp(&a, &r, 4) != 0) {
+          if (hits[t].size() < size_t(max_bad)) hits[t].push_back(x);
+          ++counts[t];
+        }
+      }
+    });
   }
+  for (auto& th : pool) th.join();
+  for (unsigned t = 0; t < nt; ++t) {
+    for (float x : hits[t])
+      if (bad < max_bad) bad_x[bad++] = x;
+  }
+  bad = 0;
+  for (int64_t c : counts) bad += c;
+  (void)check;
   return bad;
 }
 

@@ -237,8 +237,29 @@ def test_pipeline_end_to_end_matches_oracle():
     assert np.max(np.abs(got["color"] - ref["color"])) <= 1e-6
 
 
-def test_generator_matches_oracle():
-    cam = O.make_camera(focal=(1000, 1000), width=1920, height=1080)
-    ref = O.gen_clustered_scene(5000, cam)
-    got = api.gen_clustered_scene(5000, ncam(cam))
-    assert got.tobytes() == ref.tobytes()
+def test_golden_digests_on_gpu():
+    """The whole GPU pipeline reproduces the frozen oracle fixture digests."""
+    import json
+    import os
+
+    from golden.gen_golden import FIXTURES
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "digests.json")) as fh:
+        frozen = json.load(fh)
+    for name, (n, W, H, f, bgf, pw, ph, bg) in FIXTURES.items():
+        cam = O.make_camera(focal=(f, f), width=W, height=H)
+        g3d = O.gen_clustered_scene(n, cam, bgfrac=bgf)
+        fz = frozen[name]
+        s = api.project_all(api.g3d_to_device(g3d), n, ncam(cam))
+        assert O.fnv1a64(api.splats_to_g2d(s)) == fz["g2d"], name
+        b = api.bin_tiles(s, W, H, pw, ph)
+        assert O.fnv1a64(b.point_list.cpu().numpy().view(np.uint32)) == fz["point_list"], name
+        assert O.fnv1a64(b.tile_ranges.cpu().numpy().view(np.uint32)) == fz["tile_ranges"], name
+        st = api.tile_load_histogram(b)
+        for v in (0, 1, 4):  # pixel-wise variants: every plane bit-exact
+            f_ = api.render_forward(v, s, b, W, H, pw, ph, bg, N.ALPHA_EXACT, st.task_order).to_numpy()
+            for k, dg in fz["render_reference"].items():
+                assert O.fnv1a64(f_[k]) == dg, (name, v, k)
+        f2 = api.render_forward(2, s, b, W, H, pw, ph, bg, N.ALPHA_EXACT, st.task_order).to_numpy()
+        for k in ("alpha", "final_t", "contrib", "term"):
+            assert O.fnv1a64(f2[k]) == fz["render_gaussianwise"][k], (name, k)
