@@ -1,14 +1,21 @@
 // binning.cu — P5: tile binning, bit-exact with src/preprocess.cpp:66-115.
 //
 // The reference sorts (tile, depth, index) triples with std::sort.  Here the
-// same order comes from two stable LSD radix sorts:
+// same order comes from two stable LSD radix sorts (radix_sort.cuh):
 //   1. the n visible splats by depth key (float bits, 4 x 8-bit passes) with
-//      values in index order  -> (depth, index) order;
-//   2. the K = sum(tiles touched) (tile, splat) instances, duplicated in that
+//      values in index order  -> (depth, index) order.  Splats that touch no
+//      tile get key 0xffffffff and sink to the end (they emit nothing);
+//   2. the K = sum(tiles touched) (tile, splat) instances, expanded in that
 //      depth order, by tile id (ceil(log2 T) bits)  -> (tile, depth, index).
 // Sorting N depth keys once instead of K 45-bit keys cuts sort traffic ~3x.
-// Tile ranges come from key boundaries + an exclusive scan of per-tile counts,
-// so empty tiles get [pos, pos) exactly like the reference's range loop.
+//
+// Per-tile list lengths are known before any instance exists: every splat's
+// tile rectangle adds +1/-1 corners to a (cols+1) x (rows+1) difference grid
+// whose 2-D prefix sum is the tile histogram.  That gives the tile ranges
+// (exclusive scan; empty tiles get [pos, pos) like the reference's range loop)
+// without a boundary search over the K sorted instances.
+// The expansion is load-balanced: each thread writes 16 consecutive instances
+// (one smem search for the first, then a carry-walk over the rectangle).
 #include <math.h>
 
 #include "bs_common.cuh"
@@ -45,60 +52,214 @@ __device__ __forceinline__ bool tile_rect(float x, float y, float radius, const 
   return r.tx0 <= r.tx1 && r.ty0 <= r.ty1;
 }
 
-__global__ void k_bin_rect(const float4* __restrict__ xyab, const float4* __restrict__ cop,
-                           const float4* __restrict__ rgbr, int64_t n_cap, const int32_t* __restrict__ n_visible,
-                           Grid g, uint32_t* __restrict__ touched, uint32_t* __restrict__ dkeys,
-                           uint32_t* __restrict__ dvals) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_cap) return;
-  const int64_t n = *n_visible;
-  if (i >= n) return;
-  const float4 a = xyab[i];
-  const float radius = rgbr[i].w;
-  Rect r;
-  uint32_t cnt = 0;
-  if (tile_rect(a.x, a.y, radius, g, r)) cnt = (uint32_t)(r.tx1 - r.tx0 + 1) * (uint32_t)(r.ty1 - r.ty0 + 1);
-  touched[i] = cnt;
-  dkeys[i] = float_sort_key(cop[i].w);
-  dvals[i] = (uint32_t)i;
+// Per visible splat: tiles touched, packed rect (tx0 | ty0<<16, w | h<<16),
+// depth sort key (non-touching -> 0xffffffff), value = index, and the four
+// difference-grid corners of its rectangle.  SMEM_DIFF: the CTA accumulates
+// the corners in a private shared-memory grid (grid-stride over splats) and
+// flushes the non-zero cells once — clustered scenes put thousands of corners
+// on the same few cells, which global atomics would serialise.
+template <bool SMEM_DIFF>
+__global__ void __launch_bounds__(256) k_bin_rect(const float4* __restrict__ xyab, const float4* __restrict__ cop,
+                                                  const float4* __restrict__ rgbr, int64_t n_cap,
+                                                  const int32_t* __restrict__ n_visible, Grid g,
+                                                  uint32_t* __restrict__ touched, uint2* __restrict__ rects,
+                                                  uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
+                                                  int* __restrict__ diff) {
+  extern __shared__ int s_diff[];
+  const int stride = g.cols + 1;
+  const int cells = stride * (g.rows + 1);
+  int* dd = SMEM_DIFF ? s_diff : diff;
+  if (SMEM_DIFF) {
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) s_diff[i] = 0;
+    __syncthreads();
+  }
+  const int64_t n = min((int64_t)*n_visible, n_cap);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = xyab[i];
+    Rect r;
+    uint32_t cnt = 0;
+    uint2 pk = make_uint2(0u, 0u);
+    if (tile_rect(a.x, a.y, rgbr[i].w, g, r)) {
+      const uint32_t w = (uint32_t)(r.tx1 - r.tx0 + 1), h = (uint32_t)(r.ty1 - r.ty0 + 1);
+      cnt = w * h;
+      pk = make_uint2((uint32_t)r.tx0 | ((uint32_t)r.ty0 << 16), w | (h << 16));
+      atomicAdd(&dd[r.ty0 * stride + r.tx0], 1);
+      atomicAdd(&dd[r.ty0 * stride + r.tx1 + 1], -1);
+      atomicAdd(&dd[(r.ty1 + 1) * stride + r.tx0], -1);
+      atomicAdd(&dd[(r.ty1 + 1) * stride + r.tx1 + 1], 1);
+    }
+    touched[i] = cnt;
+    rects[i] = pk;
+    dkeys[i] = cnt ? float_sort_key(cop[i].w) : 0xffffffffu;
+    dvals[i] = (uint32_t)i;
+  }
+  if (SMEM_DIFF) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) {
+      const int v = s_diff[i];
+      if (v) atomicAdd(&diff[i], v);
+    }
+  }
 }
 
-__global__ void k_gather_touched(const uint32_t* __restrict__ order, const uint32_t* __restrict__ touched,
-                                 int64_t n_cap, const int32_t* __restrict__ n_visible, uint32_t* __restrict__ out) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_cap || j >= *n_visible) return;
-  out[j] = touched[order[j]];
+// One CTA: 2-D inclusive prefix of the difference grid in shared memory ->
+// per-tile counts.
+__global__ void __launch_bounds__(1024) k_diff_scan(const int* __restrict__ diff, Grid g, uint32_t* __restrict__ counts) {
+  extern __shared__ int s_grid[];
+  const int stride = g.cols + 1, cells = stride * (g.rows + 1);
+  for (int i = threadIdx.x; i < cells; i += blockDim.x) s_grid[i] = diff[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = warp; r < g.rows; r += nw) {  // rows: warp scans in 32-wide chunks
+    int carry = 0;
+    for (int x0 = 0; x0 < g.cols; x0 += 32) {
+      const int x = x0 + lane;
+      int v = x < g.cols ? s_grid[r * stride + x] : 0;
+      v = warp_inclusive_scan(v) + carry;
+      if (x < g.cols) s_grid[r * stride + x] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  for (int tx = threadIdx.x; tx < g.cols; tx += blockDim.x) {  // columns: sequential down rows
+    int run = 0;
+    for (int ty = 0; ty < g.rows; ++ty) {
+      run += s_grid[ty * stride + tx];
+      counts[ty * g.cols + tx] = (uint32_t)run;
+    }
+  }
 }
 
-// One thread per splat in depth order writes its rect's tile ids row-major
-// (ty outer, tx inner — the reference's push_back order, irrelevant after the
-// stable sort but kept) at offs[j].
-__global__ void k_duplicate(const float4* __restrict__ xyab, const float4* __restrict__ rgbr,
-                            const uint32_t* __restrict__ order, const uint64_t* __restrict__ offs, int64_t n_cap,
-                            const int32_t* __restrict__ n_visible, Grid g, uint32_t* __restrict__ keys,
-                            uint32_t* __restrict__ vals) {
+// Fallback for grids beyond shared memory: row CTAs, then a thread per column.
+__global__ void __launch_bounds__(256) k_diff_rows(int* __restrict__ diff, int stride) {
+  int* row = diff + (size_t)blockIdx.x * stride;
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < stride; base += 256) {
+    const int x = base + threadIdx.x;
+    const int v = x < stride ? row[x] : 0;
+    int tot;
+    const int ex = block_exclusive_scan<int>(v, &tot);
+    const int c = carry;
+    if (x < stride) row[x] = c + ex + v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c + tot;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_diff_cols(const int* __restrict__ diff, Grid g, uint32_t* __restrict__ counts) {
+  const int tx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tx >= g.cols) return;
+  const int stride = g.cols + 1;
+  int run = 0;
+  for (int ty = 0; ty < g.rows; ++ty) {
+    run += diff[ty * stride + tx];
+    counts[ty * g.cols + tx] = (uint32_t)run;
+  }
+}
+
+constexpr size_t kMaxDiffSmem = 200 * 1024;  // <= 227 KB opt-in
+
+__global__ void k_gather_sorted(const uint32_t* __restrict__ order, const uint32_t* __restrict__ touched,
+                                const uint2* __restrict__ rects, int64_t n_cap, const int32_t* __restrict__ n_visible,
+                                uint32_t* __restrict__ touched_sorted, uint2* __restrict__ rects_sorted) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n_cap || j >= *n_visible) return;
   const uint32_t i = order[j];
-  const float4 a = xyab[i];
-  Rect r;
-  if (!tile_rect(a.x, a.y, rgbr[i].w, g, r)) return;
-  uint64_t o = offs[j];
-  for (int ty = r.ty0; ty <= r.ty1; ++ty)
-    for (int tx = r.tx0; tx <= r.tx1; ++tx) {
-      keys[o] = (uint32_t)(ty * g.cols + tx);
-      vals[o] = i;
-      ++o;
-    }
+  touched_sorted[j] = touched[i];
+  rects_sorted[j] = rects[i];
 }
 
-__global__ void k_tile_bounds(const uint32_t* __restrict__ keys, int64_t K, uint32_t* __restrict__ counts) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  const uint32_t t = keys[k];
-  // count[t] = last+1 - first, assembled from the two boundary writers
-  if (k == 0 || keys[k - 1] != t) atomicSub(&counts[t], (uint32_t)k);
-  if (k == K - 1 || keys[k + 1] != t) atomicAdd(&counts[t], (uint32_t)(k + 1));
+// Expansion: block b writes instances [b*4096, b*4096+4096); thread t the 16
+// consecutive ones at b*4096 + 16t.  Every splat of the depth-sorted prefix
+// emits >= 1 instance, so the window of 4097 offsets in smem always covers a
+// block (thread 0 finds its start by binary search).  Each thread searches
+// the window once, then walks its rectangle with a carry (no division after
+// the first output) and stores 4 x uint4.
+constexpr int kExpandItems = 4096;
+constexpr int kExpandPer = 16;
+constexpr int kExpandWin = kExpandItems + 1;
+
+// block_j0[b] = the splat (depth order) whose instance range holds output
+// b*4096: every splat marks the expansion blocks whose first output it owns.
+__global__ void k_mark_starts(const uint64_t* __restrict__ offs, const uint32_t* __restrict__ touched_sorted,
+                              int64_t n_cap, const int32_t* __restrict__ n_visible, uint32_t* __restrict__ block_j0) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_cap || j >= *n_visible) return;
+  const uint64_t lo = offs[j], hi = lo + touched_sorted[j];
+  for (uint64_t b = (lo + kExpandItems - 1) / kExpandItems; b * kExpandItems < hi; ++b) block_j0[b] = (uint32_t)j;
+}
+
+__global__ void __launch_bounds__(256) k_expand(const uint64_t* __restrict__ offs, const uint32_t* __restrict__ order,
+                                                const uint2* __restrict__ rects_sorted, int64_t n_cap,
+                                                const int32_t* __restrict__ n_visible, int64_t K, int cols,
+                                                const uint32_t* __restrict__ block_j0, uint32_t* __restrict__ keys,
+                                                uint32_t* __restrict__ vals) {
+  __shared__ uint64_t s_offs[kExpandWin + 1];
+  const int tid = threadIdx.x;
+  const int64_t o0 = (int64_t)blockIdx.x * kExpandItems;
+  const int64_t n = min((int64_t)*n_visible, n_cap);
+  const int64_t j0 = block_j0[blockIdx.x];
+  const int win = (int)min((int64_t)kExpandWin, n - j0);
+  for (int i = tid; i <= win; i += 256) s_offs[i] = (j0 + i < n) ? offs[j0 + i] : (uint64_t)K;
+  __syncthreads();
+  const int64_t ot = o0 + (int64_t)tid * kExpandPer;
+  if (ot >= K) return;
+  int lo = 0, hi = win;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (s_offs[mid] <= (uint64_t)ot) lo = mid;
+    else hi = mid;
+  }
+  int i = lo;
+  uint64_t next_off = s_offs[i + 1];
+  uint2 rc = rects_sorted[j0 + i];
+  uint32_t id = order[j0 + i];
+  uint32_t w = rc.y & 0xffffu, tx0 = rc.x & 0xffffu;
+  uint32_t m = (uint32_t)(ot - (int64_t)s_offs[i]);
+  uint32_t tx = tx0 + m % w, ty = (rc.x >> 16) + m / w;
+  uint32_t kk[kExpandPer], vv[kExpandPer];
+  const int cnt = (int)min((int64_t)kExpandPer, K - ot);
+#pragma unroll
+  for (int q = 0; q < kExpandPer; ++q) {
+    if (q < cnt) {
+      const uint64_t o = (uint64_t)(ot + q);
+      if (o >= next_off) {
+        ++i;
+        next_off = s_offs[i + 1];
+        rc = rects_sorted[j0 + i];
+        id = order[j0 + i];
+        w = rc.y & 0xffffu;
+        tx0 = rc.x & 0xffffu;
+        tx = tx0;
+        ty = rc.x >> 16;
+      }
+      kk[q] = ty * (uint32_t)cols + tx;
+      vv[q] = id;
+      if (++tx == tx0 + w) {
+        tx = tx0;
+        ++ty;
+      }
+    }
+  }
+  if (cnt == kExpandPer) {
+    uint4* k4 = reinterpret_cast<uint4*>(keys + ot);
+    uint4* v4 = reinterpret_cast<uint4*>(vals + ot);
+#pragma unroll
+    for (int q = 0; q < kExpandPer / 4; ++q) {
+      k4[q] = make_uint4(kk[4 * q], kk[4 * q + 1], kk[4 * q + 2], kk[4 * q + 3]);
+      v4[q] = make_uint4(vv[4 * q], vv[4 * q + 1], vv[4 * q + 2], vv[4 * q + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kExpandPer; ++q)
+      if (q < cnt) {
+        keys[ot + q] = kk[q];
+        vals[ot + q] = vv[q];
+      }
+  }
 }
 
 __global__ void k_ranges(const uint32_t* __restrict__ starts, const uint32_t* __restrict__ counts, int T,
@@ -124,49 +285,46 @@ inline int bits_for(int64_t values) {  // bits to represent 0..values-1
   return b;
 }
 
-// Workspace layout shared by bs_bin_count and bs_bin_sort (same carve order).
+// Workspace layout shared by bs_bin_count and bs_bin_sort (same carve order;
+// the k-sized tail is last so a count-phase carve is a prefix of it).
 struct BinWs {
-  // count phase (n-sized)
   uint32_t *touched, *dk0, *dv0, *dk1, *dv1, *touched_sorted;
+  uint2 *rects, *rects_sorted;
   uint64_t* offs;
   uint64_t* offs_partials;
   RadixWs rws_n;
-  // sort phase (k-sized)
-  uint32_t *tk0, *tv0, *tk1;
-  RadixWs rws_k;
+  int* diff;
   uint32_t *counts, *starts, *cpartials;
+  uint32_t *tk0, *tv_alt, *tk1, *block_j0;
+  RadixWs rws_k;
 };
 
 template <typename C>
-inline void bin_ws_layout(C& c, int64_t n_cap, int64_t T, int64_t k_cap, BinWs* w) {
+inline void bin_ws_layout(C& c, int64_t n_cap, const Grid& g, int64_t k_cap, BinWs* w) {
   BinWs tmp;
   BinWs& o = w ? *w : tmp;
-  o.touched = (uint32_t*)c.template take<uint32_t>((size_t)n_cap);
-  o.dk0 = (uint32_t*)c.template take<uint32_t>((size_t)n_cap);
-  o.dv0 = (uint32_t*)c.template take<uint32_t>((size_t)n_cap);
-  o.dk1 = (uint32_t*)c.template take<uint32_t>((size_t)n_cap);
-  o.dv1 = (uint32_t*)c.template take<uint32_t>((size_t)n_cap);
-  o.touched_sorted = (uint32_t*)c.template take<uint32_t>((size_t)n_cap);
-  o.offs = (uint64_t*)c.template take<uint64_t>((size_t)n_cap);
-  o.offs_partials = (uint64_t*)c.template take<uint64_t>((size_t)scan_num_blocks(n_cap) + 1);
-  {
-    const int64_t nb = radix_num_blocks(n_cap);
-    o.rws_n.hist = (uint32_t*)c.template take<uint32_t>((size_t)(256 * nb));
-    o.rws_n.partials = (uint32_t*)c.template take<uint32_t>((size_t)scan_num_blocks(256 * nb));
-  }
-  o.counts = (uint32_t*)c.template take<uint32_t>((size_t)T);
-  o.starts = (uint32_t*)c.template take<uint32_t>((size_t)T);
-  o.cpartials = (uint32_t*)c.template take<uint32_t>((size_t)scan_num_blocks(T) + 1);
-  o.tk0 = (uint32_t*)c.template take<uint32_t>((size_t)k_cap);
-  o.tv0 = (uint32_t*)c.template take<uint32_t>((size_t)k_cap);
-  o.tk1 = (uint32_t*)c.template take<uint32_t>((size_t)k_cap);
-  {
-    const int64_t nb = radix_num_blocks(k_cap);
-    o.rws_k.hist = (uint32_t*)c.template take<uint32_t>((size_t)(256 * nb));
-    o.rws_k.partials = (uint32_t*)c.template take<uint32_t>((size_t)scan_num_blocks(256 * nb));
-  }
+  const int64_t T = (int64_t)g.cols * g.rows;
+  o.touched = c.template take<uint32_t>((size_t)n_cap);
+  o.dk0 = c.template take<uint32_t>((size_t)n_cap);
+  o.dv0 = c.template take<uint32_t>((size_t)n_cap);
+  o.dk1 = c.template take<uint32_t>((size_t)n_cap);
+  o.dv1 = c.template take<uint32_t>((size_t)n_cap);
+  o.touched_sorted = c.template take<uint32_t>((size_t)n_cap);
+  o.rects = c.template take<uint2>((size_t)n_cap);
+  o.rects_sorted = c.template take<uint2>((size_t)n_cap);
+  o.offs = c.template take<uint64_t>((size_t)n_cap);
+  o.offs_partials = c.template take<uint64_t>((size_t)scan_num_blocks(n_cap) + 1);
+  radix_ws_layout(c, n_cap, &o.rws_n);
+  o.diff = c.template take<int>((size_t)(g.cols + 1) * (g.rows + 1));
+  o.counts = c.template take<uint32_t>((size_t)T);
+  o.starts = c.template take<uint32_t>((size_t)T);
+  o.cpartials = c.template take<uint32_t>((size_t)scan_num_blocks(T) + 1);
+  o.tk0 = c.template take<uint32_t>((size_t)k_cap);
+  o.tv_alt = c.template take<uint32_t>((size_t)k_cap);
+  o.tk1 = c.template take<uint32_t>((size_t)k_cap);
+  o.block_j0 = c.template take<uint32_t>((size_t)(k_cap / kExpandItems + 1));
+  radix_ws_layout(c, k_cap, &o.rws_k);
 }
-
 
 __global__ void k_store_k(const uint64_t* __restrict__ total, int64_t* __restrict__ k_total) {
   *k_total = (int64_t)*total;
@@ -181,14 +339,14 @@ extern "C" size_t bs_bin_workspace_bytes(int64_t n_cap, int32_t width, int32_t h
   if (n_cap < 0 || width <= 0 || height <= 0 || pw <= 0 || ph <= 0 || k_cap < 0) return 0;
   const Grid g = make_grid(width, height, pw, ph);
   WsSizer s;
-  bin_ws_layout(s, n_cap, (int64_t)g.cols * g.rows, k_cap, nullptr);
+  bin_ws_layout(s, n_cap, g, k_cap, nullptr);
   return s.off + 256;
 }
 
 static int check_grid(int32_t W, int32_t H, int32_t pw, int32_t ph) {
   if (W <= 0 || H <= 0 || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
-  const int64_t T = (int64_t)((W + pw - 1) / pw) * ((H + ph - 1) / ph);
-  if (T > (1 << 24)) return BS_ERR_UNSUPPORTED;
+  const int64_t cols = (W + pw - 1) / pw, rows = (H + ph - 1) / ph;
+  if (cols > 65535 || rows > 65535 || cols * rows > (1 << 24)) return BS_ERR_UNSUPPORTED;
   return BS_OK;
 }
 
@@ -197,67 +355,96 @@ extern "C" int bs_bin_count(bs_splats g, int64_t n_cap, const int32_t* n_visible
   int s = check_grid(width, height, pw, ph);
   if (s) return s;
   if (n_cap < 0 || !n_visible || !k_total || (n_cap > 0 && (!g.xyab || !g.cop || !g.rgbr))) return BS_ERR_INVALID_ARGUMENT;
-  if (n_cap >= (int64_t)0x7fffffff) return BS_ERR_CAPACITY;
+  if (n_cap >= (int64_t)1 << 30) return BS_ERR_CAPACITY;
   cudaStream_t st = (cudaStream_t)stream;
   const Grid gr = make_grid(width, height, pw, ph);
   const int64_t T = (int64_t)gr.cols * gr.rows;
   if (!ws || ws_bytes < bs_bin_workspace_bytes(n_cap, width, height, pw, ph, 0)) return BS_ERR_WORKSPACE;
   WsCarver c(ws, ws_bytes);
   BinWs w;
-  bin_ws_layout(c, n_cap, T, 0, &w);
-  if (n_cap == 0) {
-    BS_CUDA_TRY(cudaMemsetAsync(k_total, 0, sizeof(int64_t), st));
-    return BS_OK;
+  bin_ws_layout(c, n_cap, gr, 0, &w);
+  BS_CUDA_TRY(cudaMemsetAsync(w.diff, 0, sizeof(int) * (size_t)(gr.cols + 1) * (gr.rows + 1), st));
+  const size_t diff_bytes = sizeof(int) * (size_t)(gr.cols + 1) * (gr.rows + 1);
+  const bool smem_diff = diff_bytes <= kMaxDiffSmem;
+  static bool attr_set = false;
+  if (smem_diff && !attr_set) {
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_bin_rect<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDiffSmem));
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_diff_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDiffSmem));
+    attr_set = true;
   }
-  const unsigned nb = (unsigned)((n_cap + 255) / 256);
-  k_bin_rect<<<nb, 256, 0, st>>>(reinterpret_cast<const float4*>(g.xyab), reinterpret_cast<const float4*>(g.cop),
-                                 reinterpret_cast<const float4*>(g.rgbr), n_cap, n_visible, gr, w.touched, w.dk0, w.dv0);
-  BS_LAUNCH_CHECK();
-  bool alt = false;
-  BS_CUDA_TRY(radix_sort_pairs(w.dk0, w.dv0, w.dk1, w.dv1, n_cap, n_visible, 32, w.rws_n, &alt, st));
-  const uint32_t* order = alt ? w.dv1 : w.dv0;
-  k_gather_touched<<<nb, 256, 0, st>>>(order, w.touched, n_cap, n_visible, w.touched_sorted);
-  BS_LAUNCH_CHECK();
-  uint64_t* total = w.offs_partials + scan_num_blocks(n_cap);
-  BS_CUDA_TRY((exclusive_scan<uint32_t, uint64_t>(w.touched_sorted, w.offs, n_cap, n_visible, w.offs_partials, total, st)));
-  k_store_k<<<1, 1, 0, st>>>(total, k_total);
-  BS_LAUNCH_CHECK();
+  if (n_cap > 0) {
+    const unsigned nb = (unsigned)((n_cap + 255) / 256);
+    const float4* xa = reinterpret_cast<const float4*>(g.xyab);
+    const float4* xc = reinterpret_cast<const float4*>(g.cop);
+    const float4* xr = reinterpret_cast<const float4*>(g.rgbr);
+    if (smem_diff) {
+      int dev = 0, sms = 148;
+      BS_CUDA_TRY(cudaGetDevice(&dev));
+      BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const unsigned grid = (unsigned)min((int64_t)nb, (int64_t)sms * 2);
+      k_bin_rect<true><<<grid, 256, diff_bytes, st>>>(xa, xc, xr, n_cap, n_visible, gr, w.touched, w.rects, w.dk0,
+                                                      w.dv0, w.diff);
+    } else {
+      k_bin_rect<false><<<nb, 256, 0, st>>>(xa, xc, xr, n_cap, n_visible, gr, w.touched, w.rects, w.dk0, w.dv0,
+                                            w.diff);
+    }
+    BS_LAUNCH_CHECK();
+    bool alt = false;
+    BS_CUDA_TRY(radix_sort_pairs(w.dk0, w.dv0, w.dk1, w.dv1, n_cap, n_visible, 32, w.rws_n, &alt, st));
+    const uint32_t* order = alt ? w.dv1 : w.dv0;  // 4 passes: back in dv0
+    k_gather_sorted<<<nb, 256, 0, st>>>(order, w.touched, w.rects, n_cap, n_visible, w.touched_sorted,
+                                        w.rects_sorted);
+    BS_LAUNCH_CHECK();
+    uint64_t* total = w.offs_partials + scan_num_blocks(n_cap);
+    BS_CUDA_TRY((exclusive_scan<uint32_t, uint64_t>(w.touched_sorted, w.offs, n_cap, n_visible, w.offs_partials,
+                                                    total, st)));
+    k_store_k<<<1, 1, 0, st>>>(total, k_total);
+    BS_LAUNCH_CHECK();
+  } else {
+    BS_CUDA_TRY(cudaMemsetAsync(k_total, 0, sizeof(int64_t), st));
+  }
+  // tile histogram from the difference grid -> counts, starts, digit counts
+  if (smem_diff) {
+    k_diff_scan<<<1, 1024, diff_bytes, st>>>(w.diff, gr, w.counts);
+    BS_LAUNCH_CHECK();
+  } else {
+    k_diff_rows<<<(unsigned)(gr.rows + 1), 256, 0, st>>>(w.diff, gr.cols + 1);
+    BS_LAUNCH_CHECK();
+    k_diff_cols<<<(unsigned)((gr.cols + 255) / 256), 256, 0, st>>>(w.diff, gr, w.counts);
+    BS_LAUNCH_CHECK();
+  }
+  BS_CUDA_TRY((exclusive_scan<uint32_t, uint32_t>(w.counts, w.starts, T, nullptr, w.cpartials, nullptr, st)));
   return BS_OK;
 }
 
 extern "C" int bs_bin_sort(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height,
                            int32_t pw, int32_t ph, int64_t k, uint32_t* point_list, uint32_t* tile_ranges, void* ws,
                            size_t ws_bytes, void* stream) {
+  (void)g;
   int s = check_grid(width, height, pw, ph);
   if (s) return s;
   if (n_cap < 0 || k < 0 || !n_visible || !tile_ranges || (k > 0 && !point_list)) return BS_ERR_INVALID_ARGUMENT;
-  if (k > (int64_t)0xfffffffe) return BS_ERR_CAPACITY;
+  if (k >= (int64_t)1 << 30) return BS_ERR_CAPACITY;
   cudaStream_t st = (cudaStream_t)stream;
   const Grid gr = make_grid(width, height, pw, ph);
   const int64_t T = (int64_t)gr.cols * gr.rows;
   if (!ws || ws_bytes < bs_bin_workspace_bytes(n_cap, width, height, pw, ph, k)) return BS_ERR_WORKSPACE;
   WsCarver c(ws, ws_bytes);
   BinWs w;
-  // k_cap = the largest k this workspace can hold (same layout prefix)
-  bin_ws_layout(c, n_cap, T, k, &w);
-  BS_CUDA_TRY(cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * (size_t)T, st));
+  bin_ws_layout(c, n_cap, gr, k, &w);
   if (k > 0) {
-    // 4 passes of 8 bits leave the depth order back in dv0.
-    const uint32_t* order = w.dv0;
-    const unsigned nb = (unsigned)((n_cap + 255) / 256);
-    // values go straight into point_list; (tk1, tv0) is the ping-pong pair
-    k_duplicate<<<nb, 256, 0, st>>>(reinterpret_cast<const float4*>(g.xyab), reinterpret_cast<const float4*>(g.rgbr),
-                                    order, w.offs, n_cap, n_visible, gr, w.tk0, point_list);
+    const uint32_t* order = w.dv0;  // depth order (4 passes end in dv0)
+    const int bits = bits_for(T);
+    k_mark_starts<<<(unsigned)((n_cap + 255) / 256), 256, 0, st>>>(w.offs, w.touched_sorted, n_cap, n_visible,
+                                                                 w.block_j0);
+    BS_LAUNCH_CHECK();
+    k_expand<<<(unsigned)((k + kExpandItems - 1) / kExpandItems), 256, 0, st>>>(
+        w.offs, order, w.rects_sorted, n_cap, n_visible, k, gr.cols, w.block_j0, w.tk0, point_list);
     BS_LAUNCH_CHECK();
     bool alt = false;
-    uint32_t* tv_alt = w.tv0;
-    BS_CUDA_TRY(radix_sort_pairs(w.tk0, point_list, w.tk1, tv_alt, k, nullptr, bits_for(T), w.rws_k, &alt, st));
-    const uint32_t* sorted_keys = alt ? w.tk1 : w.tk0;
-    if (alt) BS_CUDA_TRY(cudaMemcpyAsync(point_list, tv_alt, sizeof(uint32_t) * (size_t)k, cudaMemcpyDeviceToDevice, st));
-    k_tile_bounds<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(sorted_keys, k, w.counts);
-    BS_LAUNCH_CHECK();
+    BS_CUDA_TRY(radix_sort_pairs(w.tk0, point_list, w.tk1, w.tv_alt, k, nullptr, bits, w.rws_k, &alt, st));
+    if (alt) BS_CUDA_TRY(cudaMemcpyAsync(point_list, w.tv_alt, sizeof(uint32_t) * (size_t)k, cudaMemcpyDeviceToDevice, st));
   }
-  BS_CUDA_TRY((exclusive_scan<uint32_t, uint32_t>(w.counts, w.starts, T, nullptr, w.cpartials, nullptr, st)));
   k_ranges<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(w.starts, w.counts, (int)T, tile_ranges);
   BS_LAUNCH_CHECK();
   return BS_OK;

@@ -70,9 +70,7 @@ inline void stats_ws_layout(C& c, int64_t T, uint32_t** k0, uint32_t** v0, uint3
   *k1 = c.template take<uint32_t>((size_t)T);
   *v1 = c.template take<uint32_t>((size_t)T);
   *counts = c.template take<uint32_t>((size_t)T);
-  const int64_t nb = radix_num_blocks(T);
-  rw->hist = c.template take<uint32_t>((size_t)(256 * nb));
-  rw->partials = c.template take<uint32_t>((size_t)scan_num_blocks(256 * nb));
+  radix_ws_layout(c, T, rw);
 }
 
 
