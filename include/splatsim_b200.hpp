@@ -1,0 +1,228 @@
+// splatsim_b200.hpp — C++ drop-in for the reference's render API
+// (/root/reference/proj/core/include/splatsim, namespace splatsim), backed by
+// the B200 C-ABI (splatsim_b200.h).  Same names, argument meaning, value
+// semantics and exceptions; POD std::array fields replace Eigen types (field
+// order as the reference's structs, rotation stored w,x,y,z).
+//
+//   reference                               here
+//   project_gaussian / project_all          preprocess.hpp:57-59   -> bs_preprocess
+//   bin_tiles                               preprocess.hpp:64-65   -> bs_bin_count + bs_bin_sort
+//   tile_load_histogram / binning_csv       preprocess.hpp:67-70   -> bs_tile_stats
+//   render_reference                        blend.hpp:100-102      -> bs_render_forward(Naive)
+//   run_kernel / make_task_specs /
+//   trace_from_work / warp_steps_* /
+//   trace_csv / variant_name(_from_name)    kernels.hpp:25-108     -> bs_render_forward(v)
+//   dispatch_for                            machine.hpp:38
+//   SelectionState / checkpoint             adaptive.hpp:15-55     (measured B200 times)
+//   compare_outputs / write_ppm / ...       image_io.hpp:14-27
+//   gen_clustered_scene / Rng / fnv1a64     workload.hpp:68-76, rng.hpp
+//
+// Every compute call runs on the GPU (no CPU fallback); host data is copied
+// in and results copied out, as the value-typed reference API requires.  For
+// device-resident pipelines use the C-ABI directly.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <utility>
+#include <vector>
+
+namespace splatsim {
+
+struct Gaussian3D {
+  std::array<float, 3> mean{0, 0, 0};
+  std::array<float, 3> scale{1, 1, 1};
+  std::array<float, 4> rotation{1, 0, 0, 0};  // w, x, y, z
+  float opacity = 1.0f;
+  std::array<float, 3> color{0, 0, 0};
+};
+
+struct Camera {
+  std::array<float, 16> view_transform{1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1};  // row-major world->camera
+  std::array<float, 2> focal{100.0f, 100.0f};
+  int width = 0;
+  int height = 0;
+};
+
+struct Gaussian2D {
+  std::array<float, 2> xy{0, 0};
+  float conic_a = 1.0f;
+  float conic_b = 0.0f;
+  float conic_c = 1.0f;
+  float opacity = 1.0f;
+  std::array<float, 3> color{0, 0, 0};
+  float depth = 1.0f;
+  float radius = 0.0f;
+};
+
+struct TileBinning {
+  int tile_cols = 0;
+  int tile_rows = 0;
+  std::vector<std::uint32_t> point_list;
+  std::vector<std::pair<std::uint32_t, std::uint32_t>> tile_ranges;  // [start, end)
+  int tile_count() const { return tile_cols * tile_rows; }
+  int tile_size(int t) const { return static_cast<int>(tile_ranges[t].second - tile_ranges[t].first); }
+};
+
+struct TileHistogram {
+  std::vector<std::uint32_t> counts;
+  std::uint32_t min = 0;
+  std::uint32_t max = 0;
+  double mean = 0.0;
+  std::uint32_t p50 = 0;
+  std::uint32_t p99 = 0;
+};
+
+inline constexpr float kNearPlane = 0.01f;
+inline constexpr float kAlphaClamp = 0.99f;
+inline constexpr float kAlphaSkip = 1.0f / 255.0f;
+inline constexpr float kStopThreshold = 1e-4f;
+
+struct RenderOutput {
+  int width = 0;
+  int height = 0;
+  std::vector<float> color;
+  std::vector<float> alpha;
+  std::vector<float> depth;
+  std::vector<float> final_t;
+  std::vector<std::int32_t> contrib;
+  std::vector<std::int32_t> term;
+  std::size_t pixels() const { return static_cast<std::size_t>(width) * height; }
+};
+
+enum class KernelVariant { Naive, DynamicBlocks, GaussianWise, FineGrainedCombined, SharedMemOpt };
+inline constexpr std::array<KernelVariant, 5> kAllVariants = {
+    KernelVariant::Naive, KernelVariant::DynamicBlocks, KernelVariant::GaussianWise,
+    KernelVariant::FineGrainedCombined, KernelVariant::SharedMemOpt};
+std::string_view variant_name(KernelVariant v);
+std::optional<KernelVariant> variant_from_name(std::string_view name);
+
+inline constexpr int kBlockThreads = 128;
+inline constexpr int kWarpsPerTask = 4;
+inline constexpr int kWarpLanes = 32;
+inline constexpr int kFinePixelsPerTask = 4;
+inline constexpr int kFineTasksPerTile = kBlockThreads / kFinePixelsPerTask;
+
+struct PixelCoord {
+  int x = 0, y = 0;
+};
+struct TaskSpec {
+  std::int32_t task_id = 0;
+  std::int32_t tile_id = 0;
+  std::array<std::vector<PixelCoord>, kWarpsPerTask> warp_pixels;
+  std::size_t pixel_count() const {
+    std::size_t n = 0;
+    for (const auto& w : warp_pixels) n += w.size();
+    return n;
+  }
+};
+std::vector<TaskSpec> make_task_specs(KernelVariant variant, int width, int height, int patch_width,
+                                      int patch_height);
+
+struct WarpCounts {
+  std::int64_t compute_steps = 0;
+  std::int64_t prefix_groups = 0;
+  std::int32_t reduce_ops = 0;
+  std::int32_t writeback_ops = 0;
+};
+struct TaskTrace {
+  std::int32_t task_id = 0;
+  std::int32_t tile_id = 0;
+  std::int64_t shared_chunks = 0;
+  std::array<WarpCounts, kWarpsPerTask> warps;
+};
+struct WorkTrace {
+  KernelVariant variant = KernelVariant::Naive;
+  std::vector<TaskTrace> tasks;
+};
+struct TileWork {
+  std::int32_t list_len = 0;
+  std::vector<std::int32_t> consumed;
+};
+std::int64_t warp_steps_pixelwise(const std::vector<std::optional<std::int64_t>>& term_indices, std::int64_t list_len);
+std::int64_t warp_steps_gaussianwise(std::optional<std::int64_t> term_index, std::int64_t list_len);
+WorkTrace trace_from_work(KernelVariant variant, const std::vector<TileWork>& tiles);
+std::string trace_csv(const WorkTrace& trace, const std::string& config_comment);
+
+struct KernelRun {
+  RenderOutput output;
+  WorkTrace trace;
+};
+
+enum class Dispatch { Static, Dynamic };
+Dispatch dispatch_for(KernelVariant v);
+
+// ---- alpha arithmetic of the GPU kernels (BS_ALPHA_EXACT by default) ----
+enum class AlphaMode { Exact, Fast };
+void set_alpha_mode(AlphaMode m);
+AlphaMode alpha_mode();
+
+// ---- preprocess (include/splatsim/preprocess.hpp) ----
+std::optional<Gaussian2D> project_gaussian(const Gaussian3D& g, const Camera& cam);
+std::vector<Gaussian2D> project_all(const std::vector<Gaussian3D>& gaussians, const Camera& cam);
+TileBinning bin_tiles(const std::vector<Gaussian2D>& gaussians, int width, int height, int patch_width,
+                      int patch_height);
+TileHistogram tile_load_histogram(const TileBinning& binning);
+std::string binning_csv(const TileBinning& binning, const std::string& config_comment);
+
+// ---- render (blend.hpp / kernels.hpp) ----
+RenderOutput render_reference(const TileBinning& binning, const std::vector<Gaussian2D>& gaussians, int width,
+                              int height, int patch_width, int patch_height, const std::array<float, 3>& background);
+KernelRun run_kernel(KernelVariant variant, const TileBinning& binning, const std::vector<Gaussian2D>& gaussians,
+                     int width, int height, int patch_width, int patch_height,
+                     const std::array<float, 3>& background);
+// Device time (ms, CUDA events) of one render of `variant` on this frame.
+double time_kernel_ms(KernelVariant variant, const TileBinning& binning, const std::vector<Gaussian2D>& gaussians,
+                      int width, int height, int patch_width, int patch_height, int repeats = 3);
+
+// ---- selector (adaptive.hpp), with measured B200 kernel times ----
+struct SelectionState {
+  KernelVariant current = KernelVariant::FineGrainedCombined;
+  bool switched = false;
+  int check_interval = 1000;
+  struct Checkpoint {
+    int iter = 0;
+    double t_balanced = 0.0;
+    double t_baseline = 0.0;
+  };
+  std::vector<Checkpoint> history;
+};
+// src/adaptive.cpp:16-32 with the two makespans replaced by measured times:
+// throws std::logic_error if already switched, std::invalid_argument if iter
+// is not a multiple of check_interval; switches permanently to SharedMemOpt
+// when the balanced kernel was slower.
+SelectionState checkpoint(SelectionState state, int iter, double t_balanced_ms, double t_baseline_ms);
+// Same, timing FineGrainedCombined and SharedMemOpt on the given frame.
+SelectionState checkpoint(SelectionState state, int iter, const TileBinning& binning,
+                          const std::vector<Gaussian2D>& gaussians, int width, int height, int patch_width,
+                          int patch_height);
+// Per-frame predictor from tile statistics (bs_select_variant).
+KernelVariant select_variant(const TileHistogram& h, int width, int height, int patch_width, int patch_height);
+
+// ---- image_io (image_io.hpp) ----
+struct Deviation {
+  double max_abs = 0.0;
+  double max_rel = 0.0;
+  bool contrib_equal = true;
+};
+Deviation compare_outputs(const RenderOutput& reference, const RenderOutput& candidate);
+void write_ppm(const RenderOutput& out, const std::string& path);
+void write_float_grid(const std::vector<float>& grid, int width, int height, const std::string& path);
+std::string render_digest_csv(const RenderOutput& out, const std::string& config_comment);
+
+// ---- workload (workload.hpp / rng.hpp) ----
+struct ClusterSceneParams {
+  int n_gaussians = 2000;
+  int n_clusters = 4;
+  std::uint64_t seed = 42;
+  double cluster_sigma = 0.035;
+  double background_fraction = 0.12;
+};
+std::vector<Gaussian3D> gen_clustered_scene(const ClusterSceneParams& params, const Camera& cam);
+std::uint64_t fnv1a64(const void* data, std::size_t size, std::uint64_t h = 0xcbf29ce484222325ull);
+
+}  // namespace splatsim

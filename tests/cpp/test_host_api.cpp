@@ -1,0 +1,149 @@
+// test_host_api.cpp — the C++ drop-in API (splatsim_b200.hpp) against the CPU
+// oracle (test infrastructure), the way the reference's own C++ tests would
+// call it.  Exit code 0 = all checks passed.  Run by tests/test_cpp_api.py.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+
+#include "../../oracle/oracle.hpp"
+#include "splatsim_b200.hpp"
+
+static int failures = 0;
+#define CHECK(cond)                                                        \
+  do {                                                                     \
+    if (!(cond)) {                                                         \
+      std::fprintf(stderr, "FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond); \
+      ++failures;                                                          \
+    }                                                                      \
+  } while (0)
+
+template <typename A, typename B>
+static bool same_bytes(const A& a, const B& b, size_t n) {
+  return std::memcmp(a, b, n) == 0;
+}
+
+int main() {
+  const int W = 250, H = 130, pw = 16, ph = 8;
+  splatsim::Camera cam;
+  cam.focal = {250.0f, 250.0f};
+  cam.width = W;
+  cam.height = H;
+  splatsim::ClusterSceneParams p;
+  p.n_gaussians = 6000;
+  p.background_fraction = 0.3;
+  const auto g3d = splatsim::gen_clustered_scene(p, cam);
+
+  // oracle inputs (same bytes)
+  oracle::Camera ocam;
+  std::memcpy(ocam.view, cam.view_transform.data(), sizeof(ocam.view));
+  ocam.focal[0] = cam.focal[0];
+  ocam.focal[1] = cam.focal[1];
+  ocam.width = W;
+  ocam.height = H;
+  oracle::ClusterSceneParams op;
+  op.n_gaussians = p.n_gaussians;
+  op.background_fraction = p.background_fraction;
+  const auto og3d = oracle::gen_clustered_scene(op, ocam);
+  CHECK(og3d.size() == g3d.size() && same_bytes(og3d.data(), g3d.data(), g3d.size() * sizeof(g3d[0])));
+
+  // project_all: bit-exact
+  const auto g2d = splatsim::project_all(g3d, cam);
+  const auto og2d = oracle::project_all(og3d, ocam);
+  CHECK(g2d.size() == og2d.size() && same_bytes(g2d.data(), og2d.data(), g2d.size() * sizeof(g2d[0])));
+  auto one = splatsim::project_gaussian(g3d[0], cam);
+  auto oone = oracle::project_gaussian(og3d[0], ocam);
+  CHECK(bool(one) == bool(oone));
+
+  // bin_tiles: bit-exact
+  const auto b = splatsim::bin_tiles(g2d, W, H, pw, ph);
+  const auto ob = oracle::bin_tiles(og2d.data(), og2d.size(), W, H, pw, ph);
+  CHECK(b.tile_cols == ob.tile_cols && b.tile_rows == ob.tile_rows);
+  CHECK(b.point_list == ob.point_list);
+  bool ranges_ok = int(b.tile_ranges.size()) == b.tile_count();
+  for (int t = 0; ranges_ok && t < b.tile_count(); ++t)
+    ranges_ok = b.tile_ranges[size_t(t)].first == ob.tile_ranges[2 * size_t(t)] &&
+                b.tile_ranges[size_t(t)].second == ob.tile_ranges[2 * size_t(t) + 1];
+  CHECK(ranges_ok);
+
+  // tile_load_histogram
+  const auto h = splatsim::tile_load_histogram(b);
+  const auto oh = oracle::tile_load_histogram(ob);
+  CHECK(h.counts == oh.counts && h.min == oh.min && h.max == oh.max && h.p50 == oh.p50 && h.p99 == oh.p99 &&
+        h.mean == oh.mean);
+
+  // render_reference / run_kernel: exact mode
+  const std::array<float, 3> bg = {0.1f, 0.2f, 0.3f};
+  const float obg[3] = {0.1f, 0.2f, 0.3f};
+  const auto ref = oracle::render(oracle::Variant::Naive, ob, og2d.data(), og2d.size(), W, H, pw, ph, obg);
+  const auto rr = splatsim::render_reference(b, g2d, W, H, pw, ph, bg);
+  CHECK(rr.color == ref.color && rr.alpha == ref.alpha && rr.depth == ref.depth && rr.final_t == ref.final_t &&
+        rr.contrib == ref.contrib && rr.term == ref.term);
+  for (auto v : splatsim::kAllVariants) {
+    const auto run = splatsim::run_kernel(v, b, g2d, W, H, pw, ph, bg);
+    const auto o = oracle::render(static_cast<oracle::Variant>(int(v)), ob, og2d.data(), og2d.size(), W, H, pw, ph, obg);
+    CHECK(run.output.contrib == o.contrib && run.output.term == o.term && run.output.final_t == o.final_t);
+    double err = 0;
+    for (size_t i = 0; i < o.color.size(); ++i) err = std::max(err, std::abs(double(o.color[i]) - run.output.color[i]));
+    CHECK(err <= 1e-6);
+    const auto dev = splatsim::compare_outputs(rr, run.output);
+    CHECK(dev.contrib_equal && dev.max_rel <= 1e-5);
+    // trace shape (src/kernels.cpp:159-266): one task per tile, FG: ceil(pw*ph/4) per tile
+    const size_t expect_tasks = size_t(b.tile_count()) * (v == splatsim::KernelVariant::FineGrainedCombined ? 32 : 1);
+    CHECK(run.trace.tasks.size() == expect_tasks);
+    CHECK(splatsim::make_task_specs(v, W, H, pw, ph).size() == expect_tasks);
+  }
+
+  // exceptions as the reference throws them
+  bool threw = false;
+  try {
+    splatsim::run_kernel(splatsim::KernelVariant::Naive, b, g2d, W + 64, H, pw, ph, bg);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+  splatsim::SelectionState s;
+  s = splatsim::checkpoint(s, 0, 2.0, 1.0);
+  CHECK(s.switched && s.current == splatsim::KernelVariant::SharedMemOpt);
+  threw = false;
+  try {
+    splatsim::checkpoint(s, 1000, 1.0, 2.0);
+  } catch (const std::logic_error&) {
+    threw = true;
+  }
+  CHECK(threw);
+  threw = false;
+  try {
+    splatsim::checkpoint(splatsim::SelectionState{}, 7, 1.0, 2.0);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+  splatsim::SelectionState live = splatsim::checkpoint(splatsim::SelectionState{}, 0, b, g2d, W, H, pw, ph);
+  CHECK(live.history.size() == 1 && live.history[0].t_balanced > 0 && live.history[0].t_baseline > 0);
+
+  // 960x540 @ 16x8: 4080 tiles, 130,560 fine tasks
+  CHECK(splatsim::make_task_specs(splatsim::KernelVariant::FineGrainedCombined, 960, 540, 16, 8).size() == 130560);
+  CHECK(splatsim::variant_name(splatsim::KernelVariant::GaussianWise) == "GaussianWise");
+  CHECK(splatsim::variant_from_name("SharedMemOpt") == splatsim::KernelVariant::SharedMemOpt);
+  CHECK(!splatsim::variant_from_name("nope"));
+
+  // fast mode stays within the north-star tolerance on matched pixels
+  splatsim::set_alpha_mode(splatsim::AlphaMode::Fast);
+  const auto fast = splatsim::run_kernel(splatsim::KernelVariant::FineGrainedCombined, b, g2d, W, H, pw, ph, bg);
+  splatsim::set_alpha_mode(splatsim::AlphaMode::Exact);
+  size_t mism = 0;
+  double ferr = 0;
+  for (size_t i = 0; i < ref.contrib.size(); ++i) {
+    if (fast.output.contrib[i] != ref.contrib[i] || fast.output.term[i] != ref.term[i]) {
+      ++mism;
+      continue;
+    }
+    for (int c = 0; c < 3; ++c) ferr = std::max(ferr, std::abs(double(fast.output.color[3 * i + c]) - ref.color[3 * i + c]));
+  }
+  CHECK(ferr <= 1e-4);
+  CHECK(double(mism) / double(ref.contrib.size()) < 2e-3);
+
+  std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
+  return failures ? 1 : 0;
+}
