@@ -223,8 +223,8 @@ def config_desc(cfg, W, H, n, pw, ph) -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--alpha", default="exact", choices=["exact", "fast"])
@@ -268,6 +268,8 @@ def main():
         v = (rank + world * i) % N_VIEWS
         return pipe.forward(g3d_dev, n, cams[v], variant=variant)
 
+    clk = ClockSampler(local)
+    clk.start()  # sampling spans warm-up + timed region (the timed region alone is < 1 s)
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
@@ -275,8 +277,6 @@ def main():
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     used = {}
-    clk = ClockSampler(local)
-    clk.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -335,6 +335,18 @@ def main():
 def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, pipe, W, H, pw, ph, n, mode, dev, world) -> dict:
     res = {}
     peaks = load_peaks()
+    # warm per-stage breakdown of the full forward (events between stages)
+    stage_ms = {}
+    reps = 20
+    for i in range(reps):
+        evs = []
+        pipe.forward(g3d_dev, n, cams[i % N_VIEWS], variant=("auto" if args.variant == "auto"
+                                                              else api.variant_from_name(args.variant)),
+                     stage_events=evs)
+        torch.cuda.synchronize()
+        for (_, a), (name, b) in zip(evs[:-1], evs[1:]):
+            stage_ms[name] = stage_ms.get(name, 0.0) + a.elapsed_time(b) / reps
+    res["stage_ms"] = {k: round(v, 4) for k, v in stage_ms.items()}
     cam_id = api.camera(np.eye(4, dtype=np.float32), cams[0].focal, W, H)  # C2 identity view
     frame, v_auto = pipe.forward(g3d_dev, n, cam_id, variant="auto")
     s, b, st = pipe.splats, pipe.last_binning, pipe.last_stats

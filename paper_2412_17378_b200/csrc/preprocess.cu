@@ -107,9 +107,12 @@ __device__ __forceinline__ bool project_one(const bs_gaussian3d& g, const CamDev
 // power < cut  =>  opacity * expf(power) < 1/255 (1% margin in the exponent,
 // far above every rounding error), so the exact exp can be skipped without
 // changing a single decision.  opacity <= 0 -> everything skips.
+// The cut is also clamped at glibc expf's underflow bound (x < -0x1.9fe368p6
+// -> expf(x) = 0 -> alpha 0 -> skip), so the render path only ever evaluates
+// the exact exp on [-103.97, 0] and needs no range guard.
 __device__ __forceinline__ float power_cut_of(float opacity) {
   if (!(opacity > 0.0f)) return INFINITY;
-  return logf(1.0f / (255.0f * opacity)) - 0.01f;
+  return fmaxf(logf(1.0f / (255.0f * opacity)) - 0.01f, -0x1.9fe368p6f);
 }
 
 __device__ __forceinline__ void load_g3d(const bs_gaussian3d* __restrict__ src, int64_t i, bs_gaussian3d& g) {

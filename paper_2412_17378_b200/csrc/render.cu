@@ -10,9 +10,11 @@
 //                      pixel with its 32 lanes on 32 consecutive list entries,
 //                      prefix product of (1-alpha) by shfl_up doubling, lane-31
 //                      carry                                  (paper Alg. 2/6)
-//   FineGrainedCombined persistent CTAs (4 warps = 4 pixels) claim 4-pixel
+//   FineGrainedCombined persistent CTAs whose warps each claim 8x4-pixel
 //                      sub-tile tasks from an atomicAdd queue ordered by tile
-//                      list length, longest first (LPT)          (paper Alg. 3)
+//                      list length, longest first (LPT); sub-tile culling,
+//                      pixel-wise batches, Gaussian-wise stragglers
+//                                          (paper Alg. 3, re-cut for B200)
 //
 // Semantics: pixel-wise variants == render_reference
 // (src/blend.cpp:55-107); Gaussian-wise variants == render_gaussianwise
@@ -71,7 +73,7 @@ __device__ __forceinline__ bool eval_step(const float4 a, const float4 c, float 
   if (power > 0.0f) return false;   // alpha forced to 0 -> skipped
   float e;
   if (MODE == BS_ALPHA_EXACT) {
-    e = glibc_expf(power, tab);
+    e = glibc_expf_inrange(power, tab);  // power in [power_cut, 0], power_cut >= -103.97
   } else {
     float p2 = power * 1.4426950408889634f;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(p2));
@@ -93,6 +95,14 @@ struct Accum<BS_ALPHA_EXACT> {
     g = __dadd_rn(g, __dmul_rn((double)col.y, w));
     b = __dadd_rn(b, __dmul_rn((double)col.z, w));
     d = __dadd_rn(d, __dmul_rn((double)dep, w));
+  }
+  // colour/depth already widened to double (rg = (r, g), bd = (b, depth))
+  __device__ __forceinline__ void add_wide(float alpha, float t, double2 rg, double2 bd) {
+    const double w = __dmul_rn((double)alpha, (double)t);
+    r = __dadd_rn(r, __dmul_rn(rg.x, w));
+    g = __dadd_rn(g, __dmul_rn(rg.y, w));
+    b = __dadd_rn(b, __dmul_rn(bd.x, w));
+    d = __dadd_rn(d, __dmul_rn(bd.y, w));
   }
   __device__ __forceinline__ void merge(const Accum& o) {
     r = __dadd_rn(r, o.r);
@@ -131,6 +141,7 @@ struct Accum<BS_ALPHA_FAST> {
     b = fmaf(col.z, w, b);
     d = fmaf(dep, w, d);
   }
+  __device__ __forceinline__ void add_wide(float, float, double2, double2) {}
   __device__ __forceinline__ void merge(const Accum& o) {
     r += o.r;
     g += o.g;
@@ -503,7 +514,13 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
       const int pos = __popc(km & lanemask_lt());
       s[0][pos] = pa;
       s[1][pos] = pc;
-      s[2][pos] = pr;
+      if (MODE == BS_ALPHA_EXACT) {
+        // colour/depth widened to double once per staged entry (not per commit)
+        reinterpret_cast<double2*>(s[2])[pos] = make_double2((double)pr.x, (double)pr.y);
+        reinterpret_cast<double2*>(s[3])[pos] = make_double2((double)pr.z, (double)pc.w);
+      } else {
+        s[2][pos] = pr;
+      }
       s_k[pos] = (int)(base - start) + lane + 1;  // 1-based list position (term)
     }
     __syncwarp();
@@ -522,7 +539,10 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
         term = s_k[j];
         continue;
       }
-      acc.add(alpha, t, s[2][j], c.w);
+      if (MODE == BS_ALPHA_EXACT)
+        acc.add_wide(alpha, t, reinterpret_cast<const double2*>(s[2])[j], reinterpret_cast<const double2*>(s[3])[j]);
+      else
+        acc.add(alpha, t, s[2][j], c.w);
       t = tmp;
       ++contrib;
     }
@@ -534,7 +554,7 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
 
 template <int MODE>
 __global__ void __launch_bounds__(kFineThreads) k_render_fine(RArgs A, int subs, int total_tasks) {
-  __shared__ float4 s_rec[kFineWarps][3][32];
+  __shared__ float4 s_rec[kFineWarps][4][32];
   __shared__ int s_k[kFineWarps][32];
   __shared__ unsigned long long s_tab[32];
   load_tab(s_tab);
