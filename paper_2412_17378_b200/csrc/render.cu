@@ -30,6 +30,7 @@
 // kernel is bound by FP32/MUFU/FP64 issue for long lists and by L2 for short
 // ones.
 #include <math.h>
+#include <stdlib.h>
 
 #include "bs_common.cuh"
 #include "exact_expf.cuh"
@@ -331,15 +332,17 @@ __device__ __forceinline__ int gw_group(bool ns, float alpha, float4 col, float 
 }
 
 // ---------------------------------------------------------------------------
-// Gaussian-wise: kFgWarps warps, warp w blends pixel `pix[w]` of `tile`; the
-// CTA stages the list in 128-entry chunks shared by the 4 warps; each warp
-// walks a chunk in 32-wide groups.
-template <int MODE>
+// Gaussian-wise task: WARPS warps, warp w blends pixel sub*WARPS + w of
+// `tile`; the CTA stages the list in 32*WARPS-entry chunks shared by the
+// warps; each warp walks a chunk in 32-wide groups.  SERIAL_W selects the
+// colour weights (see gw_group).
+template <int MODE, int WARPS, bool SERIAL_W>
 __device__ __forceinline__ void gaussianwise_task(const RArgs& A, int tile, int sub, float4* s_xyab, float4* s_cop,
                                                   float4* s_rgb, const unsigned long long* s_tab) {
+  constexpr int CH = WARPS * 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tx = tile % A.cols, ty = tile / A.cols;
-  const int local = sub * kFgWarps + warp;
+  const int local = sub * WARPS + warp;
   const int lx = local % A.pw, ly = local / A.pw;
   const int px = tx * A.pw + lx, py = ty * A.ph + ly;
   const bool inside = local < A.pw * A.ph && px < A.W && py < A.H;
@@ -351,7 +354,7 @@ __device__ __forceinline__ void gaussianwise_task(const RArgs& A, int tile, int 
   int contrib = 0, term = 0;
   Accum<MODE> acc;
 
-  for (uint32_t base = start; base < end; base += kFgThreads) {
+  for (uint32_t base = start; base < end; base += CH) {
     if (__syncthreads_count(!done) == 0) break;
     const uint32_t k = base + tid;
     if (k < end) {
@@ -362,7 +365,7 @@ __device__ __forceinline__ void gaussianwise_task(const RArgs& A, int tile, int 
     }
     __syncthreads();
     if (done) continue;
-    const uint32_t cnt = min((uint32_t)kFgThreads, end - base);
+    const uint32_t cnt = min((uint32_t)CH, end - base);
     for (uint32_t g0 = 0; g0 < cnt; g0 += 32) {
       const uint32_t j = g0 + lane;
       const bool active = j < cnt;
@@ -374,7 +377,7 @@ __device__ __forceinline__ void gaussianwise_task(const RArgs& A, int tile, int 
         ns = eval_step<MODE>(s_xyab[j], c, sx, sy, s_tab, alpha);
       }
       const float4 col = ns ? s_rgb[j] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const int stop = gw_group<MODE, false>(ns, alpha, col, c.w, t, contrib, acc, lane);
+      const int stop = gw_group<MODE, SERIAL_W>(ns, alpha, col, c.w, t, contrib, acc, lane);
       if (stop < 32) {
         term = (int)(base - start + g0) + stop + 1;
         done = true;
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(kFgThreads) k_render_gaussianwise(RArgs A) {
   const int subs = (A.pw * A.ph + kFgWarps - 1) / kFgWarps;
   for (int s = 0; s < subs; ++s) {
     __syncthreads();
-    gaussianwise_task<MODE>(A, tile, s, s_xyab, s_cop, s_rgb, s_tab);
+    gaussianwise_task<MODE, kFgWarps, false>(A, tile, s, s_xyab, s_cop, s_rgb, s_tab);
   }
 }
 
@@ -420,6 +423,7 @@ __global__ void __launch_bounds__(kFgThreads) k_render_gaussianwise(RArgs A) {
 constexpr int kFineWarps = 8;
 constexpr int kFineThreads = kFineWarps * 32;
 constexpr int kStragglers = 8;
+constexpr int kFineHeavyListDefault = 16384;
 constexpr int kStragglerMinRemain = 64;
 
 __device__ __forceinline__ void load_rec(const RArgs& A, uint32_t k, float4& a, float4& c, float4& r) {
@@ -552,22 +556,55 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
   if (inside) acc.finish(A, (size_t)py * A.W + px, t, contrib, term);
 }
 
+// Two task phases over the LPT tile order:
+//   heavy tiles (list length >= heavy_len, a prefix of the LPT order) are cut
+//     into kFineWarps-pixel CTA tasks: one pixel per warp, Gaussian-wise over
+//     CTA-staged chunks (paper Alg. 3's granularity, where the tail lives);
+//   the remaining tiles are cut into 8x4-pixel warp tasks (warp_task).
+// queue[0] counts CTA tasks, queue[1] warp tasks.
 template <int MODE>
-__global__ void __launch_bounds__(kFineThreads) k_render_fine(RArgs A, int subs, int total_tasks) {
+__global__ void __launch_bounds__(kFineThreads) k_render_fine(RArgs A, int subs, int heavy_len) {
   __shared__ float4 s_rec[kFineWarps][4][32];
   __shared__ int s_k[kFineWarps][32];
   __shared__ unsigned long long s_tab[32];
+  __shared__ int s_task, s_nheavy;
   load_tab(s_tab);
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    int lo = 0, hi = A.task_order ? A.T : 0;  // first LPT position with length < heavy_len
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const uint32_t t = A.task_order[mid];
+      if ((int64_t)(A.ranges[2 * t + 1] - A.ranges[2 * t]) >= (int64_t)heavy_len) lo = mid + 1;
+      else hi = mid;
+    }
+    s_nheavy = lo;
+  }
+  __syncthreads();
+  const int n_heavy = s_nheavy;
+  const int heavy_per_tile = (A.pw * A.ph + kFineWarps - 1) / kFineWarps;
+  const int heavy_tasks = n_heavy * heavy_per_tile;
+  float4* flat = &s_rec[0][0][0];  // 1024 float4: three 256-entry chunk arrays
+  for (;;) {
+    if (threadIdx.x == 0) s_task = (int)atomicAdd(A.queue, 1u);
+    __syncthreads();
+    const int task = s_task;
+    __syncthreads();
+    if (task >= heavy_tasks) break;
+    const int q = task / heavy_per_tile;
+    gaussianwise_task<MODE, kFineWarps, true>(A, (int)A.task_order[q], task - q * heavy_per_tile, flat,
+                                              flat + kFineThreads, flat + 2 * kFineThreads, s_tab);
+    __syncthreads();
+  }
+  const int light_tasks = (A.T - n_heavy) * subs;
   for (;;) {
     int task = 0;
-    if (lane == 0) task = (int)atomicAdd(A.queue, 1u);
+    if (lane == 0) task = (int)atomicAdd(A.queue + 1, 1u);
     task = __shfl_sync(kFull, task, 0);
-    if (task >= total_tasks) return;
-    const int q = task / subs;
+    if (task >= light_tasks) return;
+    const int q = n_heavy + task / subs;
     const int tile = A.task_order ? (int)A.task_order[q] : q;
-    warp_task<MODE>(A, tile, task - q * subs, s_rec[warp], s_k[warp], s_tab);
+    warp_task<MODE>(A, tile, task % subs, s_rec[warp], s_k[warp], s_tab);
   }
 }
 
@@ -593,6 +630,14 @@ __global__ void k_frame_work(const int32_t* __restrict__ term, const int32_t* __
     atomicAdd(out + 0, e);
     atomicAdd(out + 1, c);
   }
+}
+
+// List length from which FineGrainedCombined cuts a tile into per-pixel
+// Gaussian-wise CTA tasks (BS_FINE_HEAVY_LIST overrides; 0 = every tile).
+static int fine_heavy_len() {
+  const char* e = getenv("BS_FINE_HEAVY_LIST");
+  const int v = e ? atoi(e) : kFineHeavyListDefault;
+  return v < 0 ? 0 : v;
 }
 
 template <int MODE>
@@ -641,7 +686,7 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
       if (total > 0x7fffffff) return BS_ERR_UNSUPPORTED;
       const int64_t ctas = (total + kFineWarps - 1) / kFineWarps;
       const int grid = (int)max((int64_t)1, min(ctas, (int64_t)sms * max(1, per_sm)));
-      k_render_fine<MODE><<<grid, kFineThreads, 0, st>>>(A, subs, (int)total);
+      k_render_fine<MODE><<<grid, kFineThreads, 0, st>>>(A, subs, fine_heavy_len());
       break;
     }
     default:
@@ -685,7 +730,7 @@ extern "C" int bs_render_forward(int variant, int alpha_mode, bs_splats g, const
   A.contrib = out.contrib; A.term = out.term;
   A.queue = reinterpret_cast<unsigned int*>(ws);
   if (variant == BS_DYNAMIC_BLOCKS || variant == BS_FINE_GRAINED_COMBINED)
-    BS_CUDA_TRY(cudaMemsetAsync(ws, 0, sizeof(unsigned int), st));
+    BS_CUDA_TRY(cudaMemsetAsync(ws, 0, 2 * sizeof(unsigned int), st));
   const int block_pixels = pw * ph;
   return alpha_mode == BS_ALPHA_EXACT ? launch_variant<BS_ALPHA_EXACT>(variant, A, block_pixels, st)
                                       : launch_variant<BS_ALPHA_FAST>(variant, A, block_pixels, st);

@@ -263,3 +263,26 @@ def test_golden_digests_on_gpu():
         f2 = api.render_forward(2, s, b, W, H, pw, ph, bg, N.ALPHA_EXACT, st.task_order).to_numpy()
         for k in ("alpha", "final_t", "contrib", "term"):
             assert O.fnv1a64(f2[k]) == fz["render_gaussianwise"][k], (name, k)
+
+
+@pytest.mark.parametrize("heavy", ["0", "64"])
+def test_fine_heavy_tile_path(heavy, monkeypatch):
+    """FineGrainedCombined's per-pixel Gaussian-wise CTA tasks for heavy tiles
+    (forced on with a low BS_FINE_HEAVY_LIST) keep the exact semantics."""
+    monkeypatch.setenv("BS_FINE_HEAVY_LIST", heavy)
+    W, H, pw, ph = 192, 128, 16, 16
+    g3d, cam = scene(8000, W, H, 192.0, bgfrac=0.12)
+    g2d = O.project_all(g3d, cam)
+    bg = (0.1, 0.2, 0.3)
+    ref = _oracle_render(0, g2d, W, H, pw, ph, bg)
+    for mode in (N.ALPHA_EXACT, N.ALPHA_FAST):
+        got, _ = _gpu_render(3, g2d, W, H, pw, ph, bg, mode)
+        if mode == N.ALPHA_EXACT:
+            assert np.array_equal(got["contrib"], ref["contrib"]) and np.array_equal(got["term"], ref["term"])
+            assert np.array_equal(got["final_t"].view(np.uint32), ref["final_t"].view(np.uint32))
+            assert np.max(np.abs(got["color"] - ref["color"])) <= 1e-6
+        else:
+            match = (got["contrib"] == ref["contrib"]) & (got["term"] == ref["term"])
+            assert 1.0 - match.mean() < 2e-3
+            err = np.abs(got["color"] - ref["color"]).reshape(-1, 3).max(axis=1)
+            assert err[match].max() <= 1e-4

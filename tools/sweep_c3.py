@@ -40,9 +40,9 @@ def time_render(v, m, s, b, st, frame, W, H, reps=5):
     return float(np.median([a.elapsed_time(e) for a, e in ev]))
 
 
-def point(bgf, sigma, oscale, n=1_000_000, W=1920, H=1080, f=1000.0):
+def point(bgf, sigma, oscale, n=1_000_000, W=1920, H=1080, f=1000.0, n_clusters=4):
     cam = api.camera(None, (f, f), W, H)
-    g3d = api.gen_clustered_scene(n, cam, cluster_sigma=sigma, background_fraction=bgf)
+    g3d = api.gen_clustered_scene(n, cam, n_clusters=n_clusters, cluster_sigma=sigma, background_fraction=bgf)
     g3d["opacity"] *= oscale
     pipe = api.Pipeline(W, H, 16, 16, "cuda", N.ALPHA_EXACT)
     frame, _ = pipe.forward(api.g3d_to_device(g3d), n, cam, variant=0)
@@ -57,7 +57,7 @@ def point(bgf, sigma, oscale, n=1_000_000, W=1920, H=1080, f=1000.0):
     pad = np.zeros((rows * 16, cols * 16), np.int64)
     pad[:H, :W] = cons
     tile_work = pad.reshape(rows, 16, cols, 16).sum(axis=(1, 3))
-    out = {"bgf": bgf, "sigma": sigma, "opacity_scale": oscale, "K": b.k, "E": E, "C": C,
+    out = {"n": n, "W": W, "H": H, "n_clusters": n_clusters, "bgf": bgf, "sigma": sigma, "opacity_scale": oscale, "K": b.k, "E": E, "C": C,
            "list_max": int(lens.max()), "list_mean": float(lens.mean()),
            "tile_work_max": int(tile_work.max()), "tile_work_mean": float(tile_work.mean()),
            "work_imbalance": float(tile_work.max() / max(1.0, tile_work.mean())),
@@ -75,19 +75,25 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "c3_sweep.jsonl"))
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--extreme", action="store_true", help="single-cluster extremes + C1")
     a = ap.parse_args()
     pts = [(g, s, 1.0) for g, s in GEOM] + [(GEOM[-1][0], GEOM[-1][1], o) for o in OPACITY[1:]]
     if a.quick:
         pts = pts[:2] + pts[-2:]
+    extra = []
+    if a.extreme:
+        pts = []
+        extra = [dict(bgf=0.05, sigma=0.01, oscale=o, n_clusters=1) for o in (1.0, 0.25, 0.05, 0.02)]
+        extra += [dict(bgf=1.0, sigma=0.035, oscale=1.0, n=10_000, W=256, H=256, f=256.0)]
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     with open(a.out, "w") as fh:
-        for bgf, sig, osc in pts:
-            r = point(bgf, sig, osc)
+        for kw in [dict(bgf=g, sigma=s_, oscale=o) for g, s_, o in pts] + extra:
+            r = point(**kw)
             fh.write(json.dumps(r) + "\n")
             fh.flush()
-            print(json.dumps({k: r[k] for k in ("bgf", "sigma", "opacity_scale", "work_imbalance", "selector",
-                                                 "regret_exact", "fg_vs_naive_exact", "fg_vs_naive_fast")}),
-                  flush=True)
+            print(json.dumps({k: r[k] for k in ("n", "n_clusters", "bgf", "sigma", "opacity_scale", "work_imbalance",
+                                                 "selector", "regret_exact", "fg_vs_naive_exact", "fg_vs_naive_fast",
+                                                 "ms_exact")}), flush=True)
 
 
 if __name__ == "__main__":
