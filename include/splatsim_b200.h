@@ -184,7 +184,8 @@ int bs_tile_stats(const uint32_t* tile_ranges, int32_t tiles, bs_tile_histogram*
  * Output equals render_reference (pixel-wise variants) or
  * render_gaussianwise (GaussianWise / FineGrainedCombined).
  * Workspace holds the dynamic-queue counter (reset by the call). */
-size_t bs_render_workspace_bytes(void);
+/* queue counters + the FineGrainedCombined tail hand-off buffer (48 B/pixel) */
+size_t bs_render_workspace_bytes(int32_t width, int32_t height);
 int bs_render_forward(int variant, int alpha_mode, bs_splats g, const uint32_t* point_list,
                       const uint32_t* tile_ranges, const uint32_t* task_order, int32_t width, int32_t height,
                       int32_t pw, int32_t ph, const float bg[3], bs_frame_out out, void* ws, size_t ws_bytes,

@@ -256,8 +256,9 @@ def render_forward(variant: int, s: DeviceSplats, b: DeviceBinning, width: int, 
         raise ValueError("run_kernel: binning grid does not match image dims")
     out = out or DeviceFrame.empty(width, height, dev)
     key = str(dev)
-    if key not in _render_ws:
-        _render_ws[key] = _ws(N.lib().bs_render_workspace_bytes(), dev)
+    need = N.lib().bs_render_workspace_bytes(width, height)
+    if key not in _render_ws or _render_ws[key].numel() < need:
+        _render_ws[key] = _ws(need, dev)
     ws = _render_ws[key]
     bgc = (C.c_float * 3)(*[float(x) for x in bg])
     N.call("bs_render_forward", int(variant), int(alpha_mode), s.c(), _ptr(b.point_list) if b.k else None,

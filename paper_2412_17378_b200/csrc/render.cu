@@ -58,7 +58,12 @@ struct RArgs {
   float* __restrict__ final_t;
   int32_t* __restrict__ contrib;
   int32_t* __restrict__ term;
-  unsigned int* queue;
+  unsigned int* queue;      // [0] warp-task ticket, [1] pixels parked, [2] parked-task ticket, [3] tasks parked
+  struct Donation* donate;  // FineGrainedCombined tail hand-off (see k_render_donated)
+  uint2* donated_tasks;     // (first Donation, count) per parked warp task
+  int total_tasks;
+  int donate_after;       // list entries a task walks before it may hand off
+  int donate_min_remain;  // ... and only if this many entries remain
 };
 
 // R1 eval_alpha + the power>0 arm + skip rule (src/blend.cpp:8-21, 90).
@@ -105,6 +110,8 @@ struct Accum<BS_ALPHA_EXACT> {
     b = __dadd_rn(b, __dmul_rn(bd.x, w));
     d = __dadd_rn(d, __dmul_rn(bd.y, w));
   }
+  __device__ __forceinline__ void store(double* o) const { o[0] = r; o[1] = g; o[2] = b; o[3] = d; }
+  __device__ __forceinline__ void load(const double* o) { r = o[0]; g = o[1]; b = o[2]; d = o[3]; }
   __device__ __forceinline__ void merge(const Accum& o) {
     r = __dadd_rn(r, o.r);
     g = __dadd_rn(g, o.g);
@@ -143,6 +150,10 @@ struct Accum<BS_ALPHA_FAST> {
     d = fmaf(dep, w, d);
   }
   __device__ __forceinline__ void add_wide(float, float, double2, double2) {}
+  __device__ __forceinline__ void store(double* o) const { o[0] = r; o[1] = g; o[2] = b; o[3] = d; }
+  __device__ __forceinline__ void load(const double* o) {
+    r = (float)o[0]; g = (float)o[1]; b = (float)o[2]; d = (float)o[3];
+  }
   __device__ __forceinline__ void merge(const Accum& o) {
     r += o.r;
     g += o.g;
@@ -423,7 +434,8 @@ __global__ void __launch_bounds__(kFgThreads) k_render_gaussianwise(RArgs A) {
 constexpr int kFineWarps = 8;
 constexpr int kFineThreads = kFineWarps * 32;
 constexpr int kStragglers = 8;
-constexpr int kFineHeavyListDefault = 16384;
+constexpr int kDonateAfter = 512;       // list entries a task walks before it may hand off
+constexpr int kDonateMinRemain = 1024;  // ... and only if this many entries remain
 constexpr int kStragglerMinRemain = 64;
 
 __device__ __forceinline__ void load_rec(const RArgs& A, uint32_t k, float4& a, float4& c, float4& r) {
@@ -450,6 +462,46 @@ __device__ __forceinline__ bool cull_subtile(const float4 a, const float4 c, flo
   return (a.x + ex < rx0) || (a.x - ex > rx1) || (a.y + ey < ry0) || (a.y - ey > ry1);
 }
 
+struct Donation {
+  uint32_t pixel, start, from, end;
+  float t;
+  int32_t contrib;
+  double acc[4];
+};
+
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Gaussian-wise continuation of one pixel (sample point psx, psy; current
+// transmittance pt) over list entries [from, end) of a tile starting at
+// `start`: 32 lanes on 32 consecutive entries, next group prefetched, serial-
+// exact decisions and render_reference weights (gw_group<MODE, true>).  The
+// colour partials come back warp-reduced in `part`.
+template <int MODE>
+__device__ __forceinline__ void gw_finish_pixel(const RArgs& A, uint32_t start, uint32_t from, uint32_t end,
+                                                float psx, float psy, const unsigned long long* s_tab, float& pt,
+                                                int& pcnt, int& ptrm, Accum<MODE>& part) {
+  const int lane = threadIdx.x & 31;
+  float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nc = na, nr = na;
+  if (from + lane < end) load_rec(A, from + lane, na, nc, nr);
+  for (uint32_t g = from; g < end; g += 32) {
+    const bool active = g + lane < end;
+    const float4 a = na, c = nc, r = nr;
+    if (g + 32 + lane < end) load_rec(A, g + 32 + lane, na, nc, nr);  // prefetch next group
+    float alpha = 0.0f;
+    const bool ns = active && eval_step<MODE>(a, c, psx, psy, s_tab, alpha);
+    const int stop = gw_group<MODE, true>(ns, alpha, r, c.w, pt, pcnt, part, lane);
+    if (stop < 32) {
+      ptrm = (int)(g - start) + stop + 1;
+      break;
+    }
+  }
+  part.warp_sum();
+}
+
 template <int MODE>
 __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, float4 (*s)[32], int* s_k,
                                           const unsigned long long* s_tab) {
@@ -465,10 +517,11 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
   const float rx0 = (float)ox + 0.5f, rx1 = (float)ox + 7.5f, ry0 = (float)oy + 0.5f, ry1 = (float)oy + 3.5f;
   const uint32_t start = A.ranges[2 * tile], end = A.ranges[2 * tile + 1];
 
-  bool done = !inside;
+  bool done = !inside, donated = false, donate_now = false;
   float t = 1.0f;
   int contrib = 0, term = 0;
   Accum<MODE> acc;
+  unsigned qpoll = 0;
 
   uint32_t base = start;
   float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pc = pa, pr = pa;
@@ -486,21 +539,7 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
         float pt = __shfl_sync(kFull, t, p);
         int pcnt = 0, ptrm = 0;
         Accum<MODE> part;
-        float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nc = na, nr = na;
-        if (base + lane < end) load_rec(A, base + lane, na, nc, nr);
-        for (uint32_t g = base; g < end; g += 32) {
-          const bool active = g + lane < end;
-          const float4 a = na, c = nc, r = nr;
-          if (g + 32 + lane < end) load_rec(A, g + 32 + lane, na, nc, nr);  // prefetch next group
-          float alpha = 0.0f;
-          const bool ns = active && eval_step<MODE>(a, c, psx, psy, s_tab, alpha);
-          const int stop = gw_group<MODE, true>(ns, alpha, r, c.w, pt, pcnt, part, lane);
-          if (stop < 32) {
-            ptrm = (int)(g - start) + stop + 1;
-            break;
-          }
-        }
-        part.warp_sum();
+        gw_finish_pixel<MODE>(A, start, base, end, psx, psy, s_tab, pt, pcnt, ptrm, part);
         if (lane == p) {
           acc.merge(part);
           t = pt;
@@ -508,6 +547,31 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
           term = ptrm;
           done = true;
         }
+      }
+      break;
+    }
+    if (donate_now && __popc(live) > kStragglers && end - base >= (uint32_t)A.donate_min_remain) {
+      // ---- tail hand-off: the global queue is drained and this task is
+      // still long; park every live pixel's blend state for k_render_donated
+      unsigned slot0 = 0;
+      if (lane == 0) {
+        const unsigned nl = (unsigned)__popc(live), units = (nl + kFineWarps - 1) / kFineWarps;
+        slot0 = atomicAdd(A.queue + 1, nl);
+        const unsigned u0 = atomicAdd(A.queue + 3, units);
+        for (unsigned u = 0; u < units; ++u)  // one CTA unit = up to kFineWarps pixels
+          A.donated_tasks[u0 + u] = make_uint2(slot0 + u * kFineWarps, min((unsigned)kFineWarps, nl - u * kFineWarps));
+      }
+      slot0 = __shfl_sync(kFull, slot0, 0);
+      if (!done) {
+        Donation& d = A.donate[slot0 + __popc(live & lanemask_lt())];
+        d.pixel = (uint32_t)py * (uint32_t)A.W + (uint32_t)px;
+        d.start = start;
+        d.from = base;
+        d.end = end;
+        d.t = t;
+        d.contrib = contrib;
+        acc.store(d.acc);
+        donated = true;
       }
       break;
     }
@@ -530,6 +594,13 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
     __syncwarp();
     const uint32_t nb = base + 32;
     if (nb + lane < end) load_rec(A, nb + lane, pa, pc, pr);
+    // queue poll every 8th batch; the value is consumed 8 batches later, so
+    // the L2 round trip never stalls the blend loop
+    const bool poll_point = A.donate && ((nb - start) & (8u * 32u - 1u)) == 0;
+    if (poll_point) {
+      donate_now = __shfl_sync(kFull, qpoll, 0) >= (unsigned)A.total_tasks && nb - start >= (uint32_t)A.donate_after;
+      if (lane == 0) qpoll = ld_relaxed_u32(A.queue);
+    }
     const int cnt = __popc(km);
 #pragma unroll 2
     for (int j = 0; j < cnt; ++j) {
@@ -553,58 +624,92 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
     __syncwarp();
     base = nb;
   }
-  if (inside) acc.finish(A, (size_t)py * A.W + px, t, contrib, term);
+  if (inside && !donated) acc.finish(A, (size_t)py * A.W + px, t, contrib, term);
 }
 
-// Two task phases over the LPT tile order:
-//   heavy tiles (list length >= heavy_len, a prefix of the LPT order) are cut
-//     into kFineWarps-pixel CTA tasks: one pixel per warp, Gaussian-wise over
-//     CTA-staged chunks (paper Alg. 3's granularity, where the tail lives);
-//   the remaining tiles are cut into 8x4-pixel warp tasks (warp_task).
-// queue[0] counts CTA tasks, queue[1] warp tasks.
 template <int MODE>
-__global__ void __launch_bounds__(kFineThreads) k_render_fine(RArgs A, int subs, int heavy_len) {
+__global__ void __launch_bounds__(kFineThreads) k_render_fine(RArgs A, int subs) {
   __shared__ float4 s_rec[kFineWarps][4][32];
   __shared__ int s_k[kFineWarps][32];
   __shared__ unsigned long long s_tab[32];
-  __shared__ int s_task, s_nheavy;
   load_tab(s_tab);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    int lo = 0, hi = A.task_order ? A.T : 0;  // first LPT position with length < heavy_len
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      const uint32_t t = A.task_order[mid];
-      if ((int64_t)(A.ranges[2 * t + 1] - A.ranges[2 * t]) >= (int64_t)heavy_len) lo = mid + 1;
-      else hi = mid;
-    }
-    s_nheavy = lo;
-  }
   __syncthreads();
-  const int n_heavy = s_nheavy;
-  const int heavy_per_tile = (A.pw * A.ph + kFineWarps - 1) / kFineWarps;
-  const int heavy_tasks = n_heavy * heavy_per_tile;
-  float4* flat = &s_rec[0][0][0];  // 1024 float4: three 256-entry chunk arrays
-  for (;;) {
-    if (threadIdx.x == 0) s_task = (int)atomicAdd(A.queue, 1u);
-    __syncthreads();
-    const int task = s_task;
-    __syncthreads();
-    if (task >= heavy_tasks) break;
-    const int q = task / heavy_per_tile;
-    gaussianwise_task<MODE, kFineWarps, true>(A, (int)A.task_order[q], task - q * heavy_per_tile, flat,
-                                              flat + kFineThreads, flat + 2 * kFineThreads, s_tab);
-    __syncthreads();
-  }
-  const int light_tasks = (A.T - n_heavy) * subs;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (;;) {
     int task = 0;
-    if (lane == 0) task = (int)atomicAdd(A.queue + 1, 1u);
+    if (lane == 0) task = (int)atomicAdd(A.queue, 1u);
     task = __shfl_sync(kFull, task, 0);
-    if (task >= light_tasks) return;
-    const int q = n_heavy + task / subs;
+    if (task >= A.total_tasks) return;
+    const int q = task / subs;
     const int tile = A.task_order ? (int)A.task_order[q] : q;
-    warp_task<MODE>(A, tile, task % subs, s_rec[warp], s_k[warp], s_tab);
+    warp_task<MODE>(A, tile, task - q * subs, s_rec[warp], s_k[warp], s_tab);
+  }
+}
+
+// Second launch: the warp tasks parked at the tail (their warp saw the queue
+// drained with a long list left) are finished by CTAs: each parked task is
+// cut into units of up to kFineWarps pixels, one unit per CTA, one pixel per
+// warp,
+// Gaussian-wise (gw_group, serial-exact) over 256-entry chunks staged once
+// for all 8 warps — the tail of the heaviest tiles is spread over all SMs.
+template <int MODE>
+__global__ void __launch_bounds__(kFineThreads) k_render_donated(RArgs A) {
+  __shared__ float4 s_xyab[kFineThreads];
+  __shared__ float4 s_cop[kFineThreads];
+  __shared__ float4 s_rgb[kFineThreads];
+  __shared__ unsigned long long s_tab[32];
+  __shared__ unsigned s_task;
+  load_tab(s_tab);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned ntasks = *(volatile unsigned*)(A.queue + 3);
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_task = atomicAdd(A.queue + 2, 1u);
+    __syncthreads();
+    const unsigned task = s_task;
+    if (task >= ntasks) return;
+    const uint2 tr = A.donated_tasks[task];  // (first Donation, count <= kFineWarps)
+    const Donation& d0 = A.donate[tr.x];
+    const uint32_t start = d0.start, from = d0.from, end = d0.end;
+    {
+      const bool active = (unsigned)warp < tr.y;  // warp-uniform
+      const Donation* d = active ? &A.donate[tr.x + warp] : nullptr;
+      const uint32_t pixel = active ? d->pixel : 0u;
+      const float sx = __fadd_rn((float)(pixel % (uint32_t)A.W), 0.5f);
+      const float sy = __fadd_rn((float)(pixel / (uint32_t)A.W), 0.5f);
+      float t = active ? d->t : 1.0f;
+      int cnt = 0, trm = 0;
+      bool done = !active;
+      Accum<MODE> part;
+      for (uint32_t base = from; base < end; base += kFineThreads) {
+        if (__syncthreads_count(!done) == 0) break;
+        if (base + tid < end) load_rec(A, base + tid, s_xyab[tid], s_cop[tid], s_rgb[tid]);
+        __syncthreads();
+        if (done) continue;
+        const uint32_t n = min((uint32_t)kFineThreads, end - base);
+        for (uint32_t g0 = 0; g0 < n; g0 += 32) {
+          const uint32_t j = g0 + lane;
+          float alpha = 0.0f;
+          const bool ns = j < n && eval_step<MODE>(s_xyab[j], s_cop[j], sx, sy, s_tab, alpha);
+          const int stop = gw_group<MODE, true>(ns, alpha, ns ? s_rgb[j] : make_float4(0.f, 0.f, 0.f, 0.f),
+                                               ns ? s_cop[j].w : 0.0f, t, cnt, part, lane);
+          if (stop < 32) {
+            trm = (int)(base - start + g0) + stop + 1;
+            done = true;
+            break;
+          }
+        }
+      }
+      if (active) {
+        part.warp_sum();
+        if (lane == 0) {
+          Accum<MODE> acc;
+          acc.load(d->acc);
+          acc.merge(part);
+          acc.finish(A, pixel, t, d->contrib + cnt, trm);
+        }
+      }
+    }
   }
 }
 
@@ -632,12 +737,16 @@ __global__ void k_frame_work(const int32_t* __restrict__ term, const int32_t* __
   }
 }
 
-// List length from which FineGrainedCombined cuts a tile into per-pixel
-// Gaussian-wise CTA tasks (BS_FINE_HEAVY_LIST overrides; 0 = every tile).
-static int fine_heavy_len() {
-  const char* e = getenv("BS_FINE_HEAVY_LIST");
-  const int v = e ? atoi(e) : kFineHeavyListDefault;
-  return v < 0 ? 0 : v;
+// Tail hand-off switch (BS_FINE_DONATE=0 disables it, for A/B measurement).
+// Tuning overrides for experiments / tests (defaults are the calibrated ones).
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+static bool fine_donate_enabled() {
+  const char* e = getenv("BS_FINE_DONATE");
+  return !(e && e[0] == '0');
 }
 
 template <int MODE>
@@ -686,7 +795,18 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
       if (total > 0x7fffffff) return BS_ERR_UNSUPPORTED;
       const int64_t ctas = (total + kFineWarps - 1) / kFineWarps;
       const int grid = (int)max((int64_t)1, min(ctas, (int64_t)sms * max(1, per_sm)));
-      k_render_fine<MODE><<<grid, kFineThreads, 0, st>>>(A, subs, fine_heavy_len());
+      RArgs B = A;
+      B.total_tasks = (int)total;
+      if (!fine_donate_enabled()) B.donate = nullptr;
+      B.donate_after = env_int("BS_FINE_DONATE_AFTER", kDonateAfter);
+      B.donate_min_remain = env_int("BS_FINE_DONATE_MIN", kDonateMinRemain);
+      k_render_fine<MODE><<<grid, kFineThreads, 0, st>>>(B, subs);
+      BS_LAUNCH_CHECK();
+      if (B.donate) {
+        int per_sm2 = 0;
+        BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_render_donated<MODE>, kFineThreads, 0));
+        k_render_donated<MODE><<<sms * max(1, per_sm2), kFineThreads, 0, st>>>(B);
+      }
       break;
     }
     default:
@@ -700,7 +820,12 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
 
 using namespace bs;
 
-extern "C" size_t bs_render_workspace_bytes(void) { return 256; }
+// queue counters + one Donation slot per pixel (FineGrainedCombined tail hand-off)
+extern "C" size_t bs_render_workspace_bytes(int32_t width, int32_t height) {
+  if (width <= 0 || height <= 0) return 0;
+  const size_t P = (size_t)width * (size_t)height;
+  return 256 + sizeof(Donation) * P + sizeof(uint2) * (P / 4 + 1);  // >= 9 pixels -> <= 2 units per 9
+}
 
 extern "C" int bs_render_forward(int variant, int alpha_mode, bs_splats g, const uint32_t* point_list,
                                  const uint32_t* tile_ranges, const uint32_t* task_order, int32_t width,
@@ -711,7 +836,7 @@ extern "C" int bs_render_forward(int variant, int alpha_mode, bs_splats g, const
   if (alpha_mode != BS_ALPHA_EXACT && alpha_mode != BS_ALPHA_FAST) return BS_ERR_INVALID_ARGUMENT;
   if (!out.color || !out.alpha || !out.depth || !out.final_t || !out.contrib || !out.term) return BS_ERR_INVALID_ARGUMENT;
   if ((int64_t)pw * ph > 1024) return BS_ERR_UNSUPPORTED;
-  if (!ws || ws_bytes < bs_render_workspace_bytes()) return BS_ERR_WORKSPACE;
+  if (!ws || ws_bytes < bs_render_workspace_bytes(width, height)) return BS_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   RArgs A;
   A.xyab = reinterpret_cast<const float4*>(g.xyab);
@@ -729,8 +854,11 @@ extern "C" int bs_render_forward(int variant, int alpha_mode, bs_splats g, const
   A.color = out.color; A.alpha = out.alpha; A.depth = out.depth; A.final_t = out.final_t;
   A.contrib = out.contrib; A.term = out.term;
   A.queue = reinterpret_cast<unsigned int*>(ws);
+  A.donate = reinterpret_cast<Donation*>(static_cast<char*>(ws) + 256);
+  A.donated_tasks = reinterpret_cast<uint2*>(A.donate + (size_t)width * height);
+  A.total_tasks = 0;
   if (variant == BS_DYNAMIC_BLOCKS || variant == BS_FINE_GRAINED_COMBINED)
-    BS_CUDA_TRY(cudaMemsetAsync(ws, 0, 2 * sizeof(unsigned int), st));
+    BS_CUDA_TRY(cudaMemsetAsync(ws, 0, 8 * sizeof(unsigned int), st));
   const int block_pixels = pw * ph;
   return alpha_mode == BS_ALPHA_EXACT ? launch_variant<BS_ALPHA_EXACT>(variant, A, block_pixels, st)
                                       : launch_variant<BS_ALPHA_FAST>(variant, A, block_pixels, st);

@@ -45,6 +45,7 @@ struct bs_context {
   bs_tile_histogram* stats_dev = nullptr;
   bs_tile_histogram* stats_host = nullptr;  // pinned
   void* render_ws = nullptr;
+  size_t render_ws_bytes = 0;
   float* planes[4] = {nullptr, nullptr, nullptr, nullptr};
   int32_t* iplanes[2] = {nullptr, nullptr};
   int64_t pixel_cap = 0;
@@ -111,7 +112,6 @@ extern "C" int bs_context_create(bs_context** out, int alpha_mode) {
       cudaMalloc(reinterpret_cast<void**>(&c->k_dev), 256) != cudaSuccess ||
       cudaMalloc(reinterpret_cast<void**>(&c->stats_dev), sizeof(bs_tile_histogram) + 256) != cudaSuccess ||
       cudaMalloc(reinterpret_cast<void**>(&c->work_dev), 256) != cudaSuccess ||
-      cudaMalloc(&c->render_ws, bs_render_workspace_bytes()) != cudaSuccess ||
       cudaMallocHost(reinterpret_cast<void**>(&c->k_host), 256) != cudaSuccess ||
       cudaMallocHost(reinterpret_cast<void**>(&c->stats_host), sizeof(bs_tile_histogram) + 256) != cudaSuccess ||
       cudaMallocHost(reinterpret_cast<void**>(&c->work_host), 256) != cudaSuccess) {
@@ -225,8 +225,10 @@ extern "C" int bs_render_frame_host(bs_context* c, const bs_gaussian3d* g3d, int
     c->pixel_cap = P;
   }
   bs_frame_out fo{c->planes[0], c->planes[1], c->planes[2], c->planes[3], c->iplanes[0], c->iplanes[1]};
+  const size_t rws = bs_render_workspace_bytes(W, H);
+  TRY(grow(&c->render_ws, &c->render_ws_bytes, rws));
   TRY(bs_render_forward(v, c->alpha_mode, sp, c->point_list, c->ranges, c->order, W, H, pw, ph, bg, fo, c->render_ws,
-                        bs_render_workspace_bytes(), st));
+                        c->render_ws_bytes, st));
   if (info) TRY(bs_frame_work(c->iplanes[1], c->iplanes[0], c->ranges, W, H, pw, ph, c->work_dev, st));
 
   // D2H

@@ -278,10 +278,11 @@ RenderOutput render_on_device(Ctx& c, KernelVariant v, const TileBinning& b, con
   device_stats(c, d, b.tile_count());
   const int64_t P = int64_t(w) * h;
   bs_frame_out fo = device_frame(c, P);
-  void* rws = c.render_ws.get(bs_render_workspace_bytes());
+  const size_t rwb = bs_render_workspace_bytes(w, h);
+  void* rws = c.render_ws.get(rwb);
   ck("run_kernel", bs_render_forward(static_cast<int>(v), mode_c(), s, d.pl, d.ranges,
                                      static_cast<uint32_t*>(c.order.p), w, h, pw, ph, bg.data(), fo, rws,
-                                     bs_render_workspace_bytes(), c.st));
+                                     rwb, c.st));
   RenderOutput o;
   o.width = w;
   o.height = h;
@@ -345,7 +346,8 @@ double time_kernel_ms(KernelVariant variant, const TileBinning& binning, const s
   DeviceBinning d = upload_binning(c, binning);
   device_stats(c, d, binning.tile_count());
   bs_frame_out fo = device_frame(c, int64_t(width) * height);
-  void* rws = c.render_ws.get(bs_render_workspace_bytes());
+  const size_t rwb = bs_render_workspace_bytes(width, height);
+  void* rws = c.render_ws.get(rwb);
   const float bg[3] = {0, 0, 0};
   cudaEvent_t a, b;
   cu("event", cudaEventCreate(&a));
@@ -353,7 +355,7 @@ double time_kernel_ms(KernelVariant variant, const TileBinning& binning, const s
   auto launch = [&]() {
     ck("time_kernel_ms", bs_render_forward(static_cast<int>(variant), mode_c(), s, d.pl, d.ranges,
                                            static_cast<uint32_t*>(c.order.p), width, height, patch_width,
-                                           patch_height, bg, fo, rws, bs_render_workspace_bytes(), c.st));
+                                           patch_height, bg, fo, rws, rwb, c.st));
   };
   launch();  // warm-up
   cu("event", cudaEventRecord(a, c.st));

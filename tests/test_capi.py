@@ -58,7 +58,7 @@ def test_workspace_queries():
     assert 0 < a < b < c
     assert L.bs_bin_workspace_bytes(10, 0, 256, 16, 16, 0) == 0
     assert L.bs_preprocess_workspace_bytes(10**6) > L.bs_preprocess_workspace_bytes(10)
-    assert L.bs_tile_stats_workspace_bytes(8160) > 0 and L.bs_render_workspace_bytes() >= 4
+    assert L.bs_tile_stats_workspace_bytes(8160) > 0 and L.bs_render_workspace_bytes(64, 64) >= 64 * 64 * 48 and L.bs_render_workspace_bytes(0, 64) == 0
 
 
 def test_argument_validation_without_device():
@@ -77,12 +77,15 @@ def test_argument_validation_without_device():
 def test_selector_rule():
     L = N.lib()
     h = N.TileHistogram()
-    # balanced: every tile ~ mean -> SharedMemOpt
+    # balanced 1080p frame: the culled fine-grained kernel still wins on B200
     h.total, h.max, h.tiles, h.mean = 8160 * 1000, 1500, 8160, 1000.0
-    assert L.bs_select_variant(C.byref(h), 1920, 1080, 16, 16, 148) == 4
+    assert L.bs_select_variant(C.byref(h), 1920, 1080, 16, 16, 148) == 3
     # one tile dominates the balanced share -> FineGrainedCombined
     h.max = 200000
     assert L.bs_select_variant(C.byref(h), 1920, 1080, 16, 16, 148) == 3
+    # (almost) no work: the fixed queue cost loses -> SharedMemOpt
+    h.total, h.max, h.tiles, h.mean = 200, 2, 8160, 200 / 8160
+    assert L.bs_select_variant(C.byref(h), 1920, 1080, 16, 16, 148) == 4
     assert L.bs_select_variant(None, 1920, 1080, 16, 16, 148) == -1
 
 

@@ -265,11 +265,13 @@ def test_golden_digests_on_gpu():
             assert O.fnv1a64(f2[k]) == fz["render_gaussianwise"][k], (name, k)
 
 
-@pytest.mark.parametrize("heavy", ["0", "64"])
-def test_fine_heavy_tile_path(heavy, monkeypatch):
-    """FineGrainedCombined's per-pixel Gaussian-wise CTA tasks for heavy tiles
-    (forced on with a low BS_FINE_HEAVY_LIST) keep the exact semantics."""
-    monkeypatch.setenv("BS_FINE_HEAVY_LIST", heavy)
+@pytest.mark.parametrize("after,remain", [("0", "1"), ("32", "64"), ("100000000", "100000000")])
+def test_fine_donation_path(after, remain, monkeypatch):
+    """FineGrainedCombined's tail hand-off (live pixels parked mid-list and
+    finished Gaussian-wise by k_render_donated), forced on with tiny
+    thresholds, keeps the exact semantics; the last case disables it."""
+    monkeypatch.setenv("BS_FINE_DONATE_AFTER", after)
+    monkeypatch.setenv("BS_FINE_DONATE_MIN", remain)
     W, H, pw, ph = 192, 128, 16, 16
     g3d, cam = scene(8000, W, H, 192.0, bgfrac=0.12)
     g2d = O.project_all(g3d, cam)
