@@ -17,6 +17,7 @@
 // The expansion is load-balanced: each thread writes 16 consecutive instances
 // (one smem search for the first, then a carry-walk over the rectangle).
 #include <math.h>
+#include <stdlib.h>
 
 #include "bs_common.cuh"
 #include "radix_sort.cuh"
@@ -262,6 +263,222 @@ __global__ void __launch_bounds__(256) k_expand(const uint64_t* __restrict__ off
   }
 }
 
+// ---------------------------------------------------------------------------
+// Chunked counting scatter (default path; replaces expand + tile radix sort).
+// The depth-sorted splats are cut into chunks of ~Q consecutive instances.
+//   k_chunk_bounds  chunk c = splats [first[c], first[c+1]) (those whose first
+//                   instance lies in [cQ, (c+1)Q)); first[nchunks] = number of
+//                   splats that touch a tile (they precede the non-touching
+//                   ones in depth-key order)
+//   k_chunk_hist    per chunk, a shared-memory difference grid of its
+//                   rectangles -> per-tile counts M[c][t]
+//   k_chunk_scan    in place, M[c][t] <- starts[t] + sum_{c' < c} M[c'][t]
+//   k_chunk_scatter per chunk, the offsets row in shared memory; warp w owns
+//                   the tiles (tx, ty) = (w % 4, w / 4) (mod 4) and walks the chunk's
+//                   splats in depth order, 32 instances per step; equal tiles
+//                   inside a step are ranked by match.any (lane order = depth
+//                   order), so every tile list is written in (depth, index)
+//                   order directly — point_list is the final order without
+//                   materialising or sorting K keys.
+constexpr int kScWarps = 16;
+constexpr int kScThreads = kScWarps * 32;
+constexpr int kOwnX = 4, kOwnY = kScWarps / kOwnX;  // tile ownership pattern (powers of 2)
+constexpr int kScBuf = 512;                          // per-warp instance window (entries)
+constexpr int64_t kMaxChunkMatrix = (int64_t)16 << 20;  // entries of M (64 MB)
+constexpr int kMaxChunks = 4096;
+constexpr size_t kMaxScatterSmem = 200 * 1024;           // offsets row (T u32) + warp buffers
+
+// first[c] = lower_bound(offs[0, nt), c*q) for c < nchunks, first[nchunks] =
+// nt (the touching splats).  Splat j marks the chunks whose first instance
+// offset c*q falls in (offs[j-1], offs[j]]; the last touching splat also
+// marks every chunk past its own offset.  One coalesced pass, no searches.
+__global__ void k_chunk_bounds(const uint64_t* __restrict__ offs, const uint32_t* __restrict__ touched_sorted,
+                               int64_t n_cap, const int32_t* __restrict__ n_visible, int64_t q, int nchunks,
+                               uint32_t* __restrict__ first) {
+  const int64_t n = min((int64_t)*n_visible, n_cap);
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n || touched_sorted[j] == 0) return;
+  const uint64_t hi = offs[j];
+  const int64_t c_lo = j == 0 ? 0 : (int64_t)((offs[j - 1] + (uint64_t)q) / (uint64_t)q);  // c*q > offs[j-1]
+  const int64_t c_hi = (int64_t)(hi / (uint64_t)q);                                        // c*q <= offs[j]
+  for (int64_t c = c_lo; c <= c_hi && c < nchunks; ++c) first[c] = (uint32_t)j;
+  if (j + 1 == n || touched_sorted[j + 1] == 0) {
+    for (int64_t c = c_hi + 1; c <= nchunks; ++c) first[c] = (uint32_t)(j + 1);
+  }
+}
+
+__global__ void __launch_bounds__(kScThreads) k_chunk_hist(const uint2* __restrict__ rects_sorted,
+                                                           const uint32_t* __restrict__ first, Grid g,
+                                                           uint32_t* __restrict__ m) {
+  extern __shared__ int s_grid[];
+  const int stride = g.cols + 1, cells = stride * (g.rows + 1);
+  const int c = blockIdx.x, tid = threadIdx.x;
+  for (int i = tid; i < cells; i += kScThreads) s_grid[i] = 0;
+  __syncthreads();
+  const uint32_t j0 = first[c], j1 = first[c + 1];
+  for (uint32_t j = j0 + tid; j < j1; j += kScThreads) {
+    const uint2 rc = rects_sorted[j];
+    const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16;
+    const int tx1 = tx0 + (int)(rc.y & 0xffff), ty1 = ty0 + (int)(rc.y >> 16);  // exclusive
+    atomicAdd(&s_grid[ty0 * stride + tx0], 1);
+    atomicAdd(&s_grid[ty0 * stride + tx1], -1);
+    atomicAdd(&s_grid[ty1 * stride + tx0], -1);
+    atomicAdd(&s_grid[ty1 * stride + tx1], 1);
+  }
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int r = warp; r < g.rows; r += kScWarps) {
+    int carry = 0;
+    for (int x0 = 0; x0 < g.cols; x0 += 32) {
+      const int x = x0 + lane;
+      int v = x < g.cols ? s_grid[r * stride + x] : 0;
+      v = warp_inclusive_scan(v) + carry;
+      if (x < g.cols) s_grid[r * stride + x] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  uint32_t* row = m + (int64_t)c * g.cols * g.rows;
+  for (int tx = tid; tx < g.cols; tx += kScThreads) {
+    int run = 0;
+    for (int ty = 0; ty < g.rows; ++ty) {
+      run += s_grid[ty * stride + tx];
+      row[ty * g.cols + tx] = (uint32_t)run;
+    }
+  }
+}
+
+// CTA = 32 consecutive tiles (lane) x 32 warps (chunk segments): enough
+// independent loads in flight to stream M at HBM rate.
+constexpr int kCsSeg = 32;
+__global__ void __launch_bounds__(kCsSeg * 32) k_chunk_scan(uint32_t* __restrict__ m,
+                                                            const uint32_t* __restrict__ starts, int T, int nchunks) {
+  __shared__ uint32_t s_part[kCsSeg][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + lane;
+  const int c0 = (int)((int64_t)nchunks * warp / kCsSeg), c1 = (int)((int64_t)nchunks * (warp + 1) / kCsSeg);
+  uint32_t sum = 0;
+  if (t < T) {
+#pragma unroll 4
+    for (int c = c0; c < c1; ++c) sum += m[(int64_t)c * T + t];
+  }
+  s_part[warp][lane] = sum;
+  __syncthreads();
+  if (t >= T) return;
+  uint32_t run = starts[t];
+  for (int w = 0; w < warp; ++w) run += s_part[w][lane];
+#pragma unroll 4
+  for (int c = c0; c < c1; ++c) {
+    const int64_t i = (int64_t)c * T + t;
+    const uint32_t v = m[i];
+    m[i] = run;
+    run += v;
+  }
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __restrict__ m,
+                                                              const uint32_t* __restrict__ first,
+                                                              const uint2* __restrict__ rects_sorted,
+                                                              const uint32_t* __restrict__ order, int T, int cols,
+                                                              uint32_t* __restrict__ point_list) {
+  extern __shared__ uint32_t s_off[];
+  const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t* row = m + (int64_t)c * T;
+  for (int t = tid; t < T; t += kScThreads) s_off[t] = row[t];
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_off);
+  const uint32_t wbuf = sbase + 4u * (uint32_t)(((T + 31) & ~31) + warp * kScBuf);
+  __syncthreads();
+  const uint32_t j0 = first[c], j1 = first[c + 1];
+  const uint32_t lt = lanemask_lt();
+  const uint32_t row_step = (uint32_t)(kOwnY * cols);
+  // warp w owns the tiles tx = w % kOwnX (mod kOwnX), ty = w / kOwnX (mod
+  // kOwnY): clustered hot spots spread evenly over the warps
+  const uint32_t own_x = (uint32_t)(warp % kOwnX), own_y = (uint32_t)(warp / kOwnX);
+  // next batch prefetched into registers (load latency overlaps this batch)
+  uint2 nrc = make_uint2(0u, 0u);
+  uint32_t nid = 0;
+  if (j0 + lane < j1) {
+    nrc = rects_sorted[j0 + lane];
+    nid = order[j0 + lane];
+  }
+  for (uint32_t b = j0; b < j1; b += 32) {
+    // this lane's splat: its owned tiles form an nc x nr sub-grid from tb,
+    // strides (kOwnX, kOwnY) — listed flat (row-major) at [excl, excl + cnt)
+    const uint2 rc = nrc;
+    const uint32_t id = nid;
+    const bool valid = b + lane < j1;
+    if (b + 32 + lane < j1) {
+      nrc = rects_sorted[b + 32 + lane];
+      nid = order[b + 32 + lane];
+    }
+    const uint32_t rx0 = rc.x & 0xffffu, ry0 = rc.x >> 16, rw = rc.y & 0xffffu, rh = rc.y >> 16;
+    const uint32_t fc = rx0 + ((own_x - rx0) & (kOwnX - 1));
+    const uint32_t fr = ry0 + ((own_y - ry0) & (kOwnY - 1));
+    const uint32_t nc = (rx0 + rw + (kOwnX - 1) - fc) / kOwnX;  // 0 when fc is past the rectangle
+    const uint32_t nr = (ry0 + rh + (kOwnY - 1) - fr) / kOwnY;
+    const int cnt = valid ? (int)(nc * nr) : 0;
+    const uint32_t tb = fr * (uint32_t)cols + fc;
+    const int incl = warp_inclusive_scan(cnt);
+    const int excl = incl - cnt;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int wb = 0; wb < total; wb += kScBuf) {
+      // every lane lists its owned tiles that fall in the window
+      // [wb, wb + kScBuf) as (tile | lane << 16): no per-instance division,
+      // no lane search; then the warp drains the window 32 per step
+      const int k0 = max(0, wb - excl), k1 = min(cnt, wb + kScBuf - excl);
+      if (k0 < k1) {
+        uint32_t r = 0, cc = 0;
+        if (k0) {  // only when a batch spills past one window
+          r = (uint32_t)k0 / nc;
+          cc = (uint32_t)k0 - r * nc;
+        }
+        uint32_t rowbase = tb + r * row_step, t = rowbase + cc * kOwnX;
+        uint32_t dst = wbuf + 4u * (uint32_t)(excl + k0 - wb);
+        const uint32_t tag = (uint32_t)lane << 16;
+#pragma unroll 1
+        for (int k = k0; k < k1; ++k) {
+          sts_u32(dst, t | tag);
+          dst += 4u;
+          t += kOwnX;
+          if (++cc == nc) {
+            cc = 0;
+            rowbase += row_step;
+            t = rowbase;
+          }
+        }
+      }
+      __syncwarp();
+      const int n = min(kScBuf, total - wb);
+      for (int f0 = 0; f0 < n; f0 += 32) {
+        const int f = f0 + lane;
+        const bool act = f < n;
+        const uint32_t v = act ? lds_u32(wbuf + 4u * (uint32_t)f) : 0xffffffffu;
+        const uint32_t sid = __shfl_sync(0xffffffffu, id, (int)(v >> 16) & 31);
+        const uint32_t tile = v & 0xffffu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, act ? tile : 0xffffffffu);
+        const uint32_t a = sbase + 4u * tile;
+        uint32_t pos = 0;
+        if (act) {
+          pos = lds_u32(a) + __popc(peers & lt);
+          point_list[pos] = sid;
+        }
+        __syncwarp();
+        if (act && (peers >> lane) == 1u) sts_u32(a, pos + 1);  // highest peer publishes
+        __syncwarp();
+      }
+    }
+  }
+}
+
 __global__ void k_ranges(const uint32_t* __restrict__ starts, const uint32_t* __restrict__ counts, int T,
                          uint32_t* __restrict__ ranges) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -297,7 +514,26 @@ struct BinWs {
   uint32_t *counts, *starts, *cpartials;
   uint32_t *tk0, *tv_alt, *tk1, *block_j0;
   RadixWs rws_k;
+  uint32_t *chunk_first, *chunk_m;
 };
+
+// The chunked counting scatter needs the per-chunk offsets row (T u32) and
+// the difference grid in shared memory; BS_BIN_RADIX=1 forces the expand +
+// tile radix sort path (A/B measurement, parity tests of both paths).
+inline bool bin_chunked(const Grid& g) {
+  static const int forced_radix = [] {
+    const char* e = getenv("BS_BIN_RADIX");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  const int64_t T = (int64_t)g.cols * g.rows;
+  return !forced_radix && (size_t)(T + 32 + kScWarps * kScBuf) * 4 <= kMaxScatterSmem &&
+         sizeof(int) * (size_t)(g.cols + 1) * (g.rows + 1) <= kMaxDiffSmem;
+}
+
+inline int64_t max_chunks(const Grid& g) {
+  const int64_t T = max((int64_t)1, (int64_t)g.cols * g.rows);
+  return max((int64_t)1, min((int64_t)kMaxChunks, kMaxChunkMatrix / T));
+}
 
 template <typename C>
 inline void bin_ws_layout(C& c, int64_t n_cap, const Grid& g, int64_t k_cap, BinWs* w) {
@@ -319,6 +555,12 @@ inline void bin_ws_layout(C& c, int64_t n_cap, const Grid& g, int64_t k_cap, Bin
   o.counts = c.template take<uint32_t>((size_t)T);
   o.starts = c.template take<uint32_t>((size_t)T);
   o.cpartials = c.template take<uint32_t>((size_t)scan_num_blocks(T) + 1);
+  if (bin_chunked(g)) {
+    // chunked counting scatter: chunk bounds + the chunk x tile offsets matrix
+    o.chunk_first = c.template take<uint32_t>((size_t)kMaxChunks + 1);
+    o.chunk_m = c.template take<uint32_t>((size_t)(max_chunks(g) * T));
+    return;
+  }
   o.tk0 = c.template take<uint32_t>((size_t)k_cap);
   o.tv_alt = c.template take<uint32_t>((size_t)k_cap);
   o.tk1 = c.template take<uint32_t>((size_t)k_cap);
@@ -432,7 +674,40 @@ extern "C" int bs_bin_sort(bs_splats g, int64_t n_cap, const int32_t* n_visible,
   WsCarver c(ws, ws_bytes);
   BinWs w;
   bin_ws_layout(c, n_cap, gr, k, &w);
-  if (k > 0) {
+  if (k > 0 && bin_chunked(gr)) {
+    const uint32_t* order = w.dv0;  // depth order (4 passes end in dv0)
+    static bool attr_set = false;
+    if (!attr_set) {
+      BS_CUDA_TRY(cudaFuncSetAttribute(k_chunk_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDiffSmem));
+      BS_CUDA_TRY(cudaFuncSetAttribute(k_chunk_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kMaxScatterSmem));
+      attr_set = true;
+    }
+    const size_t off_bytes = sizeof(uint32_t) * ((size_t)((T + 31) & ~31) + (size_t)kScWarps * kScBuf);
+    const size_t diff_bytes = sizeof(int) * (size_t)(gr.cols + 1) * (gr.rows + 1);
+    int dev = 0, sms = 148, per_sm = 1;
+    BS_CUDA_TRY(cudaGetDevice(&dev));
+    BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chunk_scatter, kScThreads, off_bytes));
+    // one wave of chunks (more only for very large K), >= 4096 instances each
+    const int64_t slots = (int64_t)sms * max(1, per_sm);
+    static const int64_t min_waves = [] {
+      const char* e = getenv("BS_BIN_CHUNK_WAVES");  // tuning override
+      return (int64_t)(e ? max(1, atoi(e)) : 1);
+    }();
+    const int64_t waves = max(min_waves, (k + slots * (1 << 18) - 1) / (slots * (1 << 18)));
+    const int64_t nch = max((int64_t)1, min(max_chunks(gr), min(slots * waves, (k + 4095) / 4096)));
+    const int64_t q = (k + nch - 1) / nch;
+    k_chunk_bounds<<<(unsigned)((n_cap + 255) / 256), 256, 0, st>>>(w.offs, w.touched_sorted, n_cap, n_visible, q, (int)nch, w.chunk_first);
+    BS_LAUNCH_CHECK();
+    k_chunk_hist<<<(unsigned)nch, kScThreads, diff_bytes, st>>>(w.rects_sorted, w.chunk_first, gr, w.chunk_m);
+    BS_LAUNCH_CHECK();
+    k_chunk_scan<<<(unsigned)((T + 31) / 32), kCsSeg * 32, 0, st>>>(w.chunk_m, w.starts, (int)T, (int)nch);
+    BS_LAUNCH_CHECK();
+    k_chunk_scatter<<<(unsigned)nch, kScThreads, off_bytes, st>>>(w.chunk_m, w.chunk_first, w.rects_sorted, order,
+                                                                   (int)T, gr.cols, point_list);
+    BS_LAUNCH_CHECK();
+  } else if (k > 0) {
     const uint32_t* order = w.dv0;  // depth order (4 passes end in dv0)
     const int bits = bits_for(T);
     k_mark_starts<<<(unsigned)((n_cap + 255) / 256), 256, 0, st>>>(w.offs, w.touched_sorted, n_cap, n_visible,

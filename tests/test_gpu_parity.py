@@ -100,6 +100,35 @@ def test_binning_bit_exact(W, H, pw, ph, n):
     assert np.array_equal(b.point_list.cpu().numpy().view(np.uint32), pl_ref)
 
 
+@pytest.mark.parametrize("W,H,f,n,bgfrac", [(1920, 1080, 1000.0, 200_000, 0.12),   # ~600 chunks
+                                             (3840, 2160, 2000.0, 60_000, 0.12),    # C4 grid: 32,400 tiles
+                                             (8192, 4096, 4096.0, 3000, 1.0)])      # 131,072 tiles: radix fallback
+def test_binning_bit_exact_large(W, H, f, n, bgfrac):
+    """Chunked counting scatter at full 1080p / 4K grids (many chunks, splats
+    straddling chunk bounds) and the radix fallback beyond its smem limit."""
+    g3d, cam = scene(n, W, H, f, bgfrac=bgfrac)
+    g2d = O.project_all(g3d, cam)
+    pl_ref, rg_ref = O.bin_tiles(g2d, W, H, 16, 16)
+    b = api.bin_tiles(to_dev_splats(g2d), W, H, 16, 16)
+    assert b.k == len(pl_ref)
+    assert np.array_equal(b.tile_ranges.cpu().numpy().view(np.uint32), rg_ref)
+    assert np.array_equal(b.point_list.cpu().numpy().view(np.uint32), pl_ref)
+
+
+def test_binning_radix_path_bit_exact():
+    """BS_BIN_RADIX=1 (expand + stable tile radix sort) stays bit-exact too."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys; sys.path[:0] = ['tests', '.']; import test_gpu_parity as t; "
+            "t.test_binning_bit_exact(960, 540, 16, 8, 30000); t.test_binning_depth_ties_and_empty(); "
+            "t.test_binning_bit_exact_large(1920, 1080, 1000.0, 100000, 0.12); print('radix ok')")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, BS_BIN_RADIX="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "radix ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_binning_depth_ties_and_empty():
     # many equal depths: ties must resolve by compacted index
     g2d = np.zeros(500, dtype=O.G2D_DTYPE)
