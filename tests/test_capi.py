@@ -55,7 +55,11 @@ def test_workspace_queries():
     a = L.bs_bin_workspace_bytes(1000, 256, 256, 16, 16, 0)
     b = L.bs_bin_workspace_bytes(1000, 256, 256, 16, 16, 100000)
     c = L.bs_bin_workspace_bytes(100000, 256, 256, 16, 16, 100000)
-    assert 0 < a < b < c
+    assert 0 < a <= b < c  # chunked scatter: no K-sized buffers
+    # beyond the chunked path's shared-memory limit the radix path sizes by K
+    ra = L.bs_bin_workspace_bytes(1000, 8192, 8192, 16, 16, 0)
+    rb = L.bs_bin_workspace_bytes(1000, 8192, 8192, 16, 16, 100000)
+    assert 0 < ra < rb
     assert L.bs_bin_workspace_bytes(10, 0, 256, 16, 16, 0) == 0
     assert L.bs_preprocess_workspace_bytes(10**6) > L.bs_preprocess_workspace_bytes(10)
     assert L.bs_tile_stats_workspace_bytes(8160) > 0 and L.bs_render_workspace_bytes(64, 64) >= 64 * 64 * 48 and L.bs_render_workspace_bytes(0, 64) == 0
