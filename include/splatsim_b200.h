@@ -191,6 +191,15 @@ int bs_render_forward(int variant, int alpha_mode, bs_splats g, const uint32_t* 
                       int32_t pw, int32_t ph, const float bg[3], bs_frame_out out, void* ws, size_t ws_bytes,
                       void* stream);
 
+/* Sync-free auto mode: variant_dev points to the device int32 written by
+ * bs_select_variant_device.  Launches the selector's candidates
+ * (FineGrainedCombined, SharedMemOpt); all but the selected one exit at
+ * entry, so the host never waits for the selection. */
+int bs_render_forward_auto(const int32_t* variant_dev, int alpha_mode, bs_splats g, const uint32_t* point_list,
+                           const uint32_t* tile_ranges, const uint32_t* task_order, int32_t width, int32_t height,
+                           int32_t pw, int32_t ph, const float bg[3], bs_frame_out out, void* ws, size_t ws_bytes,
+                           void* stream);
+
 /* Work counters of a rendered frame (src/kernels.cpp:283-298):
  *   evaluated = sum_p consumed(p), consumed = term > 0 ? term : list_len(tile(p))
  *   committed = sum_p contrib(p)
@@ -203,6 +212,12 @@ int bs_frame_work(const int32_t* term, const int32_t* contrib, const uint32_t* t
  * with these tile statistics.  Host-only logic. */
 int bs_select_variant(const bs_tile_histogram* stats, int32_t width, int32_t height, int32_t pw, int32_t ph,
                       int32_t sm_count);
+
+/* Device form of bs_select_variant: reads the histogram bs_tile_stats wrote
+ * (device pointer) and writes the chosen bs_variant to *variant (device
+ * int32), stream-ordered — same formula, same decision. */
+int bs_select_variant_device(const bs_tile_histogram* stats, int32_t width, int32_t height, int32_t pw, int32_t ph,
+                             int32_t sm_count, int32_t* variant, void* stream);
 
 /* ---- diagnostics ----
  * y[i] = the device exp the render kernels use in alpha_mode (EXACT: the
@@ -241,6 +256,22 @@ void* bs_context_stream(bs_context* ctx);
 int bs_render_frame_host(bs_context* ctx, const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, int32_t pw,
                          int32_t ph, int32_t variant, const float bg[3], float* color, float* alpha, float* depth,
                          float* final_t, int32_t* contrib, int32_t* term, bs_frame_info* info);
+
+/* Same pipeline on DEVICE Gaussians (g3d_dev), stream-ordered on the context
+ * stream (bs_context_set_stream; NULL = the context's own stream).  out: the
+ * caller's device planes, or all-NULL for context-owned planes.  The only
+ * host wait is the 8-byte K readback that sizes point_list; with variant = -1
+ * the variant is selected on the device.  info != NULL additionally waits for
+ * the frame and fills it (otherwise bs_context_last_info does that later). */
+int bs_render_frame_device(bs_context* ctx, const bs_gaussian3d* g3d_dev, int64_t n, const bs_camera* cam, int32_t pw,
+                           int32_t ph, int32_t variant, const float bg[3], bs_frame_out out, bs_frame_info* info);
+int bs_context_set_stream(bs_context* ctx, void* stream);
+int bs_context_last_info(bs_context* ctx, bs_frame_info* info);
+/* Per-stage CUDA-event timing of the following frames (6 stages: preprocess,
+ * bin_count, k_readback, bin_sort, stats_select, render); bs_context_stage_ms
+ * waits for the last frame and writes n >= 6 floats (ms). */
+int bs_context_enable_timing(bs_context* ctx, int32_t on);
+int bs_context_stage_ms(bs_context* ctx, float* ms, int32_t n);
 
 /* Number of kernel launches issued by this library since load (evidence
  * counter for bench.py's gpu_launches). */

@@ -78,6 +78,15 @@ SIGNATURES = {
     "bs_context_stream": (_vp, [_vp]),
     "bs_render_frame_host": (C.c_int, [_vp, _vp, _i64, C.POINTER(Camera), _i32, _i32, _i32, _f32p, _vp, _vp, _vp,
                                        _vp, _vp, _vp, _vp]),
+    "bs_render_frame_device": (C.c_int, [_vp, _vp, _i64, C.POINTER(Camera), _i32, _i32, _i32, _f32p, FrameOut,
+                                         _vp]),
+    "bs_context_set_stream": (C.c_int, [_vp, _vp]),
+    "bs_context_last_info": (C.c_int, [_vp, C.POINTER(FrameInfo)]),
+    "bs_context_enable_timing": (C.c_int, [_vp, _i32]),
+    "bs_context_stage_ms": (C.c_int, [_vp, _f32p, _i32]),
+    "bs_select_variant_device": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "bs_render_forward_auto": (C.c_int, [_vp, C.c_int, Splats, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _f32p,
+                                         FrameOut, _vp, _sz, _vp]),
     "bs_kernel_launches": (_u64, []),
     "bs_host_gen_clustered_scene": (C.c_int, [_i32, _i32, _u64, C.c_double, C.c_double, C.POINTER(Camera), _vp]),
 }

@@ -347,3 +347,54 @@ class Pipeline:
         mark("render")
         self.last_variant, self.last_k, self.last_stats, self.last_binning = v, b.k, st, b
         return self.frame, v
+
+
+STAGES = ("preprocess", "bin_count", "k_readback", "bin_sort", "stats_select", "render")
+
+
+class FramePipeline:
+    """The whole forward through the native frame context
+    (``bs_render_frame_device``): one C-ABI call per frame, stream-ordered on
+    torch's current stream, one 8-byte host wait (K) and on-device variant
+    selection for ``variant="auto"``.  Outputs land in ``self.frame``."""
+
+    def __init__(self, width: int, height: int, pw: int = 16, ph: int = 16, device="cuda",
+                 alpha_mode: int = ALPHA_EXACT, timing: bool = False):
+        self.width, self.height, self.pw, self.ph, self.device = width, height, pw, ph, device
+        self.ctx = C.c_void_p()
+        N.call("bs_context_create", C.byref(self.ctx), int(alpha_mode))
+        N.call("bs_context_set_stream", self.ctx, _stream(device))
+        if timing:
+            N.call("bs_context_enable_timing", self.ctx, 1)
+        self.frame = DeviceFrame.empty(width, height, device)
+
+    def forward(self, g3d_dev: torch.Tensor, n: int, cam: N.Camera, variant="auto", bg=(0.0, 0.0, 0.0),
+                info: bool = False):
+        v = -1 if variant == "auto" else (variant if isinstance(variant, int) else variant_from_name(variant))
+        bgc = (C.c_float * 3)(*[float(x) for x in bg])
+        fi = N.FrameInfo() if info else None
+        N.call("bs_render_frame_device", self.ctx, _ptr(g3d_dev), int(n), C.byref(cam), self.pw, self.ph, int(v), bgc,
+               self.frame.c(), C.byref(fi) if info else None)
+        return self.frame, fi
+
+    def last_info(self) -> N.FrameInfo:
+        fi = N.FrameInfo()
+        N.call("bs_context_last_info", self.ctx, C.byref(fi))
+        return fi
+
+    def stage_ms(self) -> dict:
+        ms = (C.c_float * len(STAGES))()
+        N.call("bs_context_stage_ms", self.ctx, ms, len(STAGES))
+        return dict(zip(STAGES, [float(x) for x in ms]))
+
+    def close(self):
+        if self.ctx:
+            torch.cuda.synchronize(self.device)
+            N.call("bs_context_destroy", self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 #include "splatsim_b200.h"
@@ -60,6 +61,28 @@ struct WsSizer {
     return nullptr;
   }
 };
+
+// Per-frame variant predictor, shared by the host entry point
+// bs_select_variant and the device-side selection of the sync-free pipeline.
+// With L_t the list length of tile t, a static one-CTA-per-tile launch
+// finishes no earlier than the heaviest tile (L_max) and no earlier than the
+// balanced share sum(L)/(S*k) of S SMs with k resident tile-CTAs each; the
+// fine-grained queue removes the first bound and (sub-tile culling) does less
+// work per list entry, at a fixed queue/launch cost:
+//   t_static ~ max(L_max, sum(L)/(S*k)),   t_fine ~ rho * sum(L)/(S*k) + c0
+// FineGrainedCombined when t_static > t_fine, else SharedMemOpt (the
+// selector's fallback, src/adaptive.cpp:27-28).  rho = 0.75 and c0 = 64 list
+// entries are the B200 calibration from the C3 sweep (profiles/r1_c3_*.jsonl).
+__host__ __device__ inline int select_variant_formula(uint64_t total, uint32_t max_len, int pw, int ph, int sm_count) {
+  const double S = sm_count > 0 ? (double)sm_count : 148.0;
+  const int pixels = pw * ph;
+  const double k = pixels <= 128 ? 12.0 : (pixels <= 256 ? 6.0 : 3.0);  // resident tile CTAs per SM
+  const double rho = 0.75, c0 = 64.0;
+  const double balanced = (double)total / (S * k);
+  const double t_static = fmax((double)max_len, balanced);
+  const double t_fine = rho * balanced + c0;
+  return t_static > t_fine ? BS_FINE_GRAINED_COMBINED : BS_SHARED_MEM_OPT;
+}
 
 // Sortable key of a float under operator< (ties -0 == +0 collapse).
 __device__ __forceinline__ uint32_t float_sort_key(float f) {

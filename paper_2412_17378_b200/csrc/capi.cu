@@ -61,29 +61,24 @@ extern "C" int bs_device_sm_count(int32_t* sm_count) {
   return BS_OK;
 }
 
-// Per-frame predictor.  With L_t the list length of tile t,
-// a static one-CTA-per-tile launch finishes no earlier than the heaviest tile
-// (L_max) and no earlier than the balanced share sum(L)/(S*k) of S SMs with k
-// resident tile-CTAs each; the fine-grained queue removes the first bound and
-// (sub-tile culling) does less work per list entry, at a fixed queue/launch
-// cost:
-//   t_static ~ max(L_max, sum(L)/(S*k)),   t_fine ~ rho * sum(L)/(S*k) + c0
-// FineGrainedCombined when t_static > t_fine, else SharedMemOpt (the
-// selector's fallback, src/adaptive.cpp:27-28).  rho = 0.75 and c0 = 64 list
-// entries are the B200 calibration from the C3 sweep (profiles/r1_c3_*.jsonl:
-// FineGrainedCombined / SharedMemOpt render time 0.70-0.79 on the balanced
-// end, lower everywhere else), so SharedMemOpt is only chosen for frames with
-// almost no work.
+// Per-frame predictor (formula in bs_common.cuh).
 extern "C" int bs_select_variant(const bs_tile_histogram* stats, int32_t width, int32_t height, int32_t pw, int32_t ph,
                                  int32_t sm_count) {
   if (!stats || width <= 0 || height <= 0 || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
-  const double S = sm_count > 0 ? (double)sm_count : 148.0;
-  const int pixels = pw * ph;
-  const double k = pixels <= 128 ? 12.0 : (pixels <= 256 ? 6.0 : 3.0);  // resident tile CTAs per SM
-  const double rho = 0.75, c0 = 64.0;
-  const double sumL = (double)stats->total;
-  const double balanced = sumL / (S * k);
-  const double t_static = fmax((double)stats->max, balanced);
-  const double t_fine = rho * balanced + c0;
-  return t_static > t_fine ? BS_FINE_GRAINED_COMBINED : BS_SHARED_MEM_OPT;
+  return bs::select_variant_formula(stats->total, stats->max, pw, ph, sm_count);
+}
+
+namespace bs {
+__global__ void k_select_variant(const bs_tile_histogram* __restrict__ stats, int pw, int ph, int sm_count,
+                                 int32_t* __restrict__ variant) {
+  *variant = select_variant_formula(stats->total, stats->max, pw, ph, sm_count);
+}
+}  // namespace bs
+
+extern "C" int bs_select_variant_device(const bs_tile_histogram* stats, int32_t width, int32_t height, int32_t pw,
+                                        int32_t ph, int32_t sm_count, int32_t* variant, void* stream) {
+  if (!stats || !variant || width <= 0 || height <= 0 || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
+  bs::k_select_variant<<<1, 1, 0, (cudaStream_t)stream>>>(stats, pw, ph, sm_count, variant);
+  BS_LAUNCH_CHECK();
+  return BS_OK;
 }

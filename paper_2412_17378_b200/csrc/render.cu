@@ -64,7 +64,12 @@ struct RArgs {
   int total_tasks;
   int donate_after;       // list entries a task walks before it may hand off
   int donate_min_remain;  // ... and only if this many entries remain
+  const int32_t* gate;    // device-selected variant (bs_render_forward_auto) or null
 };
+
+// Sync-free auto mode: every candidate kernel is launched and all but the
+// device-selected one return at once.
+__device__ __forceinline__ bool gated_out(const RArgs& A, int variant) { return A.gate && *A.gate != variant; }
 
 // R1 eval_alpha + the power>0 arm + skip rule (src/blend.cpp:8-21, 90).
 // Returns true when the step is NOT skipped; alpha is the reference's alpha.
@@ -248,6 +253,7 @@ __device__ __forceinline__ void pixelwise_tile(const RArgs& A, int tile, float4*
 
 template <int MODE, bool STAGE_COLOR, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_render_pixelwise(RArgs A) {
+  if (gated_out(A, STAGE_COLOR ? BS_SHARED_MEM_OPT : BS_NAIVE)) return;
   constexpr int CHUNK = PwChunk<MODE, STAGE_COLOR, BLOCK>::value;
   __shared__ float4 s_xyab[CHUNK];
   __shared__ float4 s_cop[CHUNK];
@@ -267,6 +273,7 @@ __global__ void __launch_bounds__(BLOCK) k_render_dynamic(RArgs A) {
   __shared__ uint32_t s_id[BLOCK];
   __shared__ unsigned long long s_tab[32];
   __shared__ int s_tile;
+  if (gated_out(A, BS_DYNAMIC_BLOCKS)) return;
   load_tab(s_tab);
   for (;;) {
     __syncthreads();
@@ -408,6 +415,7 @@ __global__ void __launch_bounds__(kFgThreads) k_render_gaussianwise(RArgs A) {
   __shared__ float4 s_cop[kFgThreads];
   __shared__ float4 s_rgb[kFgThreads];
   __shared__ unsigned long long s_tab[32];
+  if (gated_out(A, BS_GAUSSIAN_WISE)) return;
   load_tab(s_tab);
   const int tile = blockIdx.x;
   const int subs = (A.pw * A.ph + kFgWarps - 1) / kFgWarps;
@@ -632,6 +640,7 @@ __global__ void __launch_bounds__(kFineThreads) k_render_fine(RArgs A, int subs)
   __shared__ float4 s_rec[kFineWarps][4][32];
   __shared__ int s_k[kFineWarps][32];
   __shared__ unsigned long long s_tab[32];
+  if (gated_out(A, BS_FINE_GRAINED_COMBINED)) return;
   load_tab(s_tab);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -659,6 +668,7 @@ __global__ void __launch_bounds__(kFineThreads) k_render_donated(RArgs A) {
   __shared__ float4 s_rgb[kFineThreads];
   __shared__ unsigned long long s_tab[32];
   __shared__ unsigned s_task;
+  if (gated_out(A, BS_FINE_GRAINED_COMBINED)) return;
   load_tab(s_tab);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned ntasks = *(volatile unsigned*)(A.queue + 3);
@@ -827,12 +837,11 @@ extern "C" size_t bs_render_workspace_bytes(int32_t width, int32_t height) {
   return 256 + sizeof(Donation) * P + sizeof(uint2) * (P / 4 + 1);  // >= 9 pixels -> <= 2 units per 9
 }
 
-extern "C" int bs_render_forward(int variant, int alpha_mode, bs_splats g, const uint32_t* point_list,
-                                 const uint32_t* tile_ranges, const uint32_t* task_order, int32_t width,
-                                 int32_t height, int32_t pw, int32_t ph, const float bg[3], bs_frame_out out,
-                                 void* ws, size_t ws_bytes, void* stream) {
+static int render_impl(int variant, const int32_t* gate, int alpha_mode, bs_splats g, const uint32_t* point_list,
+                       const uint32_t* tile_ranges, const uint32_t* task_order, int32_t width, int32_t height,
+                       int32_t pw, int32_t ph, const float bg[3], bs_frame_out out, void* ws, size_t ws_bytes,
+                       void* stream) {
   if (width <= 0 || height <= 0 || pw <= 0 || ph <= 0 || !bg || !tile_ranges) return BS_ERR_INVALID_ARGUMENT;
-  if (variant < 0 || variant > 4) return BS_ERR_INVALID_ARGUMENT;
   if (alpha_mode != BS_ALPHA_EXACT && alpha_mode != BS_ALPHA_FAST) return BS_ERR_INVALID_ARGUMENT;
   if (!out.color || !out.alpha || !out.depth || !out.final_t || !out.contrib || !out.term) return BS_ERR_INVALID_ARGUMENT;
   if ((int64_t)pw * ph > 1024) return BS_ERR_UNSUPPORTED;
@@ -857,11 +866,38 @@ extern "C" int bs_render_forward(int variant, int alpha_mode, bs_splats g, const
   A.donate = reinterpret_cast<Donation*>(static_cast<char*>(ws) + 256);
   A.donated_tasks = reinterpret_cast<uint2*>(A.donate + (size_t)width * height);
   A.total_tasks = 0;
-  if (variant == BS_DYNAMIC_BLOCKS || variant == BS_FINE_GRAINED_COMBINED)
+  A.gate = gate;
+  if (gate || variant == BS_DYNAMIC_BLOCKS || variant == BS_FINE_GRAINED_COMBINED)
     BS_CUDA_TRY(cudaMemsetAsync(ws, 0, 8 * sizeof(unsigned int), st));
   const int block_pixels = pw * ph;
-  return alpha_mode == BS_ALPHA_EXACT ? launch_variant<BS_ALPHA_EXACT>(variant, A, block_pixels, st)
-                                      : launch_variant<BS_ALPHA_FAST>(variant, A, block_pixels, st);
+  auto launch = [&](int v) {
+    return alpha_mode == BS_ALPHA_EXACT ? launch_variant<BS_ALPHA_EXACT>(v, A, block_pixels, st)
+                                        : launch_variant<BS_ALPHA_FAST>(v, A, block_pixels, st);
+  };
+  if (!gate) return launch(variant);
+  // auto: the selector's two candidates (select_variant_formula)
+  const int s1 = launch(BS_FINE_GRAINED_COMBINED);
+  if (s1 != BS_OK) return s1;
+  return launch(BS_SHARED_MEM_OPT);
+}
+
+extern "C" int bs_render_forward(int variant, int alpha_mode, bs_splats g, const uint32_t* point_list,
+                                 const uint32_t* tile_ranges, const uint32_t* task_order, int32_t width,
+                                 int32_t height, int32_t pw, int32_t ph, const float bg[3], bs_frame_out out,
+                                 void* ws, size_t ws_bytes, void* stream) {
+  if (variant < 0 || variant > 4) return BS_ERR_INVALID_ARGUMENT;
+  return render_impl(variant, nullptr, alpha_mode, g, point_list, tile_ranges, task_order, width, height, pw, ph, bg,
+                     out, ws, ws_bytes, stream);
+}
+
+extern "C" int bs_render_forward_auto(const int32_t* variant_dev, int alpha_mode, bs_splats g,
+                                      const uint32_t* point_list, const uint32_t* tile_ranges,
+                                      const uint32_t* task_order, int32_t width, int32_t height, int32_t pw,
+                                      int32_t ph, const float bg[3], bs_frame_out out, void* ws, size_t ws_bytes,
+                                      void* stream) {
+  if (!variant_dev) return BS_ERR_INVALID_ARGUMENT;
+  return render_impl(-1, variant_dev, alpha_mode, g, point_list, tile_ranges, task_order, width, height, pw, ph, bg,
+                     out, ws, ws_bytes, stream);
 }
 
 namespace bs {

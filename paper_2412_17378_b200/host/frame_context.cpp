@@ -16,6 +16,8 @@
 
 #include "splatsim_b200.h"
 
+constexpr int kStages = 6;  // preprocess, bin_count, k_readback, bin_sort, stats_select, render
+
 struct bs_context {
   int alpha_mode = BS_ALPHA_EXACT;
   cudaStream_t stream = nullptr;
@@ -51,6 +53,18 @@ struct bs_context {
   int64_t pixel_cap = 0;
   uint64_t* work_dev = nullptr;
   uint64_t* work_host = nullptr;  // pinned
+  int32_t* variant_dev = nullptr;
+  int32_t* variant_host = nullptr;  // pinned
+  cudaStream_t user_stream = nullptr;
+  bool use_user_stream = false;
+  // last frame (bs_context_last_info)
+  int32_t last_variant = -1;  // host-known variant, -1 = device-selected
+  int64_t last_k = 0;
+  int last_W = 0, last_H = 0, last_pw = 0, last_ph = 0;
+  // per-stage timing (bs_context_enable_timing)
+  bs_frame_out last_out{};
+  bool timing = false;
+  cudaEvent_t ev[kStages + 1] = {};
 };
 
 namespace {
@@ -112,6 +126,8 @@ extern "C" int bs_context_create(bs_context** out, int alpha_mode) {
       cudaMalloc(reinterpret_cast<void**>(&c->k_dev), 256) != cudaSuccess ||
       cudaMalloc(reinterpret_cast<void**>(&c->stats_dev), sizeof(bs_tile_histogram) + 256) != cudaSuccess ||
       cudaMalloc(reinterpret_cast<void**>(&c->work_dev), 256) != cudaSuccess ||
+      cudaMalloc(reinterpret_cast<void**>(&c->variant_dev), 256) != cudaSuccess ||
+      cudaMallocHost(reinterpret_cast<void**>(&c->variant_host), 256) != cudaSuccess ||
       cudaMallocHost(reinterpret_cast<void**>(&c->k_host), 256) != cudaSuccess ||
       cudaMallocHost(reinterpret_cast<void**>(&c->stats_host), sizeof(bs_tile_histogram) + 256) != cudaSuccess ||
       cudaMallocHost(reinterpret_cast<void**>(&c->work_host), 256) != cudaSuccess) {
@@ -128,33 +144,64 @@ extern "C" int bs_context_destroy(bs_context* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   void* dev[] = {c->g3d, c->splat[0], c->splat[1], c->splat[2], c->n_visible, c->k_dev, c->pre_ws, c->bin_ws,
                  c->point_list, c->ranges, c->stats_ws, c->order, c->stats_dev, c->render_ws, c->planes[0],
-                 c->planes[1], c->planes[2], c->planes[3], c->iplanes[0], c->iplanes[1], c->work_dev};
+                 c->planes[1], c->planes[2], c->planes[3], c->iplanes[0], c->iplanes[1], c->work_dev,
+                 c->variant_dev};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (c->k_host) cudaFreeHost(c->k_host);
   if (c->stats_host) cudaFreeHost(c->stats_host);
   if (c->work_host) cudaFreeHost(c->work_host);
+  if (c->variant_host) cudaFreeHost(c->variant_host);
+  for (cudaEvent_t e : c->ev)
+    if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return BS_OK;
 }
 
-extern "C" void* bs_context_stream(bs_context* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+extern "C" void* bs_context_stream(bs_context* c) {
+  if (!c) return nullptr;
+  return static_cast<void*>(c->use_user_stream ? c->user_stream : c->stream);
+}
 
-extern "C" int bs_render_frame_host(bs_context* c, const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam,
-                                    int32_t pw, int32_t ph, int32_t variant, const float bg[3], float* color,
-                                    float* alpha, float* depth, float* final_t, int32_t* contrib, int32_t* term,
-                                    bs_frame_info* info) {
-  if (!c || !cam || !bg || n < 0 || (n > 0 && !g3d) || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
-  if (variant < -1 || variant > 4) return BS_ERR_INVALID_ARGUMENT;
+extern "C" int bs_context_set_stream(bs_context* c, void* stream) {
+  if (!c) return BS_ERR_INVALID_ARGUMENT;
+  c->use_user_stream = stream != nullptr;
+  c->user_stream = static_cast<cudaStream_t>(stream);
+  return BS_OK;
+}
+
+extern "C" int bs_context_enable_timing(bs_context* c, int32_t on) {
+  if (!c) return BS_ERR_INVALID_ARGUMENT;
+  if (on && !c->ev[0])
+    for (cudaEvent_t& e : c->ev) CUTRY(cudaEventCreate(&e));
+  c->timing = on != 0;
+  return BS_OK;
+}
+
+extern "C" int bs_context_stage_ms(bs_context* c, float* ms, int32_t n) {
+  if (!c || !ms || n < kStages || !c->timing) return BS_ERR_INVALID_ARGUMENT;
+  CUTRY(cudaEventSynchronize(c->ev[kStages]));
+  for (int i = 0; i < kStages; ++i) CUTRY(cudaEventElapsedTime(&ms[i], c->ev[i], c->ev[i + 1]));
+  return BS_OK;
+}
+
+namespace {
+
+// The whole forward on device input, stream-ordered on the context stream.
+// One host sync (the 8-byte K readback that sizes point_list); variant = -1
+// selects on the device (bs_select_variant_device + bs_render_forward_auto),
+// so no sync follows it.
+int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const bs_camera* cam, int32_t pw, int32_t ph,
+                 int32_t variant, const float bg[3], bs_frame_out fo_in, cudaStream_t st) {
   const int32_t W = cam->width, H = cam->height;
-  if (W <= 0 || H <= 0) return BS_ERR_INVALID_ARGUMENT;
-  cudaStream_t st = c->stream;
   const int64_t cols = (W + pw - 1) / pw, rows = (H + ph - 1) / ph, T = cols * rows;
   const int64_t P = int64_t(W) * H;
-
+  auto mark = [&](int i) {
+    if (c->timing) cudaEventRecord(c->ev[i], st);
+  };
+  mark(0);
   // P1-P4
-  TRY(grow(&c->g3d, &c->g3d_bytes, size_t(std::max<int64_t>(n, 1)) * sizeof(bs_gaussian3d)));
   if (n > c->splat_cap) {
     for (auto& p : c->splat) {
       if (p) cudaFree(p);
@@ -163,11 +210,11 @@ extern "C" int bs_render_frame_host(bs_context* c, const bs_gaussian3d* g3d, int
     for (auto& p : c->splat) CUTRY(cudaMalloc(reinterpret_cast<void**>(&p), size_t(n) * sizeof(float4)));
     c->splat_cap = n;
   }
-  if (n > 0) CUTRY(cudaMemcpyAsync(c->g3d, g3d, size_t(n) * sizeof(bs_gaussian3d), cudaMemcpyHostToDevice, st));
   bs_splats sp{reinterpret_cast<float*>(c->splat[0]), reinterpret_cast<float*>(c->splat[1]),
                reinterpret_cast<float*>(c->splat[2])};
   TRY(grow(&c->pre_ws, &c->pre_ws_bytes, bs_preprocess_workspace_bytes(n)));
-  TRY(bs_preprocess(static_cast<const bs_gaussian3d*>(c->g3d), n, cam, sp, c->n_visible, c->pre_ws, c->pre_ws_bytes, st));
+  TRY(bs_preprocess(g3d_dev, n, cam, sp, c->n_visible, c->pre_ws, c->pre_ws_bytes, st));
+  mark(1);
 
   // P5 count (workspace keyed on n and the tile grid; k part grown below)
   const int key[4] = {W, H, pw, ph};
@@ -179,10 +226,11 @@ extern "C" int bs_render_frame_host(bs_context* c, const bs_gaussian3d* g3d, int
     TRY(grow(&c->bin_ws, &c->bin_ws_bytes, bs_bin_workspace_bytes(c->bin_n, W, H, pw, ph, c->bin_k)));
   }
   TRY(bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, st));
+  mark(2);
   CUTRY(cudaMemcpyAsync(c->k_host, c->k_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   CUTRY(cudaStreamSynchronize(st));
   const int64_t k = *c->k_host;
-  if (k > c->bin_k) {
+  if (k > c->bin_k && bs_bin_workspace_bytes(c->bin_n, W, H, pw, ph, k) > c->bin_ws_bytes) {
     // the count state lives in the workspace: grow, then count again
     c->bin_k = int64_t(double(k) * 1.25) + 1024;
     void* fresh = nullptr;
@@ -193,44 +241,112 @@ extern "C" int bs_render_frame_host(bs_context* c, const bs_gaussian3d* g3d, int
     c->bin_ws_bytes = fresh_bytes;
     TRY(bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, st));
   }
+  mark(3);
   TRY(grow_n(&c->point_list, &c->pl_cap, std::max<int64_t>(k, 1), 1.25));
   TRY(grow_n(&c->ranges, &c->ranges_cap, 2 * T));
   TRY(bs_bin_sort(sp, n, c->n_visible, W, H, pw, ph, k, c->point_list, c->ranges, c->bin_ws, c->bin_ws_bytes, st));
+  mark(4);
 
-  // P6
+  // P6 + selection
   TRY(grow(&c->stats_ws, &c->stats_ws_bytes, bs_tile_stats_workspace_bytes(int32_t(T))));
   TRY(grow_n(&c->order, &c->order_cap, T));
   TRY(bs_tile_stats(c->ranges, int32_t(T), c->stats_dev, nullptr, c->order, c->stats_ws, c->stats_ws_bytes, st));
-  int v = variant;
-  if (v < 0) {
-    CUTRY(cudaMemcpyAsync(c->stats_host, c->stats_dev, sizeof(bs_tile_histogram), cudaMemcpyDeviceToHost, st));
-    CUTRY(cudaStreamSynchronize(st));
-    v = bs_select_variant(c->stats_host, W, H, pw, ph, c->sm_count);
-    if (v < 0) return v;
-  }
+  if (variant < 0) TRY(bs_select_variant_device(c->stats_dev, W, H, pw, ph, c->sm_count, c->variant_dev, st));
+  mark(5);
 
-  // R: render into device planes
-  if (P > c->pixel_cap) {
-    for (auto& p : c->planes) {
-      if (p) cudaFree(p);
-      p = nullptr;
+  // R
+  bs_frame_out fo = fo_in;
+  if (!fo.color) {
+    if (P > c->pixel_cap) {
+      for (auto& p : c->planes) {
+        if (p) cudaFree(p);
+        p = nullptr;
+      }
+      for (auto& p : c->iplanes) {
+        if (p) cudaFree(p);
+        p = nullptr;
+      }
+      CUTRY(cudaMalloc(reinterpret_cast<void**>(&c->planes[0]), size_t(P) * 3 * sizeof(float)));
+      for (int i = 1; i < 4; ++i) CUTRY(cudaMalloc(reinterpret_cast<void**>(&c->planes[i]), size_t(P) * sizeof(float)));
+      for (auto& p : c->iplanes) CUTRY(cudaMalloc(reinterpret_cast<void**>(&p), size_t(P) * sizeof(int32_t)));
+      c->pixel_cap = P;
     }
-    for (auto& p : c->iplanes) {
-      if (p) cudaFree(p);
-      p = nullptr;
-    }
-    CUTRY(cudaMalloc(reinterpret_cast<void**>(&c->planes[0]), size_t(P) * 3 * sizeof(float)));
-    for (int i = 1; i < 4; ++i) CUTRY(cudaMalloc(reinterpret_cast<void**>(&c->planes[i]), size_t(P) * sizeof(float)));
-    for (auto& p : c->iplanes) CUTRY(cudaMalloc(reinterpret_cast<void**>(&p), size_t(P) * sizeof(int32_t)));
-    c->pixel_cap = P;
+    fo = bs_frame_out{c->planes[0], c->planes[1], c->planes[2], c->planes[3], c->iplanes[0], c->iplanes[1]};
   }
-  bs_frame_out fo{c->planes[0], c->planes[1], c->planes[2], c->planes[3], c->iplanes[0], c->iplanes[1]};
-  const size_t rws = bs_render_workspace_bytes(W, H);
-  TRY(grow(&c->render_ws, &c->render_ws_bytes, rws));
-  TRY(bs_render_forward(v, c->alpha_mode, sp, c->point_list, c->ranges, c->order, W, H, pw, ph, bg, fo, c->render_ws,
-                        c->render_ws_bytes, st));
-  if (info) TRY(bs_frame_work(c->iplanes[1], c->iplanes[0], c->ranges, W, H, pw, ph, c->work_dev, st));
+  TRY(grow(&c->render_ws, &c->render_ws_bytes, bs_render_workspace_bytes(W, H)));
+  if (variant < 0)
+    TRY(bs_render_forward_auto(c->variant_dev, c->alpha_mode, sp, c->point_list, c->ranges, c->order, W, H, pw, ph,
+                               bg, fo, c->render_ws, c->render_ws_bytes, st));
+  else
+    TRY(bs_render_forward(variant, c->alpha_mode, sp, c->point_list, c->ranges, c->order, W, H, pw, ph, bg, fo,
+                          c->render_ws, c->render_ws_bytes, st));
+  mark(6);
+  c->last_variant = variant;
+  c->last_k = k;
+  c->last_W = W;
+  c->last_H = H;
+  c->last_pw = pw;
+  c->last_ph = ph;
+  c->last_out = fo;
+  return BS_OK;
+}
 
+int fill_info(bs_context* c, cudaStream_t st, bs_frame_info* info) {
+  if (!c->last_out.term) return BS_ERR_INVALID_ARGUMENT;
+  TRY(bs_frame_work(c->last_out.term, c->last_out.contrib, c->ranges, c->last_W, c->last_H, c->last_pw, c->last_ph,
+                    c->work_dev, st));
+  CUTRY(cudaMemcpyAsync(c->stats_host, c->stats_dev, sizeof(bs_tile_histogram), cudaMemcpyDeviceToHost, st));
+  CUTRY(cudaMemcpyAsync(c->work_host, c->work_dev, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  if (c->last_variant < 0)
+    CUTRY(cudaMemcpyAsync(c->variant_host, c->variant_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  int32_t nv = 0;
+  CUTRY(cudaMemcpyAsync(c->variant_host + 1, c->n_visible, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CUTRY(cudaStreamSynchronize(st));
+  nv = c->variant_host[1];
+  info->variant = c->last_variant < 0 ? c->variant_host[0] : c->last_variant;
+  info->n_visible = nv;
+  info->k = c->last_k;
+  info->stats = *c->stats_host;
+  info->evaluated = c->work_host[0];
+  info->committed = c->work_host[1];
+  return BS_OK;
+}
+
+}  // namespace
+
+extern "C" int bs_render_frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const bs_camera* cam,
+                                      int32_t pw, int32_t ph, int32_t variant, const float bg[3], bs_frame_out out,
+                                      bs_frame_info* info) {
+  if (!c || !cam || !bg || n < 0 || (n > 0 && !g3d_dev) || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
+  if (variant < -1 || variant > 4) return BS_ERR_INVALID_ARGUMENT;
+  if (cam->width <= 0 || cam->height <= 0) return BS_ERR_INVALID_ARGUMENT;
+  const bool own = !out.color && !out.alpha && !out.depth && !out.final_t && !out.contrib && !out.term;
+  if (!own && (!out.color || !out.alpha || !out.depth || !out.final_t || !out.contrib || !out.term))
+    return BS_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(bs_context_stream(c));
+  TRY(frame_device(c, g3d_dev, n, cam, pw, ph, variant, bg, out, st));
+  if (info) TRY(fill_info(c, st, info));
+  return BS_OK;
+}
+
+extern "C" int bs_context_last_info(bs_context* c, bs_frame_info* info) {
+  if (!c || !info) return BS_ERR_INVALID_ARGUMENT;
+  return fill_info(c, static_cast<cudaStream_t>(bs_context_stream(c)), info);
+}
+
+extern "C" int bs_render_frame_host(bs_context* c, const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam,
+                                    int32_t pw, int32_t ph, int32_t variant, const float bg[3], float* color,
+                                    float* alpha, float* depth, float* final_t, int32_t* contrib, int32_t* term,
+                                    bs_frame_info* info) {
+  if (!c || !cam || !bg || n < 0 || (n > 0 && !g3d) || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
+  if (variant < -1 || variant > 4) return BS_ERR_INVALID_ARGUMENT;
+  const int32_t W = cam->width, H = cam->height;
+  if (W <= 0 || H <= 0) return BS_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(bs_context_stream(c));
+  const int64_t P = int64_t(W) * H;
+  TRY(grow(&c->g3d, &c->g3d_bytes, size_t(std::max<int64_t>(n, 1)) * sizeof(bs_gaussian3d)));
+  if (n > 0) CUTRY(cudaMemcpyAsync(c->g3d, g3d, size_t(n) * sizeof(bs_gaussian3d), cudaMemcpyHostToDevice, st));
+  TRY(frame_device(c, static_cast<const bs_gaussian3d*>(c->g3d), n, cam, pw, ph, variant, bg, bs_frame_out{}, st));
   // D2H
   const size_t pb = size_t(P) * sizeof(float);
   if (color) CUTRY(cudaMemcpyAsync(color, c->planes[0], pb * 3, cudaMemcpyDeviceToHost, st));
@@ -239,20 +355,7 @@ extern "C" int bs_render_frame_host(bs_context* c, const bs_gaussian3d* g3d, int
   if (final_t) CUTRY(cudaMemcpyAsync(final_t, c->planes[3], pb, cudaMemcpyDeviceToHost, st));
   if (contrib) CUTRY(cudaMemcpyAsync(contrib, c->iplanes[0], pb, cudaMemcpyDeviceToHost, st));
   if (term) CUTRY(cudaMemcpyAsync(term, c->iplanes[1], pb, cudaMemcpyDeviceToHost, st));
-  if (info) {
-    CUTRY(cudaMemcpyAsync(c->stats_host, c->stats_dev, sizeof(bs_tile_histogram), cudaMemcpyDeviceToHost, st));
-    CUTRY(cudaMemcpyAsync(c->work_host, c->work_dev, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-  }
+  if (info) TRY(fill_info(c, st, info));
   CUTRY(cudaStreamSynchronize(st));
-  if (info) {
-    int32_t nv = 0;
-    CUTRY(cudaMemcpy(&nv, c->n_visible, sizeof(int32_t), cudaMemcpyDeviceToHost));
-    info->variant = v;
-    info->n_visible = nv;
-    info->k = k;
-    info->stats = *c->stats_host;
-    info->evaluated = c->work_host[0];
-    info->committed = c->work_host[1];
-  }
   return BS_OK;
 }

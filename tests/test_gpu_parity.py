@@ -317,3 +317,33 @@ def test_fine_donation_path(after, remain, monkeypatch):
             assert 1.0 - match.mean() < 2e-3
             err = np.abs(got["color"] - ref["color"]).reshape(-1, 3).max(axis=1)
             assert err[match].max() <= 1e-4
+
+
+@pytest.mark.parametrize("n,bgfrac", [(60, 1.0), (8000, 0.12)])
+def test_frame_pipeline_device_selection(n, bgfrac):
+    """bs_render_frame_device with variant=-1: the variant is chosen on the
+    device (bs_select_variant_device) and only that kernel renders; the frame
+    equals the oracle's render of the chosen variant and the choice equals the
+    host selector's on the same tile statistics."""
+    W = H = 256
+    g3d, cam = scene(n, W, H, 256.0, bgfrac=bgfrac)
+    g2d = O.project_all(g3d, cam)
+    pl, rg = O.bin_tiles(g2d, W, H, 16, 16)
+    fp = api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT)
+    frame, fi = fp.forward(api.g3d_to_device(g3d), n, ncam(cam), variant="auto", bg=(0.1, 0.2, 0.3), info=True)
+    got = frame.to_numpy()
+    v_host = N.lib().bs_select_variant(C.byref(fi.stats), W, H, 16, 16, api.sm_count())
+    assert fi.variant == v_host and fi.k == len(pl)
+    ref = O.render(fi.variant, pl, rg, g2d, W, H, 16, 16, (0.1, 0.2, 0.3), lazy=True, threads=0)
+    for k in ("contrib", "term", "final_t", "alpha"):
+        assert np.array_equal(got[k], ref[k]), k
+    assert float(np.abs(got["color"] - ref["color"]).max()) <= 1e-6
+    # forced variants through the same context
+    for v in (BS_FG, BS_SMO):
+        frame, fi2 = fp.forward(api.g3d_to_device(g3d), n, ncam(cam), variant=v, bg=(0.1, 0.2, 0.3), info=True)
+        assert fi2.variant == v
+        assert np.array_equal(frame.to_numpy()["contrib"], ref["contrib"])
+    fp.close()
+
+
+BS_FG, BS_SMO = 3, 4
