@@ -177,6 +177,14 @@ size_t bs_tile_stats_workspace_bytes(int32_t tiles);
 int bs_tile_stats(const uint32_t* tile_ranges, int32_t tiles, bs_tile_histogram* stats, uint32_t* counts,
                   uint32_t* task_order, void* ws, size_t ws_bytes, void* stream);
 
+/* Frame-pipeline form of the above (one launch, T <= 32768): sum / max /
+ * mean / nonempty in *stats (device; min, p50, p99 left 0) and task_order =
+ * tiles by eighth-octave length bucket descending, tile id ascending within a
+ * bucket (lengths inside a bucket differ by < 9 %: an LPT order for the
+ * fine-grained queue without a full sort). */
+int bs_tile_order(const uint32_t* tile_ranges, int32_t tiles, bs_tile_histogram* stats, uint32_t* task_order,
+                  void* stream);
+
 /* ---- R1-R8: forward render ----
  * variant: bs_variant (not AUTO).  task_order: LPT tile order from
  * bs_tile_stats (required for BS_FINE_GRAINED_COMBINED, ignored otherwise;

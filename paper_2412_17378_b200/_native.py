@@ -67,6 +67,7 @@ SIGNATURES = {
     "bs_bin_sort": (C.c_int, [Splats, _i64, _vp, _i32, _i32, _i32, _i32, _i64, _vp, _vp, _vp, _sz, _vp]),
     "bs_tile_stats_workspace_bytes": (_sz, [_i32]),
     "bs_tile_stats": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "bs_tile_order": (C.c_int, [_vp, _i32, _vp, _vp, _vp]),
     "bs_render_workspace_bytes": (_sz, [_i32, _i32]),
     "bs_render_forward": (C.c_int, [C.c_int, C.c_int, Splats, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _f32p,
                                     FrameOut, _vp, _sz, _vp]),

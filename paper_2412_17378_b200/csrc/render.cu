@@ -853,7 +853,7 @@ static int render_impl(int variant, const int32_t* gate, int alpha_mode, bs_spla
   A.rgbr = reinterpret_cast<const float4*>(g.rgbr);
   A.point_list = point_list;
   A.ranges = tile_ranges;
-  A.task_order = task_order;
+  A.task_order = env_int("BS_FINE_NO_LPT", 0) ? nullptr : task_order;  // A/B: index order
   A.W = width; A.H = height; A.pw = pw; A.ph = ph;
   A.cols = (width + pw - 1) / pw;
   const int64_t T = (int64_t)A.cols * ((height + ph - 1) / ph);

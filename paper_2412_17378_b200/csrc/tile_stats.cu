@@ -62,6 +62,92 @@ __global__ void __launch_bounds__(1024) k_stats_finish(const uint32_t* __restric
   }
 }
 
+// Frame-pipeline form (bs_tile_order): one CTA, counts -> sum / max / nonempty
+// and a stable counting sort of the tiles by an eighth-octave length bucket,
+// longest bucket first, tile id ascending inside a bucket.  Lengths within a
+// bucket differ by < 9 %, which is all the LPT queue order needs.
+constexpr int kOrderBuckets = 256;
+constexpr int kOrderMaxTiles = 32768;
+
+__device__ __forceinline__ uint32_t len_bucket(uint32_t c) {
+  const uint32_t v = c + 1u;  // >= 1
+  const uint32_t e = 31u - __clz(v);
+  return e < 3u ? v : min(8u * e + ((v >> (e - 3u)) & 7u), (uint32_t)kOrderBuckets - 1u);
+}
+
+__global__ void __launch_bounds__(1024) k_tile_order(const uint32_t* __restrict__ ranges, int T,
+                                                     uint32_t* __restrict__ order_out,
+                                                     bs_tile_histogram* __restrict__ out) {
+  __shared__ uint32_t s_cnt[32][kOrderBuckets];  // (warp, bucket) counts, then bases
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 32 * kOrderBuckets; i += 1024) (&s_cnt[0][0])[i] = 0;
+  __syncthreads();
+  const int per = (T + 31) / 32, t0 = warp * per, t1 = min(T, t0 + per);  // warp's contiguous tile range
+  unsigned long long sum = 0, nonempty = 0;
+  uint32_t mx = 0;
+  for (int t = t0 + lane; t < t1; t += 32) {
+    const uint32_t c = ranges[2 * t + 1] - ranges[2 * t];
+    sum += c;
+    nonempty += c > 0;
+    mx = max(mx, c);
+    atomicAdd(&s_cnt[warp][len_bucket(c)], 1u);
+  }
+  sum = block_reduce_sum(sum);
+  nonempty = block_reduce_sum(nonempty);
+  {
+    __shared__ uint32_t s_max[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) s_max[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t m = 0;
+      for (int w = 0; w < 32; ++w) m = max(m, s_max[w]);
+      bs_tile_histogram s;
+      s.tiles = T;
+      s.total = sum;
+      s.nonempty = (int32_t)nonempty;
+      s.max = m;
+      s.min = s.p50 = s.p99 = 0;  // order statistics: bs_tile_stats
+      s.mean = T ? (double)sum / (double)T : 0.0;
+      *out = s;
+    }
+  }
+  // bases: buckets descending, warps ascending inside a bucket
+  {
+    const int b = kOrderBuckets - 1 - tid;  // threads 0..255 walk buckets high -> low
+    uint32_t tot = 0;
+    if (tid < kOrderBuckets)
+      for (int w = 0; w < 32; ++w) tot += s_cnt[w][b];
+    uint32_t all;
+    const uint32_t start = block_exclusive_scan<uint32_t>(tid < kOrderBuckets ? tot : 0u, &all);
+    if (tid < kOrderBuckets) {
+      uint32_t run = start;
+      for (int w = 0; w < 32; ++w) {
+        const uint32_t c = s_cnt[w][b];
+        s_cnt[w][b] = run;
+        run += c;
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t lt = lanemask_lt();
+  for (int base = t0; base < t1; base += 32) {
+    const int t = base + lane;
+    const bool act = t < t1;
+    const uint32_t bk = act ? len_bucket(ranges[2 * t + 1] - ranges[2 * t]) : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, bk);
+    uint32_t pos = 0;
+    if (act) {
+      pos = s_cnt[warp][bk] + __popc(peers & lt);
+      order_out[pos] = (uint32_t)t;
+    }
+    __syncwarp();
+    if (act && (peers >> lane) == 1u) s_cnt[warp][bk] = pos + 1;
+    __syncwarp();
+  }
+}
+
 template <typename C>
 inline void stats_ws_layout(C& c, int64_t T, uint32_t** k0, uint32_t** v0, uint32_t** k1, uint32_t** v1,
                             uint32_t** counts, RadixWs* rw) {
@@ -108,6 +194,15 @@ extern "C" int bs_tile_stats(const uint32_t* tile_ranges, int32_t tiles, bs_tile
   } else {
     k_stats_finish<<<1, 1024, 0, st>>>(cnt, nullptr, 0, stats);
   }
+  BS_LAUNCH_CHECK();
+  return BS_OK;
+}
+
+extern "C" int bs_tile_order(const uint32_t* tile_ranges, int32_t tiles, bs_tile_histogram* stats,
+                             uint32_t* task_order, void* stream) {
+  if (tiles < 0 || !stats || !task_order || (tiles > 0 && !tile_ranges)) return BS_ERR_INVALID_ARGUMENT;
+  if (tiles > kOrderMaxTiles) return BS_ERR_UNSUPPORTED;
+  k_tile_order<<<1, 1024, 0, (cudaStream_t)stream>>>(tile_ranges, tiles, task_order, stats);
   BS_LAUNCH_CHECK();
   return BS_OK;
 }

@@ -250,7 +250,10 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   // P6 + selection
   TRY(grow(&c->stats_ws, &c->stats_ws_bytes, bs_tile_stats_workspace_bytes(int32_t(T))));
   TRY(grow_n(&c->order, &c->order_cap, T));
-  TRY(bs_tile_stats(c->ranges, int32_t(T), c->stats_dev, nullptr, c->order, c->stats_ws, c->stats_ws_bytes, st));
+  if (T <= 32768)  // LPT order at eighth-octave granularity + the selector's inputs, one launch
+    TRY(bs_tile_order(c->ranges, int32_t(T), c->stats_dev, c->order, st));
+  else
+    TRY(bs_tile_stats(c->ranges, int32_t(T), c->stats_dev, nullptr, c->order, c->stats_ws, c->stats_ws_bytes, st));
   if (variant < 0) TRY(bs_select_variant_device(c->stats_dev, W, H, pw, ph, c->sm_count, c->variant_dev, st));
   mark(5);
 
@@ -295,6 +298,9 @@ int fill_info(bs_context* c, cudaStream_t st, bs_frame_info* info) {
   if (!c->last_out.term) return BS_ERR_INVALID_ARGUMENT;
   TRY(bs_frame_work(c->last_out.term, c->last_out.contrib, c->ranges, c->last_W, c->last_H, c->last_pw, c->last_ph,
                     c->work_dev, st));
+  // full tile_load_histogram (order statistics too) on request only
+  const int32_t T = int32_t(((c->last_W + c->last_pw - 1) / c->last_pw) * ((c->last_H + c->last_ph - 1) / c->last_ph));
+  TRY(bs_tile_stats(c->ranges, T, c->stats_dev, nullptr, nullptr, c->stats_ws, c->stats_ws_bytes, st));
   CUTRY(cudaMemcpyAsync(c->stats_host, c->stats_dev, sizeof(bs_tile_histogram), cudaMemcpyDeviceToHost, st));
   CUTRY(cudaMemcpyAsync(c->work_host, c->work_dev, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   if (c->last_variant < 0)

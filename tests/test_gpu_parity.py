@@ -147,22 +147,27 @@ def test_binning_depth_ties_and_empty():
     assert e.k == 0 and not e.tile_ranges.cpu().numpy().any()
 
 
-def test_tile_stats_match_oracle():
-    g3d, cam = scene(30000, 960, 540, 960.0)
+@pytest.mark.parametrize("W,H,pw,ph,n", [(960, 540, 16, 8, 30000),      # 4,080 tiles
+                                         (1920, 1080, 16, 16, 30000),   # 8,160: single-CTA bitonic path
+                                         (3840, 2160, 16, 16, 20000)])  # 32,400: radix path
+def test_tile_stats_match_oracle(W, H, pw, ph, n):
+    g3d, cam = scene(n, W, H, float(W))
     g2d = O.project_all(g3d, cam)
-    pl, rg = O.bin_tiles(g2d, 960, 540, 16, 8)
-    ref = O.tile_load_histogram(rg, 60, 68)
-    b = api.bin_tiles(to_dev_splats(g2d), 960, 540, 16, 8)
+    pl, rg = O.bin_tiles(g2d, W, H, pw, ph)
+    cols, rows = (W + pw - 1) // pw, (H + ph - 1) // ph
+    T = cols * rows
+    ref = O.tile_load_histogram(rg, cols, rows)
+    b = api.bin_tiles(to_dev_splats(g2d), W, H, pw, ph)
     st = api.tile_load_histogram(b)
     s = st.summary()
     for k in ("min", "max", "p50", "p99"):
         assert s[k] == ref[k], k
     assert s["mean"] == ref["mean"]
-    assert s["tiles"] == 4080
-    counts = st.counts.cpu().numpy().view(np.uint32)[:4080]
+    assert s["tiles"] == T
+    counts = st.counts.cpu().numpy().view(np.uint32)[:T]
     assert np.array_equal(counts, ref["counts"])
-    order = st.task_order.cpu().numpy()[:4080]
-    exp = np.lexsort((np.arange(4080), -ref["counts"].astype(np.int64)))
+    order = st.task_order.cpu().numpy()[:T]
+    exp = np.lexsort((np.arange(T), -ref["counts"].astype(np.int64)))
     assert np.array_equal(order, exp)
 
 
@@ -347,3 +352,37 @@ def test_frame_pipeline_device_selection(n, bgfrac):
 
 
 BS_FG, BS_SMO = 3, 4
+
+
+def _len_bucket(c):
+    out = np.empty(len(c), dtype=np.int64)
+    for i, x in enumerate(c.tolist()):
+        v = x + 1
+        e = v.bit_length() - 1
+        out[i] = v if e < 3 else min(8 * e + ((v >> (e - 3)) & 7), 255)
+    return out
+
+
+@pytest.mark.parametrize("W,H,n", [(1920, 1080, 100_000), (3840, 2160, 20_000), (64, 64, 0)])
+def test_tile_order_lpt_buckets(W, H, n):
+    """bs_tile_order: sum/max/mean/nonempty as tile_load_histogram, and the
+    task order = stable sort by eighth-octave length bucket, descending."""
+    cols, rows = (W + 15) // 16, (H + 15) // 16
+    T = cols * rows
+    if n:
+        g3d, cam = scene(n, W, H, W / 2.0)
+        g2d = O.project_all(g3d, cam)
+    else:
+        g2d = np.zeros(0, dtype=O.G2D_DTYPE)
+    pl, rg = O.bin_tiles(g2d, W, H, 16, 16)
+    ref = O.tile_load_histogram(rg, cols, rows)
+    rgd = torch.from_numpy(rg.view(np.int32).copy()).to(DEV)
+    hist = torch.zeros(64, dtype=torch.uint8, device=DEV)
+    order = torch.empty(T, dtype=torch.int32, device=DEV)
+    N.call("bs_tile_order", rgd.data_ptr(), T, hist.data_ptr(), order.data_ptr(), api._stream(DEV))
+    h = N.TileHistogram.from_buffer_copy(hist.cpu().numpy().tobytes()[: C.sizeof(N.TileHistogram)])
+    assert h.total == len(pl) and h.max == ref["max"] and h.mean == ref["mean"] and h.tiles == T
+    assert h.nonempty == int((ref["counts"] > 0).sum())
+    b = _len_bucket(ref["counts"])
+    exp = np.lexsort((np.arange(T), -b))
+    assert np.array_equal(order.cpu().numpy(), exp)
