@@ -230,6 +230,7 @@ def main():
     ap.add_argument("--alpha", default="exact", choices=["exact", "fast"])
     ap.add_argument("--variant", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sync-frames", action="store_true", help="wait for K inside each frame (no async mode)")
     ap.add_argument("--no-extras", action="store_true", help="skip per-variant sweep / e2e / cpu baseline")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
@@ -261,7 +262,9 @@ def main():
     g3d = api.gen_clustered_scene(n, cam0, cluster_sigma=sig, background_fraction=bgf)
     g3d_dev = api.g3d_to_device(g3d, dev)  # scene replica, uploaded once (outside timing)
     cams = [api.camera(orbit_view(k), (f, f), W, H) for k in range(N_VIEWS)]
-    fp = api.FramePipeline(W, H, pw, ph, dev, mode)  # the native frame pipeline (one C-ABI call per view)
+    # the native frame pipeline: one C-ABI call per view, no host wait inside a
+    # frame (async mode: K verified one call later, overflowed frames re-rendered)
+    fp = api.FramePipeline(W, H, pw, ph, dev, mode, async_mode=not args.sync_frames)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def view_of(i):
@@ -282,14 +285,17 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    reruns_warm = fp.sync()
     launches0 = N.lib().bs_kernel_launches()
     for i in range(args.steps):
         flush.zero_()  # L2 flush between timed steps (untimed)
         starts[i].record()
         step(args.warmup + i)
         ends[i].record()
+    fp.sync()  # verifies the last timed frame (a re-render would be enqueued before the sync point)
     torch.cuda.synchronize()
     launches = int(N.lib().bs_kernel_launches() - launches0)
+    reruns = fp.sync() - reruns_warm
     # which variant the on-device selector picked for each timed view (replayed untimed)
     for i in range(args.steps):
         _, fi = fp.forward(g3d_dev, n, cams[view_of(args.warmup + i)], variant=variant, info=True)
@@ -297,7 +303,8 @@ def main():
     if world > 1:
         dist.barrier()
     clocks = clk.stop()
-    total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -331,6 +338,8 @@ def main():
                        parallelism=f"view-sharded x{world} (scene replicated, no data-path collective)",
                        l2="flushed between timed steps (256 MiB write, untimed)"),
         "gpu_launches": launches,
+        "async_reruns": reruns,
+        "step_ms_p50_max": [round(float(np.median(step_ms)), 4), round(float(max(step_ms)), 4)],
         "clocks": clocks,
     }
     out.update(extras)

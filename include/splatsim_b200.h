@@ -168,6 +168,16 @@ int bs_bin_sort(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t wi
                 int32_t ph, int64_t k, uint32_t* point_list, uint32_t* tile_ranges, void* ws, size_t ws_bytes,
                 void* stream);
 
+/* Sync-free form of bs_bin_sort (chunked path; bs_bin_async_supported says
+ * whether the grid qualifies): K stays on the device and point_list holds
+ * k_cap entries.  If K > k_cap nothing is written to point_list and every
+ * tile range is written empty; the caller reads K (the k_total of the
+ * matching bs_bin_count) later, grows point_list and runs again. */
+int bs_bin_sort_async(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height, int32_t pw,
+                      int32_t ph, int64_t k_cap, uint32_t* point_list, uint32_t* tile_ranges, void* ws,
+                      size_t ws_bytes, void* stream);
+int bs_bin_async_supported(int32_t width, int32_t height, int32_t pw, int32_t ph);
+
 /* ---- P6: tile statistics + LPT task order ----
  * counts[t] = end - start; stats as tile_load_histogram (written to device
  * memory at *stats); task_order = tiles by list length descending, ties by
@@ -273,7 +283,19 @@ int bs_render_frame_host(bs_context* ctx, const bs_gaussian3d* g3d, int64_t n, c
  * the frame and fills it (otherwise bs_context_last_info does that later). */
 int bs_render_frame_device(bs_context* ctx, const bs_gaussian3d* g3d_dev, int64_t n, const bs_camera* cam, int32_t pw,
                            int32_t ph, int32_t variant, const float bg[3], bs_frame_out out, bs_frame_info* info);
+/* Stream for the following frames: NULL = the legacy default stream; the
+ * context's own stream is the value bs_context_stream() returned before. */
 int bs_context_set_stream(bs_context* ctx, void* stream);
+/* Async mode for bs_render_frame_device: no host wait inside a frame.
+ * point_list is sized from a capacity (grown to 1.25 x the largest K seen);
+ * a frame's K is checked at the NEXT call on the context (or at
+ * bs_context_sync / bs_context_last_info), and a frame whose K exceeded the
+ * capacity is rendered again then, before anything else, with the same
+ * inputs — so inputs and outputs must stay valid until that next call.
+ * Outputs are final once bs_context_sync returns (reruns = frames re-rendered
+ * so far). */
+int bs_context_set_async(bs_context* ctx, int32_t on);
+int bs_context_sync(bs_context* ctx, int64_t* reruns);
 int bs_context_last_info(bs_context* ctx, bs_frame_info* info);
 /* Per-stage CUDA-event timing of the following frames (6 stages: preprocess,
  * bin_count, k_readback, bin_sort, stats_select, render); bs_context_stage_ms

@@ -359,11 +359,13 @@ class FramePipeline:
     selection for ``variant="auto"``.  Outputs land in ``self.frame``."""
 
     def __init__(self, width: int, height: int, pw: int = 16, ph: int = 16, device="cuda",
-                 alpha_mode: int = ALPHA_EXACT, timing: bool = False):
+                 alpha_mode: int = ALPHA_EXACT, timing: bool = False, async_mode: bool = False):
         self.width, self.height, self.pw, self.ph, self.device = width, height, pw, ph, device
         self.ctx = C.c_void_p()
         N.call("bs_context_create", C.byref(self.ctx), int(alpha_mode))
         N.call("bs_context_set_stream", self.ctx, _stream(device))
+        if async_mode:  # no host wait inside a frame; K checked at the next call (bs_context_set_async)
+            N.call("bs_context_set_async", self.ctx, 1)
         if timing:
             N.call("bs_context_enable_timing", self.ctx, 1)
         self.frame = DeviceFrame.empty(width, height, device)
@@ -376,6 +378,13 @@ class FramePipeline:
         N.call("bs_render_frame_device", self.ctx, _ptr(g3d_dev), int(n), C.byref(cam), self.pw, self.ph, int(v), bgc,
                self.frame.c(), C.byref(fi) if info else None)
         return self.frame, fi
+
+    def sync(self) -> int:
+        """Finish every pending frame (re-rendering any whose K overflowed the
+        point_list capacity); returns the number of such re-renders so far."""
+        r = C.c_int64(0)
+        N.call("bs_context_sync", self.ctx, C.byref(r))
+        return int(r.value)
 
     def last_info(self) -> N.FrameInfo:
         fi = N.FrameInfo()

@@ -293,8 +293,11 @@ constexpr size_t kMaxScatterSmem = 200 * 1024;           // offsets row (T u32) 
 // offset c*q falls in (offs[j-1], offs[j]]; the last touching splat also
 // marks every chunk past its own offset.  One coalesced pass, no searches.
 __global__ void k_chunk_bounds(const uint64_t* __restrict__ offs, const uint32_t* __restrict__ touched_sorted,
-                               int64_t n_cap, const int32_t* __restrict__ n_visible, int64_t q, int nchunks,
-                               uint32_t* __restrict__ first) {
+                               int64_t n_cap, const int32_t* __restrict__ n_visible, const uint64_t* __restrict__ kd,
+                               int64_t k_cap, int nchunks, uint32_t* __restrict__ first) {
+  const uint64_t K = *kd;
+  if (K == 0 || K > (uint64_t)k_cap) return;  // nothing to do / point_list too small (bs_bin_sort_async)
+  const int64_t q = (int64_t)((K + (uint64_t)nchunks - 1) / (uint64_t)nchunks);
   const int64_t n = min((int64_t)*n_visible, n_cap);
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n || touched_sorted[j] == 0) return;
@@ -309,7 +312,9 @@ __global__ void k_chunk_bounds(const uint64_t* __restrict__ offs, const uint32_t
 
 __global__ void __launch_bounds__(kScThreads) k_chunk_hist(const uint2* __restrict__ rects_sorted,
                                                            const uint32_t* __restrict__ first, Grid g,
-                                                           uint32_t* __restrict__ m) {
+                                                           uint32_t* __restrict__ m, const uint64_t* __restrict__ kd,
+                                                           int64_t k_cap) {
+  if (*kd == 0 || *kd > (uint64_t)k_cap) return;
   extern __shared__ int s_grid[];
   const int stride = g.cols + 1, cells = stride * (g.rows + 1);
   const int c = blockIdx.x, tid = threadIdx.x;
@@ -352,7 +357,9 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_hist(const uint2* __restri
 // independent loads in flight to stream M at HBM rate.
 constexpr int kCsSeg = 32;
 __global__ void __launch_bounds__(kCsSeg * 32) k_chunk_scan(uint32_t* __restrict__ m,
-                                                            const uint32_t* __restrict__ starts, int T, int nchunks) {
+                                                            const uint32_t* __restrict__ starts, int T, int nchunks,
+                                                            const uint64_t* __restrict__ kd, int64_t k_cap) {
+  if (*kd == 0 || *kd > (uint64_t)k_cap) return;
   __shared__ uint32_t s_part[kCsSeg][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = blockIdx.x * 32 + lane;
@@ -389,7 +396,9 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
                                                               const uint32_t* __restrict__ first,
                                                               const uint2* __restrict__ rects_sorted,
                                                               const uint32_t* __restrict__ order, int T, int cols,
-                                                              uint32_t* __restrict__ point_list) {
+                                                              uint32_t* __restrict__ point_list,
+                                                              const uint64_t* __restrict__ kd, int64_t k_cap) {
+  if (*kd == 0 || *kd > (uint64_t)k_cap) return;
   extern __shared__ uint32_t s_off[];
   const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t* row = m + (int64_t)c * T;
@@ -479,10 +488,17 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
   }
 }
 
+// Tile ranges from the exclusive scan of the counts.  On a point_list
+// overflow (kd > k_cap) every range is written empty so a render enqueued
+// behind it reads nothing.
 __global__ void k_ranges(const uint32_t* __restrict__ starts, const uint32_t* __restrict__ counts, int T,
-                         uint32_t* __restrict__ ranges) {
+                         uint32_t* __restrict__ ranges, const uint64_t* __restrict__ kd, int64_t k_cap) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
+  if (kd && *kd > (uint64_t)k_cap) {
+    ranges[2 * t] = ranges[2 * t + 1] = 0u;
+    return;
+  }
   const uint32_t s = starts[t];
   ranges[2 * t] = s;
   ranges[2 * t + 1] = s + counts[t];
@@ -659,22 +675,21 @@ extern "C" int bs_bin_count(bs_splats g, int64_t n_cap, const int32_t* n_visible
   return BS_OK;
 }
 
-extern "C" int bs_bin_sort(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height,
-                           int32_t pw, int32_t ph, int64_t k, uint32_t* point_list, uint32_t* tile_ranges, void* ws,
-                           size_t ws_bytes, void* stream) {
-  (void)g;
-  int s = check_grid(width, height, pw, ph);
-  if (s) return s;
-  if (n_cap < 0 || k < 0 || !n_visible || !tile_ranges || (k > 0 && !point_list)) return BS_ERR_INVALID_ARGUMENT;
-  if (k >= (int64_t)1 << 30) return BS_ERR_CAPACITY;
-  cudaStream_t st = (cudaStream_t)stream;
+// k >= 0: K known on the host (bs_bin_sort).  k < 0: K only on the device
+// (bs_bin_sort_async; chunked path only) and point_list holds k_cap entries.
+static int bin_sort_impl(int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height, int32_t pw,
+                         int32_t ph, int64_t k, int64_t k_cap, uint32_t* point_list, uint32_t* tile_ranges, void* ws,
+                         size_t ws_bytes, cudaStream_t st) {
   const Grid gr = make_grid(width, height, pw, ph);
   const int64_t T = (int64_t)gr.cols * gr.rows;
-  if (!ws || ws_bytes < bs_bin_workspace_bytes(n_cap, width, height, pw, ph, k)) return BS_ERR_WORKSPACE;
+  if (!ws || ws_bytes < bs_bin_workspace_bytes(n_cap, width, height, pw, ph, k < 0 ? 0 : k)) return BS_ERR_WORKSPACE;
   WsCarver c(ws, ws_bytes);
   BinWs w;
-  bin_ws_layout(c, n_cap, gr, k, &w);
-  if (k > 0 && bin_chunked(gr)) {
+  bin_ws_layout(c, n_cap, gr, k < 0 ? 0 : k, &w);
+  const uint64_t* kd = w.offs_partials + scan_num_blocks(n_cap);  // K, written by bs_bin_count's scan
+  const bool chunked = bin_chunked(gr);
+  if (k < 0 && !chunked) return BS_ERR_UNSUPPORTED;
+  if ((k > 0 || k < 0) && chunked && k_cap > 0) {
     const uint32_t* order = w.dv0;  // depth order (4 passes end in dv0)
     static bool attr_set = false;
     if (!attr_set) {
@@ -689,23 +704,27 @@ extern "C" int bs_bin_sort(bs_splats g, int64_t n_cap, const int32_t* n_visible,
     BS_CUDA_TRY(cudaGetDevice(&dev));
     BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chunk_scatter, kScThreads, off_bytes));
-    // one wave of chunks (more only for very large K), >= 4096 instances each
+    // one wave of chunks (more only for very large K), >= 4096 instances
+    // each; sized from the capacity when K lives on the device (the chunk
+    // length q = ceil(K / nch) is computed on the device)
+    const int64_t kk = k < 0 ? k_cap : k;
     const int64_t slots = (int64_t)sms * max(1, per_sm);
     static const int64_t min_waves = [] {
       const char* e = getenv("BS_BIN_CHUNK_WAVES");  // tuning override
       return (int64_t)(e ? max(1, atoi(e)) : 1);
     }();
-    const int64_t waves = max(min_waves, (k + slots * (1 << 18) - 1) / (slots * (1 << 18)));
-    const int64_t nch = max((int64_t)1, min(max_chunks(gr), min(slots * waves, (k + 4095) / 4096)));
-    const int64_t q = (k + nch - 1) / nch;
-    k_chunk_bounds<<<(unsigned)((n_cap + 255) / 256), 256, 0, st>>>(w.offs, w.touched_sorted, n_cap, n_visible, q, (int)nch, w.chunk_first);
+    const int64_t waves = max(min_waves, (kk + slots * (1 << 18) - 1) / (slots * (1 << 18)));
+    const int64_t nch = max((int64_t)1, min(max_chunks(gr), min(slots * waves, (kk + 4095) / 4096)));
+    k_chunk_bounds<<<(unsigned)((n_cap + 255) / 256), 256, 0, st>>>(w.offs, w.touched_sorted, n_cap, n_visible, kd,
+                                                                   k_cap, (int)nch, w.chunk_first);
     BS_LAUNCH_CHECK();
-    k_chunk_hist<<<(unsigned)nch, kScThreads, diff_bytes, st>>>(w.rects_sorted, w.chunk_first, gr, w.chunk_m);
+    k_chunk_hist<<<(unsigned)nch, kScThreads, diff_bytes, st>>>(w.rects_sorted, w.chunk_first, gr, w.chunk_m, kd,
+                                                                k_cap);
     BS_LAUNCH_CHECK();
-    k_chunk_scan<<<(unsigned)((T + 31) / 32), kCsSeg * 32, 0, st>>>(w.chunk_m, w.starts, (int)T, (int)nch);
+    k_chunk_scan<<<(unsigned)((T + 31) / 32), kCsSeg * 32, 0, st>>>(w.chunk_m, w.starts, (int)T, (int)nch, kd, k_cap);
     BS_LAUNCH_CHECK();
     k_chunk_scatter<<<(unsigned)nch, kScThreads, off_bytes, st>>>(w.chunk_m, w.chunk_first, w.rects_sorted, order,
-                                                                   (int)T, gr.cols, point_list);
+                                                                   (int)T, gr.cols, point_list, kd, k_cap);
     BS_LAUNCH_CHECK();
   } else if (k > 0) {
     const uint32_t* order = w.dv0;  // depth order (4 passes end in dv0)
@@ -720,7 +739,38 @@ extern "C" int bs_bin_sort(bs_splats g, int64_t n_cap, const int32_t* n_visible,
     BS_CUDA_TRY(radix_sort_pairs(w.tk0, point_list, w.tk1, w.tv_alt, k, nullptr, bits, w.rws_k, &alt, st));
     if (alt) BS_CUDA_TRY(cudaMemcpyAsync(point_list, w.tv_alt, sizeof(uint32_t) * (size_t)k, cudaMemcpyDeviceToDevice, st));
   }
-  k_ranges<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(w.starts, w.counts, (int)T, tile_ranges);
+  k_ranges<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(w.starts, w.counts, (int)T, tile_ranges,
+                                                        n_cap > 0 ? kd : nullptr, k < 0 ? k_cap : k);
   BS_LAUNCH_CHECK();
   return BS_OK;
+}
+
+extern "C" int bs_bin_sort(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height,
+                           int32_t pw, int32_t ph, int64_t k, uint32_t* point_list, uint32_t* tile_ranges, void* ws,
+                           size_t ws_bytes, void* stream) {
+  (void)g;
+  int s = check_grid(width, height, pw, ph);
+  if (s) return s;
+  if (n_cap < 0 || k < 0 || !n_visible || !tile_ranges || (k > 0 && !point_list)) return BS_ERR_INVALID_ARGUMENT;
+  if (k >= (int64_t)1 << 30) return BS_ERR_CAPACITY;
+  return bin_sort_impl(n_cap, n_visible, width, height, pw, ph, k, k, point_list, tile_ranges, ws, ws_bytes,
+                       (cudaStream_t)stream);
+}
+
+extern "C" int bs_bin_sort_async(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height,
+                                 int32_t pw, int32_t ph, int64_t k_cap, uint32_t* point_list, uint32_t* tile_ranges,
+                                 void* ws, size_t ws_bytes, void* stream) {
+  (void)g;
+  int s = check_grid(width, height, pw, ph);
+  if (s) return s;
+  if (n_cap < 0 || k_cap < 0 || !n_visible || !tile_ranges || (k_cap > 0 && !point_list))
+    return BS_ERR_INVALID_ARGUMENT;
+  if (k_cap >= (int64_t)1 << 30) return BS_ERR_CAPACITY;
+  return bin_sort_impl(n_cap, n_visible, width, height, pw, ph, -1, k_cap, point_list, tile_ranges, ws, ws_bytes,
+                       (cudaStream_t)stream);
+}
+
+extern "C" int bs_bin_async_supported(int32_t width, int32_t height, int32_t pw, int32_t ph) {
+  if (check_grid(width, height, pw, ph)) return 0;
+  return bin_chunked(make_grid(width, height, pw, ph)) ? 1 : 0;
 }

@@ -81,4 +81,35 @@ __device__ __forceinline__ float glibc_expf_inrange(float x, const unsigned long
   return __float_as_uint(x) == 0xC27C65D9u ? __uint_as_float(0x11FA2993u) : out;
 }
 
+// Loop-invariant operands of glibc_expf_fast: the double constants live in
+// __constant__ memory so every FP64 instruction takes them as a constant-bank
+// operand (immediate 64-bit constants are re-materialised through uniform
+// registers on every call otherwise), and the table's shared-memory pointer.
+__constant__ double c_expf_k[4] = {0x1.71547652b82fep+0 * 32.0, 0x1.c6af84b912394p-5 / 32.0 / 32.0 / 32.0,
+                                   0x1.ebfce50fac4f3p-3 / 32.0 / 32.0, 0x1.62e42ff0c52d6p-1 / 32.0};
+
+struct ExpK {
+  const unsigned long long* tab;
+};
+
+__device__ __forceinline__ ExpK make_expk(const unsigned long long* s_tab) { return ExpK{s_tab}; }
+
+// glibc_expf_inrange with constant-bank operands (same operations, same bits).
+__device__ __forceinline__ float glibc_expf_fast(float x, const ExpK& k) {
+  const double kShift = 0x1.8p+52;
+  const double z = __dmul_rn(c_expf_k[0], (double)x);
+  const double kds = __dadd_rn(z, kShift);
+  const unsigned lo = (unsigned)__double2loint(kds);
+  const double r = __dsub_rn(z, __dsub_rn(kds, kShift));
+  const unsigned long long tv = k.tab[lo & 31u];
+  const double s = __hiloint2double((int)((unsigned)(tv >> 32) + (lo << 15)), (int)(unsigned)tv);
+  const double zz = __fma_rn(c_expf_k[1], r, c_expf_k[2]);
+  const double r2 = __dmul_rn(r, r);
+  double y = __fma_rn(c_expf_k[3], r, 1.0);
+  y = __fma_rn(zz, r2, y);
+  y = __dmul_rn(y, s);
+  const float out = __double2float_rn(y);
+  return __float_as_uint(x) == 0xC27C65D9u ? __uint_as_float(0x11FA2993u) : out;
+}
+
 }  // namespace bs

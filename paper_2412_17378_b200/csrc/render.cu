@@ -75,7 +75,7 @@ __device__ __forceinline__ bool gated_out(const RArgs& A, int variant) { return 
 // Returns true when the step is NOT skipped; alpha is the reference's alpha.
 template <int MODE>
 __device__ __forceinline__ bool eval_step(const float4 a, const float4 c, float sx, float sy,
-                                          const unsigned long long* tab, float& alpha) {
+                                          const ExpK& ek, float& alpha) {
   const float dx = __fsub_rn(sx, a.x);
   const float dy = __fsub_rn(sy, a.y);
   const float q = __fadd_rn(__fmul_rn(__fmul_rn(a.z, dx), dx), __fmul_rn(__fmul_rn(c.x, dy), dy));
@@ -84,7 +84,7 @@ __device__ __forceinline__ bool eval_step(const float4 a, const float4 c, float 
   if (power > 0.0f) return false;   // alpha forced to 0 -> skipped
   float e;
   if (MODE == BS_ALPHA_EXACT) {
-    e = glibc_expf_inrange(power, tab);  // power in [power_cut, 0], power_cut >= -103.97
+    e = glibc_expf_fast(power, ek);  // power in [power_cut, 0], power_cut >= -103.97
   } else {
     float p2 = power * 1.4426950408889634f;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(p2));
@@ -203,7 +203,7 @@ struct PwChunk {
 
 template <int MODE, bool STAGE_COLOR, int BLOCK>
 __device__ __forceinline__ void pixelwise_tile(const RArgs& A, int tile, float4* s_xyab, float4* s_cop,
-                                               float4* s_rgb, uint32_t* s_id, const unsigned long long* s_tab) {
+                                               float4* s_rgb, uint32_t* s_id, const ExpK& ek) {
   const int tid = threadIdx.x;
   const int tx = tile % A.cols, ty = tile / A.cols;
   const int lx = tid % A.pw, ly = tid / A.pw;
@@ -234,7 +234,7 @@ __device__ __forceinline__ void pixelwise_tile(const RArgs& A, int tile, float4*
       for (int j = 0; j < cnt; ++j) {
         float alpha;
         const float4 c = s_cop[j];
-        if (!eval_step<MODE>(s_xyab[j], c, sx, sy, s_tab, alpha)) continue;
+        if (!eval_step<MODE>(s_xyab[j], c, sx, sy, ek, alpha)) continue;
         const float tmp = __fmul_rn(t, __fsub_rn(1.0f, alpha));
         if (tmp < kStopThreshold) {
           done = true;
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(BLOCK) k_render_pixelwise(RArgs A) {
   __shared__ unsigned long long s_tab[32];
   load_tab(s_tab);
   __syncthreads();
-  pixelwise_tile<MODE, STAGE_COLOR, BLOCK>(A, blockIdx.x, s_xyab, s_cop, s_rgb, s_id, s_tab);
+  pixelwise_tile<MODE, STAGE_COLOR, BLOCK>(A, blockIdx.x, s_xyab, s_cop, s_rgb, s_id, make_expk(s_tab));
 }
 
 // Paper Alg. 1 (with the exit test fixed to >=).
@@ -275,13 +275,14 @@ __global__ void __launch_bounds__(BLOCK) k_render_dynamic(RArgs A) {
   __shared__ int s_tile;
   if (gated_out(A, BS_DYNAMIC_BLOCKS)) return;
   load_tab(s_tab);
+  const ExpK ek = make_expk(s_tab);
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) s_tile = (int)atomicAdd(A.queue, 1u);
     __syncthreads();
     const int tile = s_tile;
     if (tile >= A.T) return;
-    pixelwise_tile<MODE, false, BLOCK>(A, tile, s_xyab, s_cop, nullptr, s_id, s_tab);
+    pixelwise_tile<MODE, false, BLOCK>(A, tile, s_xyab, s_cop, nullptr, s_id, ek);
   }
 }
 
@@ -356,7 +357,7 @@ __device__ __forceinline__ int gw_group(bool ns, float alpha, float4 col, float 
 // colour weights (see gw_group).
 template <int MODE, int WARPS, bool SERIAL_W>
 __device__ __forceinline__ void gaussianwise_task(const RArgs& A, int tile, int sub, float4* s_xyab, float4* s_cop,
-                                                  float4* s_rgb, const unsigned long long* s_tab) {
+                                                  float4* s_rgb, const ExpK& ek) {
   constexpr int CH = WARPS * 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tx = tile % A.cols, ty = tile / A.cols;
@@ -392,7 +393,7 @@ __device__ __forceinline__ void gaussianwise_task(const RArgs& A, int tile, int 
       float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
       if (active) {
         c = s_cop[j];
-        ns = eval_step<MODE>(s_xyab[j], c, sx, sy, s_tab, alpha);
+        ns = eval_step<MODE>(s_xyab[j], c, sx, sy, ek, alpha);
       }
       const float4 col = ns ? s_rgb[j] : make_float4(0.f, 0.f, 0.f, 0.f);
       const int stop = gw_group<MODE, SERIAL_W>(ns, alpha, col, c.w, t, contrib, acc, lane);
@@ -417,11 +418,12 @@ __global__ void __launch_bounds__(kFgThreads) k_render_gaussianwise(RArgs A) {
   __shared__ unsigned long long s_tab[32];
   if (gated_out(A, BS_GAUSSIAN_WISE)) return;
   load_tab(s_tab);
+  const ExpK ek = make_expk(s_tab);
   const int tile = blockIdx.x;
   const int subs = (A.pw * A.ph + kFgWarps - 1) / kFgWarps;
   for (int s = 0; s < subs; ++s) {
     __syncthreads();
-    gaussianwise_task<MODE, kFgWarps, false>(A, tile, s, s_xyab, s_cop, s_rgb, s_tab);
+    gaussianwise_task<MODE, kFgWarps, false>(A, tile, s, s_xyab, s_cop, s_rgb, ek);
   }
 }
 
@@ -490,7 +492,7 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
 // colour partials come back warp-reduced in `part`.
 template <int MODE>
 __device__ __forceinline__ void gw_finish_pixel(const RArgs& A, uint32_t start, uint32_t from, uint32_t end,
-                                                float psx, float psy, const unsigned long long* s_tab, float& pt,
+                                                float psx, float psy, const ExpK& ek, float& pt,
                                                 int& pcnt, int& ptrm, Accum<MODE>& part) {
   const int lane = threadIdx.x & 31;
   float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nc = na, nr = na;
@@ -500,7 +502,7 @@ __device__ __forceinline__ void gw_finish_pixel(const RArgs& A, uint32_t start, 
     const float4 a = na, c = nc, r = nr;
     if (g + 32 + lane < end) load_rec(A, g + 32 + lane, na, nc, nr);  // prefetch next group
     float alpha = 0.0f;
-    const bool ns = active && eval_step<MODE>(a, c, psx, psy, s_tab, alpha);
+    const bool ns = active && eval_step<MODE>(a, c, psx, psy, ek, alpha);
     const int stop = gw_group<MODE, true>(ns, alpha, r, c.w, pt, pcnt, part, lane);
     if (stop < 32) {
       ptrm = (int)(g - start) + stop + 1;
@@ -512,7 +514,7 @@ __device__ __forceinline__ void gw_finish_pixel(const RArgs& A, uint32_t start, 
 
 template <int MODE>
 __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, float4 (*s)[32], int* s_k,
-                                          const unsigned long long* s_tab) {
+                                          const ExpK& ek) {
   const int lane = threadIdx.x & 31;
   const int tx = tile % A.cols, ty = tile / A.cols;
   // 8x4-pixel sub-tiles tile the pw x ph patch row-major
@@ -547,7 +549,7 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
         float pt = __shfl_sync(kFull, t, p);
         int pcnt = 0, ptrm = 0;
         Accum<MODE> part;
-        gw_finish_pixel<MODE>(A, start, base, end, psx, psy, s_tab, pt, pcnt, ptrm, part);
+        gw_finish_pixel<MODE>(A, start, base, end, psx, psy, ek, pt, pcnt, ptrm, part);
         if (lane == p) {
           acc.merge(part);
           t = pt;
@@ -615,7 +617,7 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
       if (done) continue;
       float alpha;
       const float4 c = s[1][j];
-      if (!eval_step<MODE>(s[0][j], c, sx, sy, s_tab, alpha)) continue;
+      if (!eval_step<MODE>(s[0][j], c, sx, sy, ek, alpha)) continue;
       const float tmp = __fmul_rn(t, __fsub_rn(1.0f, alpha));
       if (tmp < kStopThreshold) {
         done = true;
@@ -642,6 +644,7 @@ __global__ void __launch_bounds__(kFineThreads) k_render_fine(RArgs A, int subs)
   __shared__ unsigned long long s_tab[32];
   if (gated_out(A, BS_FINE_GRAINED_COMBINED)) return;
   load_tab(s_tab);
+  const ExpK ek = make_expk(s_tab);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (;;) {
@@ -651,7 +654,7 @@ __global__ void __launch_bounds__(kFineThreads) k_render_fine(RArgs A, int subs)
     if (task >= A.total_tasks) return;
     const int q = task / subs;
     const int tile = A.task_order ? (int)A.task_order[q] : q;
-    warp_task<MODE>(A, tile, task - q * subs, s_rec[warp], s_k[warp], s_tab);
+    warp_task<MODE>(A, tile, task - q * subs, s_rec[warp], s_k[warp], ek);
   }
 }
 
@@ -670,6 +673,7 @@ __global__ void __launch_bounds__(kFineThreads) k_render_donated(RArgs A) {
   __shared__ unsigned s_task;
   if (gated_out(A, BS_FINE_GRAINED_COMBINED)) return;
   load_tab(s_tab);
+  const ExpK ek = make_expk(s_tab);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned ntasks = *(volatile unsigned*)(A.queue + 3);
   for (;;) {
@@ -700,7 +704,7 @@ __global__ void __launch_bounds__(kFineThreads) k_render_donated(RArgs A) {
         for (uint32_t g0 = 0; g0 < n; g0 += 32) {
           const uint32_t j = g0 + lane;
           float alpha = 0.0f;
-          const bool ns = j < n && eval_step<MODE>(s_xyab[j], s_cop[j], sx, sy, s_tab, alpha);
+          const bool ns = j < n && eval_step<MODE>(s_xyab[j], s_cop[j], sx, sy, ek, alpha);
           const int stop = gw_group<MODE, true>(ns, alpha, ns ? s_rgb[j] : make_float4(0.f, 0.f, 0.f, 0.f),
                                                ns ? s_cop[j].w : 0.0f, t, cnt, part, lane);
           if (stop < 32) {

@@ -64,6 +64,20 @@ struct bs_context {
   // per-stage timing (bs_context_enable_timing)
   bs_frame_out last_out{};
   bool timing = false;
+  // async mode (bs_context_set_async): point_list sized from a capacity, K
+  // checked one call later; an overflowed frame is re-rendered then
+  bool async_mode = false;
+  cudaEvent_t ev_k = nullptr;
+  struct Pending {
+    bool on = false;
+    const bs_gaussian3d* g3d = nullptr;
+    int64_t n = 0;
+    bs_camera cam{};
+    int32_t pw = 0, ph = 0, variant = 0;
+    float bg[3] = {0, 0, 0};
+    bs_frame_out out{};
+  } pending;
+  int64_t reruns = 0;
   cudaEvent_t ev[kStages + 1] = {};
 };
 
@@ -154,6 +168,7 @@ extern "C" int bs_context_destroy(bs_context* c) {
   if (c->variant_host) cudaFreeHost(c->variant_host);
   for (cudaEvent_t e : c->ev)
     if (e) cudaEventDestroy(e);
+  if (c->ev_k) cudaEventDestroy(c->ev_k);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return BS_OK;
@@ -162,13 +177,6 @@ extern "C" int bs_context_destroy(bs_context* c) {
 extern "C" void* bs_context_stream(bs_context* c) {
   if (!c) return nullptr;
   return static_cast<void*>(c->use_user_stream ? c->user_stream : c->stream);
-}
-
-extern "C" int bs_context_set_stream(bs_context* c, void* stream) {
-  if (!c) return BS_ERR_INVALID_ARGUMENT;
-  c->use_user_stream = stream != nullptr;
-  c->user_stream = static_cast<cudaStream_t>(stream);
-  return BS_OK;
 }
 
 extern "C" int bs_context_enable_timing(bs_context* c, int32_t on) {
@@ -188,12 +196,14 @@ extern "C" int bs_context_stage_ms(bs_context* c, float* ms, int32_t n) {
 
 namespace {
 
+int grow_pl_async(bs_context* c, int64_t cap, cudaStream_t st);
+
 // The whole forward on device input, stream-ordered on the context stream.
 // One host sync (the 8-byte K readback that sizes point_list); variant = -1
 // selects on the device (bs_select_variant_device + bs_render_forward_auto),
 // so no sync follows it.
 int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const bs_camera* cam, int32_t pw, int32_t ph,
-                 int32_t variant, const float bg[3], bs_frame_out fo_in, cudaStream_t st) {
+                 int32_t variant, const float bg[3], bs_frame_out fo_in, cudaStream_t st, bool allow_async) {
   const int32_t W = cam->width, H = cam->height;
   const int64_t cols = (W + pw - 1) / pw, rows = (H + ph - 1) / ph, T = cols * rows;
   const int64_t P = int64_t(W) * H;
@@ -228,23 +238,45 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   TRY(bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, st));
   mark(2);
   CUTRY(cudaMemcpyAsync(c->k_host, c->k_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CUTRY(cudaStreamSynchronize(st));
-  const int64_t k = *c->k_host;
-  if (k > c->bin_k && bs_bin_workspace_bytes(c->bin_n, W, H, pw, ph, k) > c->bin_ws_bytes) {
-    // the count state lives in the workspace: grow, then count again
-    c->bin_k = int64_t(double(k) * 1.25) + 1024;
-    void* fresh = nullptr;
-    size_t fresh_bytes = 0;
-    TRY(grow(&fresh, &fresh_bytes, bs_bin_workspace_bytes(c->bin_n, W, H, pw, ph, c->bin_k)));
-    if (c->bin_ws) cudaFree(c->bin_ws);
-    c->bin_ws = fresh;
-    c->bin_ws_bytes = fresh_bytes;
-    TRY(bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, st));
+  const bool async = allow_async && c->async_mode && bs_bin_async_supported(W, H, pw, ph);
+  if (async) {
+    // no wait: sort into the current capacity; K is checked at the next call
+    if (!c->ev_k) CUTRY(cudaEventCreateWithFlags(&c->ev_k, cudaEventDisableTiming));
+    CUTRY(cudaEventRecord(c->ev_k, st));
+    mark(3);
+    if (!c->point_list) TRY(grow_pl_async(c, std::max<int64_t>(n, 1) * 16, st));
+    TRY(grow_n(&c->ranges, &c->ranges_cap, 2 * T));
+    TRY(bs_bin_sort_async(sp, n, c->n_visible, W, H, pw, ph, std::min<int64_t>(c->pl_cap, (int64_t(1) << 30) - 1),
+                          c->point_list, c->ranges, c->bin_ws, c->bin_ws_bytes, st));
+    c->pending.on = true;
+    c->pending.g3d = g3d_dev;
+    c->pending.n = n;
+    c->pending.cam = *cam;
+    c->pending.pw = pw;
+    c->pending.ph = ph;
+    c->pending.variant = variant;
+    std::copy(bg, bg + 3, c->pending.bg);
+    c->pending.out = fo_in;
+  } else {
+    CUTRY(cudaStreamSynchronize(st));
+    const int64_t k = *c->k_host;
+    if (k > c->bin_k && bs_bin_workspace_bytes(c->bin_n, W, H, pw, ph, k) > c->bin_ws_bytes) {
+      // the count state lives in the workspace: grow, then count again
+      c->bin_k = int64_t(double(k) * 1.25) + 1024;
+      void* fresh = nullptr;
+      size_t fresh_bytes = 0;
+      TRY(grow(&fresh, &fresh_bytes, bs_bin_workspace_bytes(c->bin_n, W, H, pw, ph, c->bin_k)));
+      if (c->bin_ws) cudaFree(c->bin_ws);
+      c->bin_ws = fresh;
+      c->bin_ws_bytes = fresh_bytes;
+      TRY(bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, st));
+    }
+    mark(3);
+    if (k > c->pl_cap) TRY(grow_pl_async(c, int64_t(double(std::max<int64_t>(k, 1)) * 1.25), st));
+    TRY(grow_n(&c->ranges, &c->ranges_cap, 2 * T));
+    TRY(bs_bin_sort(sp, n, c->n_visible, W, H, pw, ph, k, c->point_list, c->ranges, c->bin_ws, c->bin_ws_bytes, st));
+    c->last_k = k;
   }
-  mark(3);
-  TRY(grow_n(&c->point_list, &c->pl_cap, std::max<int64_t>(k, 1), 1.25));
-  TRY(grow_n(&c->ranges, &c->ranges_cap, 2 * T));
-  TRY(bs_bin_sort(sp, n, c->n_visible, W, H, pw, ph, k, c->point_list, c->ranges, c->bin_ws, c->bin_ws_bytes, st));
   mark(4);
 
   // P6 + selection
@@ -285,7 +317,6 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
                           c->render_ws, c->render_ws_bytes, st));
   mark(6);
   c->last_variant = variant;
-  c->last_k = k;
   c->last_W = W;
   c->last_H = H;
   c->last_pw = pw;
@@ -294,7 +325,43 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   return BS_OK;
 }
 
+// point_list growth without a device-wide sync: stream-ordered free of the
+// old buffer (after every frame already enqueued on st) and allocation of the
+// new one (cudaFreeAsync / cudaMallocAsync on the default pool).
+int grow_pl_async(bs_context* c, int64_t cap, cudaStream_t st) {
+  if (cap <= c->pl_cap) return BS_OK;
+  if (c->point_list) CUTRY(cudaFreeAsync(c->point_list, st));
+  c->point_list = nullptr;
+  c->pl_cap = 0;
+  void* p = nullptr;
+  CUTRY(cudaMallocAsync(&p, size_t(cap) * sizeof(uint32_t), st));
+  c->point_list = static_cast<uint32_t*>(p);
+  c->pl_cap = cap;
+  return BS_OK;
+}
+
+// Async mode: wait for the pending frame's K (its binning, not its render),
+// and if it overflowed the point_list capacity grow it and render that frame
+// again, synchronously (same inputs; stream order puts it after the first try).
+int verify_pending(bs_context* c, cudaStream_t st) {
+  if (!c->pending.on) return BS_OK;
+  c->pending.on = false;
+  CUTRY(cudaEventSynchronize(c->ev_k));
+  const int64_t k = *c->k_host;
+  c->last_k = k;
+  if (k <= c->pl_cap) {
+    // keep >= 25 % headroom over every K seen: grow ahead of an overflow
+    if (double(k) * 1.25 > double(c->pl_cap)) TRY(grow_pl_async(c, int64_t(double(k) * 1.5) + 1024, st));
+    return BS_OK;
+  }
+  ++c->reruns;
+  const auto p = c->pending;
+  TRY(grow_pl_async(c, int64_t(double(k) * 1.5) + 1024, st));
+  return frame_device(c, p.g3d, p.n, &p.cam, p.pw, p.ph, p.variant, p.bg, p.out, st, false);
+}
+
 int fill_info(bs_context* c, cudaStream_t st, bs_frame_info* info) {
+  TRY(verify_pending(c, st));
   if (!c->last_out.term) return BS_ERR_INVALID_ARGUMENT;
   TRY(bs_frame_work(c->last_out.term, c->last_out.contrib, c->ranges, c->last_W, c->last_H, c->last_pw, c->last_ph,
                     c->work_dev, st));
@@ -330,8 +397,25 @@ extern "C" int bs_render_frame_device(bs_context* c, const bs_gaussian3d* g3d_de
   if (!own && (!out.color || !out.alpha || !out.depth || !out.final_t || !out.contrib || !out.term))
     return BS_ERR_INVALID_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(bs_context_stream(c));
-  TRY(frame_device(c, g3d_dev, n, cam, pw, ph, variant, bg, out, st));
+  TRY(verify_pending(c, st));
+  TRY(frame_device(c, g3d_dev, n, cam, pw, ph, variant, bg, out, st, true));
   if (info) TRY(fill_info(c, st, info));
+  return BS_OK;
+}
+
+extern "C" int bs_context_set_async(bs_context* c, int32_t on) {
+  if (!c) return BS_ERR_INVALID_ARGUMENT;
+  TRY(verify_pending(c, static_cast<cudaStream_t>(bs_context_stream(c))));
+  c->async_mode = on != 0;
+  return BS_OK;
+}
+
+extern "C" int bs_context_sync(bs_context* c, int64_t* reruns) {
+  if (!c) return BS_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(bs_context_stream(c));
+  TRY(verify_pending(c, st));
+  CUTRY(cudaStreamSynchronize(st));
+  if (reruns) *reruns = c->reruns;
   return BS_OK;
 }
 
@@ -352,7 +436,9 @@ extern "C" int bs_render_frame_host(bs_context* c, const bs_gaussian3d* g3d, int
   const int64_t P = int64_t(W) * H;
   TRY(grow(&c->g3d, &c->g3d_bytes, size_t(std::max<int64_t>(n, 1)) * sizeof(bs_gaussian3d)));
   if (n > 0) CUTRY(cudaMemcpyAsync(c->g3d, g3d, size_t(n) * sizeof(bs_gaussian3d), cudaMemcpyHostToDevice, st));
-  TRY(frame_device(c, static_cast<const bs_gaussian3d*>(c->g3d), n, cam, pw, ph, variant, bg, bs_frame_out{}, st));
+  TRY(verify_pending(c, st));
+  TRY(frame_device(c, static_cast<const bs_gaussian3d*>(c->g3d), n, cam, pw, ph, variant, bg, bs_frame_out{}, st,
+                   false));
   // D2H
   const size_t pb = size_t(P) * sizeof(float);
   if (color) CUTRY(cudaMemcpyAsync(color, c->planes[0], pb * 3, cudaMemcpyDeviceToHost, st));
@@ -365,3 +451,15 @@ extern "C" int bs_render_frame_host(bs_context* c, const bs_gaussian3d* g3d, int
   CUTRY(cudaStreamSynchronize(st));
   return BS_OK;
 }
+
+// NULL selects the legacy default stream (what torch's default stream is),
+// not the context's own stream — pass bs_context_stream()'s earlier value
+// to go back to that one.
+extern "C" int bs_context_set_stream(bs_context* c, void* stream) {
+  if (!c) return BS_ERR_INVALID_ARGUMENT;
+  TRY(verify_pending(c, static_cast<cudaStream_t>(bs_context_stream(c))));
+  c->use_user_stream = static_cast<cudaStream_t>(stream) != c->stream;
+  c->user_stream = static_cast<cudaStream_t>(stream);
+  return BS_OK;
+}
+

@@ -386,3 +386,48 @@ def test_tile_order_lpt_buckets(W, H, n):
     b = _len_bucket(ref["counts"])
     exp = np.lexsort((np.arange(T), -b))
     assert np.array_equal(order.cpu().numpy(), exp)
+
+
+def test_frame_pipeline_async_overflow_rerun():
+    """Async mode: the first frame's K exceeds the initial point_list
+    capacity (16 per Gaussian), so it is rendered again at the next sync point
+    with a grown capacity; the final output equals the oracle's, and later
+    frames need no re-render."""
+    W = H = 512
+    n = 300
+    g3d, cam = scene(n, W, H, 2048.0, bgfrac=1.0)
+    g2d = O.project_all(g3d, cam)
+    pl, rg = O.bin_tiles(g2d, W, H, 16, 16)
+    assert len(pl) > 16 * n  # the initial capacity overflows
+    fp = api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT, async_mode=True)
+    d = api.g3d_to_device(g3d)
+    fp.forward(d, n, ncam(cam), variant=BS_FG, bg=(0.1, 0.2, 0.3))
+    assert fp.sync() == 1
+    ref = O.render(BS_FG, pl, rg, g2d, W, H, 16, 16, (0.1, 0.2, 0.3), lazy=True, threads=0)
+    got = fp.frame.to_numpy()
+    for k in ("contrib", "term", "final_t"):
+        assert np.array_equal(got[k], ref[k]), k
+    for _ in range(3):
+        fp.forward(d, n, ncam(cam), variant="auto", bg=(0.1, 0.2, 0.3))
+    assert fp.sync() == 1
+    got = fp.frame.to_numpy()
+    assert np.array_equal(got["contrib"], ref["contrib"]) and np.array_equal(got["final_t"], ref["final_t"])
+    fp.close()
+
+
+def test_frame_pipeline_runs_on_torch_stream():
+    """FramePipeline enqueues on torch's current stream: reading the frame on
+    that stream right after forward (no explicit sync) sees the finished frame."""
+    W, H = 960, 540
+    g3d, cam = scene(100_000, W, H, 500.0)
+    d = api.g3d_to_device(g3d)
+    fp = api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT, async_mode=True)
+    fp.forward(d, len(g3d), ncam(cam), variant=BS_FG)
+    fp.sync()
+    ref = fp.frame.color.clone()
+    for _ in range(3):
+        fp.frame.color.zero_()
+        fp.forward(d, len(g3d), ncam(cam), variant=BS_FG)
+        got = fp.frame.color.cpu()  # stream-ordered read on torch's current stream
+        assert torch.equal(got, ref.cpu())
+    fp.close()

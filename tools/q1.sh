@@ -1,4 +1,7 @@
 mkdir -p gpurun_out/q1
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/q1/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/q1/pytest.log
-timeout 300 python bench.py --steps 100 --no-cpu-baseline > gpurun_out/q1/bench.json 2> gpurun_out/q1/bench.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/q1/launches.csv python bench.py --steps 2 --warmup 3 --no-extras > /dev/null 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q -k "frame_pipeline" > gpurun_out/q1/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/q1/pytest.log
+python tools/diag_async2.py > gpurun_out/q1/diag2.txt 2>&1
+for r in 1 2; do
+timeout 300 python bench.py --steps 200 --no-extras > gpurun_out/q1/async$r.json 2> gpurun_out/q1/bench.err
+timeout 300 python bench.py --steps 200 --no-extras --sync-frames > gpurun_out/q1/sync$r.json 2>> gpurun_out/q1/bench.err
+done
