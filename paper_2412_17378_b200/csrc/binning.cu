@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(256) k_expand(const uint64_t* __restrict__ off
 constexpr int kScWarps = 16;
 constexpr int kScThreads = kScWarps * 32;
 constexpr int kOwnX = 4, kOwnY = kScWarps / kOwnX;  // tile ownership pattern (powers of 2)
-constexpr int kScBuf = 512;                          // per-warp instance window (entries)
+constexpr int kScMaxRows = 1024;                     // tile rows the row-band split supports
 constexpr int64_t kMaxChunkMatrix = (int64_t)16 << 20;  // entries of M (64 MB)
 constexpr int kMaxChunks = 4096;
 constexpr size_t kMaxScatterSmem = 200 * 1024;           // offsets row (T u32) + warp buffers
@@ -310,27 +310,43 @@ __global__ void k_chunk_bounds(const uint64_t* __restrict__ offs, const uint32_t
   }
 }
 
+// Also writes the chunk's per-row instance counts rowc[c][ty] (the scatter
+// splits the rows among its warps by them).
 __global__ void __launch_bounds__(kScThreads) k_chunk_hist(const uint2* __restrict__ rects_sorted,
                                                            const uint32_t* __restrict__ first, Grid g,
-                                                           uint32_t* __restrict__ m, const uint64_t* __restrict__ kd,
-                                                           int64_t k_cap) {
+                                                           uint32_t* __restrict__ m, uint32_t* __restrict__ rowc,
+                                                           const uint64_t* __restrict__ kd, int64_t k_cap) {
   if (*kd == 0 || *kd > (uint64_t)k_cap) return;
   extern __shared__ int s_grid[];
   const int stride = g.cols + 1, cells = stride * (g.rows + 1);
+  int* s_rowd = s_grid + cells;  // rows + 1 (difference array of per-row counts)
   const int c = blockIdx.x, tid = threadIdx.x;
-  for (int i = tid; i < cells; i += kScThreads) s_grid[i] = 0;
+  for (int i = tid; i < cells + g.rows + 1; i += kScThreads) s_grid[i] = 0;
   __syncthreads();
   const uint32_t j0 = first[c], j1 = first[c + 1];
   for (uint32_t j = j0 + tid; j < j1; j += kScThreads) {
     const uint2 rc = rects_sorted[j];
     const int tx0 = rc.x & 0xffff, ty0 = rc.x >> 16;
-    const int tx1 = tx0 + (int)(rc.y & 0xffff), ty1 = ty0 + (int)(rc.y >> 16);  // exclusive
+    const int w = (int)(rc.y & 0xffff);
+    const int tx1 = tx0 + w, ty1 = ty0 + (int)(rc.y >> 16);  // exclusive
     atomicAdd(&s_grid[ty0 * stride + tx0], 1);
     atomicAdd(&s_grid[ty0 * stride + tx1], -1);
     atomicAdd(&s_grid[ty1 * stride + tx0], -1);
     atomicAdd(&s_grid[ty1 * stride + tx1], 1);
+    atomicAdd(&s_rowd[ty0], w);
+    atomicAdd(&s_rowd[ty1], -w);
   }
   __syncthreads();
+  if (tid < 32) {
+    int carry = 0;
+    for (int r0 = 0; r0 < g.rows; r0 += 32) {
+      const int r = r0 + tid;
+      int v = r < g.rows ? s_rowd[r] : 0;
+      v = warp_inclusive_scan(v) + carry;
+      if (r < g.rows) rowc[(int64_t)c * g.rows + r] = (uint32_t)v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
   const int lane = tid & 31, warp = tid >> 5;
   for (int r = warp; r < g.rows; r += kScWarps) {
     int carry = 0;
@@ -392,100 +408,157 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
+// Per chunk: the offsets row in shared memory; the tile rows are split into
+// kScWarps contiguous bands of about equal instance count (from the chunk's
+// per-row counts), warp w owning band w.  Each warp walks the chunk's splats
+// in depth order, keeps those whose rectangle meets its band (ballot
+// compaction into a per-warp queue), and for every 32 queued splats lists
+// their band tiles (row-major, tile | lane << 16) in a per-warp window and
+// drains it 32 instances per step: equal tiles in a step are ranked by
+// match.any (lane order = depth order), the highest peer advances the
+// tile's offset.  Every tile list comes out in (depth, index) order.
+struct ScQ {
+  uint32_t rx, ry, id;  // packed rect (tx0 | ty0 << 16, w | h << 16) and splat id
+};
+
 __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __restrict__ m,
+                                                              const uint32_t* __restrict__ rowc,
                                                               const uint32_t* __restrict__ first,
                                                               const uint2* __restrict__ rects_sorted,
                                                               const uint32_t* __restrict__ order, int T, int cols,
-                                                              uint32_t* __restrict__ point_list,
+                                                              int rows, uint32_t* __restrict__ point_list,
                                                               const uint64_t* __restrict__ kd, int64_t k_cap) {
   if (*kd == 0 || *kd > (uint64_t)k_cap) return;
   extern __shared__ uint32_t s_off[];
+  __shared__ ScQ s_q[kScWarps][64];
+  __shared__ uint32_t s_rowp[kScMaxRows + 1];
   const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t* row = m + (int64_t)c * T;
-  for (int t = tid; t < T; t += kScThreads) s_off[t] = row[t];
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_off);
-  const uint32_t wbuf = sbase + 4u * (uint32_t)(((T + 31) & ~31) + warp * kScBuf);
-  __syncthreads();
-  const uint32_t j0 = first[c], j1 = first[c + 1];
-  const uint32_t lt = lanemask_lt();
-  const uint32_t row_step = (uint32_t)(kOwnY * cols);
-  // warp w owns the tiles tx = w % kOwnX (mod kOwnX), ty = w / kOwnX (mod
-  // kOwnY): clustered hot spots spread evenly over the warps
-  const uint32_t own_x = (uint32_t)(warp % kOwnX), own_y = (uint32_t)(warp / kOwnX);
-  // next batch prefetched into registers (load latency overlaps this batch)
-  uint2 nrc = make_uint2(0u, 0u);
-  uint32_t nid = 0;
-  if (j0 + lane < j1) {
-    nrc = rects_sorted[j0 + lane];
-    nid = order[j0 + lane];
-  }
-  for (uint32_t b = j0; b < j1; b += 32) {
-    // this lane's splat: its owned tiles form an nc x nr sub-grid from tb,
-    // strides (kOwnX, kOwnY) — listed flat (row-major) at [excl, excl + cnt)
-    const uint2 rc = nrc;
-    const uint32_t id = nid;
-    const bool valid = b + lane < j1;
-    if (b + 32 + lane < j1) {
-      nrc = rects_sorted[b + 32 + lane];
-      nid = order[b + 32 + lane];
+  const uint32_t* mrow = m + (int64_t)c * T;
+  for (int t = tid; t < T; t += kScThreads) s_off[t] = mrow[t];
+  if (warp == 0) {  // inclusive prefix of the chunk's per-row counts
+    uint32_t carry = 0;
+    if (lane == 0) s_rowp[0] = 0;
+    for (int r0 = 0; r0 < rows; r0 += 32) {
+      const int r = r0 + lane;
+      uint32_t v = r < rows ? rowc[(int64_t)c * rows + r] : 0u;
+      v = warp_inclusive_scan(v) + carry;
+      if (r < rows) s_rowp[r + 1] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
     }
-    const uint32_t rx0 = rc.x & 0xffffu, ry0 = rc.x >> 16, rw = rc.y & 0xffffu, rh = rc.y >> 16;
-    const uint32_t fc = rx0 + ((own_x - rx0) & (kOwnX - 1));
-    const uint32_t fr = ry0 + ((own_y - ry0) & (kOwnY - 1));
-    const uint32_t nc = (rx0 + rw + (kOwnX - 1) - fc) / kOwnX;  // 0 when fc is past the rectangle
-    const uint32_t nr = (ry0 + rh + (kOwnY - 1) - fr) / kOwnY;
-    const int cnt = valid ? (int)(nc * nr) : 0;
-    const uint32_t tb = fr * (uint32_t)cols + fc;
+  }
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_off);
+  __syncthreads();
+  // band of this warp: row r belongs to warp floor(kScWarps * mid(r) / total),
+  // mid(r) = the row's middle instance (monotone in r -> contiguous bands)
+  const uint64_t total = s_rowp[rows];
+  if (total == 0) return;
+  auto owner = [&](int r) -> int {
+    const uint64_t mid2 = (uint64_t)s_rowp[r] + s_rowp[r + 1];  // 2 * middle
+    return (int)min((uint64_t)(kScWarps - 1), (mid2 * kScWarps) / (2 * total));
+  };
+  auto band_start = [&](int w) -> int {  // first row whose owner >= w
+    int lo = 0, hi = rows;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (owner(mid) < w) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
+  const uint32_t r0 = (uint32_t)band_start(warp), r1 = (uint32_t)band_start(warp + 1);
+  const uint32_t lt = lanemask_lt();
+  const uint32_t j0 = first[c], j1 = first[c + 1];
+  int qn = 0;  // queued splats (warp-uniform)
+
+  // drain the first nq queue entries' band tiles, 32 instances per step:
+  // instance f of the flat (splat, row, column) enumeration belongs to the
+  // last lane whose exclusive count is <= f (5-step shuffle search); its
+  // row / column come from one float multiply by the lane's 1/w (exact:
+  // f < 2^22).  Equal tiles inside a step are ranked by match.any (lane
+  // order = depth order); the highest peer advances the tile's offset.
+  auto flush32 = [&](int nq) {
+    const ScQ q = s_q[warp][lane];
+    int cnt = 0;
+    uint32_t tb = 0, w = 1;
+    if (lane < nq) {
+      const uint32_t rx0 = q.rx & 0xffffu, ry0 = q.rx >> 16;
+      w = q.ry & 0xffffu;
+      const uint32_t ya = max(ry0, r0), yb = min(ry0 + (q.ry >> 16), r1);
+      cnt = (int)((yb - ya) * w);
+      tb = ya * (uint32_t)cols + rx0;
+    }
+    const float inv = __frcp_rn((float)w);
     const int incl = warp_inclusive_scan(cnt);
     const int excl = incl - cnt;
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    for (int wb = 0; wb < total; wb += kScBuf) {
-      // every lane lists its owned tiles that fall in the window
-      // [wb, wb + kScBuf) as (tile | lane << 16): no per-instance division,
-      // no lane search; then the warp drains the window 32 per step
-      const int k0 = max(0, wb - excl), k1 = min(cnt, wb + kScBuf - excl);
-      if (k0 < k1) {
-        uint32_t r = 0, cc = 0;
-        if (k0) {  // only when a batch spills past one window
-          r = (uint32_t)k0 / nc;
-          cc = (uint32_t)k0 - r * nc;
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    for (int f0 = 0; f0 < tot; f0 += 32) {
+      const int f = f0 + lane;
+      const bool act = f < tot;
+      int sl = 0, e0 = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int e = __shfl_sync(0xffffffffu, excl, sl + step);
+        if (e <= f) {
+          sl += step;
+          e0 = e;
         }
-        uint32_t rowbase = tb + r * row_step, t = rowbase + cc * kOwnX;
-        uint32_t dst = wbuf + 4u * (uint32_t)(excl + k0 - wb);
-        const uint32_t tag = (uint32_t)lane << 16;
-#pragma unroll 1
-        for (int k = k0; k < k1; ++k) {
-          sts_u32(dst, t | tag);
-          dst += 4u;
-          t += kOwnX;
-          if (++cc == nc) {
-            cc = 0;
-            rowbase += row_step;
-            t = rowbase;
-          }
-        }
+      }
+      const uint32_t local = (uint32_t)(f - e0);
+      const uint32_t ws = __shfl_sync(0xffffffffu, w, sl);
+      const float iv = __shfl_sync(0xffffffffu, inv, sl);
+      const uint32_t t0 = __shfl_sync(0xffffffffu, tb, sl);
+      const uint32_t sid = __shfl_sync(0xffffffffu, q.id, sl);
+      const uint32_t r = (uint32_t)(((float)local + 0.5f) * iv);
+      const uint32_t tile = t0 + r * (uint32_t)cols + (local - r * ws);
+      const uint32_t peers = __match_any_sync(0xffffffffu, act ? tile : 0xffffffffu);
+      const uint32_t a = sbase + 4u * tile;
+      uint32_t pos = 0;
+      if (act) {
+        pos = lds_u32(a) + __popc(peers & lt);
+        point_list[pos] = sid;
       }
       __syncwarp();
-      const int n = min(kScBuf, total - wb);
-      for (int f0 = 0; f0 < n; f0 += 32) {
-        const int f = f0 + lane;
-        const bool act = f < n;
-        const uint32_t v = act ? lds_u32(wbuf + 4u * (uint32_t)f) : 0xffffffffu;
-        const uint32_t sid = __shfl_sync(0xffffffffu, id, (int)(v >> 16) & 31);
-        const uint32_t tile = v & 0xffffu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, act ? tile : 0xffffffffu);
-        const uint32_t a = sbase + 4u * tile;
-        uint32_t pos = 0;
-        if (act) {
-          pos = lds_u32(a) + __popc(peers & lt);
-          point_list[pos] = sid;
-        }
-        __syncwarp();
-        if (act && (peers >> lane) == 1u) sts_u32(a, pos + 1);  // highest peer publishes
-        __syncwarp();
-      }
+      if (act && (peers >> lane) == 1u) sts_u32(a, pos + 1);  // highest peer publishes
+      __syncwarp();
+    }
+  };
+
+  // each warp walks the chunk on its own (no CTA barrier couples the warps'
+  // unequal flush work), the batch two ahead in flight
+  uint2 rc1 = make_uint2(0u, 0u), rc2 = rc1;
+  uint32_t id1 = 0, id2 = 0;
+  if (j0 + lane < j1) {
+    rc1 = rects_sorted[j0 + lane];
+    id1 = order[j0 + lane];
+  }
+  if (j0 + 32 + lane < j1) {
+    rc2 = rects_sorted[j0 + 32 + lane];
+    id2 = order[j0 + 32 + lane];
+  }
+  for (uint32_t b = j0; b < j1; b += 32) {
+    const ScQ e = ScQ{rc1.x, rc1.y, id1};
+    const bool valid = b + lane < j1;
+    rc1 = rc2;
+    id1 = id2;
+    if (b + 64 + lane < j1) {
+      rc2 = rects_sorted[b + 64 + lane];
+      id2 = order[b + 64 + lane];
+    }
+    const uint32_t ry0 = e.rx >> 16, rh = e.ry >> 16;
+    const bool hit = valid && ry0 < r1 && ry0 + rh > r0;
+    const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+    if (hit) s_q[warp][qn + __popc(hm & lt)] = e;
+    qn += __popc(hm);
+    __syncwarp();
+    if (qn >= 32) {
+      flush32(32);
+      __syncwarp();
+      qn -= 32;
+      if (lane < qn) s_q[warp][lane] = s_q[warp][lane + 32];
+      __syncwarp();
     }
   }
+  if (qn > 0) flush32(qn);
 }
 
 // Tile ranges from the exclusive scan of the counts.  On a point_list
@@ -530,7 +603,7 @@ struct BinWs {
   uint32_t *counts, *starts, *cpartials;
   uint32_t *tk0, *tv_alt, *tk1, *block_j0;
   RadixWs rws_k;
-  uint32_t *chunk_first, *chunk_m;
+  uint32_t *chunk_first, *chunk_m, *chunk_rowc;
 };
 
 // The chunked counting scatter needs the per-chunk offsets row (T u32) and
@@ -542,7 +615,7 @@ inline bool bin_chunked(const Grid& g) {
     return (e && e[0] == '1') ? 1 : 0;
   }();
   const int64_t T = (int64_t)g.cols * g.rows;
-  return !forced_radix && (size_t)(T + 32 + kScWarps * kScBuf) * 4 <= kMaxScatterSmem &&
+  return !forced_radix && g.rows <= kScMaxRows && (size_t)(T + 32) * 4 <= kMaxScatterSmem &&
          sizeof(int) * (size_t)(g.cols + 1) * (g.rows + 1) <= kMaxDiffSmem;
 }
 
@@ -575,6 +648,7 @@ inline void bin_ws_layout(C& c, int64_t n_cap, const Grid& g, int64_t k_cap, Bin
     // chunked counting scatter: chunk bounds + the chunk x tile offsets matrix
     o.chunk_first = c.template take<uint32_t>((size_t)kMaxChunks + 1);
     o.chunk_m = c.template take<uint32_t>((size_t)(max_chunks(g) * T));
+    o.chunk_rowc = c.template take<uint32_t>((size_t)(max_chunks(g) * g.rows));
     return;
   }
   o.tk0 = c.template take<uint32_t>((size_t)k_cap);
@@ -698,7 +772,7 @@ static int bin_sort_impl(int64_t n_cap, const int32_t* n_visible, int32_t width,
                                        (int)kMaxScatterSmem));
       attr_set = true;
     }
-    const size_t off_bytes = sizeof(uint32_t) * ((size_t)((T + 31) & ~31) + (size_t)kScWarps * kScBuf);
+    const size_t off_bytes = sizeof(uint32_t) * (size_t)((T + 31) & ~31);
     const size_t diff_bytes = sizeof(int) * (size_t)(gr.cols + 1) * (gr.rows + 1);
     int dev = 0, sms = 148, per_sm = 1;
     BS_CUDA_TRY(cudaGetDevice(&dev));
@@ -718,13 +792,14 @@ static int bin_sort_impl(int64_t n_cap, const int32_t* n_visible, int32_t width,
     k_chunk_bounds<<<(unsigned)((n_cap + 255) / 256), 256, 0, st>>>(w.offs, w.touched_sorted, n_cap, n_visible, kd,
                                                                    k_cap, (int)nch, w.chunk_first);
     BS_LAUNCH_CHECK();
-    k_chunk_hist<<<(unsigned)nch, kScThreads, diff_bytes, st>>>(w.rects_sorted, w.chunk_first, gr, w.chunk_m, kd,
-                                                                k_cap);
+    k_chunk_hist<<<(unsigned)nch, kScThreads, diff_bytes + sizeof(int) * (size_t)(gr.rows + 1), st>>>(
+        w.rects_sorted, w.chunk_first, gr, w.chunk_m, w.chunk_rowc, kd, k_cap);
     BS_LAUNCH_CHECK();
     k_chunk_scan<<<(unsigned)((T + 31) / 32), kCsSeg * 32, 0, st>>>(w.chunk_m, w.starts, (int)T, (int)nch, kd, k_cap);
     BS_LAUNCH_CHECK();
-    k_chunk_scatter<<<(unsigned)nch, kScThreads, off_bytes, st>>>(w.chunk_m, w.chunk_first, w.rects_sorted, order,
-                                                                   (int)T, gr.cols, point_list, kd, k_cap);
+    k_chunk_scatter<<<(unsigned)nch, kScThreads, off_bytes, st>>>(w.chunk_m, w.chunk_rowc, w.chunk_first,
+                                                                   w.rects_sorted, order, (int)T, gr.cols, gr.rows,
+                                                                   point_list, kd, k_cap);
     BS_LAUNCH_CHECK();
   } else if (k > 0) {
     const uint32_t* order = w.dv0;  // depth order (4 passes end in dv0)
