@@ -16,4 +16,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_render_fine -c 1 \
   -o "$OUT/render_fine_full" -f python tools/profile_render.py --variant FineGrainedCombined --alpha exact --reps 1 \
   > "$OUT/ncu_full.log" 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_chunk_scatter -c 1 \
+  -o "$OUT/chunk_scatter_full" -f python tools/profile_render.py --variant FineGrainedCombined --alpha exact --reps 1 \
+  > "$OUT/ncu_full2.log" 2>&1
 echo done
