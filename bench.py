@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes as C
+import gc
 import json
 import math
 import os
@@ -62,6 +63,64 @@ def load_peaks() -> dict:
             return json.load(f)
     except Exception:
         return {}
+
+
+class NvmlClockSampler:
+    """SM clock + clock-event reasons sampled in-process through NVML (what
+    nvidia-smi reports) during the timed region — no subprocess, so no extra
+    driver client polling the GPU while frames run."""
+
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+
+    def __init__(self, gpu_index: int, period_s: float = 0.05):
+        self.gpu, self.period = gpu_index, period_s
+        self.sm, self.smax, self.reasons = [], None, set()
+        self.stop_ev = threading.Event()
+        self.t = None
+
+    def start(self):
+        import pynvml as nv
+        nv.nvmlInit()
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].strip().isdigit() else self.gpu
+        self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(idx)
+        self.smax = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_ev.is_set():
+            self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for name, const in self.NAMES:
+                if r & getattr(nv, const):
+                    self.reasons.add(name)
+            self.stop_ev.wait(self.period)
+
+    def stop(self) -> dict:
+        self.stop_ev.set()
+        if self.t:
+            self.t.join(timeout=2)
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None, "sm_max_mhz": self.smax,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml"}
+
+
+def make_clock_sampler(gpu_index: int):
+    """NVML in-process sampler; nvidia-smi subprocess if NVML is unusable."""
+    if os.environ.get("BS_CLOCKS", "nvml") == "nvml":
+        try:
+            s = NvmlClockSampler(gpu_index)
+            s.start()
+            return s
+        except Exception:
+            pass
+    s = ClockSampler(gpu_index)
+    s.start()
+    return s
 
 
 class ClockSampler:
@@ -273,8 +332,7 @@ def main():
     def step(i):
         return fp.forward(g3d_dev, n, cams[view_of(i)], variant=variant)
 
-    clk = ClockSampler(local)
-    clk.start()  # sampling spans warm-up + timed region (the timed region alone is < 1 s)
+    clk = make_clock_sampler(local)  # sampling spans warm-up + timed region (the timed region alone is < 1 s)
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
@@ -287,12 +345,14 @@ def main():
     torch.cuda.synchronize()
     reruns_warm = fp.sync()
     launches0 = N.lib().bs_kernel_launches()
+    gc.disable()  # no collector pauses while the host enqueues the timed frames
     for i in range(args.steps):
         flush.zero_()  # L2 flush between timed steps (untimed)
         starts[i].record()
         step(args.warmup + i)
         ends[i].record()
-    fp.sync()  # verifies the last timed frame (a re-render would be enqueued before the sync point)
+    fp.sync()  # verifies the last timed frames (a re-render would be enqueued before the sync point)
+    gc.enable()
     torch.cuda.synchronize()
     launches = int(N.lib().bs_kernel_launches() - launches0)
     reruns = fp.sync() - reruns_warm

@@ -67,16 +67,18 @@ struct bs_context {
   // async mode (bs_context_set_async): point_list sized from a capacity, K
   // checked one call later; an overflowed frame is re-rendered then
   bool async_mode = false;
-  cudaEvent_t ev_k = nullptr;
+  static constexpr int kDepth = 2;  // frames the host may run ahead of their K check
+  cudaEvent_t ev_k[kDepth] = {};
   struct Pending {
-    bool on = false;
     const bs_gaussian3d* g3d = nullptr;
     int64_t n = 0;
     bs_camera cam{};
     int32_t pw = 0, ph = 0, variant = 0;
     float bg[3] = {0, 0, 0};
     bs_frame_out out{};
-  } pending;
+    int slot = 0;
+  } pending[kDepth];
+  int n_pending = 0, next_slot = 0;
   int64_t reruns = 0;
   cudaEvent_t ev[kStages + 1] = {};
 };
@@ -149,6 +151,15 @@ extern "C" int bs_context_create(bs_context** out, int alpha_mode) {
     bs_context_destroy(c);
     return BS_ERR_CUDA;
   }
+  // point_list grows through cudaMallocAsync: keep freed pool memory mapped so
+  // a regrowth never goes back to the OS mid-run (tens of ms per remap)
+  int dev = 0;
+  cudaMemPool_t pool = nullptr;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  (void)cudaGetLastError();
   *out = c;
   return BS_OK;
 }
@@ -168,7 +179,8 @@ extern "C" int bs_context_destroy(bs_context* c) {
   if (c->variant_host) cudaFreeHost(c->variant_host);
   for (cudaEvent_t e : c->ev)
     if (e) cudaEventDestroy(e);
-  if (c->ev_k) cudaEventDestroy(c->ev_k);
+  for (cudaEvent_t e : c->ev_k)
+    if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return BS_OK;
@@ -237,29 +249,32 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   }
   TRY(bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, st));
   mark(2);
-  CUTRY(cudaMemcpyAsync(c->k_host, c->k_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   const bool async = allow_async && c->async_mode && bs_bin_async_supported(W, H, pw, ph);
+  const int slot = async ? c->next_slot : 0;
+  CUTRY(cudaMemcpyAsync(c->k_host + 1 + slot, c->k_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   if (async) {
-    // no wait: sort into the current capacity; K is checked at the next call
-    if (!c->ev_k) CUTRY(cudaEventCreateWithFlags(&c->ev_k, cudaEventDisableTiming));
-    CUTRY(cudaEventRecord(c->ev_k, st));
+    // no wait: sort into the current capacity; K is checked kDepth calls later
+    if (!c->ev_k[slot]) CUTRY(cudaEventCreateWithFlags(&c->ev_k[slot], cudaEventDisableTiming));
+    CUTRY(cudaEventRecord(c->ev_k[slot], st));
     mark(3);
     if (!c->point_list) TRY(grow_pl_async(c, std::max<int64_t>(n, 1) * 16, st));
     TRY(grow_n(&c->ranges, &c->ranges_cap, 2 * T));
     TRY(bs_bin_sort_async(sp, n, c->n_visible, W, H, pw, ph, std::min<int64_t>(c->pl_cap, (int64_t(1) << 30) - 1),
                           c->point_list, c->ranges, c->bin_ws, c->bin_ws_bytes, st));
-    c->pending.on = true;
-    c->pending.g3d = g3d_dev;
-    c->pending.n = n;
-    c->pending.cam = *cam;
-    c->pending.pw = pw;
-    c->pending.ph = ph;
-    c->pending.variant = variant;
-    std::copy(bg, bg + 3, c->pending.bg);
-    c->pending.out = fo_in;
+    bs_context::Pending& q = c->pending[c->n_pending++];
+    q.g3d = g3d_dev;
+    q.n = n;
+    q.cam = *cam;
+    q.pw = pw;
+    q.ph = ph;
+    q.variant = variant;
+    std::copy(bg, bg + 3, q.bg);
+    q.out = fo_in;
+    q.slot = slot;
+    c->next_slot = (slot + 1) % bs_context::kDepth;
   } else {
     CUTRY(cudaStreamSynchronize(st));
-    const int64_t k = *c->k_host;
+    const int64_t k = c->k_host[1];
     if (k > c->bin_k && bs_bin_workspace_bytes(c->bin_n, W, H, pw, ph, k) > c->bin_ws_bytes) {
       // the count state lives in the workspace: grow, then count again
       c->bin_k = int64_t(double(k) * 1.25) + 1024;
@@ -340,24 +355,36 @@ int grow_pl_async(bs_context* c, int64_t cap, cudaStream_t st) {
   return BS_OK;
 }
 
-// Async mode: wait for the pending frame's K (its binning, not its render),
-// and if it overflowed the point_list capacity grow it and render that frame
-// again, synchronously (same inputs; stream order puts it after the first try).
-int verify_pending(bs_context* c, cudaStream_t st) {
-  if (!c->pending.on) return BS_OK;
-  c->pending.on = false;
-  CUTRY(cudaEventSynchronize(c->ev_k));
-  const int64_t k = *c->k_host;
-  c->last_k = k;
-  if (k <= c->pl_cap) {
-    // keep >= 25 % headroom over every K seen: grow ahead of an overflow
-    if (double(k) * 1.25 > double(c->pl_cap)) TRY(grow_pl_async(c, int64_t(double(k) * 1.5) + 1024, st));
-    return BS_OK;
+// Async mode: wait for the oldest pending frame's K (its binning, not its
+// render).  If it overflowed the point_list capacity: grow it and render that
+// frame and every newer pending one again, in order, synchronously (same
+// inputs; stream order puts them after the first tries, so shared outputs end
+// with the newest frame).  keep = pending frames that may stay unchecked.
+int verify_pending(bs_context* c, cudaStream_t st, int keep = 0) {
+  while (c->n_pending > keep) {
+    const bs_context::Pending p0 = c->pending[0];
+    CUTRY(cudaEventSynchronize(c->ev_k[p0.slot]));
+    const int64_t k = c->k_host[1 + p0.slot];
+    c->last_k = k;
+    if (k <= c->pl_cap) {
+      // keep >= 25 % headroom over every K seen: grow ahead of an overflow
+      if (double(k) * 1.25 > double(c->pl_cap)) TRY(grow_pl_async(c, int64_t(double(k) * 1.5) + 1024, st));
+      for (int i = 1; i < c->n_pending; ++i) c->pending[i - 1] = c->pending[i];
+      --c->n_pending;
+      continue;
+    }
+    bs_context::Pending redo[bs_context::kDepth];
+    const int nr = c->n_pending;
+    std::copy(c->pending, c->pending + nr, redo);
+    c->n_pending = 0;
+    TRY(grow_pl_async(c, int64_t(double(k) * 1.5) + 1024, st));
+    for (int i = 0; i < nr; ++i) {
+      ++c->reruns;
+      const bs_context::Pending& p = redo[i];
+      TRY(frame_device(c, p.g3d, p.n, &p.cam, p.pw, p.ph, p.variant, p.bg, p.out, st, false));
+    }
   }
-  ++c->reruns;
-  const auto p = c->pending;
-  TRY(grow_pl_async(c, int64_t(double(k) * 1.5) + 1024, st));
-  return frame_device(c, p.g3d, p.n, &p.cam, p.pw, p.ph, p.variant, p.bg, p.out, st, false);
+  return BS_OK;
 }
 
 int fill_info(bs_context* c, cudaStream_t st, bs_frame_info* info) {
@@ -397,7 +424,7 @@ extern "C" int bs_render_frame_device(bs_context* c, const bs_gaussian3d* g3d_de
   if (!own && (!out.color || !out.alpha || !out.depth || !out.final_t || !out.contrib || !out.term))
     return BS_ERR_INVALID_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(bs_context_stream(c));
-  TRY(verify_pending(c, st));
+  TRY(verify_pending(c, st, bs_context::kDepth - 1));
   TRY(frame_device(c, g3d_dev, n, cam, pw, ph, variant, bg, out, st, true));
   if (info) TRY(fill_info(c, st, info));
   return BS_OK;
