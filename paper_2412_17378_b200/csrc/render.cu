@@ -638,7 +638,7 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kFineThreads) k_render_fine(RArgs A, int subs) {
+__global__ void __launch_bounds__(kFineThreads, 4) k_render_fine(RArgs A, int subs) {
   __shared__ float4 s_rec[kFineWarps][4][32];
   __shared__ int s_k[kFineWarps][32];
   __shared__ unsigned long long s_tab[32];
