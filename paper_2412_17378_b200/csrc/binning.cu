@@ -491,9 +491,9 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
     const int incl = warp_inclusive_scan(cnt);
     const int excl = incl - cnt;
     const int tot = __shfl_sync(0xffffffffu, incl, 31);
-    for (int f0 = 0; f0 < tot; f0 += 32) {
+    // instance f -> (tile, splat id); 0xffffffff tile past the end
+    auto resolve = [&](int f0, uint32_t& tile, uint32_t& sid) {
       const int f = f0 + lane;
-      const bool act = f < tot;
       int sl = 0, e0 = 0;
 #pragma unroll
       for (int step = 16; step > 0; step >>= 1) {
@@ -507,10 +507,19 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
       const uint32_t ws = __shfl_sync(0xffffffffu, w, sl);
       const float iv = __shfl_sync(0xffffffffu, inv, sl);
       const uint32_t t0 = __shfl_sync(0xffffffffu, tb, sl);
-      const uint32_t sid = __shfl_sync(0xffffffffu, q.id, sl);
+      sid = __shfl_sync(0xffffffffu, q.id, sl);
       const uint32_t r = (uint32_t)(((float)local + 0.5f) * iv);
-      const uint32_t tile = t0 + r * (uint32_t)cols + (local - r * ws);
-      const uint32_t peers = __match_any_sync(0xffffffffu, act ? tile : 0xffffffffu);
+      tile = f < tot ? t0 + r * (uint32_t)cols + (local - r * ws) : 0xffffffffu;
+    };
+    // software-pipelined: the next step's shuffle search is independent of
+    // this step's match / shared-memory chain, so their latencies overlap
+    uint32_t tile, sid;
+    resolve(0, tile, sid);
+    for (int f0 = 0; f0 < tot; f0 += 32) {
+      uint32_t ntile = 0xffffffffu, nsid = 0;
+      if (f0 + 32 < tot) resolve(f0 + 32, ntile, nsid);
+      const bool act = tile != 0xffffffffu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, tile);
       const uint32_t a = sbase + 4u * tile;
       uint32_t pos = 0;
       if (act) {
@@ -520,6 +529,8 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
       __syncwarp();
       if (act && (peers >> lane) == 1u) sts_u32(a, pos + 1);  // highest peer publishes
       __syncwarp();
+      tile = ntile;
+      sid = nsid;
     }
   };
 
