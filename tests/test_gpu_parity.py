@@ -431,3 +431,74 @@ def test_frame_pipeline_runs_on_torch_stream():
         got = fp.frame.color.cpu()  # stream-ordered read on torch's current stream
         assert torch.equal(got, ref.cpu())
     fp.close()
+
+
+def _rect_rule(g2d, W, H, pw, ph):
+    """The reference's tile rectangle (src/preprocess.cpp:81-92) in float32,
+    vectorised: (tx0, tx1, ty0, ty1, touches)."""
+    x, y = g2d["x"], g2d["y"]
+    rr = np.ceil(g2d["radius"]).astype(np.float32)
+    x0, x1, y0, y1 = x - rr, x + rr, y - rr, y + rr
+    cols, rows = (W + pw - 1) // pw, (H + ph - 1) // ph
+    ok = ~((x1 < 0) | (y1 < 0) | (x0 >= np.float32(W)) | (y0 >= np.float32(H)))
+    with np.errstate(invalid="ignore", over="ignore"):
+        tx0 = np.maximum(0, np.floor(x0 / np.float32(pw))).astype(np.int64)
+        tx1 = np.minimum(cols - 1, np.floor(x1 / np.float32(pw))).astype(np.int64)
+        ty0 = np.maximum(0, np.floor(y0 / np.float32(ph))).astype(np.int64)
+        ty1 = np.minimum(rows - 1, np.floor(y1 / np.float32(ph))).astype(np.int64)
+    return tx0, tx1, ty0, ty1, ok & (tx0 <= tx1) & (ty0 <= ty1)
+
+
+@pytest.mark.parametrize("mode", [N.ALPHA_EXACT])
+def test_c4_tile_sampled(mode):
+    """C4 at full size (3840x2160, 3M clustered Gaussians, K ~ 5e8):
+    tile-sampled parity (the 64 longest tiles + 1 % random tiles,
+    seed 42).  For every sampled tile the GPU list must be exactly the splats
+    whose rectangle contains it, in (depth, index) order, and the
+    FineGrainedCombined frame must equal the oracle's render of those lists."""
+    W, H, f, n = 3840, 2160, 2000.0, 3_000_000
+    cam = N.make_camera(None, (f, f), W, H)
+    g3d = api.gen_clustered_scene(n, cam)
+    fp = api.FramePipeline(W, H, 16, 16, DEV, mode)
+    frame, fi = fp.forward(api.g3d_to_device(g3d), n, cam, variant=BS_FG, bg=(0.1, 0.2, 0.3), info=True)
+    got = frame.to_numpy()
+    ocam = O.Camera.from_buffer_copy(bytes(cam))
+    g2d = O.project_all(g3d.view(O.G3D_DTYPE), ocam)
+    assert fi.n_visible == len(g2d)
+    cols, rows = 240, 135
+    T = cols * rows
+    # the pipeline's binning (same context buffers) for the sampled tiles
+    pipe = api.Pipeline(W, H, 16, 16, DEV, mode)
+    pipe.forward(api.g3d_to_device(g3d), n, cam, variant=BS_FG)
+    b = pipe.last_binning
+    assert b.k == fi.k
+    rg = b.tile_ranges.cpu().numpy().view(np.uint32)
+    lens = (rg[1::2] - rg[0::2]).astype(np.int64)
+    rng = np.random.default_rng(42)
+    tiles = np.unique(np.concatenate([np.argsort(-lens, kind="stable")[:64], rng.choice(T, T // 100, replace=False)]))
+    tx0, tx1, ty0, ty1, ok = _rect_rule(g2d, W, H, 16, 16)
+    key = np.lexsort((np.arange(len(g2d)), g2d["depth"]))  # (depth, index) order
+    rank = np.empty(len(g2d), np.int64)
+    rank[key] = np.arange(len(g2d))
+    pl_dev = b.point_list
+    sub_pl, sub_rg = [], np.zeros(2 * T, np.uint32)
+    pos = 0
+    for t in tiles.tolist():
+        tx, ty = t % cols, t // cols
+        lst = pl_dev[int(rg[2 * t]):int(rg[2 * t + 1])].cpu().numpy().view(np.uint32)
+        inside = np.nonzero(ok & (tx0 <= tx) & (tx <= tx1) & (ty0 <= ty) & (ty <= ty1))[0]
+        exp = inside[np.argsort(rank[inside], kind="stable")]
+        assert np.array_equal(lst, exp.astype(np.uint32)), t
+        sub_rg[2 * t], sub_rg[2 * t + 1] = pos, pos + len(lst)
+        sub_pl.append(lst)
+        pos += len(lst)
+    ref = O.render(BS_FG, np.concatenate(sub_pl), sub_rg, g2d, W, H, 16, 16, (0.1, 0.2, 0.3), lazy=True, threads=0,
+                   tiles=tiles.astype(np.int32))
+    px = np.zeros((H, W), bool)
+    for t in tiles.tolist():
+        px[(t // cols) * 16:(t // cols) * 16 + 16, (t % cols) * 16:(t % cols) * 16 + 16] = True
+    m = px.reshape(-1)
+    for k in ("contrib", "term", "final_t", "alpha"):
+        assert np.array_equal(got[k][m], ref[k][m]), k
+    assert float(np.abs(got["color"].reshape(-1, 3)[m] - ref["color"].reshape(-1, 3)[m]).max()) <= 1e-6
+    fp.close()
