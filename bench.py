@@ -344,6 +344,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     reruns_warm = fp.sync()
+    grows_warm = fp.capacity()[1]
     launches0 = N.lib().bs_kernel_launches()
     gc.disable()  # no collector pauses while the host enqueues the timed frames
     for i in range(args.steps):
@@ -356,6 +357,7 @@ def main():
     torch.cuda.synchronize()
     launches = int(N.lib().bs_kernel_launches() - launches0)
     reruns = fp.sync() - reruns_warm
+    grows = fp.capacity()[1] - grows_warm
     # which variant the on-device selector picked for each timed view (replayed untimed)
     for i in range(args.steps):
         _, fi = fp.forward(g3d_dev, n, cams[view_of(args.warmup + i)], variant=variant, info=True)
@@ -399,6 +401,7 @@ def main():
                        l2="flushed between timed steps (256 MiB write, untimed)"),
         "gpu_launches": launches,
         "async_reruns": reruns,
+        "point_list_grows": grows,
         "step_ms_p50_max": [round(float(np.median(step_ms)), 4), round(float(max(step_ms)), 4)],
         "clocks": clocks,
     }

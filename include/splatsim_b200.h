@@ -287,7 +287,8 @@ int bs_render_frame_device(bs_context* ctx, const bs_gaussian3d* g3d_dev, int64_
  * context's own stream is the value bs_context_stream() returned before. */
 int bs_context_set_stream(bs_context* ctx, void* stream);
 /* Async mode for bs_render_frame_device: no host wait inside a frame.
- * point_list is sized from a capacity (grown to 1.25 x the largest K seen);
+ * point_list is sized from a capacity (3 x the first K, regrown to 3 x K
+ * whenever a K passes 2/3 of it);
  * a frame's K is checked at the NEXT call on the context (or at
  * bs_context_sync / bs_context_last_info), and a frame whose K exceeded the
  * capacity is rendered again then, before anything else, with the same
@@ -296,6 +297,8 @@ int bs_context_set_stream(bs_context* ctx, void* stream);
  * so far). */
 int bs_context_set_async(bs_context* ctx, int32_t on);
 int bs_context_sync(bs_context* ctx, int64_t* reruns);
+/* point_list capacity (entries) and how many times it has grown (diagnostics). */
+int bs_context_capacity(bs_context* ctx, int64_t* point_list_cap, int64_t* grows);
 int bs_context_last_info(bs_context* ctx, bs_frame_info* info);
 /* Per-stage CUDA-event timing of the following frames (6 stages: preprocess,
  * bin_count, k_readback, bin_sort, stats_select, render); bs_context_stage_ms

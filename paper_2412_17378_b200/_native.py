@@ -84,6 +84,7 @@ SIGNATURES = {
     "bs_context_set_stream": (C.c_int, [_vp, _vp]),
     "bs_context_set_async": (C.c_int, [_vp, _i32]),
     "bs_context_sync": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
+    "bs_context_capacity": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "bs_bin_sort_async": (C.c_int, [Splats, _i64, _vp, _i32, _i32, _i32, _i32, _i64, _vp, _vp, _vp, _sz, _vp]),
     "bs_bin_async_supported": (C.c_int, [_i32, _i32, _i32, _i32]),
     "bs_context_last_info": (C.c_int, [_vp, C.POINTER(FrameInfo)]),

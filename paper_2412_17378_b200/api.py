@@ -386,6 +386,12 @@ class FramePipeline:
         N.call("bs_context_sync", self.ctx, C.byref(r))
         return int(r.value)
 
+    def capacity(self) -> tuple[int, int]:
+        """(point_list capacity, times grown) — growth inside a timed run is a stall."""
+        cap, g = C.c_int64(0), C.c_int64(0)
+        N.call("bs_context_capacity", self.ctx, C.byref(cap), C.byref(g))
+        return int(cap.value), int(g.value)
+
     def last_info(self) -> N.FrameInfo:
         fi = N.FrameInfo()
         N.call("bs_context_last_info", self.ctx, C.byref(fi))

@@ -284,6 +284,7 @@ constexpr int kScWarps = 16;
 constexpr int kScThreads = kScWarps * 32;
 constexpr int kOwnX = 4, kOwnY = kScWarps / kOwnX;  // tile ownership pattern (powers of 2)
 constexpr int kScMaxRows = 1024;                     // tile rows the row-band split supports
+constexpr int64_t kScTableBytes = 40 * 1024;         // offsets-row slice per CTA (row bands beyond)
 constexpr int64_t kMaxChunkMatrix = (int64_t)16 << 20;  // entries of M (64 MB)
 constexpr int kMaxChunks = 4096;
 constexpr size_t kMaxScatterSmem = 200 * 1024;           // offsets row (T u32) + warp buffers
@@ -427,37 +428,42 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
                                                               const uint2* __restrict__ rects_sorted,
                                                               const uint32_t* __restrict__ order, int T, int cols,
                                                               int rows, uint32_t* __restrict__ point_list,
-                                                              const uint64_t* __restrict__ kd, int64_t k_cap) {
+                                                              const uint64_t* __restrict__ kd, int64_t k_cap,
+                                                              int band_rows) {
   if (*kd == 0 || *kd > (uint64_t)k_cap) return;
   extern __shared__ uint32_t s_off[];
   __shared__ ScQ s_q[kScWarps][64];
   __shared__ uint32_t s_rowp[kScMaxRows + 1];
   const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t* mrow = m + (int64_t)c * T;
-  for (int t = tid; t < T; t += kScThreads) s_off[t] = mrow[t];
-  if (warp == 0) {  // inclusive prefix of the chunk's per-row counts
+  // this CTA: tile rows [R0, R0 + nbr) of chunk c (grids whose offsets row
+  // would not fit shared memory are split into row bands, blockIdx.y)
+  const int R0 = blockIdx.y * band_rows, nbr = min(rows - R0, band_rows);
+  const uint32_t* mrow = m + (int64_t)c * T + (int64_t)R0 * cols;
+  for (int t = tid; t < nbr * cols; t += kScThreads) s_off[t] = mrow[t];
+  if (warp == 0) {  // inclusive prefix of the chunk's per-row counts (this band)
     uint32_t carry = 0;
     if (lane == 0) s_rowp[0] = 0;
-    for (int r0 = 0; r0 < rows; r0 += 32) {
+    for (int r0 = 0; r0 < nbr; r0 += 32) {
       const int r = r0 + lane;
-      uint32_t v = r < rows ? rowc[(int64_t)c * rows + r] : 0u;
+      uint32_t v = r < nbr ? rowc[(int64_t)c * rows + R0 + r] : 0u;
       v = warp_inclusive_scan(v) + carry;
-      if (r < rows) s_rowp[r + 1] = v;
+      if (r < nbr) s_rowp[r + 1] = v;
       carry = __shfl_sync(0xffffffffu, v, 31);
     }
   }
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_off);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_off) - 4u * (uint32_t)(R0 * cols);
   __syncthreads();
   // band of this warp: row r belongs to warp floor(kScWarps * mid(r) / total),
   // mid(r) = the row's middle instance (monotone in r -> contiguous bands)
-  const uint64_t total = s_rowp[rows];
+  const int rows_b = nbr;
+  const uint64_t total = s_rowp[rows_b];
   if (total == 0) return;
   auto owner = [&](int r) -> int {
     const uint64_t mid2 = (uint64_t)s_rowp[r] + s_rowp[r + 1];  // 2 * middle
     return (int)min((uint64_t)(kScWarps - 1), (mid2 * kScWarps) / (2 * total));
   };
   auto band_start = [&](int w) -> int {  // first row whose owner >= w
-    int lo = 0, hi = rows;
+    int lo = 0, hi = rows_b;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       if (owner(mid) < w) lo = mid + 1;
@@ -465,7 +471,7 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
     }
     return lo;
   };
-  const uint32_t r0 = (uint32_t)band_start(warp), r1 = (uint32_t)band_start(warp + 1);
+  const uint32_t r0 = (uint32_t)(R0 + band_start(warp)), r1 = (uint32_t)(R0 + band_start(warp + 1));
   const uint32_t lt = lanemask_lt();
   const uint32_t j0 = first[c], j1 = first[c + 1];
   int qn = 0;  // queued splats (warp-uniform)
@@ -626,7 +632,7 @@ inline bool bin_chunked(const Grid& g) {
     return (e && e[0] == '1') ? 1 : 0;
   }();
   const int64_t T = (int64_t)g.cols * g.rows;
-  return !forced_radix && g.rows <= kScMaxRows && (size_t)(T + 32) * 4 <= kMaxScatterSmem &&
+  return !forced_radix && g.rows <= kScMaxRows && (size_t)(g.cols + 32) * 4 <= (size_t)kScTableBytes &&
          sizeof(int) * (size_t)(g.cols + 1) * (g.rows + 1) <= kMaxDiffSmem;
 }
 
@@ -783,7 +789,10 @@ static int bin_sort_impl(int64_t n_cap, const int32_t* n_visible, int32_t width,
                                        (int)kMaxScatterSmem));
       attr_set = true;
     }
-    const size_t off_bytes = sizeof(uint32_t) * (size_t)((T + 31) & ~31);
+    // offsets row per CTA: the whole grid, or row bands of <= kScTableBytes
+    const int nbands = (int)min((int64_t)gr.rows, ((int64_t)T * 4 + kScTableBytes - 1) / kScTableBytes);
+    const int band_rows = (gr.rows + nbands - 1) / nbands;
+    const size_t off_bytes = sizeof(uint32_t) * (size_t)((band_rows * gr.cols + 31) & ~31);
     const size_t diff_bytes = sizeof(int) * (size_t)(gr.cols + 1) * (gr.rows + 1);
     int dev = 0, sms = 148, per_sm = 1;
     BS_CUDA_TRY(cudaGetDevice(&dev));
@@ -799,7 +808,8 @@ static int bin_sort_impl(int64_t n_cap, const int32_t* n_visible, int32_t width,
       return (int64_t)(e ? max(1, atoi(e)) : 1);
     }();
     const int64_t waves = max(min_waves, (kk + slots * (1 << 18) - 1) / (slots * (1 << 18)));
-    const int64_t nch = max((int64_t)1, min(max_chunks(gr), min(slots * waves, (kk + 4095) / 4096)));
+    const int64_t nch = max((int64_t)1, min(max_chunks(gr), min(max((int64_t)1, slots * waves / nbands),
+                                                                 (kk + 4095) / 4096)));
     k_chunk_bounds<<<(unsigned)((n_cap + 255) / 256), 256, 0, st>>>(w.offs, w.touched_sorted, n_cap, n_visible, kd,
                                                                    k_cap, (int)nch, w.chunk_first);
     BS_LAUNCH_CHECK();
@@ -808,9 +818,9 @@ static int bin_sort_impl(int64_t n_cap, const int32_t* n_visible, int32_t width,
     BS_LAUNCH_CHECK();
     k_chunk_scan<<<(unsigned)((T + 31) / 32), kCsSeg * 32, 0, st>>>(w.chunk_m, w.starts, (int)T, (int)nch, kd, k_cap);
     BS_LAUNCH_CHECK();
-    k_chunk_scatter<<<(unsigned)nch, kScThreads, off_bytes, st>>>(w.chunk_m, w.chunk_rowc, w.chunk_first,
-                                                                   w.rects_sorted, order, (int)T, gr.cols, gr.rows,
-                                                                   point_list, kd, k_cap);
+    k_chunk_scatter<<<dim3((unsigned)nch, (unsigned)nbands), kScThreads, off_bytes, st>>>(
+        w.chunk_m, w.chunk_rowc, w.chunk_first, w.rects_sorted, order, (int)T, gr.cols, gr.rows, point_list, kd, k_cap,
+        band_rows);
     BS_LAUNCH_CHECK();
   } else if (k > 0) {
     const uint32_t* order = w.dv0;  // depth order (4 passes end in dv0)

@@ -80,6 +80,8 @@ struct bs_context {
   } pending[kDepth];
   int n_pending = 0, next_slot = 0;
   int64_t reruns = 0;
+  int64_t pl_grows = 0;
+  bool pl_calibrated = false;
   cudaEvent_t ev[kStages + 1] = {};
 };
 
@@ -257,7 +259,7 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
     if (!c->ev_k[slot]) CUTRY(cudaEventCreateWithFlags(&c->ev_k[slot], cudaEventDisableTiming));
     CUTRY(cudaEventRecord(c->ev_k[slot], st));
     mark(3);
-    if (!c->point_list) TRY(grow_pl_async(c, std::max<int64_t>(n, 1) * 16, st));
+    if (!c->point_list) TRY(grow_pl_async(c, std::max<int64_t>(n, 1) * 64, st));  // 64 tiles / splat to start
     TRY(grow_n(&c->ranges, &c->ranges_cap, 2 * T));
     TRY(bs_bin_sort_async(sp, n, c->n_visible, W, H, pw, ph, std::min<int64_t>(c->pl_cap, (int64_t(1) << 30) - 1),
                           c->point_list, c->ranges, c->bin_ws, c->bin_ws_bytes, st));
@@ -345,6 +347,7 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
 // new one (cudaFreeAsync / cudaMallocAsync on the default pool).
 int grow_pl_async(bs_context* c, int64_t cap, cudaStream_t st) {
   if (cap <= c->pl_cap) return BS_OK;
+  ++c->pl_grows;
   if (c->point_list) CUTRY(cudaFreeAsync(c->point_list, st));
   c->point_list = nullptr;
   c->pl_cap = 0;
@@ -367,8 +370,12 @@ int verify_pending(bs_context* c, cudaStream_t st, int keep = 0) {
     const int64_t k = c->k_host[1 + p0.slot];
     c->last_k = k;
     if (k <= c->pl_cap) {
-      // keep >= 25 % headroom over every K seen: grow ahead of an overflow
-      if (double(k) * 1.25 > double(c->pl_cap)) TRY(grow_pl_async(c, int64_t(double(k) * 1.5) + 1024, st));
+      // keep >= 50 % headroom over every K seen, growing to 3x: a regrowth
+      // maps new memory (a multi-ms stall), so it must be rare — HBM is not
+      // (the first checked frame calibrates the capacity to 3x its K at once)
+      if (!c->pl_calibrated || double(k) * 1.5 > double(c->pl_cap))
+        TRY(grow_pl_async(c, int64_t(double(k) * 3.0) + 1024, st));
+      c->pl_calibrated = true;
       for (int i = 1; i < c->n_pending; ++i) c->pending[i - 1] = c->pending[i];
       --c->n_pending;
       continue;
@@ -377,7 +384,8 @@ int verify_pending(bs_context* c, cudaStream_t st, int keep = 0) {
     const int nr = c->n_pending;
     std::copy(c->pending, c->pending + nr, redo);
     c->n_pending = 0;
-    TRY(grow_pl_async(c, int64_t(double(k) * 1.5) + 1024, st));
+    TRY(grow_pl_async(c, int64_t(double(k) * 3.0) + 1024, st));
+    c->pl_calibrated = true;
     for (int i = 0; i < nr; ++i) {
       ++c->reruns;
       const bs_context::Pending& p = redo[i];
@@ -443,6 +451,13 @@ extern "C" int bs_context_sync(bs_context* c, int64_t* reruns) {
   TRY(verify_pending(c, st));
   CUTRY(cudaStreamSynchronize(st));
   if (reruns) *reruns = c->reruns;
+  return BS_OK;
+}
+
+extern "C" int bs_context_capacity(bs_context* c, int64_t* point_list_cap, int64_t* grows) {
+  if (!c) return BS_ERR_INVALID_ARGUMENT;
+  if (point_list_cap) *point_list_cap = c->pl_cap;
+  if (grows) *grows = c->pl_grows;
   return BS_OK;
 }
 

@@ -390,7 +390,7 @@ def test_tile_order_lpt_buckets(W, H, n):
 
 def test_frame_pipeline_async_overflow_rerun():
     """Async mode: the first frame's K exceeds the initial point_list
-    capacity (16 per Gaussian), so it is rendered again at the next sync point
+    capacity (64 per Gaussian), so it is rendered again at the next sync point
     with a grown capacity; the final output equals the oracle's, and later
     frames need no re-render."""
     W = H = 512
@@ -398,7 +398,7 @@ def test_frame_pipeline_async_overflow_rerun():
     g3d, cam = scene(n, W, H, 2048.0, bgfrac=1.0)
     g2d = O.project_all(g3d, cam)
     pl, rg = O.bin_tiles(g2d, W, H, 16, 16)
-    assert len(pl) > 16 * n  # the initial capacity overflows
+    assert len(pl) > 64 * n  # the initial capacity overflows
     fp = api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT, async_mode=True)
     d = api.g3d_to_device(g3d)
     fp.forward(d, n, ncam(cam), variant=BS_FG, bg=(0.1, 0.2, 0.3))
