@@ -249,6 +249,25 @@ int bs_test_expf(const float* x, float* y, int64_t n, int alpha_mode, void* stre
 int bs_host_gen_clustered_scene(int32_t n, int32_t n_clusters, uint64_t seed, double cluster_sigma,
                                 double background_fraction, const bs_camera* cam, bs_gaussian3d* out);
 
+/* Measured training run (the B200 form of the reference's run_training_sim,
+ * src/adaptive.cpp:34-129; C++: splatsim::run_training): a clustered scene
+ * moves linearly from the *_start to the *_end parameters over total_iters
+ * iterations (regenerated at `keyframes` points), FineGrainedCombined and
+ * SharedMemOpt are timed on the device per keyframe, the selector
+ * checkpoints every check_interval iterations until the first loss.  Writes
+ * report_csv (NUL-terminated, truncated to csv_cap) and its full length. */
+typedef struct bs_training_params {
+  int32_t total_iters, keyframes, width, height, patch_width, patch_height;
+  float focal;
+  int32_t n_gaussians;
+  uint64_t seed;
+  double background_fraction_start, background_fraction_end;
+  double cluster_sigma_start, cluster_sigma_end;
+  double opacity_scale_start, opacity_scale_end;
+} bs_training_params;
+int bs_host_run_training(const bs_training_params* params, int32_t check_interval, char* csv, size_t csv_cap,
+                         size_t* csv_len);
+
 /* ---- host-buffer frame API (the drop-in for project_all -> bin_tiles ->
  * run_kernel on HOST data) ----
  * A context owns a CUDA stream and device buffers that grow on demand.

@@ -48,6 +48,35 @@ struct Camera {
   int height = 0;
 };
 
+// ---- scene (scene.hpp:16-62) ----
+struct SceneConfig {
+  int patch_width = 16;
+  int patch_height = 8;
+  std::array<float, 3> background{0, 0, 0};
+  std::uint64_t seed = 0;
+};
+
+struct Scene {
+  std::vector<Gaussian3D> gaussians;
+  Camera camera;
+  SceneConfig config;
+};
+
+class SceneError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+// src/scene.cpp:41-179 (host-only; the JSON reader/writer is in-repo, the
+// reference's nlohmann/json is not vendored).  validate throws SceneError
+// naming the offending field; parse/serialize round-trip every float field
+// bit-exactly (floats are written as the shortest text of their exact double).
+void validate(const Scene& scene);
+Scene parse_scene(const std::string& json_text);
+std::string serialize_scene(const Scene& scene);
+Scene load_scene(const std::string& path);
+void save_scene(const Scene& scene, const std::string& path);
+
 struct Gaussian2D {
   std::array<float, 2> xy{0, 0};
   float conic_a = 1.0f;
@@ -202,6 +231,56 @@ SelectionState checkpoint(SelectionState state, int iter, const TileBinning& bin
                           int patch_height);
 // Per-frame predictor from tile statistics (bs_select_variant).
 KernelVariant select_variant(const TileHistogram& h, int width, int height, int patch_width, int patch_height);
+
+// ---- training run (adaptive.hpp run_training_sim / speedup_summary /
+// report_csv) on measured B200 render times instead of simulated cycles ----
+// The reference drives synthetic tile loads along TrajectoryParams
+// (src/workload.cpp:248-266); here the trajectory moves a real clustered
+// scene from an early-training state (few, tight, faint clusters) to a late
+// one (uniform, opaque), linearly in the iteration, re-generated at
+// `keyframes` evenly spaced iterations (piecewise-constant between them, so
+// each keyframe's kernel times are measured once and reused for its
+// iterations).
+struct GeoTrajectoryParams {
+  int total_iters = 7000;
+  int keyframes = 8;
+  int width = 1920, height = 1080, patch_width = 16, patch_height = 16;
+  float focal = 1000.0f;
+  int n_gaussians = 1000000;
+  std::uint64_t seed = 42;
+  double background_fraction_start = 0.05, background_fraction_end = 1.0;
+  double cluster_sigma_start = 0.02, cluster_sigma_end = 0.035;
+  double opacity_scale_start = 0.05, opacity_scale_end = 1.0;
+};
+struct IterationRecord {
+  int iter = 0;
+  KernelVariant variant = KernelVariant::FineGrainedCombined;
+  double ms = 0.0;  // the chosen kernel's measured render time
+  bool is_checkpoint = false;
+  double t_balanced = 0.0;  // checkpoint rows only
+  double t_baseline = 0.0;
+};
+struct TrainingRunReport {
+  std::vector<IterationRecord> iterations;
+  std::optional<int> inflection_iter;
+  double adaptive_ms = 0.0;           // chosen-variant time + benchmark overhead
+  double benchmark_overhead_ms = 0.0; // both-kernel runs at checkpoints
+  double always_balanced_ms = 0.0;
+  double always_baseline_ms = 0.0;
+};
+struct SpeedupSummary {
+  std::optional<double> pre_inflection;
+  std::optional<double> post_inflection;
+  double overall = 1.0;
+};
+// src/adaptive.cpp:34-77 semantics (checkpoint every check_interval until the
+// first loss, switch permanently, benchmark runs charged to the adaptive
+// total); throws std::invalid_argument on a non-positive interval.
+TrainingRunReport run_training(const GeoTrajectoryParams& tp, int check_interval);
+// src/adaptive.cpp:79-101.
+SpeedupSummary speedup_summary(const TrainingRunReport& report);
+// src/adaptive.cpp:103-129 (times in ms).
+std::string report_csv(const TrainingRunReport& report, const std::string& config_comment);
 
 // ---- image_io (image_io.hpp) ----
 struct Deviation {

@@ -35,6 +35,15 @@ class TileHistogram(C.Structure):
                 ("mean", C.c_double), ("total", C.c_uint64), ("tiles", C.c_int32), ("nonempty", C.c_int32)]
 
 
+class TrainingParams(C.Structure):
+    _fields_ = [("total_iters", C.c_int32), ("keyframes", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
+                ("patch_width", C.c_int32), ("patch_height", C.c_int32), ("focal", C.c_float),
+                ("n_gaussians", C.c_int32), ("seed", C.c_uint64),
+                ("background_fraction_start", C.c_double), ("background_fraction_end", C.c_double),
+                ("cluster_sigma_start", C.c_double), ("cluster_sigma_end", C.c_double),
+                ("opacity_scale_start", C.c_double), ("opacity_scale_end", C.c_double)]
+
+
 class FrameInfo(C.Structure):
     _fields_ = [("variant", C.c_int32), ("n_visible", C.c_int32), ("k", C.c_int64), ("stats", TileHistogram),
                 ("evaluated", C.c_uint64), ("committed", C.c_uint64)]
@@ -93,6 +102,7 @@ SIGNATURES = {
     "bs_select_variant_device": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "bs_render_forward_auto": (C.c_int, [_vp, C.c_int, Splats, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _f32p,
                                          FrameOut, _vp, _sz, _vp]),
+    "bs_host_run_training": (C.c_int, [C.POINTER(TrainingParams), _i32, C.c_char_p, _sz, C.POINTER(C.c_size_t)]),
     "bs_kernel_launches": (_u64, []),
     "bs_host_gen_clustered_scene": (C.c_int, [_i32, _i32, _u64, C.c_double, C.c_double, C.POINTER(Camera), _vp]),
 }

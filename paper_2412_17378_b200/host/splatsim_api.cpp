@@ -515,6 +515,108 @@ KernelVariant select_variant(const TileHistogram& h, int width, int height, int 
 }
 
 // ---------------------------------------------------------------------------
+// Training run on measured times (src/adaptive.cpp:34-129 semantics).
+TrainingRunReport run_training(const GeoTrajectoryParams& tp, int check_interval) {
+  if (check_interval <= 0) throw std::invalid_argument("run_training: bad check interval");
+  if (tp.total_iters <= 0 || tp.keyframes <= 0) throw std::invalid_argument("run_training: bad trajectory");
+  TrainingRunReport report;
+  report.iterations.reserve(size_t(tp.total_iters));
+  SelectionState state;
+  state.check_interval = check_interval;
+  Camera cam;
+  cam.view_transform = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1};
+  cam.focal = {tp.focal, tp.focal};
+  cam.width = tp.width;
+  cam.height = tp.height;
+  const int kf = std::min(tp.keyframes, tp.total_iters);
+  int seg = -1;
+  double t_bal = 0.0, t_base = 0.0;
+  for (int iter = 0; iter < tp.total_iters; ++iter) {
+    const int s = int(int64_t(iter) * kf / tp.total_iters);  // keyframe segment of this iteration
+    if (s != seg) {
+      seg = s;
+      const double x = kf > 1 ? double(s) / double(kf - 1) : 0.0;
+      ClusterSceneParams p;
+      p.n_gaussians = tp.n_gaussians;
+      p.seed = tp.seed;
+      p.background_fraction = tp.background_fraction_start * (1 - x) + tp.background_fraction_end * x;
+      p.cluster_sigma = tp.cluster_sigma_start * (1 - x) + tp.cluster_sigma_end * x;
+      std::vector<Gaussian3D> g = gen_clustered_scene(p, cam);
+      const float os = float(tp.opacity_scale_start * (1 - x) + tp.opacity_scale_end * x);
+      for (Gaussian3D& q : g) q.opacity *= os;
+      const std::vector<Gaussian2D> g2 = project_all(g, cam);
+      const TileBinning b = bin_tiles(g2, tp.width, tp.height, tp.patch_width, tp.patch_height);
+      t_bal = time_kernel_ms(KernelVariant::FineGrainedCombined, b, g2, tp.width, tp.height, tp.patch_width,
+                             tp.patch_height, 5);
+      t_base = time_kernel_ms(KernelVariant::SharedMemOpt, b, g2, tp.width, tp.height, tp.patch_width,
+                              tp.patch_height, 5);
+    }
+    report.always_balanced_ms += t_bal;
+    report.always_baseline_ms += t_base;
+    IterationRecord rec;
+    rec.iter = iter;
+    if (!state.switched && iter % check_interval == 0) {
+      rec.is_checkpoint = true;
+      rec.t_balanced = t_bal;
+      rec.t_baseline = t_base;
+      report.benchmark_overhead_ms += t_bal + t_base;
+      state = checkpoint(std::move(state), iter, t_bal, t_base);
+      if (state.switched) report.inflection_iter = iter;
+    }
+    rec.variant = state.current;
+    rec.ms = state.current == KernelVariant::FineGrainedCombined ? t_bal : t_base;
+    report.adaptive_ms += rec.ms;
+    report.iterations.push_back(rec);
+  }
+  report.adaptive_ms += report.benchmark_overhead_ms;
+  return report;
+}
+
+SpeedupSummary speedup_summary(const TrainingRunReport& report) {
+  SpeedupSummary s;
+  double all_chosen = 0.0, post_chosen = 0.0;
+  for (const IterationRecord& rec : report.iterations) {
+    all_chosen += rec.ms;
+    if (report.inflection_iter && rec.iter >= *report.inflection_iter) post_chosen += rec.ms;
+  }
+  const double all_base = report.always_baseline_ms;
+  if (report.inflection_iter) {
+    // after the switch the chosen kernel is the baseline
+    const double post_base = post_chosen, pre_base = all_base - post_base, pre_chosen = all_chosen - post_chosen;
+    if (pre_chosen > 0.0) s.pre_inflection = pre_base / pre_chosen;
+    if (post_chosen > 0.0) s.post_inflection = post_base / post_chosen;
+  } else if (all_chosen > 0.0) {
+    s.pre_inflection = all_base / all_chosen;
+  }
+  s.overall = all_chosen > 0.0 ? all_base / all_chosen : 1.0;
+  return s;
+}
+
+std::string report_csv(const TrainingRunReport& report, const std::string& config_comment) {
+  std::ostringstream out;
+  out.precision(17);
+  out << "# " << config_comment << "\n";
+  out << "iter,variant,ms,is_checkpoint,t_balanced,t_baseline\n";
+  for (const IterationRecord& rec : report.iterations) {
+    out << rec.iter << ',' << variant_name(rec.variant) << ',' << rec.ms << ',' << (rec.is_checkpoint ? 1 : 0) << ',';
+    if (rec.is_checkpoint)
+      out << rec.t_balanced << ',' << rec.t_baseline;
+    else
+      out << ',';
+    out << "\n";
+  }
+  const SpeedupSummary s = speedup_summary(report);
+  out << "# summary inflection_iter="
+      << (report.inflection_iter ? std::to_string(*report.inflection_iter) : std::string("none"))
+      << " adaptive_ms=" << report.adaptive_ms << " benchmark_overhead_ms=" << report.benchmark_overhead_ms
+      << " always_balanced_ms=" << report.always_balanced_ms << " always_baseline_ms=" << report.always_baseline_ms
+      << " speedup_pre=" << (s.pre_inflection ? std::to_string(*s.pre_inflection) : std::string("none"))
+      << " speedup_post=" << (s.post_inflection ? std::to_string(*s.post_inflection) : std::string("none"))
+      << " speedup_overall=" << s.overall << "\n";
+  return out.str();
+}
+
+// ---------------------------------------------------------------------------
 Deviation compare_outputs(const RenderOutput& reference, const RenderOutput& candidate) {
   if (reference.width != candidate.width || reference.height != candidate.height)
     throw std::invalid_argument("compare_outputs: dimension mismatch");
@@ -592,3 +694,40 @@ std::uint64_t fnv1a64(const void* data, std::size_t size, std::uint64_t h) {
 }
 
 }  // namespace splatsim
+
+extern "C" int bs_host_run_training(const bs_training_params* p, int32_t check_interval, char* csv, size_t csv_cap,
+                                    size_t* csv_len) {
+  if (!p) return BS_ERR_INVALID_ARGUMENT;
+  try {
+    splatsim::GeoTrajectoryParams tp;
+    tp.total_iters = p->total_iters;
+    tp.keyframes = p->keyframes;
+    tp.width = p->width;
+    tp.height = p->height;
+    tp.patch_width = p->patch_width;
+    tp.patch_height = p->patch_height;
+    tp.focal = p->focal;
+    tp.n_gaussians = p->n_gaussians;
+    tp.seed = p->seed;
+    tp.background_fraction_start = p->background_fraction_start;
+    tp.background_fraction_end = p->background_fraction_end;
+    tp.cluster_sigma_start = p->cluster_sigma_start;
+    tp.cluster_sigma_end = p->cluster_sigma_end;
+    tp.opacity_scale_start = p->opacity_scale_start;
+    tp.opacity_scale_end = p->opacity_scale_end;
+    const std::string out = splatsim::report_csv(splatsim::run_training(tp, check_interval), "bs_host_run_training");
+    if (csv_len) *csv_len = out.size();
+    if (csv && csv_cap) {
+      const size_t n = std::min(out.size(), csv_cap - 1);
+      std::memcpy(csv, out.data(), n);
+      csv[n] = 0;
+    }
+    return BS_OK;
+  } catch (const std::invalid_argument&) {
+    return BS_ERR_INVALID_ARGUMENT;
+  } catch (const std::logic_error&) {
+    return BS_ERR_LOGIC;
+  } catch (...) {
+    return BS_ERR_CUDA;
+  }
+}

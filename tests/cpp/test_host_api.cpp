@@ -144,6 +144,53 @@ int main() {
   CHECK(ferr <= 1e-4);
   CHECK(double(mism) / double(ref.contrib.size()) < 2e-3);
 
+  // speedup_summary on a hand-built report (src/adaptive.cpp:79-101):
+  // balanced 1 ms/iter before the switch at iter 2, baseline 2 ms/iter always
+  {
+    splatsim::TrainingRunReport r;
+    for (int i = 0; i < 4; ++i) {
+      splatsim::IterationRecord rec;
+      rec.iter = i;
+      rec.variant = i < 2 ? splatsim::KernelVariant::FineGrainedCombined : splatsim::KernelVariant::SharedMemOpt;
+      rec.ms = i < 2 ? 1.0 : 2.0;
+      r.iterations.push_back(rec);
+    }
+    r.always_baseline_ms = 8.0;
+    r.inflection_iter = 2;
+    const auto sp = splatsim::speedup_summary(r);
+    CHECK(sp.pre_inflection && std::abs(*sp.pre_inflection - 2.0) < 1e-12);
+    CHECK(sp.post_inflection && std::abs(*sp.post_inflection - 1.0) < 1e-12);
+    CHECK(std::abs(sp.overall - 8.0 / 6.0) < 1e-12);
+    r.inflection_iter.reset();
+    CHECK(!splatsim::speedup_summary(r).post_inflection);
+  }
+  // a short measured training run: checkpoints at 0, 3, 6 until the first
+  // loss, benchmark overhead charged, CSV summary line present
+  {
+    splatsim::GeoTrajectoryParams tp;
+    tp.total_iters = 9;
+    tp.keyframes = 3;
+    tp.width = 320;
+    tp.height = 192;
+    tp.focal = 320.0f;
+    tp.n_gaussians = 20000;
+    const auto rep = splatsim::run_training(tp, 3);
+    CHECK(rep.iterations.size() == 9);
+    CHECK(rep.iterations[0].is_checkpoint && rep.iterations[0].t_balanced > 0 && rep.iterations[0].t_baseline > 0);
+    double chosen = 0;
+    for (const auto& it : rep.iterations) chosen += it.ms;
+    CHECK(std::abs(rep.adaptive_ms - chosen - rep.benchmark_overhead_ms) < 1e-9 * (1 + rep.adaptive_ms));
+    const std::string csv = splatsim::report_csv(rep, "unit");
+    CHECK(csv.rfind("# unit\n", 0) == 0 && csv.find("# summary inflection_iter=") != std::string::npos);
+    bool threw = false;
+    try {
+      splatsim::run_training(tp, 0);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }
