@@ -24,10 +24,14 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "training_run.csv"))
     a = ap.parse_args()
     p = N.TrainingParams(a.iters, a.keyframes, 1920, 1080, 16, 16, 1000.0, a.n, 42, 0.05, 1.0, 0.02, 0.035, 0.05, 1.0)
+    # one run (measured times differ run to run, so the text length is not
+    # known up front): a buffer far above 7000 rows x ~80 characters
+    cap = max(1 << 20, a.iters * 160)
     need = C.c_size_t(0)
-    N.call("bs_host_run_training", C.byref(p), a.interval, None, 0, C.byref(need))
-    buf = C.create_string_buffer(need.value + 1)
-    N.call("bs_host_run_training", C.byref(p), a.interval, buf, need.value + 1, C.byref(need))
+    buf = C.create_string_buffer(cap)
+    N.call("bs_host_run_training", C.byref(p), a.interval, buf, cap, C.byref(need))
+    if need.value >= cap:
+        raise RuntimeError(f"report truncated ({need.value} bytes)")
     text = buf.value.decode()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     with open(a.out, "w") as f:
