@@ -290,6 +290,7 @@ def main():
     ap.add_argument("--variant", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sync-frames", action="store_true", help="wait for K inside each frame (no async mode)")
+    ap.add_argument("--no-graphs", action="store_true", help="launch every kernel instead of replaying a CUDA graph")
     ap.add_argument("--no-extras", action="store_true", help="skip per-variant sweep / e2e / cpu baseline")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
@@ -323,7 +324,8 @@ def main():
     cams = [api.camera(orbit_view(k), (f, f), W, H) for k in range(N_VIEWS)]
     # the native frame pipeline: one C-ABI call per view, no host wait inside a
     # frame (async mode: K verified one call later, overflowed frames re-rendered)
-    fp = api.FramePipeline(W, H, pw, ph, dev, mode, async_mode=not args.sync_frames)
+    fp = api.FramePipeline(W, H, pw, ph, dev, mode, async_mode=not args.sync_frames,
+                           graphs=not (args.sync_frames or args.no_graphs))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def view_of(i):
@@ -345,6 +347,7 @@ def main():
     torch.cuda.synchronize()
     reruns_warm = fp.sync()
     grows_warm = fp.capacity()[1]
+    glaunch0 = fp.graph_launches()
     launches0 = N.lib().bs_kernel_launches()
     gc.disable()  # no collector pauses while the host enqueues the timed frames
     for i in range(args.steps):
@@ -358,6 +361,7 @@ def main():
     launches = int(N.lib().bs_kernel_launches() - launches0)
     reruns = fp.sync() - reruns_warm
     grows = fp.capacity()[1] - grows_warm
+    graph_replays = fp.graph_launches() - glaunch0
     # which variant the on-device selector picked for each timed view (replayed untimed)
     for i in range(args.steps):
         _, fi = fp.forward(g3d_dev, n, cams[view_of(args.warmup + i)], variant=variant, info=True)
@@ -402,6 +406,7 @@ def main():
         "gpu_launches": launches,
         "async_reruns": reruns,
         "point_list_grows": grows,
+        "graph_replays": graph_replays,
         "step_ms_p50_max": [round(float(np.median(step_ms)), 4), round(float(max(step_ms)), 4)],
         "clocks": clocks,
     }

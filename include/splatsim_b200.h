@@ -146,6 +146,11 @@ size_t bs_preprocess_workspace_bytes(int64_t n);
 int bs_preprocess(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, bs_splats out, int32_t* n_visible,
                   void* ws, size_t ws_bytes, void* stream);
 
+/* Same, with the camera read from DEVICE memory at run time (what a CUDA
+ * graph of the frame replays with a per-frame camera). */
+int bs_preprocess_devcam(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam_dev, bs_splats out,
+                         int32_t* n_visible, void* ws, size_t ws_bytes, void* stream);
+
 /* Interop: device AoS Gaussian2D <-> splats (fills power_cut). */
 int bs_splats_from_g2d(const bs_gaussian2d* g2d, int64_t n, bs_splats out, void* stream);
 int bs_splats_to_g2d(bs_splats in, int64_t n, bs_gaussian2d* g2d, void* stream);
@@ -316,6 +321,17 @@ int bs_context_set_stream(bs_context* ctx, void* stream);
  * so far). */
 int bs_context_set_async(bs_context* ctx, int32_t on);
 int bs_context_sync(bs_context* ctx, int64_t* reruns);
+/* CUDA-graph mode for async frames: the first frame of a configuration
+ * (inputs, outputs, dims, variant, bg, buffers) runs normally, later ones
+ * replay a captured graph of the same kernels with the new camera (copied in
+ * ahead of the launch) — one launch instead of ~45.  Off by default.
+ * bs_context_graph_launches counts the replays. */
+int bs_context_set_graphs(bs_context* ctx, int32_t on);
+int bs_context_graph_launches(bs_context* ctx, int64_t* launches);
+/* Drops pending K checks without waiting (after capturing a frame into a
+ * CUDA graph: the captured call's check never ran).  The caller then owns
+ * capacity safety for replays. */
+int bs_context_drop_pending(bs_context* ctx);
 /* point_list capacity (entries) and how many times it has grown (diagnostics). */
 int bs_context_capacity(bs_context* ctx, int64_t* point_list_cap, int64_t* grows);
 int bs_context_last_info(bs_context* ctx, bs_frame_info* info);

@@ -94,6 +94,10 @@ SIGNATURES = {
     "bs_context_set_async": (C.c_int, [_vp, _i32]),
     "bs_context_sync": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
     "bs_context_capacity": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "bs_context_drop_pending": (C.c_int, [_vp]),
+    "bs_context_set_graphs": (C.c_int, [_vp, _i32]),
+    "bs_context_graph_launches": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
+    "bs_preprocess_devcam": (C.c_int, [_vp, _i64, _vp, Splats, _vp, _vp, _sz, _vp]),
     "bs_bin_sort_async": (C.c_int, [Splats, _i64, _vp, _i32, _i32, _i32, _i32, _i64, _vp, _vp, _vp, _sz, _vp]),
     "bs_bin_async_supported": (C.c_int, [_i32, _i32, _i32, _i32]),
     "bs_context_last_info": (C.c_int, [_vp, C.POINTER(FrameInfo)]),

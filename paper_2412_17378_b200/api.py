@@ -359,13 +359,16 @@ class FramePipeline:
     selection for ``variant="auto"``.  Outputs land in ``self.frame``."""
 
     def __init__(self, width: int, height: int, pw: int = 16, ph: int = 16, device="cuda",
-                 alpha_mode: int = ALPHA_EXACT, timing: bool = False, async_mode: bool = False):
+                 alpha_mode: int = ALPHA_EXACT, timing: bool = False, async_mode: bool = False,
+                 graphs: bool = False):
         self.width, self.height, self.pw, self.ph, self.device = width, height, pw, ph, device
         self.ctx = C.c_void_p()
         N.call("bs_context_create", C.byref(self.ctx), int(alpha_mode))
         N.call("bs_context_set_stream", self.ctx, _stream(device))
         if async_mode:  # no host wait inside a frame; K checked at the next call (bs_context_set_async)
             N.call("bs_context_set_async", self.ctx, 1)
+        if graphs:  # replay a captured CUDA graph of the frame (bs_context_set_graphs)
+            N.call("bs_context_set_graphs", self.ctx, 1)
         if timing:
             N.call("bs_context_enable_timing", self.ctx, 1)
         self.frame = DeviceFrame.empty(width, height, device)
@@ -385,6 +388,11 @@ class FramePipeline:
         r = C.c_int64(0)
         N.call("bs_context_sync", self.ctx, C.byref(r))
         return int(r.value)
+
+    def graph_launches(self) -> int:
+        v = C.c_int64(0)
+        N.call("bs_context_graph_launches", self.ctx, C.byref(v))
+        return int(v.value)
 
     def capacity(self) -> tuple[int, int]:
         """(point_list capacity, times grown) — growth inside a timed run is a stall."""

@@ -122,8 +122,24 @@ __device__ __forceinline__ void load_g3d(const bs_gaussian3d* __restrict__ src, 
   for (int k = 0; k < 14; ++k) d[k] = __ldg(s + k);
 }
 
-__global__ void __launch_bounds__(256) k_project_flags(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam,
+// camera from device memory (CUDA-graph replays of the frame pipeline read a
+// per-frame camera the host copies in ahead of the launch)
+__device__ __forceinline__ CamDev cam_of(const bs_camera* __restrict__ camd, const CamDev& cam) {
+  if (!camd) return cam;
+  CamDev c;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) c.v[k] = __ldg(&camd->view[k]);
+  c.fx = __ldg(&camd->focal[0]);
+  c.fy = __ldg(&camd->focal[1]);
+  c.w = __ldg(&camd->width);
+  c.h = __ldg(&camd->height);
+  return c;
+}
+
+__global__ void __launch_bounds__(256) k_project_flags(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam_,
+                                                       const bs_camera* __restrict__ camd,
                                                        uint32_t* __restrict__ block_counts) {
+  const CamDev cam = cam_of(camd, cam_);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool vis = false;
   if (i < n) {
@@ -136,9 +152,11 @@ __global__ void __launch_bounds__(256) k_project_flags(const bs_gaussian3d* __re
   if (threadIdx.x == 0) block_counts[blockIdx.x] = (uint32_t)cnt;
 }
 
-__global__ void __launch_bounds__(256) k_project_write(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam,
+__global__ void __launch_bounds__(256) k_project_write(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam_,
+                                                       const bs_camera* __restrict__ camd,
                                                        const uint32_t* __restrict__ block_offsets, float4* __restrict__ xyab,
                                                        float4* __restrict__ cop, float4* __restrict__ rgbr) {
+  const CamDev cam = cam_of(camd, cam_);
   __shared__ uint32_t warp_counts[8];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bs_gaussian3d g;
@@ -196,36 +214,52 @@ extern "C" size_t bs_preprocess_workspace_bytes(int64_t n) {
   return s.off + 256;
 }
 
-extern "C" int bs_preprocess(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, bs_splats out,
-                             int32_t* n_visible, void* ws, size_t ws_bytes, void* stream) {
-  if (n < 0 || !cam || !n_visible || (n > 0 && (!g3d || !out.xyab || !out.cop || !out.rgbr))) return BS_ERR_INVALID_ARGUMENT;
+static int preprocess_impl(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, const bs_camera* cam_dev,
+                           bs_splats out, int32_t* n_visible, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || (!cam && !cam_dev) || !n_visible || (n > 0 && (!g3d || !out.xyab || !out.cop || !out.rgbr)))
+    return BS_ERR_INVALID_ARGUMENT;
   if (n >= (int64_t)0x7fffffff) return BS_ERR_CAPACITY;
   cudaStream_t st = (cudaStream_t)stream;
   if (n == 0) {
     BS_CUDA_TRY(cudaMemsetAsync(n_visible, 0, sizeof(int32_t), st));
     return BS_OK;
   }
-  CamDev c;
-  for (int r = 0; r < 3; ++r)
-    for (int k = 0; k < 4; ++k) c.v[r * 4 + k] = cam->view[r * 4 + k];
-  c.fx = cam->focal[0];
-  c.fy = cam->focal[1];
-  c.w = cam->width;
-  c.h = cam->height;
+  CamDev c{};
+  if (cam) {
+    for (int r = 0; r < 3; ++r)
+      for (int k = 0; k < 4; ++k) c.v[r * 4 + k] = cam->view[r * 4 + k];
+    c.fx = cam->focal[0];
+    c.fy = cam->focal[1];
+    c.w = cam->width;
+    c.h = cam->height;
+  }
   const int64_t nb = (n + 255) / 256;
   WsCarver wc(ws, ws_bytes);
   uint32_t* counts = wc.take<uint32_t>((size_t)nb);
   uint32_t* partials = wc.take<uint32_t>((size_t)scan_num_blocks(nb));
   if (!wc.ok || !ws) return BS_ERR_WORKSPACE;
-  k_project_flags<<<(unsigned)nb, 256, 0, st>>>(g3d, n, c, counts);
+  k_project_flags<<<(unsigned)nb, 256, 0, st>>>(g3d, n, c, cam ? nullptr : cam_dev, counts);
   BS_LAUNCH_CHECK();
   // exclusive scan of block counts in place; grand total -> n_visible (u32 == i32 bits for n < 2^31)
   BS_CUDA_TRY((exclusive_scan<uint32_t, uint32_t>(counts, counts, nb, nullptr, partials,
                                                  reinterpret_cast<uint32_t*>(n_visible), st)));
-  k_project_write<<<(unsigned)nb, 256, 0, st>>>(g3d, n, c, counts, reinterpret_cast<float4*>(out.xyab),
-                                                reinterpret_cast<float4*>(out.cop), reinterpret_cast<float4*>(out.rgbr));
+  k_project_write<<<(unsigned)nb, 256, 0, st>>>(g3d, n, c, cam ? nullptr : cam_dev, counts,
+                                                reinterpret_cast<float4*>(out.xyab), reinterpret_cast<float4*>(out.cop),
+                                                reinterpret_cast<float4*>(out.rgbr));
   BS_LAUNCH_CHECK();
   return BS_OK;
+}
+
+extern "C" int bs_preprocess(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, bs_splats out,
+                             int32_t* n_visible, void* ws, size_t ws_bytes, void* stream) {
+  if (!cam) return BS_ERR_INVALID_ARGUMENT;
+  return preprocess_impl(g3d, n, cam, nullptr, out, n_visible, ws, ws_bytes, stream);
+}
+
+extern "C" int bs_preprocess_devcam(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam_dev, bs_splats out,
+                                    int32_t* n_visible, void* ws, size_t ws_bytes, void* stream) {
+  if (!cam_dev) return BS_ERR_INVALID_ARGUMENT;
+  return preprocess_impl(g3d, n, nullptr, cam_dev, out, n_visible, ws, ws_bytes, stream);
 }
 
 extern "C" int bs_splats_from_g2d(const bs_gaussian2d* g2d, int64_t n, bs_splats out, void* stream) {

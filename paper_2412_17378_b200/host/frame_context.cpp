@@ -11,10 +11,16 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
 #include "splatsim_b200.h"
+
+namespace bs {
+void count_launches(unsigned long long n);  // csrc/capi.cu: the library's kernel launch counter
+}
 
 constexpr int kStages = 6;  // preprocess, bin_count, k_readback, bin_sort, stats_select, render
 
@@ -81,14 +87,39 @@ struct bs_context {
   int n_pending = 0, next_slot = 0;
   int64_t reruns = 0;
   int64_t pl_grows = 0;
+  // CUDA-graph mode (bs_context_set_graphs): the async frame body captured
+  // once per configuration and per K slot, replayed with the camera copied
+  // into cam_dev from a pinned ring ahead of each launch
+  bool graphs = false;
+  uint64_t gen = 0;  // bumped by every (re)allocation: graphs bake pointers in
+  struct GKey {
+    const void* g3d = nullptr;
+    int64_t n = -1;
+    int32_t W = 0, H = 0, pw = 0, ph = 0, variant = 0;
+    float bg[3] = {0, 0, 0};
+    bs_frame_out out{};
+    uint64_t gen = ~0ull;
+    cudaStream_t st = nullptr;
+    bool operator==(const GKey& o) const { return std::memcmp(this, &o, sizeof(GKey)) == 0; }
+  } gkey;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  uint64_t gkernels[2] = {0, 0};  // kernel launches recorded in each graph
+  cudaStream_t cap_stream = nullptr;
+  bs_camera* cam_dev = nullptr;
+  bs_camera* cam_ring = nullptr;  // pinned, 4 slots
+  int ring_i = 0;
+  int64_t graph_launches = 0;
   bool pl_calibrated = false;
   cudaEvent_t ev[kStages + 1] = {};
 };
 
 namespace {
 
+uint64_t g_alloc_gen = 0;  // (re)allocations anywhere in a context -> graph keys change
+
 int grow(void** p, size_t* cap, size_t need) {
   if (*p && *cap >= need) return BS_OK;
+  ++g_alloc_gen;
   if (*p) cudaFree(*p);
   *p = nullptr;
   need = std::max<size_t>(need, 256);
@@ -120,12 +151,24 @@ int grow_n(T** p, int64_t* cap, int64_t need, double slack = 1.0) {
     int _s = (x);              \
     if (_s != BS_OK) return _s; \
   } while (0)
-#define CUTRY(x)                                        \
-  do {                                                  \
-    if ((x) != cudaSuccess) {                           \
-      (void)cudaGetLastError();                         \
-      return BS_ERR_CUDA;                               \
-    }                                                   \
+// BS_DEBUG=1: name the failing CUDA call on stderr
+bool debug_on() {
+  static const bool on = [] {
+    const char* e = getenv("BS_DEBUG");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+#define CUTRY(x)                                                                                    \
+  do {                                                                                              \
+    const cudaError_t _e = (x);                                                                     \
+    if (_e != cudaSuccess) {                                                                        \
+      if (debug_on()) fprintf(stderr, "bs: %s failed: %s (%s:%d)\n", #x, cudaGetErrorString(_e),     \
+                              __FILE__, __LINE__);                                                  \
+      (void)cudaGetLastError();                                                                     \
+      return BS_ERR_CUDA;                                                                           \
+    }                                                                                               \
   } while (0)
 
 }  // namespace
@@ -183,6 +226,11 @@ extern "C" int bs_context_destroy(bs_context* c) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_k)
     if (e) cudaEventDestroy(e);
+  for (cudaGraphExec_t& e : c->gexec)
+    if (e) cudaGraphExecDestroy(e);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->cam_dev) cudaFree(c->cam_dev);
+  if (c->cam_ring) cudaFreeHost(c->cam_ring);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return BS_OK;
@@ -217,7 +265,9 @@ int grow_pl_async(bs_context* c, int64_t cap, cudaStream_t st);
 // selects on the device (bs_select_variant_device + bs_render_forward_auto),
 // so no sync follows it.
 int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const bs_camera* cam, int32_t pw, int32_t ph,
-                 int32_t variant, const float bg[3], bs_frame_out fo_in, cudaStream_t st, bool allow_async) {
+                 int32_t variant, const float bg[3], bs_frame_out fo_in, cudaStream_t st, bool allow_async,
+                 const bs_camera* cam_dev = nullptr, int capture_slot = -1) {
+  const bool capturing = capture_slot >= 0;  // recording into a CUDA graph: no allocation, no pending entry
   const int32_t W = cam->width, H = cam->height;
   const int64_t cols = (W + pw - 1) / pw, rows = (H + ph - 1) / ph, T = cols * rows;
   const int64_t P = int64_t(W) * H;
@@ -227,6 +277,7 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   mark(0);
   // P1-P4
   if (n > c->splat_cap) {
+    ++g_alloc_gen;
     for (auto& p : c->splat) {
       if (p) cudaFree(p);
       p = nullptr;
@@ -237,7 +288,10 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   bs_splats sp{reinterpret_cast<float*>(c->splat[0]), reinterpret_cast<float*>(c->splat[1]),
                reinterpret_cast<float*>(c->splat[2])};
   TRY(grow(&c->pre_ws, &c->pre_ws_bytes, bs_preprocess_workspace_bytes(n)));
-  TRY(bs_preprocess(g3d_dev, n, cam, sp, c->n_visible, c->pre_ws, c->pre_ws_bytes, st));
+  if (cam_dev)
+    TRY(bs_preprocess_devcam(g3d_dev, n, cam_dev, sp, c->n_visible, c->pre_ws, c->pre_ws_bytes, st));
+  else
+    TRY(bs_preprocess(g3d_dev, n, cam, sp, c->n_visible, c->pre_ws, c->pre_ws_bytes, st));
   mark(1);
 
   // P5 count (workspace keyed on n and the tile grid; k part grown below)
@@ -252,17 +306,23 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   TRY(bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, st));
   mark(2);
   const bool async = allow_async && c->async_mode && bs_bin_async_supported(W, H, pw, ph);
-  const int slot = async ? c->next_slot : 0;
+  const int slot = capturing ? capture_slot : (async ? c->next_slot : 0);
   CUTRY(cudaMemcpyAsync(c->k_host + 1 + slot, c->k_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   if (async) {
     // no wait: sort into the current capacity; K is checked kDepth calls later
     if (!c->ev_k[slot]) CUTRY(cudaEventCreateWithFlags(&c->ev_k[slot], cudaEventDisableTiming));
-    CUTRY(cudaEventRecord(c->ev_k[slot], st));
+    // in a capture the record must be an external event-record node, or the
+    // event is only usable inside the capture (the host waits on it later)
+    if (capturing)
+      CUTRY(cudaEventRecordWithFlags(c->ev_k[slot], st, cudaEventRecordExternal));
+    else
+      CUTRY(cudaEventRecord(c->ev_k[slot], st));
     mark(3);
     if (!c->point_list) TRY(grow_pl_async(c, std::max<int64_t>(n, 1) * 64, st));  // 64 tiles / splat to start
     TRY(grow_n(&c->ranges, &c->ranges_cap, 2 * T));
     TRY(bs_bin_sort_async(sp, n, c->n_visible, W, H, pw, ph, std::min<int64_t>(c->pl_cap, (int64_t(1) << 30) - 1),
                           c->point_list, c->ranges, c->bin_ws, c->bin_ws_bytes, st));
+    if (!capturing) {
     bs_context::Pending& q = c->pending[c->n_pending++];
     q.g3d = g3d_dev;
     q.n = n;
@@ -274,6 +334,7 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
     q.out = fo_in;
     q.slot = slot;
     c->next_slot = (slot + 1) % bs_context::kDepth;
+    }
   } else {
     CUTRY(cudaStreamSynchronize(st));
     const int64_t k = c->k_host[1];
@@ -310,6 +371,7 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   bs_frame_out fo = fo_in;
   if (!fo.color) {
     if (P > c->pixel_cap) {
+      ++g_alloc_gen;
       for (auto& p : c->planes) {
         if (p) cudaFree(p);
         p = nullptr;
@@ -348,6 +410,7 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
 int grow_pl_async(bs_context* c, int64_t cap, cudaStream_t st) {
   if (cap <= c->pl_cap) return BS_OK;
   ++c->pl_grows;
+  ++g_alloc_gen;
   if (c->point_list) CUTRY(cudaFreeAsync(c->point_list, st));
   c->point_list = nullptr;
   c->pl_cap = 0;
@@ -420,6 +483,91 @@ int fill_info(bs_context* c, cudaStream_t st, bs_frame_info* info) {
   return BS_OK;
 }
 
+bs_context::GKey graph_key(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, int32_t pw, int32_t ph,
+                           int32_t variant, const float bg[3], bs_frame_out out, cudaStream_t st) {
+  bs_context::GKey k;
+  std::memset(static_cast<void*>(&k), 0, sizeof(k));  // padding too: keys compare bytewise
+  k.g3d = g3d;
+  k.n = n;
+  k.W = cam->width;
+  k.H = cam->height;
+  k.pw = pw;
+  k.ph = ph;
+  k.variant = variant;
+  std::copy(bg, bg + 3, k.bg);
+  k.out = out;
+  k.gen = g_alloc_gen;
+  k.st = st;
+  return k;
+}
+
+// Graph mode: the first frame of a configuration runs normally (it sizes
+// every buffer); later frames replay a captured graph of the same body (one
+// per K slot), the camera copied to cam_dev from a pinned ring slot right
+// before the launch (a slot is reused 4 frames later, when its copy has long
+// run: at most kDepth frames are unverified).
+int frame_graph(bs_context* c, const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, int32_t pw, int32_t ph,
+                int32_t variant, const float bg[3], bs_frame_out out, cudaStream_t st) {
+  if (!c->cam_dev) {
+    CUTRY(cudaMalloc(reinterpret_cast<void**>(&c->cam_dev), sizeof(bs_camera)));
+    CUTRY(cudaMallocHost(reinterpret_cast<void**>(&c->cam_ring), 4 * sizeof(bs_camera)));
+    CUTRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    ++g_alloc_gen;
+  }
+  bs_context::GKey k = graph_key(g3d, n, cam, pw, ph, variant, bg, out, st);
+  if (!(k == c->gkey)) {
+    for (cudaGraphExec_t& e : c->gexec)
+      if (e) {
+        cudaGraphExecDestroy(e);
+        e = nullptr;
+      }
+    // a plain frame of the new configuration (allocations happen here)
+    TRY(frame_device(c, g3d, n, cam, pw, ph, variant, bg, out, st, true));
+    c->gkey = graph_key(g3d, n, cam, pw, ph, variant, bg, out, st);
+    return BS_OK;
+  }
+  const int slot = c->next_slot;
+  if (!c->gexec[slot]) {
+    cudaGraph_t g = nullptr;
+    const uint64_t l0 = bs_kernel_launches();
+    CUTRY(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed));
+    const int rc = frame_device(c, g3d, n, cam, pw, ph, variant, bg, out, c->cap_stream, true, c->cam_dev, slot);
+    c->gkernels[slot] = bs_kernel_launches() - l0;
+    const cudaError_t ec = cudaStreamEndCapture(c->cap_stream, &g);
+    if (debug_on() && (rc != BS_OK || ec != cudaSuccess))
+      fprintf(stderr, "bs: graph capture: body status %d, end capture %s\n", rc, cudaGetErrorString(ec));
+    if (rc != BS_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    CUTRY(ec);
+    const cudaError_t ei = cudaGraphInstantiate(&c->gexec[slot], g, 0);
+    cudaGraphDestroy(g);
+    CUTRY(ei);
+    if (!(graph_key(g3d, n, cam, pw, ph, variant, bg, out, st) == c->gkey)) return BS_ERR_CUDA;  // allocated in capture
+  }
+  bs_camera* ring = c->cam_ring + c->ring_i;
+  c->ring_i = (c->ring_i + 1) % 4;
+  *ring = *cam;
+  CUTRY(cudaMemcpyAsync(c->cam_dev, ring, sizeof(bs_camera), cudaMemcpyHostToDevice, st));
+  CUTRY(cudaGraphLaunch(c->gexec[slot], st));
+  bs::count_launches(c->gkernels[slot]);  // every replay runs the graph's kernels
+  ++c->graph_launches;
+  bs_context::Pending& q = c->pending[c->n_pending++];
+  q.g3d = g3d;
+  q.n = n;
+  q.cam = *cam;
+  q.pw = pw;
+  q.ph = ph;
+  q.variant = variant;
+  std::copy(bg, bg + 3, q.bg);
+  q.out = out;
+  q.slot = slot;
+  c->next_slot = (slot + 1) % bs_context::kDepth;
+  c->last_variant = variant;
+  return BS_OK;
+}
+
 }  // namespace
 
 extern "C" int bs_render_frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const bs_camera* cam,
@@ -433,8 +581,24 @@ extern "C" int bs_render_frame_device(bs_context* c, const bs_gaussian3d* g3d_de
     return BS_ERR_INVALID_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(bs_context_stream(c));
   TRY(verify_pending(c, st, bs_context::kDepth - 1));
+  if (c->graphs && c->async_mode && !c->timing && !info && bs_bin_async_supported(cam->width, cam->height, pw, ph)) {
+    TRY(frame_graph(c, g3d_dev, n, cam, pw, ph, variant, bg, out, st));
+    return BS_OK;
+  }
   TRY(frame_device(c, g3d_dev, n, cam, pw, ph, variant, bg, out, st, true));
   if (info) TRY(fill_info(c, st, info));
+  return BS_OK;
+}
+
+extern "C" int bs_context_set_graphs(bs_context* c, int32_t on) {
+  if (!c) return BS_ERR_INVALID_ARGUMENT;
+  c->graphs = on != 0;
+  return BS_OK;
+}
+
+extern "C" int bs_context_graph_launches(bs_context* c, int64_t* launches) {
+  if (!c || !launches) return BS_ERR_INVALID_ARGUMENT;
+  *launches = c->graph_launches;
   return BS_OK;
 }
 
@@ -505,3 +669,11 @@ extern "C" int bs_context_set_stream(bs_context* c, void* stream) {
   return BS_OK;
 }
 
+// Drops the pending K checks without waiting: for a caller that captured
+// bs_render_frame_device into a CUDA graph (the captured call's check has no
+// executed event to wait on).  The caller owns capacity safety from then on.
+extern "C" int bs_context_drop_pending(bs_context* c) {
+  if (!c) return BS_ERR_INVALID_ARGUMENT;
+  c->n_pending = 0;
+  return BS_OK;
+}

@@ -502,3 +502,29 @@ def test_c4_tile_sampled(mode):
         assert np.array_equal(got[k][m], ref[k][m]), k
     assert float(np.abs(got["color"].reshape(-1, 3)[m] - ref["color"].reshape(-1, 3)[m]).max()) <= 1e-6
     fp.close()
+
+
+def test_frame_pipeline_graph_replay_matches():
+    """CUDA-graph mode: frames replayed from the captured graph (new camera
+    each time) equal the same frames rendered launch by launch."""
+    import bench
+    W, H, f, n = 960, 540, 500.0, 200_000
+    cams = [N.make_camera(bench.orbit_view(k * 9), (f, f), W, H) for k in range(7)]
+    g3d = api.gen_clustered_scene(n, cams[0])
+    d = api.g3d_to_device(g3d)
+    ref = []
+    fp = api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT, async_mode=True)
+    for cam in cams:
+        fp.forward(d, n, cam)
+        fp.sync()
+        ref.append(fp.frame.to_numpy())
+    fp.close()
+    fg = api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT, async_mode=True, graphs=True)
+    for i, cam in enumerate(cams):
+        fg.forward(d, n, cam)
+        fg.sync()
+        got = fg.frame.to_numpy()
+        for k in ("color", "contrib", "term", "final_t", "depth"):
+            assert np.array_equal(got[k], ref[i][k]), (i, k)
+    assert fg.graph_launches() >= len(cams) - 2  # the first frame (and captures) run plainly
+    fg.close()
