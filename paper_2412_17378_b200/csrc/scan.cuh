@@ -125,6 +125,30 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_downsweep(const TIn* __re
 
 inline int64_t scan_num_blocks(int64_t n_cap) { return (n_cap + kScanTile - 1) / kScanTile; }
 
+// Small arrays (block counts, tile counts; <= 16 items per thread): one CTA, each
+// thread a contiguous run of ceil(n / 1024) items — one launch instead of
+// three.
+constexpr int64_t kScanSingleMax = (int64_t)1 << 14;
+
+template <typename TIn, typename TOut>
+__global__ void __launch_bounds__(1024) k_scan_single(const TIn* __restrict__ in, TOut* __restrict__ out,
+                                                      int64_t n_cap, const int32_t* __restrict__ d_count,
+                                                      TOut* __restrict__ total_out) {
+  const int64_t n = d_count ? min((int64_t)*d_count, n_cap) : n_cap;
+  const int64_t per = (n_cap + 1023) / 1024;
+  const int64_t b = (int64_t)threadIdx.x * per, e = min(b + per, n_cap);
+  TOut local = 0;
+  for (int64_t k = b; k < e; ++k) local += k < n ? (TOut)in[k] : TOut(0);
+  TOut tot;
+  TOut run = block_exclusive_scan(local, &tot);
+  for (int64_t k = b; k < e; ++k) {
+    const TOut v = k < n ? (TOut)in[k] : TOut(0);  // (read before the write: out may alias in)
+    out[k] = run;
+    run += v;
+  }
+  if (threadIdx.x == 0 && total_out) *total_out = tot;
+}
+
 // Workspace: partials[nb].  total (device) may be null.  out may alias in.
 template <typename TIn, typename TOut>
 inline cudaError_t exclusive_scan(const TIn* in, TOut* out, int64_t n_cap, const int32_t* d_count, TOut* partials,
@@ -133,6 +157,11 @@ inline cudaError_t exclusive_scan(const TIn* in, TOut* out, int64_t n_cap, const
   if (nb == 0) {
     if (total) return cudaMemsetAsync(total, 0, sizeof(TOut), st);
     return cudaSuccess;
+  }
+  if (n_cap <= kScanSingleMax) {
+    k_scan_single<TIn, TOut><<<1, 1024, 0, st>>>(in, out, n_cap, d_count, total);
+    count_launches(1);
+    return cudaPeekAtLastError();
   }
   k_scan_reduce<TIn, TOut><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_cap, d_count, partials);
   k_scan_partials<TOut><<<1, 1024, 0, st>>>(partials, nb, total);
