@@ -480,12 +480,29 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     # SURVEY §8d roofline: t_roof = max(ops/FP32, E/MUFU, bytes/HBM); for this
     # frame the HBM term (44 B per tile instance + 32 B per pixel) is the max,
     # so the contract's "hbm" view is the headline and the issue view rides along
+    # list entries any pixel of a tile still reads under the serial semantics:
+    # the tile's longest consumed prefix (max over its pixels of term, or the
+    # whole list) — K*44 over-counts lists whose tail lies past every stop
+    term = frame.term.cpu().numpy().reshape(H, W)
+    rg = b.tile_ranges.cpu().numpy().view(np.uint32)
+    cols, rows = (W + pw - 1) // pw, (H + ph - 1) // ph
+    lens = (rg[1::2].astype(np.int64) - rg[0::2].astype(np.int64)).reshape(rows, cols)
+    cons = np.where(term > 0, term, np.repeat(np.repeat(lens, ph, 0), pw, 1)[:H, :W]).astype(np.int64)
+    pad = np.zeros((rows * ph, cols * pw), np.int64)
+    pad[:H, :W] = cons
+    prefix_entries = int(pad.reshape(rows, ph, cols, pw).max(axis=(1, 3)).sum())
+    bytes_prefix = 44 * prefix_entries + 32 * P
     res["roofline"] = {
         "bound": "hbm", "kernel": f"render {api.variant_name(vsel)} ({mname})",
         "achieved": bytes_alg / t_s / 1e9, "peak": hbm_peak / 1e9, "unit": "GB/s",
         "frac": bytes_alg / t_s / hbm_peak, "traffic": traffic, "algorithmic_bytes": bytes_alg,
+        "bytes_def": "SURVEY 8d: 44 B per tile instance (u32 index + 40 B attributes) + 32 B per output pixel",
         "peak_source": hbm_src,
         "t_roof_ms": t_roof * 1e3, "t_roof_frac": t_roof / t_s,
+        "consumed_prefix_view": {
+            "bytes": bytes_prefix, "frac": bytes_prefix / t_s / hbm_peak,
+            "def": "44 B per entry of each tile's longest consumed list prefix + 32 B per pixel: what tile-serial "
+                   "blending must read; K*44 exceeds it when list tails lie past every pixel's stop (C4)"},
         "issue_view": {"achieved_ginstr_s": ops / t_s / 1e9, "peak_ginstr_s": fp32_peak / 1e9,
                        "frac": (ops / t_s) / fp32_peak, "ops": ops,
                        "def": "FP32-pipe instructions 16E+8C (SURVEY 8d), peak 148 SMs x 128 lanes x sm_max_mhz"},
