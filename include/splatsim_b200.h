@@ -299,6 +299,17 @@ int bs_render_frame_host(bs_context* ctx, const bs_gaussian3d* g3d, int64_t n, c
                          int32_t ph, int32_t variant, const float bg[3], float* color, float* alpha, float* depth,
                          float* final_t, int32_t* contrib, int32_t* term, bs_frame_info* info);
 
+/* Pipelined form (async mode contexts): enqueues the upload, the frame and
+ * the download of the requested planes on three streams and returns; three
+ * frames are in flight, so frame i+1's upload and frame i-1's download overlap
+ * frame i's kernels.  Host buffers (pinned for overlap) must stay valid and
+ * untouched until bs_context_sync, after which every output is final (frames
+ * whose K outgrew point_list are re-rendered and re-downloaded there).  Falls
+ * back to bs_render_frame_host when the context is not in async mode. */
+int bs_render_frame_host_async(bs_context* ctx, const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, int32_t pw,
+                               int32_t ph, int32_t variant, const float bg[3], float* color, float* alpha,
+                               float* depth, float* final_t, int32_t* contrib, int32_t* term);
+
 /* Same pipeline on DEVICE Gaussians (g3d_dev), stream-ordered on the context
  * stream (bs_context_set_stream; NULL = the context's own stream).  out: the
  * caller's device planes, or all-NULL for context-owned planes.  The only

@@ -88,6 +88,8 @@ SIGNATURES = {
     "bs_context_stream": (_vp, [_vp]),
     "bs_render_frame_host": (C.c_int, [_vp, _vp, _i64, C.POINTER(Camera), _i32, _i32, _i32, _f32p, _vp, _vp, _vp,
                                        _vp, _vp, _vp, _vp]),
+    "bs_render_frame_host_async": (C.c_int, [_vp, _vp, _i64, C.POINTER(Camera), _i32, _i32, _i32, _f32p, _vp, _vp,
+                                             _vp, _vp, _vp, _vp]),
     "bs_render_frame_device": (C.c_int, [_vp, _vp, _i64, C.POINTER(Camera), _i32, _i32, _i32, _f32p, FrameOut,
                                          _vp]),
     "bs_context_set_stream": (C.c_int, [_vp, _vp]),

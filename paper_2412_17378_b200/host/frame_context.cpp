@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -83,6 +85,10 @@ struct bs_context {
     float bg[3] = {0, 0, 0};
     bs_frame_out out{};
     int slot = 0;
+    // host-buffer pipeline (bs_render_frame_host_async): host planes the
+    // frame's outputs go to (a re-render copies them again); io = -1 otherwise
+    int io = -1;
+    void* host_out[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   } pending[kDepth];
   int n_pending = 0, next_slot = 0;
   int64_t reruns = 0;
@@ -109,6 +115,19 @@ struct bs_context {
   bs_camera* cam_ring = nullptr;  // pinned, 4 slots
   int ring_i = 0;
   int64_t graph_launches = 0;
+  // host-buffer pipeline: kIo input/output slots; H2D on st_h2d, D2H on
+  // st_d2h, compute on the context stream — frame i+1's upload and frame i-1's
+  // download overlap frame i's kernels
+  static constexpr int kIo = 3;
+  cudaStream_t st_h2d = nullptr, st_d2h = nullptr;
+  void* io_g3d[kIo] = {nullptr, nullptr, nullptr};
+  size_t io_g3d_bytes[kIo] = {0, 0, 0};
+  void* io_out[kIo][6] = {};
+  int64_t io_pixels = 0;
+  cudaEvent_t ev_h2d[kIo] = {}, ev_comp[kIo] = {}, ev_d2h[kIo] = {};
+  int io_next = 0;
+  // BS_PIPE_TRACE=1: per-frame H2D / compute / D2H event timeline, printed at sync
+  std::vector<std::array<cudaEvent_t, 6>> trace;
   bool pl_calibrated = false;
   cudaEvent_t ev[kStages + 1] = {};
 };
@@ -228,6 +247,15 @@ extern "C" int bs_context_destroy(bs_context* c) {
     if (e) cudaEventDestroy(e);
   for (cudaGraphExec_t& e : c->gexec)
     if (e) cudaGraphExecDestroy(e);
+  for (int i = 0; i < bs_context::kIo; ++i) {
+    if (c->io_g3d[i]) cudaFree(c->io_g3d[i]);
+    for (void* q : c->io_out[i])
+      if (q) cudaFree(q);
+    for (cudaEvent_t e : {c->ev_h2d[i], c->ev_comp[i], c->ev_d2h[i]})
+      if (e) cudaEventDestroy(e);
+  }
+  if (c->st_h2d) cudaStreamSynchronize(c->st_h2d), cudaStreamDestroy(c->st_h2d);
+  if (c->st_d2h) cudaStreamSynchronize(c->st_d2h), cudaStreamDestroy(c->st_d2h);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->cam_dev) cudaFree(c->cam_dev);
   if (c->cam_ring) cudaFreeHost(c->cam_ring);
@@ -333,6 +361,7 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
     std::copy(bg, bg + 3, q.bg);
     q.out = fo_in;
     q.slot = slot;
+    q.io = -1;
     c->next_slot = (slot + 1) % bs_context::kDepth;
     }
   } else {
@@ -426,6 +455,14 @@ int grow_pl_async(bs_context* c, int64_t cap, cudaStream_t st) {
 // frame and every newer pending one again, in order, synchronously (same
 // inputs; stream order puts them after the first tries, so shared outputs end
 // with the newest frame).  keep = pending frames that may stay unchecked.
+int download_planes(bs_context* c, const bs_context::Pending& p, cudaStream_t st) {
+  const size_t P = size_t(p.cam.width) * size_t(p.cam.height);
+  const size_t bytes[6] = {P * 12, P * 4, P * 4, P * 4, P * 4, P * 4};
+  for (int k = 0; k < 6; ++k)
+    if (p.host_out[k]) CUTRY(cudaMemcpyAsync(p.host_out[k], c->io_out[p.io][k], bytes[k], cudaMemcpyDeviceToHost, st));
+  return BS_OK;
+}
+
 int verify_pending(bs_context* c, cudaStream_t st, int keep = 0) {
   while (c->n_pending > keep) {
     const bs_context::Pending p0 = c->pending[0];
@@ -453,6 +490,11 @@ int verify_pending(bs_context* c, cudaStream_t st, int keep = 0) {
       ++c->reruns;
       const bs_context::Pending& p = redo[i];
       TRY(frame_device(c, p.g3d, p.n, &p.cam, p.pw, p.ph, p.variant, p.bg, p.out, st, false));
+      if (p.io >= 0) {  // host pipeline: the first download carried the overflowed frame
+        CUTRY(cudaStreamSynchronize(c->st_d2h));
+        TRY(download_planes(c, p, st));
+        CUTRY(cudaStreamSynchronize(st));
+      }
     }
   }
   return BS_OK;
@@ -563,6 +605,7 @@ int frame_graph(bs_context* c, const bs_gaussian3d* g3d, int64_t n, const bs_cam
   std::copy(bg, bg + 3, q.bg);
   q.out = out;
   q.slot = slot;
+  q.io = -1;
   c->next_slot = (slot + 1) % bs_context::kDepth;
   c->last_variant = variant;
   return BS_OK;
@@ -614,6 +657,21 @@ extern "C" int bs_context_sync(bs_context* c, int64_t* reruns) {
   cudaStream_t st = static_cast<cudaStream_t>(bs_context_stream(c));
   TRY(verify_pending(c, st));
   CUTRY(cudaStreamSynchronize(st));
+  if (c->st_h2d) CUTRY(cudaStreamSynchronize(c->st_h2d));
+  if (c->st_d2h) CUTRY(cudaStreamSynchronize(c->st_d2h));
+  if (!c->trace.empty()) {
+    const cudaEvent_t t0 = c->trace[0][0];
+    for (size_t i = 0; i < c->trace.size(); ++i) {
+      float ms[6];
+      for (int k = 0; k < 6; ++k) cudaEventElapsedTime(&ms[k], t0, c->trace[i][k]);
+      fprintf(stderr, "frame %zu: h2d %.3f-%.3f  compute %.3f-%.3f  d2h %.3f-%.3f\n", i, ms[0], ms[1], ms[2], ms[3],
+              ms[4], ms[5]);
+    }
+    for (auto& tv : c->trace)
+      for (cudaEvent_t e : tv) cudaEventDestroy(e);
+    c->trace.clear();
+    (void)cudaGetLastError();
+  }
   if (reruns) *reruns = c->reruns;
   return BS_OK;
 }
@@ -675,5 +733,85 @@ extern "C" int bs_context_set_stream(bs_context* c, void* stream) {
 extern "C" int bs_context_drop_pending(bs_context* c) {
   if (!c) return BS_ERR_INVALID_ARGUMENT;
   c->n_pending = 0;
+  return BS_OK;
+}
+
+// Pipelined host-buffer frames: upload (st_h2d), the async frame body
+// (context stream), download (st_d2h), ordered by per-slot events so three
+// frames are in flight.  Outputs are final after bs_context_sync.
+extern "C" int bs_render_frame_host_async(bs_context* c, const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam,
+                                          int32_t pw, int32_t ph, int32_t variant, const float bg[3], float* color,
+                                          float* alpha, float* depth, float* final_t, int32_t* contrib,
+                                          int32_t* term) {
+  if (!c || !cam || !bg || n < 0 || (n > 0 && !g3d) || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
+  if (variant < -1 || variant > 4) return BS_ERR_INVALID_ARGUMENT;
+  const int32_t W = cam->width, H = cam->height;
+  if (W <= 0 || H <= 0) return BS_ERR_INVALID_ARGUMENT;
+  if (!c->async_mode || !bs_bin_async_supported(W, H, pw, ph)) {  // no pipeline: the synchronous form
+    return bs_render_frame_host(c, g3d, n, cam, pw, ph, variant, bg, color, alpha, depth, final_t, contrib, term,
+                                nullptr);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(bs_context_stream(c));
+  if (!c->st_h2d) {
+    CUTRY(cudaStreamCreateWithFlags(&c->st_h2d, cudaStreamNonBlocking));
+    CUTRY(cudaStreamCreateWithFlags(&c->st_d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < bs_context::kIo; ++i)
+      for (cudaEvent_t* e : {&c->ev_h2d[i], &c->ev_comp[i], &c->ev_d2h[i]})
+        CUTRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  const int io = c->io_next;
+  c->io_next = (io + 1) % bs_context::kIo;
+  const int64_t P = int64_t(W) * H;
+  if (P > c->io_pixels || !c->io_out[io][0]) {  // (re)size every slot's planes
+    CUTRY(cudaDeviceSynchronize());
+    for (int i = 0; i < bs_context::kIo; ++i)
+      for (int k = 0; k < 6; ++k) {
+        if (c->io_out[i][k]) cudaFree(c->io_out[i][k]);
+        CUTRY(cudaMalloc(&c->io_out[i][k], size_t(P) * (k == 0 ? 12 : 4)));
+      }
+    c->io_pixels = P;
+    ++g_alloc_gen;
+  }
+  // upload into slot io once the frame that last read it is done
+  CUTRY(cudaStreamWaitEvent(c->st_h2d, c->ev_comp[io], 0));
+  if (c->io_g3d_bytes[io] < size_t(std::max<int64_t>(n, 1)) * sizeof(bs_gaussian3d)) {
+    CUTRY(cudaStreamSynchronize(c->st_h2d));
+    TRY(grow(&c->io_g3d[io], &c->io_g3d_bytes[io], size_t(std::max<int64_t>(n, 1)) * sizeof(bs_gaussian3d)));
+  }
+  static const bool tracing = [] {
+    const char* e = getenv("BS_PIPE_TRACE");
+    return e && e[0] == '1';
+  }();
+  std::array<cudaEvent_t, 6> tev{};
+  if (tracing)
+    for (auto& e : tev) cudaEventCreate(&e);
+  if (tracing) cudaEventRecord(tev[0], c->st_h2d);
+  if (n > 0)
+    CUTRY(cudaMemcpyAsync(c->io_g3d[io], g3d, size_t(n) * sizeof(bs_gaussian3d), cudaMemcpyHostToDevice, c->st_h2d));
+  if (tracing) cudaEventRecord(tev[1], c->st_h2d);
+  CUTRY(cudaEventRecord(c->ev_h2d[io], c->st_h2d));
+  // compute after the upload and after the slot's previous download
+  CUTRY(cudaStreamWaitEvent(st, c->ev_h2d[io], 0));
+  CUTRY(cudaStreamWaitEvent(st, c->ev_d2h[io], 0));
+  TRY(verify_pending(c, st, bs_context::kDepth - 1));
+  const bs_frame_out fo{static_cast<float*>(c->io_out[io][0]), static_cast<float*>(c->io_out[io][1]),
+                        static_cast<float*>(c->io_out[io][2]), static_cast<float*>(c->io_out[io][3]),
+                        static_cast<int32_t*>(c->io_out[io][4]), static_cast<int32_t*>(c->io_out[io][5])};
+  const bs_gaussian3d* gd = static_cast<const bs_gaussian3d*>(c->io_g3d[io]);
+  if (tracing) cudaEventRecord(tev[2], st);
+  TRY(frame_device(c, gd, n, cam, pw, ph, variant, bg, fo, st, true));
+  if (tracing) cudaEventRecord(tev[3], st);
+  bs_context::Pending& q = c->pending[c->n_pending - 1];  // the entry frame_device just queued
+  q.io = io;
+  void* hs[6] = {color, alpha, depth, final_t, contrib, term};
+  std::copy(hs, hs + 6, q.host_out);
+  CUTRY(cudaEventRecord(c->ev_comp[io], st));
+  // download once computed
+  CUTRY(cudaStreamWaitEvent(c->st_d2h, c->ev_comp[io], 0));
+  if (tracing) cudaEventRecord(tev[4], c->st_d2h);
+  TRY(download_planes(c, q, c->st_d2h));
+  if (tracing) cudaEventRecord(tev[5], c->st_d2h);
+  CUTRY(cudaEventRecord(c->ev_d2h[io], c->st_d2h));
+  if (tracing) c->trace.push_back(tev);
   return BS_OK;
 }

@@ -528,3 +528,42 @@ def test_frame_pipeline_graph_replay_matches():
             assert np.array_equal(got[k], ref[i][k]), (i, k)
     assert fg.graph_launches() >= len(cams) - 2  # the first frame (and captures) run plainly
     fg.close()
+
+
+def test_host_async_pipeline_matches():
+    """bs_render_frame_host_async: frames uploaded / rendered / downloaded on
+    three streams equal the synchronous host-buffer frames."""
+    import bench
+    W, H, f, n = 480, 270, 250.0, 40_000
+    cams = [N.make_camera(bench.orbit_view(k * 7), (f, f), W, H) for k in range(6)]
+    g3d = api.gen_clustered_scene(n, cams[0])
+    host = torch.from_numpy(np.ascontiguousarray(g3d).view(np.uint8).reshape(-1).copy()).pin_memory()
+    P = W * H
+    bg = (C.c_float * 3)(0.1, 0.2, 0.3)
+
+    def planes():
+        return ([torch.empty(3 * P, dtype=torch.float32).pin_memory()] +
+                [torch.empty(P, dtype=torch.float32).pin_memory() for _ in range(3)] +
+                [torch.empty(P, dtype=torch.int32).pin_memory() for _ in range(2)])
+
+    ref = []
+    ctx = C.c_void_p()
+    N.call("bs_context_create", C.byref(ctx), N.ALPHA_EXACT)
+    for cam in cams:
+        out = planes()
+        N.call("bs_render_frame_host", ctx, host.data_ptr(), n, C.byref(cam), 16, 16, -1, bg,
+               *[o.data_ptr() for o in out], None)
+        ref.append([o.clone() for o in out])
+    N.call("bs_context_destroy", ctx)
+    ctx = C.c_void_p()
+    N.call("bs_context_create", C.byref(ctx), N.ALPHA_EXACT)
+    N.call("bs_context_set_async", ctx, 1)
+    outs = [planes() for _ in cams]
+    for cam, out in zip(cams, outs):
+        N.call("bs_render_frame_host_async", ctx, host.data_ptr(), n, C.byref(cam), 16, 16, -1, bg,
+               *[o.data_ptr() for o in out])
+    N.call("bs_context_sync", ctx, None)
+    N.call("bs_context_destroy", ctx)
+    for i, (a, r) in enumerate(zip(outs, ref)):
+        for k in range(6):
+            assert torch.equal(a[k], r[k]), (i, k)
