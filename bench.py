@@ -298,7 +298,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sync-frames", action="store_true", help="wait for K inside each frame (no async mode)")
     ap.add_argument("--no-graphs", action="store_true", help="launch every kernel instead of replaying a CUDA graph")
-    ap.add_argument("--streams", type=int, default=2, help="frame contexts on separate streams (views round-robin)")
+    ap.add_argument("--streams", type=int, default=3, help="frame contexts on separate streams (views round-robin)")
+    ap.add_argument("--fine-ctas", type=int, default=3, help="FineGrainedCombined CTAs per SM when streams > 1")
     ap.add_argument("--no-extras", action="store_true", help="skip per-variant sweep / e2e / cpu baseline")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
@@ -336,6 +337,8 @@ def main():
     # take the views round-robin, so view i+1's preprocess / binning overlaps
     # view i's render
     ns = max(1, args.streams)
+    if ns > 1:  # leave SM room for the other contexts' kernels during a render
+        N.call("bs_render_set_fine_occupancy", args.fine_ctas)
     streams = [torch.cuda.Stream(device=dev) for _ in range(ns)]
     fps = []
     for s_ in streams:
@@ -390,6 +393,7 @@ def main():
     launches = int(N.lib().bs_kernel_launches() - launches0)
     grows = sum(f.capacity()[1] for f in fps) - grows_warm
     graph_replays = sum(f.graph_launches() for f in fps) - glaunch0
+    N.call("bs_render_set_fine_occupancy", 0)  # kernel-level timings below: full occupancy
     # which variant the on-device selector picked for each timed view (replayed untimed)
     for i in range(args.steps):
         _, fi = fp.forward(g3d_dev, n, cams[view_of(args.warmup + i)], variant=variant, info=True)
@@ -432,7 +436,7 @@ def main():
                        variants_used={api.variant_name(k): c for k, c in used.items()},
                        parallelism=f"view-sharded x{world} (scene replicated, no data-path collective)",
                        l2="flushed before every step (256 MiB write on the step's stream, inside the timed region)",
-                       streams=ns),
+                       streams=ns, fine_ctas_per_sm=args.fine_ctas if ns > 1 else "max"),
         "gpu_launches": launches,
         "async_reruns": reruns,
         "point_list_grows": grows,

@@ -223,6 +223,12 @@ int bs_render_forward_auto(const int32_t* variant_dev, int alpha_mode, bs_splats
                            int32_t pw, int32_t ph, const float bg[3], bs_frame_out out, void* ws, size_t ws_bytes,
                            void* stream);
 
+/* Resident FineGrainedCombined CTAs per SM for the following launches (0 =
+ * as many as fit, the default).  With several frame contexts streaming
+ * views concurrently, 3 leaves room for the other context's preprocess and
+ * binning kernels to overlap the render (process-wide setting). */
+int bs_render_set_fine_occupancy(int32_t ctas_per_sm);
+
 /* Work counters of a rendered frame (src/kernels.cpp:283-298):
  *   evaluated = sum_p consumed(p), consumed = term > 0 ? term : list_len(tile(p))
  *   committed = sum_p contrib(p)

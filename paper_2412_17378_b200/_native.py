@@ -81,6 +81,7 @@ SIGNATURES = {
     "bs_render_forward": (C.c_int, [C.c_int, C.c_int, Splats, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _f32p,
                                     FrameOut, _vp, _sz, _vp]),
     "bs_frame_work": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "bs_render_set_fine_occupancy": (C.c_int, [_i32]),
     "bs_select_variant": (C.c_int, [C.POINTER(TileHistogram), _i32, _i32, _i32, _i32, _i32]),
     "bs_test_expf": (C.c_int, [_vp, _vp, _i64, C.c_int, _vp]),
     "bs_context_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),

@@ -775,6 +775,8 @@ __global__ void k_frame_work(const int32_t* __restrict__ term, const int32_t* __
   }
 }
 
+static int g_fine_ctas_per_sm = 0;  // 0 = as many as fit (bs_render_set_fine_occupancy)
+
 // Tail hand-off switch (BS_FINE_DONATE=0 disables it, for A/B measurement).
 // Tuning overrides for experiments / tests (defaults are the calibrated ones).
 static int env_int(const char* name, int dflt) {
@@ -828,6 +830,10 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
       BS_CUDA_TRY(cudaGetDevice(&dev));
       BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_fine<MODE>, kFineThreads, 0));
+      // bs_render_set_fine_occupancy / BS_FINE_CTAS_PER_SM: fewer resident
+      // CTAs leave SM room for another frame context's kernels
+      const int cap = g_fine_ctas_per_sm > 0 ? g_fine_ctas_per_sm : env_int("BS_FINE_CTAS_PER_SM", per_sm);
+      per_sm = max(1, min(per_sm, cap));
       const int subs = ((A.pw + 7) / 8) * ((A.ph + 3) / 4);  // 8x4 sub-tiles per tile
       const int64_t total = (int64_t)T * subs;
       if (total > 0x7fffffff) return BS_ERR_UNSUPPORTED;
@@ -966,5 +972,11 @@ extern "C" int bs_frame_work(const int32_t* term, const int32_t* contrib, const 
                                                             (width + pw - 1) / pw,
                                                             reinterpret_cast<unsigned long long*>(evaluated_committed));
   BS_LAUNCH_CHECK();
+  return BS_OK;
+}
+
+extern "C" int bs_render_set_fine_occupancy(int32_t ctas_per_sm) {
+  if (ctas_per_sm < 0) return BS_ERR_INVALID_ARGUMENT;
+  g_fine_ctas_per_sm = ctas_per_sm;
   return BS_OK;
 }
