@@ -285,7 +285,7 @@ constexpr int kScThreads = kScWarps * 32;
 constexpr int kOwnX = 4, kOwnY = kScWarps / kOwnX;  // tile ownership pattern (powers of 2)
 constexpr int kScMaxRows = 1024;                     // tile rows the row-band split supports
 constexpr int64_t kScTableBytes = 40 * 1024;         // offsets-row slice per CTA (row bands beyond)
-constexpr int64_t kMaxChunkMatrix = (int64_t)16 << 20;  // entries of M (64 MB)
+constexpr int64_t kMaxChunkMatrix = (int64_t)64 << 20;  // entries of M (256 MB)
 constexpr int kMaxChunks = 4096;
 constexpr size_t kMaxScatterSmem = 200 * 1024;           // offsets row (T u32) + warp buffers
 
@@ -807,7 +807,14 @@ static int bin_sort_impl(int64_t n_cap, const int32_t* n_visible, int32_t width,
       const char* e = getenv("BS_BIN_CHUNK_WAVES");  // tuning override
       return (int64_t)(e ? max(1, atoi(e)) : 1);
     }();
-    const int64_t waves = max(min_waves, (kk + slots * (1 << 18) - 1) / (slots * (1 << 18)));
+    // target instances per chunk: 2^18 (C2); large grids (4K: 32,400 tiles)
+    // balance better with 2^17 (measured); BS_BIN_CHUNK_LOG2 overrides
+    static const int env_log2 = [] {
+      const char* e = getenv("BS_BIN_CHUNK_LOG2");
+      return e ? atoi(e) : 0;
+    }();
+    const int64_t per_chunk = (int64_t)1 << (env_log2 ? env_log2 : (T > 16384 ? 17 : 18));
+    const int64_t waves = max(min_waves, (kk + slots * per_chunk - 1) / (slots * per_chunk));
     const int64_t nch = max((int64_t)1, min(max_chunks(gr), min(max((int64_t)1, slots * waves / nbands),
                                                                  (kk + 4095) / 4096)));
     k_chunk_bounds<<<(unsigned)((n_cap + 255) / 256), 256, 0, st>>>(w.offs, w.touched_sorted, n_cap, n_visible, kd,

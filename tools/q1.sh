@@ -1,4 +1,5 @@
 mkdir -p gpurun_out/q1
-timeout 900 python -m pytest tests -m gpu -x -q -k "frame_pipeline or render_exact" > gpurun_out/q1/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/q1/pytest.log
-for r in 1 2 3; do timeout 300 python bench.py --steps 200 --no-extras > gpurun_out/q1/d$r.json 2>> gpurun_out/q1/bench.err; done
-timeout 600 python bench.py --steps 200 --no-cpu-baseline > gpurun_out/q1/full.json 2>> gpurun_out/q1/bench.err
+for lg in 18 17 16; do
+BS_BIN_CHUNK_LOG2=$lg timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_chunk --csv --log-file gpurun_out/q1/c4_$lg.csv python tools/profile_render.py --variant FineGrainedCombined --n 3000000 --W 3840 --H 2160 --f 2000 --reps 2 > /dev/null 2>&1
+BS_BIN_CHUNK_LOG2=$lg timeout 300 python bench.py --steps 200 --no-extras > gpurun_out/q1/c2_$lg.json 2>> gpurun_out/q1/bench.err
+done
