@@ -327,6 +327,16 @@ int bs_render_frame_device(bs_context* ctx, const bs_gaussian3d* g3d_dev, int64_
 /* Stream for the following frames: NULL = the legacy default stream; the
  * context's own stream is the value bs_context_stream() returned before. */
 int bs_context_set_stream(bs_context* ctx, void* stream);
+/* A batch of views over several contexts from one native loop: view i
+ * renders cams[view_ids[i]] with ctxs[i % nctx] (into that context's own
+ * planes); flush_bufs (nctx device buffers, may be NULL) are zeroed, flush_bytes
+ * each, on the view's stream before it (an L2 flush when larger than L2). */
+int bs_render_views(bs_context* const* ctxs, int32_t nctx, const bs_gaussian3d* g3d_dev, int64_t n,
+                    const bs_camera* cams, const int32_t* view_ids, int32_t count, int32_t pw, int32_t ph,
+                    int32_t variant, const float bg[3], void* const* flush_bufs, size_t flush_bytes);
+/* The context-owned planes frames with an empty bs_frame_out render into
+ * (device pointers, valid until the next such frame or the context's destroy). */
+int bs_context_frame(bs_context* ctx, bs_frame_out* out);
 /* Async mode for bs_render_frame_device: no host wait inside a frame.
  * point_list is sized from a capacity (3 x the first K, regrown to 3 x K
  * whenever a K passes 2/3 of it);

@@ -94,6 +94,9 @@ SIGNATURES = {
     "bs_render_frame_device": (C.c_int, [_vp, _vp, _i64, C.POINTER(Camera), _i32, _i32, _i32, _f32p, FrameOut,
                                          _vp]),
     "bs_context_set_stream": (C.c_int, [_vp, _vp]),
+    "bs_context_frame": (C.c_int, [_vp, C.POINTER(FrameOut)]),
+    "bs_render_views": (C.c_int, [C.POINTER(C.c_void_p), _i32, _vp, _i64, C.POINTER(Camera), C.POINTER(C.c_int32),
+                                  _i32, _i32, _i32, _i32, _f32p, C.POINTER(C.c_void_p), _sz]),
     "bs_context_set_async": (C.c_int, [_vp, _i32]),
     "bs_context_sync": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
     "bs_context_capacity": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

@@ -815,3 +815,30 @@ extern "C" int bs_render_frame_host_async(bs_context* c, const bs_gaussian3d* g3
   if (tracing) c->trace.push_back(tev);
   return BS_OK;
 }
+
+// A batch of views across several contexts, round-robin, enqueued from one
+// native loop (no per-view interpreter overhead): view i renders
+// cams[view_ids[i]] on ctxs[i % nctx] into that context's own planes; with
+// flush_bufs, a cudaMemsetAsync of flush_bytes on the context's stream
+// precedes each view (an L2 flush when flush_bytes > L2).
+extern "C" int bs_render_views(bs_context* const* ctxs, int32_t nctx, const bs_gaussian3d* g3d_dev, int64_t n,
+                               const bs_camera* cams, const int32_t* view_ids, int32_t count, int32_t pw, int32_t ph,
+                               int32_t variant, const float bg[3], void* const* flush_bufs, size_t flush_bytes) {
+  if (!ctxs || nctx <= 0 || !cams || !view_ids || count < 0 || !bg) return BS_ERR_INVALID_ARGUMENT;
+  for (int32_t i = 0; i < count; ++i) {
+    bs_context* c = ctxs[i % nctx];
+    if (!c) return BS_ERR_INVALID_ARGUMENT;
+    if (flush_bufs && flush_bufs[i % nctx] && flush_bytes)
+      CUTRY(cudaMemsetAsync(flush_bufs[i % nctx], 0, flush_bytes, static_cast<cudaStream_t>(bs_context_stream(c))));
+    TRY(bs_render_frame_device(c, g3d_dev, n, &cams[view_ids[i]], pw, ph, variant, bg, bs_frame_out{}, nullptr));
+  }
+  return BS_OK;
+}
+
+// The context-owned output planes (written by frames rendered with an empty
+// bs_frame_out, e.g. by bs_render_views); all NULL before the first such frame.
+extern "C" int bs_context_frame(bs_context* c, bs_frame_out* out) {
+  if (!c || !out) return BS_ERR_INVALID_ARGUMENT;
+  *out = bs_frame_out{c->planes[0], c->planes[1], c->planes[2], c->planes[3], c->iplanes[0], c->iplanes[1]};
+  return BS_OK;
+}

@@ -530,6 +530,64 @@ def test_frame_pipeline_graph_replay_matches():
     fg.close()
 
 
+class _DevArray:
+    """A raw device pointer viewed through __cuda_array_interface__."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3}
+
+
+def test_render_views_batch_matches():
+    """bs_render_views: views enqueued round-robin over two contexts by one
+    native call (with per-view L2 flushes) equal the same views rendered one
+    call at a time; checked on each context's last view, over several batches
+    so graph capture and replay both run."""
+    import bench
+    W, H, f, n = 960, 540, 500.0, 200_000
+    cams = [N.make_camera(bench.orbit_view(k * 11), (f, f), W, H) for k in range(8)]
+    g3d = api.gen_clustered_scene(n, cams[0])
+    d = api.g3d_to_device(g3d)
+    ref = []
+    fp = api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT)
+    for cam in cams:
+        fp.forward(d, n, cam)
+        fp.sync()
+        ref.append(fp.frame.to_numpy())
+    fp.close()
+    streams = [torch.cuda.Stream(device=DEV) for _ in range(2)]
+    fps = []
+    for s_ in streams:
+        with torch.cuda.stream(s_):
+            fps.append(api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT, async_mode=True, graphs=True))
+    ctxs = (C.c_void_p * 2)(*[q.ctx.value for q in fps])
+    flush = [torch.empty(1 << 20, dtype=torch.uint8, device=DEV) for _ in range(2)]
+    flush_arr = (C.c_void_p * 2)(*[t.data_ptr() for t in flush])
+    cam_arr = (N.Camera * len(cams))(*cams)
+    bg = (C.c_float * 3)(0.0, 0.0, 0.0)
+    P = W * H
+    for batch in ([0, 1, 2, 3], [4, 5, 6, 7], [7, 2, 5, 0], [3, 6]):
+        ids = (C.c_int32 * len(batch))(*batch)
+        N.call("bs_render_views", ctxs, 2, C.c_void_p(d.data_ptr()), n, cam_arr, ids, len(batch), 16, 16, -1, bg,
+               flush_arr, 1 << 20)
+        for q in fps:
+            q.sync()
+        torch.cuda.synchronize()
+        for ci in range(2):
+            last = batch[max(j for j in range(len(batch)) if j % 2 == ci)]
+            fo = N.FrameOut()
+            N.call("bs_context_frame", ctxs[ci], C.byref(fo))
+            color = torch.as_tensor(_DevArray(fo.color, 3 * P, "<f4"), device=DEV).cpu().numpy()
+            contrib = torch.as_tensor(_DevArray(fo.contrib, P, "<i4"), device=DEV).cpu().numpy()
+            final_t = torch.as_tensor(_DevArray(fo.final_t, P, "<f4"), device=DEV).cpu().numpy()
+            assert np.array_equal(color, ref[last]["color"].reshape(-1)), (batch, ci)
+            assert np.array_equal(contrib, ref[last]["contrib"].reshape(-1)), (batch, ci)
+            assert np.array_equal(final_t, ref[last]["final_t"].reshape(-1)), (batch, ci)
+    assert sum(q.graph_launches() for q in fps) > 0
+    for q in fps:
+        q.close()
+
+
 def test_host_async_pipeline_matches():
     """bs_render_frame_host_async: frames uploaded / rendered / downloaded on
     three streams equal the synchronous host-buffer frames."""
