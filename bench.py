@@ -506,7 +506,7 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     traffic = None
     try:
         with open(NCU_TRAFFIC_PATH) as fh:
-            traffic = json.load(fh).get(f"{api.variant_name(vsel)}_{mname}")
+            traffic = json.load(fh).get(f"{args.config}_{api.variant_name(vsel)}_{mname}")  # per config
     except Exception:
         pass
     res["fwd_render_ms_per_frame"] = t_render

@@ -10,6 +10,11 @@ cp "$IN/bench_c4.json" $P/r1_bench_c4.json
 cp "$IN/bench_reference.json" $P/r1_bench_reference.json
 python tools/launches.py "$IN/launches.csv" > $P/r1_launches_c2.txt
 python tools/ncu_summary.py "$IN/render_fine_full.ncu-rep" > $P/r1_ncu_full_render_fine_exact.txt
+for c in c1 c4; do
+  [ -f "$IN/render_fine_full_$c.ncu-rep" ] && \
+    python tools/ncu_summary.py "$IN/render_fine_full_$c.ncu-rep" > $P/r1_ncu_full_render_fine_exact_$c.txt
+done
+python tools/ncu_traffic.py $P > $P/ncu_traffic.json
 python tools/ncu_summary.py "$IN/chunk_scatter_full.ncu-rep" > $P/r1_ncu_chunk_scatter.txt
 cp "$IN/c3_sweep.jsonl" $P/r1_c3_sweep.jsonl
 cp "$IN/training_run.csv" $P/r1_training_run.csv

@@ -26,9 +26,16 @@ def main():
     ap.add_argument("--H", type=int, default=1080)
     ap.add_argument("--f", type=float, default=1000.0)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--config", default=None, help="c1/c2/c4: bench.py's scene and first view (overrides n/W/H/f/sigma)")
     a = ap.parse_args()
-    cam = api.camera(None, (a.f, a.f), a.W, a.H)
-    g3d = api.gen_clustered_scene(a.n, cam, cluster_sigma=a.sigma)
+    if a.config:
+        import bench
+        a.W, a.H, a.f, a.n, bgf, a.sigma = bench.CONFIGS[a.config]
+        cam = api.camera(bench.orbit_view(0), (a.f, a.f), a.W, a.H)
+        g3d = api.gen_clustered_scene(a.n, cam, cluster_sigma=a.sigma, background_fraction=bgf)
+    else:
+        cam = api.camera(None, (a.f, a.f), a.W, a.H)
+        g3d = api.gen_clustered_scene(a.n, cam, cluster_sigma=a.sigma)
     g3d["opacity"] *= a.opacity_scale
     mode = 0 if a.alpha == "exact" else 1
     pipe = api.Pipeline(a.W, a.H, 16, 16, "cuda", mode)
