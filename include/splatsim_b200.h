@@ -169,6 +169,17 @@ int bs_splats_to_g2d(bs_splats in, int64_t n, bs_gaussian2d* g2d, void* stream);
 size_t bs_bin_workspace_bytes(int64_t n_cap, int32_t width, int32_t height, int32_t pw, int32_t ph, int64_t k_cap);
 int bs_bin_count(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height, int32_t pw,
                  int32_t ph, int64_t* k_total, void* ws, size_t ws_bytes, void* stream);
+/* Frame-pipeline fusion of bs_preprocess + bs_bin_count (no reference
+ * counterpart of its own: project_all + the counting half of bin_tiles,
+ * src/preprocess.cpp:57-64, 66-92).  Splats are NOT compacted: splat i stays
+ * at index i of out, culled splats touch no tile.  counts (2 x i32, device):
+ * counts[0] <- n, the item count to pass as n_visible to bs_bin_sort*;
+ * counts[1] <- the visible count.  Tile lists then index the uncompacted
+ * arrays, in the reference's order (compaction is monotone).  Exactly one of
+ * cam (host) / cam_dev (device) is used (cam wins).  Workspace: the bin one. */
+int bs_preprocess_bin_count(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, const bs_camera* cam_dev,
+                            bs_splats out, int32_t* counts, int32_t width, int32_t height, int32_t pw, int32_t ph,
+                            int64_t* k_total, void* ws, size_t ws_bytes, void* stream);
 int bs_bin_sort(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height, int32_t pw,
                 int32_t ph, int64_t k, uint32_t* point_list, uint32_t* tile_ranges, void* ws, size_t ws_bytes,
                 void* stream);

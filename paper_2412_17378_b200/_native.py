@@ -73,6 +73,8 @@ SIGNATURES = {
     "bs_splats_to_g2d": (C.c_int, [Splats, _i64, _vp, _vp]),
     "bs_bin_workspace_bytes": (_sz, [_i64, _i32, _i32, _i32, _i32, _i64]),
     "bs_bin_count": (C.c_int, [Splats, _i64, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _sz, _vp]),
+    "bs_preprocess_bin_count": (C.c_int, [_vp, _i64, C.POINTER(Camera), _vp, Splats, _vp, _i32, _i32, _i32, _i32, _vp,
+                                          _vp, _sz, _vp]),
     "bs_bin_sort": (C.c_int, [Splats, _i64, _vp, _i32, _i32, _i32, _i32, _i64, _vp, _vp, _vp, _sz, _vp]),
     "bs_tile_stats_workspace_bytes": (_sz, [_i32]),
     "bs_tile_stats": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),

@@ -22,36 +22,9 @@
 #include "bs_common.cuh"
 #include "radix_sort.cuh"
 #include "scan.cuh"
+#include "tiles.cuh"
 
 namespace bs {
-
-struct Grid {
-  int W, H, pw, ph, cols, rows;
-};
-
-// static_cast<int>(float) with x86-64 cvttss2si semantics (out of range /
-// NaN -> INT_MIN), the behaviour of the reference's casts on its platform.
-__device__ __forceinline__ int x86_f2i(float f) {
-  if (!(f > -2147483904.0f && f < 2147483648.0f)) return (int)0x80000000;
-  return (int)f;
-}
-
-struct Rect {
-  int tx0, tx1, ty0, ty1;
-};
-
-// src/preprocess.cpp:81-92.  Returns false when rejected / empty.
-__device__ __forceinline__ bool tile_rect(float x, float y, float radius, const Grid& g, Rect& r) {
-  const float rr = ceilf(radius);
-  const float x0 = __fsub_rn(x, rr), x1 = __fadd_rn(x, rr);
-  const float y0 = __fsub_rn(y, rr), y1 = __fadd_rn(y, rr);
-  if (x1 < 0.0f || y1 < 0.0f || x0 >= (float)g.W || y0 >= (float)g.H) return false;
-  r.tx0 = max(0, x86_f2i(floorf(__fdiv_rn(x0, (float)g.pw))));
-  r.tx1 = min(g.cols - 1, x86_f2i(floorf(__fdiv_rn(x1, (float)g.pw))));
-  r.ty0 = max(0, x86_f2i(floorf(__fdiv_rn(y0, (float)g.ph))));
-  r.ty1 = min(g.rows - 1, x86_f2i(floorf(__fdiv_rn(y1, (float)g.ph))));
-  return r.tx0 <= r.tx1 && r.ty0 <= r.ty1;
-}
 
 // Per visible splat: tiles touched, packed rect (tx0 | ty0<<16, w | h<<16),
 // depth sort key (non-touching -> 0xffffffff), value = index, and the four
@@ -699,45 +672,13 @@ static int check_grid(int32_t W, int32_t H, int32_t pw, int32_t ph) {
   return BS_OK;
 }
 
-extern "C" int bs_bin_count(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height,
-                            int32_t pw, int32_t ph, int64_t* k_total, void* ws, size_t ws_bytes, void* stream) {
-  int s = check_grid(width, height, pw, ph);
-  if (s) return s;
-  if (n_cap < 0 || !n_visible || !k_total || (n_cap > 0 && (!g.xyab || !g.cop || !g.rgbr))) return BS_ERR_INVALID_ARGUMENT;
-  if (n_cap >= (int64_t)1 << 30) return BS_ERR_CAPACITY;
-  cudaStream_t st = (cudaStream_t)stream;
-  const Grid gr = make_grid(width, height, pw, ph);
+// P5 count after the per-splat pass (k_bin_rect or the fused
+// k_project_bin): depth sort, sorted rects, instance offsets, K, tile counts.
+static int bin_count_tail(int64_t n_cap, const int32_t* n_visible, const Grid& gr, const BinWs& w, bool smem_diff,
+                          size_t diff_bytes, int64_t* k_total, cudaStream_t st) {
   const int64_t T = (int64_t)gr.cols * gr.rows;
-  if (!ws || ws_bytes < bs_bin_workspace_bytes(n_cap, width, height, pw, ph, 0)) return BS_ERR_WORKSPACE;
-  WsCarver c(ws, ws_bytes);
-  BinWs w;
-  bin_ws_layout(c, n_cap, gr, 0, &w);
-  BS_CUDA_TRY(cudaMemsetAsync(w.diff, 0, sizeof(int) * (size_t)(gr.cols + 1) * (gr.rows + 1), st));
-  const size_t diff_bytes = sizeof(int) * (size_t)(gr.cols + 1) * (gr.rows + 1);
-  const bool smem_diff = diff_bytes <= kMaxDiffSmem;
-  static bool attr_set = false;
-  if (smem_diff && !attr_set) {
-    BS_CUDA_TRY(cudaFuncSetAttribute(k_bin_rect<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDiffSmem));
-    BS_CUDA_TRY(cudaFuncSetAttribute(k_diff_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDiffSmem));
-    attr_set = true;
-  }
   if (n_cap > 0) {
     const unsigned nb = (unsigned)((n_cap + 255) / 256);
-    const float4* xa = reinterpret_cast<const float4*>(g.xyab);
-    const float4* xc = reinterpret_cast<const float4*>(g.cop);
-    const float4* xr = reinterpret_cast<const float4*>(g.rgbr);
-    if (smem_diff) {
-      int dev = 0, sms = 148;
-      BS_CUDA_TRY(cudaGetDevice(&dev));
-      BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      const unsigned grid = (unsigned)min((int64_t)nb, (int64_t)sms * 2);
-      k_bin_rect<true><<<grid, 256, diff_bytes, st>>>(xa, xc, xr, n_cap, n_visible, gr, w.touched, w.rects, w.dk0,
-                                                      w.dv0, w.diff);
-    } else {
-      k_bin_rect<false><<<nb, 256, 0, st>>>(xa, xc, xr, n_cap, n_visible, gr, w.touched, w.rects, w.dk0, w.dv0,
-                                            w.diff);
-    }
-    BS_LAUNCH_CHECK();
     bool alt = false;
     BS_CUDA_TRY(radix_sort_pairs(w.dk0, w.dv0, w.dk1, w.dv1, n_cap, n_visible, 32, w.rws_n, &alt, st));
     const uint32_t* order = alt ? w.dv1 : w.dv0;  // 4 passes: back in dv0
@@ -764,6 +705,86 @@ extern "C" int bs_bin_count(bs_splats g, int64_t n_cap, const int32_t* n_visible
   }
   BS_CUDA_TRY((exclusive_scan<uint32_t, uint32_t>(w.counts, w.starts, T, nullptr, w.cpartials, nullptr, st)));
   return BS_OK;
+}
+
+static bool g_diff_attr_set = false;
+
+extern "C" int bs_bin_count(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height,
+                            int32_t pw, int32_t ph, int64_t* k_total, void* ws, size_t ws_bytes, void* stream) {
+  int s = check_grid(width, height, pw, ph);
+  if (s) return s;
+  if (n_cap < 0 || !n_visible || !k_total || (n_cap > 0 && (!g.xyab || !g.cop || !g.rgbr))) return BS_ERR_INVALID_ARGUMENT;
+  if (n_cap >= (int64_t)1 << 30) return BS_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Grid gr = make_grid(width, height, pw, ph);
+  if (!ws || ws_bytes < bs_bin_workspace_bytes(n_cap, width, height, pw, ph, 0)) return BS_ERR_WORKSPACE;
+  WsCarver c(ws, ws_bytes);
+  BinWs w;
+  bin_ws_layout(c, n_cap, gr, 0, &w);
+  BS_CUDA_TRY(cudaMemsetAsync(w.diff, 0, sizeof(int) * (size_t)(gr.cols + 1) * (gr.rows + 1), st));
+  const size_t diff_bytes = sizeof(int) * (size_t)(gr.cols + 1) * (gr.rows + 1);
+  const bool smem_diff = diff_bytes <= kMaxDiffSmem;
+  if (smem_diff && !g_diff_attr_set) {
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_bin_rect<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDiffSmem));
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_diff_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDiffSmem));
+    g_diff_attr_set = true;
+  }
+  if (n_cap > 0) {
+    const unsigned nb = (unsigned)((n_cap + 255) / 256);
+    const float4* xa = reinterpret_cast<const float4*>(g.xyab);
+    const float4* xc = reinterpret_cast<const float4*>(g.cop);
+    const float4* xr = reinterpret_cast<const float4*>(g.rgbr);
+    if (smem_diff) {
+      int dev = 0, sms = 148;
+      BS_CUDA_TRY(cudaGetDevice(&dev));
+      BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const unsigned grid = (unsigned)min((int64_t)nb, (int64_t)sms * 2);
+      k_bin_rect<true><<<grid, 256, diff_bytes, st>>>(xa, xc, xr, n_cap, n_visible, gr, w.touched, w.rects, w.dk0,
+                                                      w.dv0, w.diff);
+    } else {
+      k_bin_rect<false><<<nb, 256, 0, st>>>(xa, xc, xr, n_cap, n_visible, gr, w.touched, w.rects, w.dk0, w.dv0,
+                                            w.diff);
+    }
+    BS_LAUNCH_CHECK();
+  }
+  return bin_count_tail(n_cap, n_visible, gr, w, smem_diff, diff_bytes, k_total, st);
+}
+
+// P1-P4 + P5 count in one pass for the frame pipeline (see
+// launch_project_bin): splats stay at their input index, counts[0] <- n
+// (what the binning kernels read as the splat count), counts[1] <- visible
+// splats.  bs_bin_sort / bs_bin_sort_async follow with n_cap = n and
+// n_visible = counts.  Tile lists index the uncompacted splat arrays; their
+// order equals the reference's (compaction is monotone).
+extern "C" int bs_preprocess_bin_count(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam,
+                                       const bs_camera* cam_dev, bs_splats out, int32_t* counts, int32_t width,
+                                       int32_t height, int32_t pw, int32_t ph, int64_t* k_total, void* ws,
+                                       size_t ws_bytes, void* stream) {
+  int s = check_grid(width, height, pw, ph);
+  if (s) return s;
+  if (n < 0 || (!cam && !cam_dev) || !counts || !k_total || (n > 0 && (!g3d || !out.xyab || !out.cop || !out.rgbr)))
+    return BS_ERR_INVALID_ARGUMENT;
+  if (n >= (int64_t)1 << 30) return BS_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Grid gr = make_grid(width, height, pw, ph);
+  if (!ws || ws_bytes < bs_bin_workspace_bytes(n, width, height, pw, ph, 0)) return BS_ERR_WORKSPACE;
+  WsCarver c(ws, ws_bytes);
+  BinWs w;
+  bin_ws_layout(c, n, gr, 0, &w);
+  const size_t diff_bytes = sizeof(int) * (size_t)(gr.cols + 1) * (gr.rows + 1);
+  const bool smem_diff = diff_bytes <= kMaxDiffSmem;
+  if (smem_diff && !g_diff_attr_set) {
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_bin_rect<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDiffSmem));
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_diff_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDiffSmem));
+    g_diff_attr_set = true;
+  }
+  BS_CUDA_TRY(cudaMemsetAsync(w.diff, 0, diff_bytes, st));
+  BS_CUDA_TRY(cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), st));
+  if (n > 0)
+    BS_CUDA_TRY(launch_project_bin(g3d, n, cam, cam_dev, gr, reinterpret_cast<float4*>(out.xyab),
+                                   reinterpret_cast<float4*>(out.cop), reinterpret_cast<float4*>(out.rgbr), w.touched,
+                                   w.rects, w.dk0, w.dv0, w.diff, diff_bytes, smem_diff, counts, st));
+  return bin_count_tail(n, counts, gr, w, smem_diff, diff_bytes, k_total, st);
 }
 
 // k >= 0: K known on the host (bs_bin_sort).  k < 0: K only on the device

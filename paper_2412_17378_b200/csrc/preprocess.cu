@@ -16,6 +16,7 @@
 
 #include "bs_common.cuh"
 #include "scan.cuh"
+#include "tiles.cuh"
 
 namespace bs {
 
@@ -178,6 +179,111 @@ __global__ void __launch_bounds__(256) k_project_write(const bs_gaussian3d* __re
     cop[dst] = make_float4(o.cc, g.opacity, power_cut_of(g.opacity), o.depth);
     rgbr[dst] = make_float4(g.color[0], g.color[1], g.color[2], o.radius);
   }
+}
+
+// Frame-pipeline form of P1-P4 + the per-splat half of P5 in one pass:
+// splat i is projected once, its float4 triple written at index i (culled
+// splats write nothing and touch no tile), and k_bin_rect's outputs (tiles
+// touched, packed rect, depth key, index, difference-grid corners) follow
+// from the registers.  Tie order is unchanged: the compacted index of the
+// reference is a monotone function of i.  SMEM_DIFF as in k_bin_rect.
+template <bool SMEM_DIFF>
+__global__ void __launch_bounds__(256) k_project_bin(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam_,
+                                                     const bs_camera* __restrict__ camd, Grid g,
+                                                     float4* __restrict__ xyab, float4* __restrict__ cop,
+                                                     float4* __restrict__ rgbr, uint32_t* __restrict__ touched,
+                                                     uint2* __restrict__ rects, uint32_t* __restrict__ dkeys,
+                                                     uint32_t* __restrict__ dvals, int* __restrict__ diff,
+                                                     int32_t* __restrict__ counts) {
+  extern __shared__ int s_diff[];
+  const CamDev cam = cam_of(camd, cam_);
+  const int stride = g.cols + 1;
+  const int cells = stride * (g.rows + 1);
+  int* dd = SMEM_DIFF ? s_diff : diff;
+  if (SMEM_DIFF) {
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) s_diff[i] = 0;
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = (int32_t)n;
+  int vis_n = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bs_gaussian3d gs;
+    load_g3d(g3d, i, gs);
+    Projected o;
+    uint32_t cnt = 0;
+    uint2 pk = make_uint2(0u, 0u);
+    if (project_one(gs, cam, o)) {
+      ++vis_n;
+      xyab[i] = make_float4(o.x, o.y, o.ca, o.cb);
+      cop[i] = make_float4(o.cc, gs.opacity, power_cut_of(gs.opacity), o.depth);
+      rgbr[i] = make_float4(gs.color[0], gs.color[1], gs.color[2], o.radius);
+      Rect r;
+      if (tile_rect(o.x, o.y, o.radius, g, r)) {
+        const uint32_t w = (uint32_t)(r.tx1 - r.tx0 + 1), h = (uint32_t)(r.ty1 - r.ty0 + 1);
+        cnt = w * h;
+        pk = make_uint2((uint32_t)r.tx0 | ((uint32_t)r.ty0 << 16), w | (h << 16));
+        atomicAdd(&dd[r.ty0 * stride + r.tx0], 1);
+        atomicAdd(&dd[r.ty0 * stride + r.tx1 + 1], -1);
+        atomicAdd(&dd[(r.ty1 + 1) * stride + r.tx0], -1);
+        atomicAdd(&dd[(r.ty1 + 1) * stride + r.tx1 + 1], 1);
+      }
+    }
+    touched[i] = cnt;
+    rects[i] = pk;
+    dkeys[i] = cnt ? float_sort_key(o.depth) : 0xffffffffu;
+    dvals[i] = (uint32_t)i;
+  }
+  const int tot = block_reduce_sum<int>(vis_n);
+  if (threadIdx.x == 0 && tot) atomicAdd(&counts[1], tot);
+  if (SMEM_DIFF) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < cells; i += blockDim.x) {
+      const int v = s_diff[i];
+      if (v) atomicAdd(&diff[i], v);
+    }
+  }
+}
+
+cudaError_t launch_project_bin(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, const bs_camera* cam_dev,
+                               const Grid& g, float4* xyab, float4* cop, float4* rgbr, uint32_t* touched,
+                               uint2* rects, uint32_t* dkeys, uint32_t* dvals, int* diff, size_t diff_bytes,
+                               bool smem_diff, int32_t* counts, cudaStream_t st) {
+  CamDev c{};
+  if (cam) {
+    for (int k = 0; k < 12; ++k) c.v[k] = cam->view[k];
+    c.fx = cam->focal[0];
+    c.fy = cam->focal[1];
+    c.w = cam->width;
+    c.h = cam->height;
+  }
+  const bs_camera* camd = cam ? nullptr : cam_dev;
+  const int64_t nb = (n + 255) / 256;
+  if (smem_diff) {
+    static int per_sm = 0, sms = 0;
+    static size_t attr_bytes = 0;
+    if (diff_bytes > attr_bytes) {
+      cudaError_t e = cudaFuncSetAttribute(k_project_bin<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)diff_bytes);
+      if (e != cudaSuccess) return e;
+      attr_bytes = diff_bytes;
+      per_sm = 0;
+    }
+    if (!per_sm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_bin<true>, 256, diff_bytes);
+      per_sm = per_sm < 1 ? 1 : (per_sm > 3 ? 3 : per_sm);  // each CTA flushes its grid once: cap the flushes
+    }
+    const int64_t grid = nb < (int64_t)sms * per_sm ? nb : (int64_t)sms * per_sm;
+    k_project_bin<true><<<(unsigned)(grid > 0 ? grid : 1), 256, diff_bytes, st>>>(
+        g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects, dkeys, dvals, diff, counts);
+  } else {
+    k_project_bin<false><<<(unsigned)(nb > 0 ? nb : 1), 256, 0, st>>>(g3d, n, c, camd, g, xyab, cop, rgbr, touched,
+                                                                      rects, dkeys, dvals, diff, counts);
+  }
+  count_launches(1);
+  return cudaPeekAtLastError();
 }
 
 __global__ void k_splats_from_g2d(const bs_gaussian2d* __restrict__ g2d, int64_t n, float4* __restrict__ xyab,

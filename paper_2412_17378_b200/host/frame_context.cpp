@@ -72,6 +72,7 @@ struct bs_context {
   // per-stage timing (bs_context_enable_timing)
   bs_frame_out last_out{};
   bool timing = false;
+  bool last_fused = false;  // last frame used bs_preprocess_bin_count (visible count in n_visible[1])
   // async mode (bs_context_set_async): point_list sized from a capacity, K
   // checked one call later; an overflowed frame is re-rendered then
   bool async_mode = false;
@@ -315,12 +316,28 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   }
   bs_splats sp{reinterpret_cast<float*>(c->splat[0]), reinterpret_cast<float*>(c->splat[1]),
                reinterpret_cast<float*>(c->splat[2])};
-  TRY(grow(&c->pre_ws, &c->pre_ws_bytes, bs_preprocess_workspace_bytes(n)));
-  if (cam_dev)
-    TRY(bs_preprocess_devcam(g3d_dev, n, cam_dev, sp, c->n_visible, c->pre_ws, c->pre_ws_bytes, st));
-  else
-    TRY(bs_preprocess(g3d_dev, n, cam, sp, c->n_visible, c->pre_ws, c->pre_ws_bytes, st));
+  // default: projection fused with the per-splat binning pass
+  // (bs_preprocess_bin_count, splats uncompacted); BS_NO_FUSED_PRE=1 runs
+  // bs_preprocess (compacting) + bs_bin_count
+  static const bool fused = [] {
+    const char* e = getenv("BS_NO_FUSED_PRE");
+    return !(e && *e == '1');
+  }();
+  c->last_fused = fused;
+  if (!fused) {
+    TRY(grow(&c->pre_ws, &c->pre_ws_bytes, bs_preprocess_workspace_bytes(n)));
+    if (cam_dev)
+      TRY(bs_preprocess_devcam(g3d_dev, n, cam_dev, sp, c->n_visible, c->pre_ws, c->pre_ws_bytes, st));
+    else
+      TRY(bs_preprocess(g3d_dev, n, cam, sp, c->n_visible, c->pre_ws, c->pre_ws_bytes, st));
+  }
   mark(1);
+  auto count = [&]() -> int {
+    if (fused)
+      return bs_preprocess_bin_count(g3d_dev, n, cam_dev ? nullptr : cam, cam_dev, sp, c->n_visible, W, H, pw, ph,
+                                     c->k_dev, c->bin_ws, c->bin_ws_bytes, st);
+    return bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, st);
+  };
 
   // P5 count (workspace keyed on n and the tile grid; k part grown below)
   const int key[4] = {W, H, pw, ph};
@@ -331,7 +348,7 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
     std::copy(key, key + 4, c->bin_key);
     TRY(grow(&c->bin_ws, &c->bin_ws_bytes, bs_bin_workspace_bytes(c->bin_n, W, H, pw, ph, c->bin_k)));
   }
-  TRY(bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, st));
+  TRY(count());
   mark(2);
   const bool async = allow_async && c->async_mode && bs_bin_async_supported(W, H, pw, ph);
   const int slot = capturing ? capture_slot : (async ? c->next_slot : 0);
@@ -376,7 +393,7 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
       if (c->bin_ws) cudaFree(c->bin_ws);
       c->bin_ws = fresh;
       c->bin_ws_bytes = fresh_bytes;
-      TRY(bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, st));
+      TRY(count());
     }
     mark(3);
     if (k > c->pl_cap) TRY(grow_pl_async(c, int64_t(double(std::max<int64_t>(k, 1)) * 1.25), st));
@@ -513,7 +530,8 @@ int fill_info(bs_context* c, cudaStream_t st, bs_frame_info* info) {
   if (c->last_variant < 0)
     CUTRY(cudaMemcpyAsync(c->variant_host, c->variant_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   int32_t nv = 0;
-  CUTRY(cudaMemcpyAsync(c->variant_host + 1, c->n_visible, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CUTRY(cudaMemcpyAsync(c->variant_host + 1, c->n_visible + (c->last_fused ? 1 : 0), sizeof(int32_t),
+                        cudaMemcpyDeviceToHost, st));
   CUTRY(cudaStreamSynchronize(st));
   nv = c->variant_host[1];
   info->variant = c->last_variant < 0 ? c->variant_host[0] : c->last_variant;

@@ -115,6 +115,51 @@ def test_binning_bit_exact_large(W, H, f, n, bgfrac):
     assert np.array_equal(b.point_list.cpu().numpy().view(np.uint32), pl_ref)
 
 
+@pytest.mark.parametrize("W,H,f,n,bgfrac", [(960, 540, 500.0, 30000, 0.3), (1920, 1080, 1000.0, 40000, 0.12)])
+def test_fused_project_bin_matches_reference(W, H, f, n, bgfrac):
+    """bs_preprocess_bin_count (the frame pipeline's projection fused with the
+    per-splat binning pass, splats left uncompacted) + bs_bin_sort: the
+    visible splats equal project_all's, and mapping every list entry through
+    the compaction gives bin_tiles' point_list and ranges exactly."""
+    g3d, cam = scene(n, W, H, f, bgfrac=bgfrac)
+    g3d["mean"][::53, 2] = 0.004  # near-plane culls scattered through the input
+    g2d = O.project_all(g3d, cam)
+    pl_ref, rg_ref = O.bin_tiles(g2d, W, H, 16, 16)
+    vis = np.array([len(O.project_all(g3d[i:i + 1], cam)) == 1 for i in range(n)])
+    assert vis.sum() == len(g2d) < n
+    d = api.g3d_to_device(g3d)
+    s = api.DeviceSplats.empty(n, DEV)
+    counts = torch.zeros(2, dtype=torch.int32, device=DEV)
+    b = api.Binner(W, H, 16, 16, DEV)
+    c = ncam(cam)
+
+    def count():
+        N.call("bs_preprocess_bin_count", d.data_ptr(), n, C.byref(c), None, s.c(), counts.data_ptr(), W, H, 16, 16,
+               b.k_dev.data_ptr(), b.ws.data_ptr(), b.ws.numel(), api._stream(DEV))
+
+    b._ensure_ws(n, 0)
+    count()
+    k = b.read_k()
+    b._ensure_ws(n, int(k * 1.25) + 1024)
+    count()
+    assert b.read_k() == k == len(pl_ref)
+    pl = torch.empty(max(k, 1), dtype=torch.int32, device=DEV)
+    N.call("bs_bin_sort", s.c(), n, counts.data_ptr(), W, H, 16, 16, k, pl.data_ptr(), b.tile_ranges.data_ptr(),
+           b.ws.data_ptr(), b.ws.numel(), api._stream(DEV))
+    torch.cuda.synchronize()
+    cnt = counts.cpu().numpy()
+    assert cnt[0] == n and cnt[1] == vis.sum()
+    assert np.array_equal(b.tile_ranges.cpu().numpy().view(np.uint32), rg_ref)
+    comp = np.cumsum(vis) - 1
+    got = pl[:k].cpu().numpy().view(np.uint32)
+    assert vis[got].all()
+    assert np.array_equal(comp[got].astype(np.uint32), pl_ref)
+    idx = torch.from_numpy(np.nonzero(vis)[0]).to(DEV)
+    sv = api.DeviceSplats(s.xyab[idx].contiguous(), s.cop[idx].contiguous(), s.rgbr[idx].contiguous(),
+                          torch.tensor([len(idx)], dtype=torch.int32, device=DEV))
+    assert api.splats_to_g2d(sv).tobytes() == g2d.tobytes()
+
+
 def test_binning_radix_path_bit_exact():
     """BS_BIN_RADIX=1 (expand + stable tile radix sort) stays bit-exact too."""
     import os
