@@ -136,16 +136,6 @@ __global__ void __launch_bounds__(256) k_diff_cols(const int* __restrict__ diff,
 
 constexpr size_t kMaxDiffSmem = 200 * 1024;  // <= 227 KB opt-in
 
-__global__ void k_gather_sorted(const uint32_t* __restrict__ order, const uint32_t* __restrict__ touched,
-                                const uint2* __restrict__ rects, int64_t n_cap, const int32_t* __restrict__ n_visible,
-                                uint32_t* __restrict__ touched_sorted, uint2* __restrict__ rects_sorted) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_cap || j >= *n_visible) return;
-  const uint32_t i = order[j];
-  touched_sorted[j] = touched[i];
-  rects_sorted[j] = rects[i];
-}
-
 // Expansion: block b writes instances [b*4096, b*4096+4096); thread t the 16
 // consecutive ones at b*4096 + 16t.  Every splat of the depth-sorted prefix
 // emits >= 1 instance, so the window of 4097 offsets in smem always covers a
@@ -679,12 +669,11 @@ static int bin_count_tail(int64_t n_cap, const int32_t* n_visible, const Grid& g
   const int64_t T = (int64_t)gr.cols * gr.rows;
   if (n_cap > 0) {
     const unsigned nb = (unsigned)((n_cap + 255) / 256);
+    (void)nb;
     bool alt = false;
-    BS_CUDA_TRY(radix_sort_pairs(w.dk0, w.dv0, w.dk1, w.dv1, n_cap, n_visible, 32, w.rws_n, &alt, st));
-    const uint32_t* order = alt ? w.dv1 : w.dv0;  // 4 passes: back in dv0
-    k_gather_sorted<<<nb, 256, 0, st>>>(order, w.touched, w.rects, n_cap, n_visible, w.touched_sorted,
-                                        w.rects_sorted);
-    BS_LAUNCH_CHECK();
+    // the last pass also gathers (touched, rect) into depth order
+    const RadixGather gat{w.touched, w.rects, w.touched_sorted, w.rects_sorted};
+    BS_CUDA_TRY(radix_sort_pairs(w.dk0, w.dv0, w.dk1, w.dv1, n_cap, n_visible, 32, w.rws_n, &alt, st, &gat));
     uint64_t* total = w.offs_partials + scan_num_blocks(n_cap);
     BS_CUDA_TRY((exclusive_scan<uint32_t, uint64_t>(w.touched_sorted, w.offs, n_cap, n_visible, w.offs_partials,
                                                     total, st)));

@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(256) k_project_write(const bs_gaussian3d* __re
 // from the registers.  Tie order is unchanged: the compacted index of the
 // reference is a monotone function of i.  SMEM_DIFF as in k_bin_rect.
 template <bool SMEM_DIFF>
-__global__ void __launch_bounds__(256) k_project_bin(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam_,
+__global__ void __launch_bounds__(256, 3) k_project_bin(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam_,
                                                      const bs_camera* __restrict__ camd, Grid g,
                                                      float4* __restrict__ xyab, float4* __restrict__ cop,
                                                      float4* __restrict__ rgbr, uint32_t* __restrict__ touched,

@@ -63,13 +63,24 @@ static __global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint32
   }
 }
 
+// Optional payload of the LAST pass: out_a[dst] = in_a[value], out_b[dst] =
+// in_b[value] (a gather by the sorted values, fused into the write-out).
+struct RadixGather {
+  const uint32_t* in_a;
+  const uint2* in_b;
+  uint32_t* out_a;
+  uint2* out_b;
+};
+
+template <bool GATHER>
 static __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(const uint32_t* __restrict__ keys_in,
                                                                        const uint32_t* __restrict__ vals_in,
                                                                        uint32_t* __restrict__ keys_out,
                                                                        uint32_t* __restrict__ vals_out, int64_t n_cap,
                                                                        const int32_t* __restrict__ d_count, int shift,
                                                                        uint32_t mask, int64_t nb,
-                                                                       const uint32_t* __restrict__ offsets) {
+                                                                       const uint32_t* __restrict__ offsets,
+                                                                       RadixGather gat) {
   __shared__ uint16_t wcnt[kSortWarps][kSortBuckets];
   __shared__ uint32_t local_start[kSortBuckets];
   __shared__ uint32_t digit_base[kSortBuckets];
@@ -146,8 +157,13 @@ static __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(const uin
     const uint32_t kk = skeys[i];
     const uint32_t d = (kk >> shift) & mask;
     const uint32_t dst = digit_base[d] + (uint32_t)i - local_start[d];
+    const uint32_t v = svals[i];
     keys_out[dst] = kk;
-    vals_out[dst] = svals[i];
+    vals_out[dst] = v;
+    if (GATHER) {
+      gat.out_a[dst] = __ldg(gat.in_a + v);
+      gat.out_b[dst] = __ldg(gat.in_b + v);
+    }
   }
 }
 
@@ -170,7 +186,7 @@ inline void radix_ws_layout(C& c, int64_t n_cap, RadixWs* w) {
 // pair holds the output.
 inline cudaError_t radix_sort_pairs(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, int64_t n_cap,
                                     const int32_t* d_count, int key_bits, const RadixWs& w, bool* result_in_alt,
-                                    cudaStream_t st) {
+                                    cudaStream_t st, const RadixGather* gather = nullptr) {
   *result_in_alt = false;
   const int64_t nb = radix_num_blocks(n_cap);
   if (nb == 0 || key_bits <= 0) return cudaSuccess;
@@ -184,7 +200,12 @@ inline cudaError_t radix_sort_pairs(uint32_t* k0, uint32_t* v0, uint32_t* k1, ui
     k_radix_hist<<<(unsigned)nb, kSortThreads, 0, st>>>(ki, n_cap, d_count, shift, mask, nb, w.hist);
     cudaError_t e = exclusive_scan<uint32_t, uint32_t>(w.hist, w.hist, buckets * nb, nullptr, w.partials, nullptr, st);
     if (e != cudaSuccess) return e;
-    k_radix_scatter<<<(unsigned)nb, kSortThreads, 0, st>>>(ki, vi, ko, vo, n_cap, d_count, shift, mask, nb, w.hist);
+    if (gather && p == passes - 1)
+      k_radix_scatter<true><<<(unsigned)nb, kSortThreads, 0, st>>>(ki, vi, ko, vo, n_cap, d_count, shift, mask, nb,
+                                                                   w.hist, *gather);
+    else
+      k_radix_scatter<false><<<(unsigned)nb, kSortThreads, 0, st>>>(ki, vi, ko, vo, n_cap, d_count, shift, mask, nb,
+                                                                    w.hist, RadixGather{});
     count_launches(2);
     uint32_t* t;
     t = ki; ki = ko; ko = t;
