@@ -348,6 +348,10 @@ int bs_render_views(bs_context* const* ctxs, int32_t nctx, const bs_gaussian3d* 
 /* The context-owned planes frames with an empty bs_frame_out render into
  * (device pointers, valid until the next such frame or the context's destroy). */
 int bs_context_frame(bs_context* ctx, bs_frame_out* out);
+/* 8 bytes device -> mapped pinned host memory (cudaMallocHost) by a 1-thread
+ * kernel on stream: unlike a D2H memcpy it does not queue behind other
+ * streams' downloads on the copy engine. */
+int bs_publish_i64(const int64_t* src_dev, int64_t* dst_host_mapped, void* stream);
 /* Async mode for bs_render_frame_device: no host wait inside a frame.
  * point_list is sized from a capacity (3 x the first K, regrown to 3 x K
  * whenever a K passes 2/3 of it);

@@ -97,6 +97,7 @@ SIGNATURES = {
                                          _vp]),
     "bs_context_set_stream": (C.c_int, [_vp, _vp]),
     "bs_context_frame": (C.c_int, [_vp, C.POINTER(FrameOut)]),
+    "bs_publish_i64": (C.c_int, [_vp, _vp, _vp]),
     "bs_render_views": (C.c_int, [C.POINTER(C.c_void_p), _i32, _vp, _i64, C.POINTER(Camera), C.POINTER(C.c_int32),
                                   _i32, _i32, _i32, _i32, _f32p, C.POINTER(C.c_void_p), _sz]),
     "bs_context_set_async": (C.c_int, [_vp, _i32]),

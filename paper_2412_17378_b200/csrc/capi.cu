@@ -82,3 +82,20 @@ extern "C" int bs_select_variant_device(const bs_tile_histogram* stats, int32_t 
   BS_LAUNCH_CHECK();
   return BS_OK;
 }
+
+namespace bs {
+__global__ void k_publish_i64(const int64_t* __restrict__ src, int64_t* dst) {
+  *reinterpret_cast<volatile int64_t*>(dst) = *src;
+  __threadfence_system();
+}
+}  // namespace bs
+
+// 8 bytes from device memory to (mapped, pinned) host memory by a 1-thread
+// kernel: no copy-engine transfer, so it never queues behind a large
+// download running on another stream (a cudaMemcpyAsync D2H would).
+extern "C" int bs_publish_i64(const int64_t* src_dev, int64_t* dst_host_mapped, void* stream) {
+  if (!src_dev || !dst_host_mapped) return BS_ERR_INVALID_ARGUMENT;
+  bs::k_publish_i64<<<1, 1, 0, (cudaStream_t)stream>>>(src_dev, dst_host_mapped);
+  BS_LAUNCH_CHECK();
+  return BS_OK;
+}

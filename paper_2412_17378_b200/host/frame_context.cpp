@@ -352,7 +352,9 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   mark(2);
   const bool async = allow_async && c->async_mode && bs_bin_async_supported(W, H, pw, ph);
   const int slot = capturing ? capture_slot : (async ? c->next_slot : 0);
-  CUTRY(cudaMemcpyAsync(c->k_host + 1 + slot, c->k_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  // K -> pinned host slot by a kernel store (a D2H memcpy would wait behind
+  // any large download on the copy engine, e.g. the previous frame's planes)
+  TRY(bs_publish_i64(c->k_dev, c->k_host + 1 + slot, st));
   if (async) {
     // no wait: sort into the current capacity; K is checked kDepth calls later
     if (!c->ev_k[slot]) CUTRY(cudaEventCreateWithFlags(&c->ev_k[slot], cudaEventDisableTiming));
