@@ -549,40 +549,59 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
 
     # e2e: host buffers through the pipelined C-ABI host frame API — every
     # step uploads the scene from pinned host memory and downloads all six
-    # output planes into pinned host buffers (a ring of 3 sets: three frames
-    # are in flight); wall clock from the first enqueue to the final sync
-    ctx = C.c_void_p()
-    N.call("bs_context_create", C.byref(ctx), int(mode))
-    N.call("bs_context_set_async", ctx, 1)
+    # output planes into pinned host buffers.  Frames go round-robin to
+    # --streams contexts (each with its own upload / frame / download streams
+    # and 3 I/O slots, a ring of 3 pinned output sets per context); wall
+    # clock from the first enqueue to the final sync of every context
+    nctx = max(1, args.streams)
+    if nctx > 1:
+        N.call("bs_render_set_fine_occupancy", args.fine_ctas)
+    ctxs = []
+    for _ in range(nctx):
+        cx = C.c_void_p()
+        N.call("bs_context_create", C.byref(cx), int(mode))
+        N.call("bs_context_set_async", cx, 1)
+        ctxs.append(cx)
     host_g3d = torch.from_numpy(np.ascontiguousarray(g3d).view(np.uint8).reshape(-1).copy()).pin_memory()
     P3 = P * 3
-    rings = [[torch.empty(P3, dtype=torch.float32).pin_memory()] +
-             [torch.empty(P, dtype=torch.float32).pin_memory() for _ in range(3)] +
-             [torch.empty(P, dtype=torch.int32).pin_memory() for _ in range(2)] for _ in range(3)]
+    rings = [[[torch.empty(P3, dtype=torch.float32).pin_memory()] +
+              [torch.empty(P, dtype=torch.float32).pin_memory() for _ in range(3)] +
+              [torch.empty(P, dtype=torch.int32).pin_memory() for _ in range(2)] for _ in range(3)]
+             for _ in range(nctx)]
     bgc = (C.c_float * 3)(0.0, 0.0, 0.0)
     vv = -1 if args.variant == "auto" else int(vsel)
 
     def e2e_step(k):
-        N.call("bs_render_frame_host_async", ctx, host_g3d.data_ptr(), n, C.byref(cams[k % N_VIEWS]), pw, ph, vv,
-               bgc, *[o.data_ptr() for o in rings[k % 3]])
+        c_, j = k % nctx, k // nctx
+        N.call("bs_render_frame_host_async", ctxs[c_], host_g3d.data_ptr(), n, C.byref(cams[k % N_VIEWS]), pw, ph,
+               vv, bgc, *[o.data_ptr() for o in rings[c_][j % 3]])
 
-    r0 = C.c_int64(0)
-    for k in range(4):
+    def e2e_sync():
+        tot = 0
+        for cx in ctxs:
+            r = C.c_int64(0)
+            N.call("bs_context_sync", cx, C.byref(r))
+            tot += r.value
+        return tot
+
+    for k in range(4 * nctx):
         e2e_step(k)
-    N.call("bs_context_sync", ctx, C.byref(r0))
-    ne = max(3, min(args.steps, 30))
+    r0 = e2e_sync()
+    ne = max(3, min(args.steps, 100))
     t0 = time.perf_counter()
     for k in range(ne):
         e2e_step(k)
-    r1 = C.c_int64(0)
-    N.call("bs_context_sync", ctx, C.byref(r1))
+    r1 = e2e_sync()
     e2e_s = (time.perf_counter() - t0) / ne
-    N.call("bs_context_destroy", ctx)
+    for cx in ctxs:
+        N.call("bs_context_destroy", cx)
+    N.call("bs_render_set_fine_occupancy", 0)
     res["e2e"] = {"value": 1.0 / e2e_s, "unit": "views/s", "h2d_bytes_per_step": int(n * 56),
                   "d2h_bytes_per_step": int(P * 32), "ms_per_step": e2e_s * 1e3, "steps": ne,
-                  "reruns": int(r1.value - r0.value),
-                  "path": "bs_render_frame_host_async (C-ABI; pinned host buffers; upload / frame / download on "
-                          "three streams, 3 frames in flight; wall clock to bs_context_sync)"}
+                  "reruns": int(r1 - r0), "contexts": nctx,
+                  "path": "bs_render_frame_host_async (C-ABI; pinned host buffers; per context upload / frame / "
+                          "download on three streams, 3 frames in flight; frames round-robin over the contexts; "
+                          "wall clock to bs_context_sync)"}
 
     if world == 1 and not args.no_cpu_baseline:
         g2d = api.splats_to_g2d(s)
