@@ -317,10 +317,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = f"cuda:{local}"
+    # BS_BENCH_SHARED_GPU=1 (test only): every rank on cuda:0 with gloo, so
+    # the N>1 path (view sharding, barriers, max over ranks) runs on a 1-GPU box
+    shared = os.environ.get("BS_BENCH_SHARED_GPU") == "1"
+    gpu = 0 if shared else local
+    torch.cuda.set_device(gpu)
+    dev = f"cuda:{gpu}"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(dev))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(dev))
 
     W, H, f, n, bgf, sig = CONFIGS[args.config]
     pw = ph = 16
@@ -370,7 +377,7 @@ def main():
     def sync_all() -> int:
         return sum(f.sync() for f in fps)
 
-    clk = make_clock_sampler(local)  # sampling spans warm-up + timed region (the timed region alone is < 1 s)
+    clk = make_clock_sampler(gpu)  # sampling spans warm-up + timed region (the timed region alone is < 1 s)
     run_views(0, max(args.warmup, 2 * ns), flush=False)  # >= 2 frames per context: capacity calibrated, graphs captured
     sync_all()
     torch.cuda.synchronize()
@@ -412,6 +419,8 @@ def main():
         total_ms *= 1.0 + reruns / args.steps
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
+        if shared:
+            t = t.cpu()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
     value = world * args.steps / (max_ms / 1e3)
