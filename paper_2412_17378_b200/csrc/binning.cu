@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
 
   // drain the first nq queue entries' band tiles, 32 instances per step:
   // instance f of the flat (splat, row, column) enumeration belongs to the
-  // last lane whose exclusive count is <= f (5-step shuffle search); its
+  // last lane whose exclusive count is <= f (window bitmask, below); its
   // row / column come from one float multiply by the lane's 1/w (exact:
   // f < 2^22).  Equal tiles inside a step are ranked by match.any (lane
   // order = depth order); the highest peer advances the tile's offset.
@@ -460,18 +460,22 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
     const int incl = warp_inclusive_scan(cnt);
     const int excl = incl - cnt;
     const int tot = __shfl_sync(0xffffffffu, incl, 31);
-    // instance f -> (tile, splat id); 0xffffffff tile past the end
+    // instance f -> (tile, splat id); 0xffffffff tile past the end.  The
+    // queued splats whose first instance falls inside the 32-instance window
+    // [f0, f0 + 32) set one bit each (one redux.or): instance f0 + lane
+    // belongs to the window's first splat plus the number of starts in
+    // (f0, f0 + lane]; sb tracks the window's first splat.  (A 5-step
+    // shuffle binary search over the exclusive counts measured 2.6 % slower.)
+    int sb = 0;
     auto resolve = [&](int f0, uint32_t& tile, uint32_t& sid) {
+      const int k = excl - f0;
+      const uint32_t m = __reduce_or_sync(0xffffffffu, (lane < nq && k >= 1 && k < 32) ? (1u << k) : 0u);
+      const bool next_starts = __ballot_sync(0xffffffffu, lane < nq && k == 32) != 0u;
+      const uint32_t upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+      const int sl = sb + __popc(m & upto);
+      sb += __popc(m) + (next_starts ? 1 : 0);
       const int f = f0 + lane;
-      int sl = 0, e0 = 0;
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int e = __shfl_sync(0xffffffffu, excl, sl + step);
-        if (e <= f) {
-          sl += step;
-          e0 = e;
-        }
-      }
+      const int e0 = __shfl_sync(0xffffffffu, excl, sl);
       const uint32_t local = (uint32_t)(f - e0);
       const uint32_t ws = __shfl_sync(0xffffffffu, w, sl);
       const float iv = __shfl_sync(0xffffffffu, inv, sl);
@@ -480,7 +484,7 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
       const uint32_t r = (uint32_t)(((float)local + 0.5f) * iv);
       tile = f < tot ? t0 + r * (uint32_t)cols + (local - r * ws) : 0xffffffffu;
     };
-    // software-pipelined: the next step's shuffle search is independent of
+    // software-pipelined: the next step's resolve is independent of
     // this step's match / shared-memory chain, so their latencies overlap
     uint32_t tile, sid;
     resolve(0, tile, sid);
