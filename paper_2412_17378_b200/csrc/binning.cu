@@ -467,9 +467,10 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
     // (f0, f0 + lane]; sb tracks the window's first splat.  (A 5-step
     // shuffle binary search over the exclusive counts measured 2.6 % slower.)
     int sb = 0;
-    auto resolve = [&](int f0, uint32_t& tile, uint32_t& sid) {
+    auto resolve = [&](int f0, uint32_t& tile, uint32_t& sid, bool& one) {
       const int k = excl - f0;
       const uint32_t m = __reduce_or_sync(0xffffffffu, (lane < nq && k >= 1 && k < 32) ? (1u << k) : 0u);
+      one = m == 0u;  // the whole window is one splat's: its tiles are distinct
       const bool next_starts = __ballot_sync(0xffffffffu, lane < nq && k == 32) != 0u;
       const uint32_t upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
       const int sl = sb + __popc(m & upto);
@@ -487,12 +488,14 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
     // software-pipelined: the next step's resolve is independent of
     // this step's match / shared-memory chain, so their latencies overlap
     uint32_t tile, sid;
-    resolve(0, tile, sid);
+    bool one;
+    resolve(0, tile, sid, one);
     for (int f0 = 0; f0 < tot; f0 += 32) {
       uint32_t ntile = 0xffffffffu, nsid = 0;
-      if (f0 + 32 < tot) resolve(f0 + 32, ntile, nsid);
+      bool none = false;
+      if (f0 + 32 < tot) resolve(f0 + 32, ntile, nsid, none);
       const bool act = tile != 0xffffffffu;
-      const uint32_t peers = __match_any_sync(0xffffffffu, tile);
+      const uint32_t peers = one ? (1u << lane) : __match_any_sync(0xffffffffu, tile);
       const uint32_t a = sbase + 4u * tile;
       uint32_t pos = 0;
       if (act) {
@@ -504,6 +507,7 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
       __syncwarp();
       tile = ntile;
       sid = nsid;
+      one = none;
     }
   };
 
