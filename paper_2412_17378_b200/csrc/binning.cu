@@ -237,15 +237,14 @@ __global__ void __launch_bounds__(256) k_expand(const uint64_t* __restrict__ off
 //                   rectangles -> per-tile counts M[c][t]
 //   k_chunk_scan    in place, M[c][t] <- starts[t] + sum_{c' < c} M[c'][t]
 //   k_chunk_scatter per chunk, the offsets row in shared memory; warp w owns
-//                   the tiles (tx, ty) = (w % 4, w / 4) (mod 4) and walks the chunk's
-//                   splats in depth order, 32 instances per step; equal tiles
+//                   a band of tile rows (equal instance counts) and walks the
+//                   chunk's splats in depth order, 32 instances per step; equal tiles
 //                   inside a step are ranked by match.any (lane order = depth
 //                   order), so every tile list is written in (depth, index)
 //                   order directly — point_list is the final order without
 //                   materialising or sorting K keys.
 constexpr int kScWarps = 16;
 constexpr int kScThreads = kScWarps * 32;
-constexpr int kOwnX = 4, kOwnY = kScWarps / kOwnX;  // tile ownership pattern (powers of 2)
 constexpr int kScMaxRows = 1024;                     // tile rows the row-band split supports
 constexpr int64_t kScTableBytes = 40 * 1024;         // offsets-row slice per CTA (row bands beyond)
 constexpr int64_t kMaxChunkMatrix = (int64_t)64 << 20;  // entries of M (256 MB)
@@ -602,7 +601,6 @@ inline bool bin_chunked(const Grid& g) {
     const char* e = getenv("BS_BIN_RADIX");
     return (e && e[0] == '1') ? 1 : 0;
   }();
-  const int64_t T = (int64_t)g.cols * g.rows;
   return !forced_radix && g.rows <= kScMaxRows && (size_t)(g.cols + 32) * 4 <= (size_t)kScTableBytes &&
          sizeof(int) * (size_t)(g.cols + 1) * (g.rows + 1) <= kMaxDiffSmem;
 }
