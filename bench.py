@@ -540,10 +540,39 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     pad[:H, :W] = cons
     prefix_entries = int(pad.reshape(rows, ph, cols, pw).max(axis=(1, 3)).sum())
     bytes_prefix = 44 * prefix_entries + 32 * P
+    # the render the timed frames run: on >= 1 Mpixel frames the frame
+    # pipeline bins into 2pw x 2ph super-tile lists and the render filters
+    # each tile's members (bs_render_forward_super) — time that render stage
+    # (CUDA events on the frame's stream) on the same view
+    N.call("bs_context_enable_timing", fp.ctx, 1)
+    t_fp = []
+    for _ in range(10):
+        fp.forward(g3d_dev, n, cam_id, variant=vsel_arg)
+        t_fp.append(fp.stage_ms()["render"])
+    N.call("bs_context_enable_timing", fp.ctx, 0)
+    sup = C.c_int32(0)
+    N.call("bs_context_list_mode", fp.ctx, C.byref(sup))
+    t_api_s = t_s
+    if sup.value:
+        t_s = float(np.mean(t_fp)) / 1e3
+    api_view = {"kernel": f"render {api.variant_name(vsel)} ({mname}) on the reference's pw x ph TileBinning "
+                          "(bs_render_forward, the API path)", "t_ms": t_api_s * 1e3,
+                "frac": bytes_alg / t_api_s / hbm_peak, "t_roof_frac": t_roof / t_api_s, "traffic": traffic}
+    if sup.value:
+        traffic = None
+        try:
+            with open(NCU_TRAFFIC_PATH) as fh:
+                traffic = json.load(fh).get(f"{args.config}_{api.variant_name(vsel)}_{mname}_super")
+        except Exception:
+            pass
+    res["fwd_render_ms_per_frame_pipeline"] = t_s * 1e3
+    kname = (f"render {api.variant_name(vsel)} ({mname}) on super-tile lists (frame pipeline: the timed frames' "
+             "render stage)") if sup.value else f"render {api.variant_name(vsel)} ({mname})"
     res["roofline"] = {
-        "bound": "hbm", "kernel": f"render {api.variant_name(vsel)} ({mname})",
+        "bound": "hbm", "kernel": kname, "t_ms": t_s * 1e3,
         "achieved": bytes_alg / t_s / 1e9, "peak": hbm_peak / 1e9, "unit": "GB/s",
         "frac": bytes_alg / t_s / hbm_peak, "traffic": traffic, "algorithmic_bytes": bytes_alg,
+        "api_kernel_view": api_view,
         "bytes_def": "SURVEY 8d: 44 B per tile instance (u32 index + 40 B attributes) + 32 B per output pixel",
         "peak_source": hbm_src,
         "t_roof_ms": t_roof * 1e3, "t_roof_frac": t_roof / t_s,

@@ -180,6 +180,17 @@ int bs_bin_count(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t w
 int bs_preprocess_bin_count(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, const bs_camera* cam_dev,
                             bs_splats out, int32_t* counts, int32_t width, int32_t height, int32_t pw, int32_t ph,
                             int64_t* k_total, void* ws, size_t ws_bytes, void* stream);
+/* Super-tile form for the frame pipeline (power-of-two pw, ph): the lists
+ * are binned at 2pw x 2ph (bs_bin_sort* follow with 2pw, 2ph) and
+ * tile_ranges (2 x T, T = pw x ph tiles) receives the pw x ph list
+ * lengths (for bs_tile_order / bs_tile_stats / bs_frame_work).  aux:
+ * bs_super_aux_bytes(width, height, pw, ph) bytes. */
+size_t bs_super_aux_bytes(int32_t width, int32_t height, int32_t pw, int32_t ph);
+int bs_preprocess_bin_count_super(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam,
+                                  const bs_camera* cam_dev, bs_splats out, int32_t* counts, int32_t width,
+                                  int32_t height, int32_t pw, int32_t ph, int64_t* k_total, void* ws,
+                                  size_t ws_bytes, uint32_t* tile_ranges, void* aux, size_t aux_bytes,
+                                  void* stream);
 int bs_bin_sort(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height, int32_t pw,
                 int32_t ph, int64_t k, uint32_t* point_list, uint32_t* tile_ranges, void* ws, size_t ws_bytes,
                 void* stream);
@@ -348,6 +359,22 @@ int bs_render_views(bs_context* const* ctxs, int32_t nctx, const bs_gaussian3d* 
 /* The context-owned planes frames with an empty bs_frame_out render into
  * (device pointers, valid until the next such frame or the context's destroy). */
 int bs_context_frame(bs_context* ctx, bs_frame_out* out);
+/* Render from super-tile lists (binned at 2pw x 2ph): tile_ranges holds, per
+ * pw x ph tile, its super-tile's range (bs_super_tile_ranges); the render
+ * keeps the entries whose pw x ph rectangle contains the tile — exactly the
+ * tile's list, term counted over it.  variant: FineGrainedCombined,
+ * SharedMemOpt, or -1 (device-selected from variant_dev, as
+ * bs_render_forward_auto).  Power-of-two pw, ph. */
+int bs_render_forward_super(int variant, const int32_t* variant_dev, int alpha_mode, bs_splats g,
+                            const uint32_t* point_list, const uint32_t* tile_ranges, const uint32_t* task_order,
+                            int32_t width, int32_t height, int32_t pw, int32_t ph, const float bg[3],
+                            bs_frame_out out, void* ws, size_t ws_bytes, void* stream);
+int bs_super_tile_ranges(const uint32_t* super_ranges, int32_t width, int32_t height, int32_t pw, int32_t ph,
+                         uint32_t* tile_ranges, void* stream);
+/* 1 if the context's last frame was binned into super-tile lists (frames
+ * >= 1 Mpixel with power-of-two patches and a FineGrainedCombined /
+ * SharedMemOpt / device-selected variant; BS_NO_SUPER=1 disables), else 0. */
+int bs_context_list_mode(bs_context* ctx, int32_t* super_lists);
 /* 8 bytes device -> mapped pinned host memory (cudaMallocHost) by a 1-thread
  * kernel on stream: unlike a D2H memcpy it does not queue behind other
  * streams' downloads on the copy engine. */

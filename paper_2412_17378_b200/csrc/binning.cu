@@ -782,6 +782,87 @@ extern "C" int bs_preprocess_bin_count(const bs_gaussian3d* g3d, int64_t n, cons
   return bin_count_tail(n, counts, gr, w, smem_diff, diff_bytes, k_total, st);
 }
 
+// ---------------------------------------------------------------------------
+// Super-tile binning for the frame pipeline: the lists are built at
+// 2pw x 2ph (about a third of the instances at C2 — the scatter is the
+// dominant binning cost) and the render keeps, per pw x ph tile, the entries
+// whose rectangle contains it (bs_render_forward_super).  The pw x ph list
+// lengths (tile statistics, LPT order, selector) come from a second
+// difference grid in the same projection pass.  Power-of-two patches only.
+static bool pow2i(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+extern "C" size_t bs_super_aux_bytes(int32_t width, int32_t height, int32_t pw, int32_t ph) {
+  if (width <= 0 || height <= 0 || pw <= 0 || ph <= 0) return 0;
+  const Grid g = make_grid(width, height, pw, ph);
+  const int64_t T = (int64_t)g.cols * g.rows;
+  WsSizer z;
+  z.take<int>((size_t)(g.cols + 1) * (g.rows + 1));  // diff
+  z.take<uint32_t>((size_t)T);                        // counts
+  z.take<uint32_t>((size_t)T);                        // starts
+  z.take<uint32_t>((size_t)scan_num_blocks(T) + 1);   // scan partials
+  return z.off + 256;
+}
+
+extern "C" int bs_preprocess_bin_count_super(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam,
+                                             const bs_camera* cam_dev, bs_splats out, int32_t* counts,
+                                             int32_t width, int32_t height, int32_t pw, int32_t ph,
+                                             int64_t* k_total, void* ws, size_t ws_bytes, uint32_t* tile_ranges,
+                                             void* aux, size_t aux_bytes, void* stream) {
+  if (!pow2i(pw) || !pow2i(ph) || pw > 16384 || ph > 16384) return BS_ERR_UNSUPPORTED;
+  int s = check_grid(width, height, 2 * pw, 2 * ph);
+  if (s) return s;
+  if (n < 0 || (!cam && !cam_dev) || !counts || !k_total || !tile_ranges ||
+      (n > 0 && (!g3d || !out.xyab || !out.cop || !out.rgbr)))
+    return BS_ERR_INVALID_ARGUMENT;
+  if (n >= (int64_t)1 << 30) return BS_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Grid gs = make_grid(width, height, 2 * pw, 2 * ph);
+  const Grid gt = make_grid(width, height, pw, ph);
+  const int64_t T = (int64_t)gt.cols * gt.rows;
+  if (!ws || ws_bytes < bs_bin_workspace_bytes(n, width, height, 2 * pw, 2 * ph, 0)) return BS_ERR_WORKSPACE;
+  if (!aux || aux_bytes < bs_super_aux_bytes(width, height, pw, ph)) return BS_ERR_WORKSPACE;
+  WsCarver c(ws, ws_bytes);
+  BinWs w;
+  bin_ws_layout(c, n, gs, 0, &w);
+  WsCarver ca(aux, aux_bytes);
+  int* diff2 = ca.take<int>((size_t)(gt.cols + 1) * (gt.rows + 1));
+  uint32_t* counts2 = ca.take<uint32_t>((size_t)T);
+  uint32_t* starts2 = ca.take<uint32_t>((size_t)T);
+  uint32_t* partials2 = ca.take<uint32_t>((size_t)scan_num_blocks(T) + 1);
+  const size_t diff_bytes = sizeof(int) * (size_t)(gs.cols + 1) * (gs.rows + 1);
+  const size_t diff2_bytes = sizeof(int) * (size_t)(gt.cols + 1) * (gt.rows + 1);
+  const bool smem_diff = diff_bytes <= kMaxDiffSmem;
+  if (!g_diff_attr_set) {
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_bin_rect<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDiffSmem));
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_diff_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDiffSmem));
+    g_diff_attr_set = true;
+  }
+  BS_CUDA_TRY(cudaMemsetAsync(w.diff, 0, diff_bytes, st));
+  BS_CUDA_TRY(cudaMemsetAsync(diff2, 0, diff2_bytes, st));
+  BS_CUDA_TRY(cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), st));
+  if (n > 0)
+    BS_CUDA_TRY(launch_project_bin(g3d, n, cam, cam_dev, gs, reinterpret_cast<float4*>(out.xyab),
+                                   reinterpret_cast<float4*>(out.cop), reinterpret_cast<float4*>(out.rgbr), w.touched,
+                                   w.rects, w.dk0, w.dv0, w.diff, diff_bytes, smem_diff, counts, st, &gt, diff2));
+  s = bin_count_tail(n, counts, gs, w, smem_diff, diff_bytes, k_total, st);
+  if (s) return s;
+  // the pw x ph list lengths -> tile_ranges (lengths exact; starts are the
+  // lists' offsets had they been materialised)
+  if (diff2_bytes <= kMaxDiffSmem) {
+    k_diff_scan<<<1, 1024, diff2_bytes, st>>>(diff2, gt, counts2);
+    BS_LAUNCH_CHECK();
+  } else {
+    k_diff_rows<<<(unsigned)(gt.rows + 1), 256, 0, st>>>(diff2, gt.cols + 1);
+    BS_LAUNCH_CHECK();
+    k_diff_cols<<<(unsigned)((gt.cols + 255) / 256), 256, 0, st>>>(diff2, gt, counts2);
+    BS_LAUNCH_CHECK();
+  }
+  BS_CUDA_TRY((exclusive_scan<uint32_t, uint32_t>(counts2, starts2, T, nullptr, partials2, nullptr, st)));
+  k_ranges<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(starts2, counts2, (int)T, tile_ranges, nullptr, 0);
+  BS_LAUNCH_CHECK();
+  return BS_OK;
+}
+
 // k >= 0: K known on the host (bs_bin_sort).  k < 0: K only on the device
 // (bs_bin_sort_async; chunked path only) and point_list holds k_cap entries.
 static int bin_sort_impl(int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height, int32_t pw,

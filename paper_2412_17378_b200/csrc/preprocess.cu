@@ -187,21 +187,28 @@ __global__ void __launch_bounds__(256) k_project_write(const bs_gaussian3d* __re
 // touched, packed rect, depth key, index, difference-grid corners) follow
 // from the registers.  Tie order is unchanged: the compacted index of the
 // reference is a monotone function of i.  SMEM_DIFF as in k_bin_rect.
-template <bool SMEM_DIFF>
+// DIFF2: a second difference grid at grid g2 (the pw x ph tiles when the
+// binning grid g is the 2pw x 2ph super-tile grid): its list lengths feed the
+// tile statistics, the LPT order and the selector.  SMEM2: that grid too in
+// shared memory (after the first), else global atomics.
+template <bool SMEM_DIFF, bool DIFF2, bool SMEM2>
 __global__ void __launch_bounds__(256, 3) k_project_bin(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam_,
                                                      const bs_camera* __restrict__ camd, Grid g,
                                                      float4* __restrict__ xyab, float4* __restrict__ cop,
                                                      float4* __restrict__ rgbr, uint32_t* __restrict__ touched,
                                                      uint2* __restrict__ rects, uint32_t* __restrict__ dkeys,
                                                      uint32_t* __restrict__ dvals, int* __restrict__ diff,
-                                                     int32_t* __restrict__ counts) {
+                                                     int32_t* __restrict__ counts, Grid g2, int* __restrict__ diff2) {
   extern __shared__ int s_diff[];
   const CamDev cam = cam_of(camd, cam_);
   const int stride = g.cols + 1;
   const int cells = stride * (g.rows + 1);
+  const int stride2 = g2.cols + 1;
+  const int cells2 = DIFF2 ? stride2 * (g2.rows + 1) : 0;
   int* dd = SMEM_DIFF ? s_diff : diff;
+  int* dd2 = SMEM2 ? s_diff + cells : diff2;
   if (SMEM_DIFF) {
-    for (int i = threadIdx.x; i < cells; i += blockDim.x) s_diff[i] = 0;
+    for (int i = threadIdx.x; i < cells + (SMEM2 ? cells2 : 0); i += blockDim.x) s_diff[i] = 0;
     __syncthreads();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = (int32_t)n;
@@ -227,6 +234,15 @@ __global__ void __launch_bounds__(256, 3) k_project_bin(const bs_gaussian3d* __r
         atomicAdd(&dd[(r.ty1 + 1) * stride + r.tx0], -1);
         atomicAdd(&dd[(r.ty1 + 1) * stride + r.tx1 + 1], 1);
       }
+      if (DIFF2) {
+        Rect r2;
+        if (tile_rect(o.x, o.y, o.radius, g2, r2)) {
+          atomicAdd(&dd2[r2.ty0 * stride2 + r2.tx0], 1);
+          atomicAdd(&dd2[r2.ty0 * stride2 + r2.tx1 + 1], -1);
+          atomicAdd(&dd2[(r2.ty1 + 1) * stride2 + r2.tx0], -1);
+          atomicAdd(&dd2[(r2.ty1 + 1) * stride2 + r2.tx1 + 1], 1);
+        }
+      }
     }
     touched[i] = cnt;
     rects[i] = pk;
@@ -241,13 +257,18 @@ __global__ void __launch_bounds__(256, 3) k_project_bin(const bs_gaussian3d* __r
       const int v = s_diff[i];
       if (v) atomicAdd(&diff[i], v);
     }
+    if (SMEM2)
+      for (int i = threadIdx.x; i < cells2; i += blockDim.x) {
+        const int v = s_diff[cells + i];
+        if (v) atomicAdd(&diff2[i], v);
+      }
   }
 }
 
 cudaError_t launch_project_bin(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, const bs_camera* cam_dev,
                                const Grid& g, float4* xyab, float4* cop, float4* rgbr, uint32_t* touched,
                                uint2* rects, uint32_t* dkeys, uint32_t* dvals, int* diff, size_t diff_bytes,
-                               bool smem_diff, int32_t* counts, cudaStream_t st) {
+                               bool smem_diff, int32_t* counts, cudaStream_t st, const Grid* g2, int* diff2) {
   CamDev c{};
   if (cam) {
     for (int k = 0; k < 12; ++k) c.v[k] = cam->view[k];
@@ -258,29 +279,48 @@ cudaError_t launch_project_bin(const bs_gaussian3d* g3d, int64_t n, const bs_cam
   }
   const bs_camera* camd = cam ? nullptr : cam_dev;
   const int64_t nb = (n + 255) / 256;
+  const Grid gg2 = g2 ? *g2 : g;
+  const size_t diff2_bytes = g2 ? sizeof(int) * (size_t)(g2->cols + 1) * (g2->rows + 1) : 0;
+  const bool smem2 = g2 && smem_diff && diff_bytes + diff2_bytes <= (size_t)64 * 1024;
   if (smem_diff) {
-    static int per_sm = 0, sms = 0;
-    static size_t attr_bytes = 0;
-    if (diff_bytes > attr_bytes) {
-      cudaError_t e = cudaFuncSetAttribute(k_project_bin<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)diff_bytes);
-      if (e != cudaSuccess) return e;
-      attr_bytes = diff_bytes;
-      per_sm = 0;
-    }
-    if (!per_sm) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_project_bin<true>, 256, diff_bytes);
-      per_sm = per_sm < 1 ? 1 : (per_sm > 3 ? 3 : per_sm);  // each CTA flushes its grid once: cap the flushes
-    }
-    const int64_t grid = nb < (int64_t)sms * per_sm ? nb : (int64_t)sms * per_sm;
-    k_project_bin<true><<<(unsigned)(grid > 0 ? grid : 1), 256, diff_bytes, st>>>(
-        g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects, dkeys, dvals, diff, counts);
+    const size_t sm = diff_bytes + (smem2 ? diff2_bytes : 0);
+    // one kernel per combination; per-combination occupancy cached
+    auto go = [&](auto kern) -> cudaError_t {
+      static size_t attr_bytes[4] = {0, 0, 0, 0};
+      static int per_sm[4] = {0, 0, 0, 0};
+      const int slot = (g2 ? 1 : 0) + (smem2 ? 2 : 0);
+      if (sm > attr_bytes[slot]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+        attr_bytes[slot] = sm;
+        per_sm[slot] = 0;
+      }
+      static int sms = 0;
+      if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      }
+      if (!per_sm[slot]) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[slot], kern, 256, sm);
+        per_sm[slot] = per_sm[slot] < 1 ? 1 : (per_sm[slot] > 3 ? 3 : per_sm[slot]);  // each CTA flushes once
+      }
+      const int64_t grid = nb < (int64_t)sms * per_sm[slot] ? nb : (int64_t)sms * per_sm[slot];
+      kern<<<(unsigned)(grid > 0 ? grid : 1), 256, sm, st>>>(g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects,
+                                                             dkeys, dvals, diff, counts, gg2, diff2);
+      return cudaSuccess;
+    };
+    cudaError_t e;
+    if (!g2) e = go(k_project_bin<true, false, false>);
+    else if (smem2) e = go(k_project_bin<true, true, true>);
+    else e = go(k_project_bin<true, true, false>);
+    if (e != cudaSuccess) return e;
+  } else if (g2) {
+    k_project_bin<false, true, false><<<(unsigned)(nb > 0 ? nb : 1), 256, 0, st>>>(
+        g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects, dkeys, dvals, diff, counts, gg2, diff2);
   } else {
-    k_project_bin<false><<<(unsigned)(nb > 0 ? nb : 1), 256, 0, st>>>(g3d, n, c, camd, g, xyab, cop, rgbr, touched,
-                                                                      rects, dkeys, dvals, diff, counts);
+    k_project_bin<false, false, false><<<(unsigned)(nb > 0 ? nb : 1), 256, 0, st>>>(
+        g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects, dkeys, dvals, diff, counts, gg2, diff2);
   }
   count_launches(1);
   return cudaPeekAtLastError();

@@ -34,6 +34,7 @@
 
 #include "bs_common.cuh"
 #include "exact_expf.cuh"
+#include "tiles.cuh"
 
 namespace bs {
 
@@ -65,7 +66,34 @@ struct RArgs {
   int donate_after;       // list entries a task walks before it may hand off
   int donate_min_remain;  // ... and only if this many entries remain
   const int32_t* gate;    // device-selected variant (bs_render_forward_auto) or null
+  // super-tile lists (bs_render_forward_super): ranges[t] is the list of the
+  // 2pw x 2ph super-tile holding tile t, and an entry belongs to tile t's
+  // list iff its S8 rectangle at pw x ph contains t (tile_member)
+  int sup, rows;
+  float ipw, iph;  // 1/pw, 1/ph (exact: power-of-two patches only)
 };
+
+// Is tile (tx, ty) inside the splat's S8 rectangle at the pw x ph grid
+// (src/preprocess.cpp:83-92, tiles.cuh tile_rect's ops; x / pw == x * (1/pw)
+// exactly for a power-of-two pw)?  The rejection tests need not be repeated:
+// they do not depend on the patch size, and a splat in a super-tile list
+// passed them.  (Loading a rectangle precomputed by the projection pass
+// instead measured slower: the extra registers spill.)
+__device__ __forceinline__ bool tile_member(const RArgs& A, float x, float y, float radius, int tx, int ty) {
+  const float rr = ceilf(radius);
+  const float x0 = __fsub_rn(x, rr), x1 = __fadd_rn(x, rr);
+  const float y0 = __fsub_rn(y, rr), y1 = __fadd_rn(y, rr);
+  const int tx0 = max(0, x86_f2i(floorf(__fmul_rn(x0, A.ipw))));
+  const int tx1 = min(A.cols - 1, x86_f2i(floorf(__fmul_rn(x1, A.ipw))));
+  const int ty0 = max(0, x86_f2i(floorf(__fmul_rn(y0, A.iph))));
+  const int ty1 = min(A.rows - 1, x86_f2i(floorf(__fmul_rn(y1, A.iph))));
+  return tx0 <= tx && tx <= tx1 && ty0 <= ty && ty <= ty1;
+}
+
+// FineGrainedCombined list mode: pw x ph lists, or super-tile lists
+// filtered by tile_member (a template parameter: the pw x ph kernel keeps
+// its register budget)
+enum { kListTile = 0, kListSuper = 1 };
 
 // Sync-free auto mode: every candidate kernel is launched and all but the
 // device-selected one return at once.
@@ -203,7 +231,7 @@ struct PwChunk {
 
 template <int MODE, bool STAGE_COLOR, int BLOCK>
 __device__ __forceinline__ void pixelwise_tile(const RArgs& A, int tile, float4* s_xyab, float4* s_cop,
-                                               float4* s_rgb, uint32_t* s_id, const ExpK& ek) {
+                                               float4* s_rgb, uint32_t* s_id, bool* s_mem, const ExpK& ek) {
   const int tid = threadIdx.x;
   const int tx = tile % A.cols, ty = tile / A.cols;
   const int lx = tid % A.pw, ly = tid / A.pw;
@@ -218,27 +246,37 @@ __device__ __forceinline__ void pixelwise_tile(const RArgs& A, int tile, float4*
   Accum<MODE> acc;
 
   constexpr int CHUNK = PwChunk<MODE, STAGE_COLOR, BLOCK>::value;
+  uint32_t mbase = 0;  // entries of this tile's list before the chunk
   for (uint32_t base = start; base < end; base += CHUNK) {
     if (__syncthreads_count(!done) == 0) break;
     const uint32_t k = base + tid;
+    bool mem = false;
     if (tid < CHUNK && k < end) {
       const uint32_t id = __ldg(A.point_list + k);
       s_xyab[tid] = __ldg(A.xyab + id);
       s_cop[tid] = __ldg(A.cop + id);
       if (STAGE_COLOR) s_rgb[tid] = __ldg(A.rgbr + id);
       else s_id[tid] = id;
+      mem = true;
+      if (A.sup) {
+        mem = tile_member(A, s_xyab[tid].x, s_xyab[tid].y, __ldg(&A.rgbr[id].w), tx, ty);
+        s_mem[tid] = mem;
+      }
     }
-    __syncthreads();
+    const uint32_t cmem = (uint32_t)__syncthreads_count(mem);
     if (!done) {
       const int cnt = (int)min((uint32_t)CHUNK, end - base);
+      int m = 0;
       for (int j = 0; j < cnt; ++j) {
+        if (A.sup && !s_mem[j]) continue;  // not in this tile's list
+        ++m;
         float alpha;
         const float4 c = s_cop[j];
         if (!eval_step<MODE>(s_xyab[j], c, sx, sy, ek, alpha)) continue;
         const float tmp = __fmul_rn(t, __fsub_rn(1.0f, alpha));
         if (tmp < kStopThreshold) {
           done = true;
-          term = (int)(base - start) + j + 1;
+          term = (int)mbase + m;
           break;
         }
         const float4 col = STAGE_COLOR ? s_rgb[j] : __ldg(A.rgbr + s_id[j]);
@@ -247,6 +285,7 @@ __device__ __forceinline__ void pixelwise_tile(const RArgs& A, int tile, float4*
         ++contrib;
       }
     }
+    mbase += cmem;
   }
   if (inside) acc.finish(A, (size_t)py * A.W + px, t, contrib, term);
 }
@@ -259,10 +298,11 @@ __global__ void __launch_bounds__(BLOCK) k_render_pixelwise(RArgs A) {
   __shared__ float4 s_cop[CHUNK];
   __shared__ float4 s_rgb[STAGE_COLOR ? CHUNK : 1];
   __shared__ uint32_t s_id[STAGE_COLOR ? 1 : CHUNK];
+  __shared__ bool s_mem[CHUNK];
   __shared__ unsigned long long s_tab[32];
   load_tab(s_tab);
   __syncthreads();
-  pixelwise_tile<MODE, STAGE_COLOR, BLOCK>(A, blockIdx.x, s_xyab, s_cop, s_rgb, s_id, make_expk(s_tab));
+  pixelwise_tile<MODE, STAGE_COLOR, BLOCK>(A, blockIdx.x, s_xyab, s_cop, s_rgb, s_id, s_mem, make_expk(s_tab));
 }
 
 // Paper Alg. 1 (with the exit test fixed to >=).
@@ -282,7 +322,7 @@ __global__ void __launch_bounds__(BLOCK) k_render_dynamic(RArgs A) {
     __syncthreads();
     const int tile = s_tile;
     if (tile >= A.T) return;
-    pixelwise_tile<MODE, false, BLOCK>(A, tile, s_xyab, s_cop, nullptr, s_id, ek);
+    pixelwise_tile<MODE, false, BLOCK>(A, tile, s_xyab, s_cop, nullptr, s_id, nullptr, ek);
   }
 }
 
@@ -454,6 +494,10 @@ __device__ __forceinline__ void load_rec(const RArgs& A, uint32_t k, float4& a, 
   c = __ldg(A.cop + id);
   r = __ldg(A.rgbr + id);
 }
+template <int LM>
+__device__ __forceinline__ bool is_member(const RArgs& A, const float4& a, const float4& r, int tx, int ty) {
+  return LM == kListTile || tile_member(A, a.x, a.y, r.w, tx, ty);
+}
 
 // Conservative sub-tile cull: true only if alpha < 1/255 at every pixel centre
 // of [rx0,rx1]x[ry0,ry1].  alpha >= 1/255 needs power >= cut, i.e.
@@ -500,6 +544,8 @@ struct Donation {
   uint32_t pixel, start, from, end;
   float t;
   int32_t contrib;
+  uint32_t mpos;  // entries of the pixel's tile list before `from` (term positions)
+  uint32_t pad_;
   double acc[4];
 };
 
@@ -514,29 +560,31 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
 // `start`: 32 lanes on 32 consecutive entries, next group prefetched, serial-
 // exact decisions and render_reference weights (gw_group<MODE, true>).  The
 // colour partials come back warp-reduced in `part`.
-template <int MODE>
-__device__ __forceinline__ void gw_finish_pixel(const RArgs& A, uint32_t start, uint32_t from, uint32_t end,
-                                                float psx, float psy, const ExpK& ek, float& pt,
+template <int MODE, int LM>
+__device__ __forceinline__ void gw_finish_pixel(const RArgs& A, uint32_t from, uint32_t end, uint32_t mpos,
+                                                int tx, int ty, float psx, float psy, const ExpK& ek, float& pt,
                                                 int& pcnt, int& ptrm, Accum<MODE>& part) {
   const int lane = threadIdx.x & 31;
   float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nc = na, nr = na;
   if (from + lane < end) load_rec(A, from + lane, na, nc, nr);
   for (uint32_t g = from; g < end; g += 32) {
-    const bool active = g + lane < end;
     const float4 a = na, c = nc, r = nr;
+    const bool member = g + lane < end && is_member<LM>(A, a, r, tx, ty);
     if (g + 32 + lane < end) load_rec(A, g + 32 + lane, na, nc, nr);  // prefetch next group
     float alpha = 0.0f;
-    const bool ns = active && eval_step<MODE>(a, c, psx, psy, ek, alpha);
+    const bool ns = member && eval_step<MODE>(a, c, psx, psy, ek, alpha);
     const int stop = gw_group<MODE, true>(ns, alpha, r, c.w, pt, pcnt, part, lane);
+    const unsigned mm = __ballot_sync(kFull, member);
     if (stop < 32) {
-      ptrm = (int)(g - start) + stop + 1;
+      ptrm = (int)mpos + __popc(mm & ((2u << stop) - 1u));
       break;
     }
+    mpos += (uint32_t)__popc(mm);
   }
   part.warp_sum();
 }
 
-template <int MODE>
+template <int MODE, int LM>
 __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, float4 (*s)[32], int* s_k,
                                           const ExpK& ek) {
   const int lane = threadIdx.x & 31;
@@ -556,6 +604,7 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
   int contrib = 0, term = 0;
   Accum<MODE> acc;
   unsigned qpoll = 0;
+  uint32_t mpos = 0;  // entries of this tile's list before `base` (term positions)
 
   uint32_t base = start;
   float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pc = pa, pr = pa;
@@ -573,7 +622,8 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
         float pt = __shfl_sync(kFull, t, p);
         int pcnt = 0, ptrm = 0;
         Accum<MODE> part;
-        gw_finish_pixel<MODE>(A, start, base, end, psx, psy, ek, pt, pcnt, ptrm, part);
+        gw_finish_pixel<MODE, LM>(A, base, end, LM == kListTile ? base - start : mpos, tx, ty, psx, psy, ek, pt, pcnt,
+                                  ptrm, part);
         if (lane == p) {
           acc.merge(part);
           t = pt;
@@ -604,13 +654,16 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
         d.end = end;
         d.t = t;
         d.contrib = contrib;
+        d.mpos = LM == kListTile ? base - start : mpos;
         acc.store(d.acc);
         donated = true;
       }
       break;
     }
     // ---- pixel-wise batch of 32 entries: cull against the sub-tile, compact
-    const bool keep = base + lane < end && !cull_subtile(pa, pc, rx0, rx1, ry0, ry1);
+    const bool member = base + lane < end && is_member<LM>(A, pa, pr, tx, ty);
+    const unsigned mm = __ballot_sync(kFull, member);
+    const bool keep = member && !cull_subtile(pa, pc, rx0, rx1, ry0, ry1);
     const unsigned km = __ballot_sync(kFull, keep);
     if (keep) {
       const int pos = __popc(km & lanemask_lt());
@@ -623,7 +676,8 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
       } else {
         s[2][pos] = pr;
       }
-      s_k[pos] = (int)(base - start) + lane + 1;  // 1-based list position (term)
+      // 1-based position in the tile's list (term)
+      s_k[pos] = LM == kListTile ? (int)(base - start) + lane + 1 : (int)mpos + __popc(mm & lanemask_lt()) + 1;
     }
     __syncwarp();
     const uint32_t nb = base + 32;
@@ -656,12 +710,13 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
       ++contrib;
     }
     __syncwarp();
+    if (LM != kListTile) mpos += (uint32_t)__popc(mm);
     base = nb;
   }
   if (inside && !donated) acc.finish(A, (size_t)py * A.W + px, t, contrib, term);
 }
 
-template <int MODE>
+template <int MODE, int LM>
 __global__ void __launch_bounds__(kFineThreads, 4) k_render_fine(RArgs A, int subs) {
   __shared__ float4 s_rec[kFineWarps][4][32];
   __shared__ int s_k[kFineWarps][32];
@@ -678,7 +733,7 @@ __global__ void __launch_bounds__(kFineThreads, 4) k_render_fine(RArgs A, int su
     if (task >= A.total_tasks) return;
     const int q = task / subs;
     const int tile = A.task_order ? (int)A.task_order[q] : q;
-    warp_task<MODE>(A, tile, task - q * subs, s_rec[warp], s_k[warp], ek);
+    warp_task<MODE, LM>(A, tile, task - q * subs, s_rec[warp], s_k[warp], ek);
   }
 }
 
@@ -693,6 +748,7 @@ __global__ void __launch_bounds__(kFineThreads) k_render_donated(RArgs A) {
   __shared__ float4 s_xyab[kFineThreads];
   __shared__ float4 s_cop[kFineThreads];
   __shared__ float4 s_rgb[kFineThreads];
+  __shared__ bool s_mem[kFineThreads];
   __shared__ unsigned long long s_tab[32];
   __shared__ unsigned s_task;
   if (gated_out(A, BS_FINE_GRAINED_COMBINED)) return;
@@ -708,7 +764,10 @@ __global__ void __launch_bounds__(kFineThreads) k_render_donated(RArgs A) {
     if (task >= ntasks) return;
     const uint2 tr = A.donated_tasks[task];  // (first Donation, count <= kFineWarps)
     const Donation& d0 = A.donate[tr.x];
-    const uint32_t start = d0.start, from = d0.from, end = d0.end;
+    const uint32_t from = d0.from, end = d0.end;
+    // one task's pixels: one tile (membership of super-tile list entries)
+    const int ttx = (int)(d0.pixel % (uint32_t)A.W) / A.pw, tty = (int)(d0.pixel / (uint32_t)A.W) / A.ph;
+    uint32_t mpos = d0.mpos;
     {
       const bool active = (unsigned)warp < tr.y;  // warp-uniform
       const Donation* d = active ? &A.donate[tr.x + warp] : nullptr;
@@ -721,21 +780,27 @@ __global__ void __launch_bounds__(kFineThreads) k_render_donated(RArgs A) {
       Accum<MODE> part;
       for (uint32_t base = from; base < end; base += kFineThreads) {
         if (__syncthreads_count(!done) == 0) break;
-        if (base + tid < end) load_rec(A, base + tid, s_xyab[tid], s_cop[tid], s_rgb[tid]);
+        if (base + tid < end) {
+          load_rec(A, base + tid, s_xyab[tid], s_cop[tid], s_rgb[tid]);
+          s_mem[tid] = !A.sup || tile_member(A, s_xyab[tid].x, s_xyab[tid].y, s_rgb[tid].w, ttx, tty);
+        }
         __syncthreads();
         if (done) continue;
         const uint32_t n = min((uint32_t)kFineThreads, end - base);
         for (uint32_t g0 = 0; g0 < n; g0 += 32) {
           const uint32_t j = g0 + lane;
+          const bool member = j < n && s_mem[j];
+          const unsigned mm = __ballot_sync(kFull, member);
           float alpha = 0.0f;
-          const bool ns = j < n && eval_step<MODE>(s_xyab[j], s_cop[j], sx, sy, ek, alpha);
+          const bool ns = member && eval_step<MODE>(s_xyab[j], s_cop[j], sx, sy, ek, alpha);
           const int stop = gw_group<MODE, true>(ns, alpha, ns ? s_rgb[j] : make_float4(0.f, 0.f, 0.f, 0.f),
                                                ns ? s_cop[j].w : 0.0f, t, cnt, part, lane);
           if (stop < 32) {
-            trm = (int)(base - start + g0) + stop + 1;
+            trm = (int)mpos + __popc(mm & ((2u << stop) - 1u));
             done = true;
             break;
           }
+          mpos += (uint32_t)__popc(mm);
         }
       }
       if (active) {
@@ -829,7 +894,9 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
       int dev = 0, sms = 0, per_sm = 0;
       BS_CUDA_TRY(cudaGetDevice(&dev));
       BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_fine<MODE>, kFineThreads, 0));
+      const int lm = A.sup ? kListSuper : kListTile;
+      BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_fine<MODE, kListTile>, kFineThreads,
+                                                                0));
       // bs_render_set_fine_occupancy / BS_FINE_CTAS_PER_SM: fewer resident
       // CTAs leave SM room for another frame context's kernels
       const int cap = g_fine_ctas_per_sm > 0 ? g_fine_ctas_per_sm : env_int("BS_FINE_CTAS_PER_SM", per_sm);
@@ -844,7 +911,10 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
       if (!fine_donate_enabled()) B.donate = nullptr;
       B.donate_after = env_int("BS_FINE_DONATE_AFTER", kDonateAfter);
       B.donate_min_remain = env_int("BS_FINE_DONATE_MIN", kDonateMinRemain);
-      k_render_fine<MODE><<<grid, kFineThreads, 0, st>>>(B, subs);
+      if (lm == kListSuper)
+        k_render_fine<MODE, kListSuper><<<grid, kFineThreads, 0, st>>>(B, subs);
+      else
+        k_render_fine<MODE, kListTile><<<grid, kFineThreads, 0, st>>>(B, subs);
       BS_LAUNCH_CHECK();
       if (B.donate) {
         int per_sm2 = 0;
@@ -871,10 +941,12 @@ extern "C" size_t bs_render_workspace_bytes(int32_t width, int32_t height) {
   return 256 + sizeof(Donation) * P + sizeof(uint2) * (P / 4 + 1);  // >= 9 pixels -> <= 2 units per 9
 }
 
+static bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
 static int render_impl(int variant, const int32_t* gate, int alpha_mode, bs_splats g, const uint32_t* point_list,
                        const uint32_t* tile_ranges, const uint32_t* task_order, int32_t width, int32_t height,
                        int32_t pw, int32_t ph, const float bg[3], bs_frame_out out, void* ws, size_t ws_bytes,
-                       void* stream) {
+                       void* stream, bool sup = false) {
   if (width <= 0 || height <= 0 || pw <= 0 || ph <= 0 || !bg || !tile_ranges) return BS_ERR_INVALID_ARGUMENT;
   if (alpha_mode != BS_ALPHA_EXACT && alpha_mode != BS_ALPHA_FAST) return BS_ERR_INVALID_ARGUMENT;
   if (!out.color || !out.alpha || !out.depth || !out.final_t || !out.contrib || !out.term) return BS_ERR_INVALID_ARGUMENT;
@@ -901,6 +973,12 @@ static int render_impl(int variant, const int32_t* gate, int alpha_mode, bs_spla
   A.donated_tasks = reinterpret_cast<uint2*>(A.donate + (size_t)width * height);
   A.total_tasks = 0;
   A.gate = gate;
+  A.sup = sup ? 1 : 0;
+  A.rows = (height + ph - 1) / ph;
+  A.ipw = 1.0f / (float)pw;
+  A.iph = 1.0f / (float)ph;
+  if (sup && (!pow2(pw) || !pow2(ph))) return BS_ERR_UNSUPPORTED;
+  if (sup && !gate && variant != BS_FINE_GRAINED_COMBINED && variant != BS_SHARED_MEM_OPT) return BS_ERR_UNSUPPORTED;
   if (gate || variant == BS_DYNAMIC_BLOCKS || variant == BS_FINE_GRAINED_COMBINED)
     BS_CUDA_TRY(cudaMemsetAsync(ws, 0, 8 * sizeof(unsigned int), st));
   const int block_pixels = pw * ph;
@@ -932,6 +1010,47 @@ extern "C" int bs_render_forward_auto(const int32_t* variant_dev, int alpha_mode
   if (!variant_dev) return BS_ERR_INVALID_ARGUMENT;
   return render_impl(-1, variant_dev, alpha_mode, g, point_list, tile_ranges, task_order, width, height, pw, ph, bg,
                      out, ws, ws_bytes, stream);
+}
+
+// Super-tile lists (the frame pipeline's binning at 2pw x 2ph): the render
+// walks tile t's super-tile list and keeps the entries whose pw x ph
+// rectangle contains t — exactly t's list, in (depth, index) order, term
+// positions counted over it.  tile_ranges here holds, per pw x ph tile, the
+// range of its super-tile (bs_super_tile_ranges).  variant -1: the device
+// selector's choice among the candidates (FineGrainedCombined,
+// SharedMemOpt), as bs_render_forward_auto.
+extern "C" int bs_render_forward_super(int variant, const int32_t* variant_dev, int alpha_mode, bs_splats g,
+                                       const uint32_t* point_list, const uint32_t* tile_ranges,
+                                       const uint32_t* task_order, int32_t width, int32_t height, int32_t pw,
+                                       int32_t ph, const float bg[3], bs_frame_out out, void* ws, size_t ws_bytes,
+                                       void* stream) {
+  if (variant < 0 && !variant_dev) return BS_ERR_INVALID_ARGUMENT;
+  return render_impl(variant < 0 ? -1 : variant, variant < 0 ? variant_dev : nullptr, alpha_mode, g, point_list,
+                     tile_ranges, task_order, width, height, pw, ph, bg, out, ws, ws_bytes, stream, true);
+}
+
+namespace bs {
+__global__ void k_super_tile_ranges(const uint32_t* __restrict__ sranges, int cols, int rows, int scols,
+                                    uint32_t* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cols * rows) return;
+  const int st = ((t / cols) >> 1) * scols + ((t % cols) >> 1);
+  reinterpret_cast<uint2*>(out)[t] = reinterpret_cast<const uint2*>(sranges)[st];
+}
+}  // namespace bs
+
+// per pw x ph tile, the range of its 2pw x 2ph super-tile
+extern "C" int bs_super_tile_ranges(const uint32_t* super_ranges, int32_t width, int32_t height, int32_t pw,
+                                    int32_t ph, uint32_t* tile_ranges, void* stream) {
+  if (!super_ranges || !tile_ranges || width <= 0 || height <= 0 || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
+  const int cols = (width + pw - 1) / pw, rows = (height + ph - 1) / ph;
+  const int scols = (width + 2 * pw - 1) / (2 * pw);
+  const int T = cols * rows;
+  if (T > 0)
+    bs::k_super_tile_ranges<<<(T + 255) / 256, 256, 0, (cudaStream_t)stream>>>(super_ranges, cols, rows, scols,
+                                                                              tile_ranges);
+  BS_LAUNCH_CHECK();
+  return BS_OK;
 }
 
 namespace bs {

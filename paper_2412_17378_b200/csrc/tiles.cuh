@@ -45,6 +45,7 @@ __device__ __forceinline__ bool tile_rect(float x, float y, float radius, const 
 cudaError_t launch_project_bin(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, const bs_camera* cam_dev,
                                const Grid& g, float4* xyab, float4* cop, float4* rgbr, uint32_t* touched,
                                uint2* rects, uint32_t* dkeys, uint32_t* dvals, int* diff, size_t diff_bytes,
-                               bool smem_diff, int32_t* counts, cudaStream_t st);
+                               bool smem_diff, int32_t* counts, cudaStream_t st, const Grid* g2 = nullptr,
+                               int* diff2 = nullptr);
 
 }  // namespace bs

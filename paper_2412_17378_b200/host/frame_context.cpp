@@ -46,8 +46,17 @@ struct bs_context {
   int bin_key[4] = {0, 0, 0, 0};
   uint32_t* point_list = nullptr;
   int64_t pl_cap = 0;
-  uint32_t* ranges = nullptr;
+  uint32_t* ranges = nullptr;  // binning-grid ranges (the 2pw x 2ph super-tiles in super mode)
   int64_t ranges_cap = 0;
+  // super mode: pw x ph list lengths (stats, LPT order, selector, info) and
+  // the per-tile super-tile ranges the render walks
+  uint32_t* ranges16 = nullptr;
+  int64_t ranges16_cap = 0;
+  uint32_t* ranges_t = nullptr;
+  int64_t ranges_t_cap = 0;
+  void* aux_ws = nullptr;
+  size_t aux_ws_bytes = 0;
+  bool last_super = false;
   void* stats_ws = nullptr;
   size_t stats_ws_bytes = 0;
   uint32_t* order = nullptr;
@@ -235,7 +244,7 @@ extern "C" int bs_context_destroy(bs_context* c) {
   void* dev[] = {c->g3d, c->splat[0], c->splat[1], c->splat[2], c->n_visible, c->k_dev, c->pre_ws, c->bin_ws,
                  c->point_list, c->ranges, c->stats_ws, c->order, c->stats_dev, c->render_ws, c->planes[0],
                  c->planes[1], c->planes[2], c->planes[3], c->iplanes[0], c->iplanes[1], c->work_dev,
-                 c->variant_dev};
+                 c->variant_dev, c->ranges16, c->ranges_t, c->aux_ws};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (c->k_host) cudaFreeHost(c->k_host);
@@ -332,7 +341,31 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
       TRY(bs_preprocess(g3d_dev, n, cam, sp, c->n_visible, c->pre_ws, c->pre_ws_bytes, st));
   }
   mark(1);
+  // super mode (default with the fused pass, power-of-two patches, and a
+  // variant the super-list render supports): lists at 2pw x 2ph, the render
+  // keeps each tile's members (bs_render_forward_super); BS_NO_SUPER=1 off
+  static const bool super_env = [] {
+    const char* e = getenv("BS_NO_SUPER");
+    return !(e && *e == '1');
+  }();
+  auto pow2 = [](int v) { return v > 0 && (v & (v - 1)) == 0; };
+  // (small frames keep the pw x ph lists: below ~1 Mpixel their scatter is
+  // cheap and the longer super-tile walks cost more — C1 measured 10 % slower)
+  const bool super = fused && super_env && pow2(pw) && pow2(ph) && 2 * pw <= 65535 && 2 * ph <= 65535 &&
+                     int64_t(W) * H >= (int64_t(1) << 20) &&
+                     (variant < 0 || variant == BS_FINE_GRAINED_COMBINED || variant == BS_SHARED_MEM_OPT);
+  c->last_super = super;
+  const int32_t bpw = super ? 2 * pw : pw, bph = super ? 2 * ph : ph;  // the binning grid's patch
+  if (super) {
+    TRY(grow(&c->aux_ws, &c->aux_ws_bytes, bs_super_aux_bytes(W, H, pw, ph)));
+    TRY(grow_n(&c->ranges16, &c->ranges16_cap, 2 * T));
+    TRY(grow_n(&c->ranges_t, &c->ranges_t_cap, 2 * T));
+  }
   auto count = [&]() -> int {
+    if (super)
+      return bs_preprocess_bin_count_super(g3d_dev, n, cam_dev ? nullptr : cam, cam_dev, sp, c->n_visible, W, H, pw,
+                                           ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, c->ranges16, c->aux_ws,
+                                           c->aux_ws_bytes, st);
     if (fused)
       return bs_preprocess_bin_count(g3d_dev, n, cam_dev ? nullptr : cam, cam_dev, sp, c->n_visible, W, H, pw, ph,
                                      c->k_dev, c->bin_ws, c->bin_ws_bytes, st);
@@ -340,17 +373,17 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   };
 
   // P5 count (workspace keyed on n and the tile grid; k part grown below)
-  const int key[4] = {W, H, pw, ph};
+  const int key[4] = {W, H, bpw, bph};
   const bool same_grid = std::equal(key, key + 4, c->bin_key);
   if (!same_grid || n > c->bin_n || !c->bin_ws) {
     c->bin_n = std::max<int64_t>(n, c->bin_n);
     c->bin_k = std::max<int64_t>(c->bin_k, 0);
     std::copy(key, key + 4, c->bin_key);
-    TRY(grow(&c->bin_ws, &c->bin_ws_bytes, bs_bin_workspace_bytes(c->bin_n, W, H, pw, ph, c->bin_k)));
+    TRY(grow(&c->bin_ws, &c->bin_ws_bytes, bs_bin_workspace_bytes(c->bin_n, W, H, bpw, bph, c->bin_k)));
   }
   TRY(count());
   mark(2);
-  const bool async = allow_async && c->async_mode && bs_bin_async_supported(W, H, pw, ph);
+  const bool async = allow_async && c->async_mode && bs_bin_async_supported(W, H, bpw, bph);
   const int slot = capturing ? capture_slot : (async ? c->next_slot : 0);
   // K -> pinned host slot by a kernel store (a D2H memcpy would wait behind
   // any large download on the copy engine, e.g. the previous frame's planes)
@@ -367,7 +400,7 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
     mark(3);
     if (!c->point_list) TRY(grow_pl_async(c, std::max<int64_t>(n, 1) * 64, st));  // 64 tiles / splat to start
     TRY(grow_n(&c->ranges, &c->ranges_cap, 2 * T));
-    TRY(bs_bin_sort_async(sp, n, c->n_visible, W, H, pw, ph, std::min<int64_t>(c->pl_cap, (int64_t(1) << 30) - 1),
+    TRY(bs_bin_sort_async(sp, n, c->n_visible, W, H, bpw, bph, std::min<int64_t>(c->pl_cap, (int64_t(1) << 30) - 1),
                           c->point_list, c->ranges, c->bin_ws, c->bin_ws_bytes, st));
     if (!capturing) {
     bs_context::Pending& q = c->pending[c->n_pending++];
@@ -386,12 +419,12 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   } else {
     CUTRY(cudaStreamSynchronize(st));
     const int64_t k = c->k_host[1];
-    if (k > c->bin_k && bs_bin_workspace_bytes(c->bin_n, W, H, pw, ph, k) > c->bin_ws_bytes) {
+    if (k > c->bin_k && bs_bin_workspace_bytes(c->bin_n, W, H, bpw, bph, k) > c->bin_ws_bytes) {
       // the count state lives in the workspace: grow, then count again
       c->bin_k = int64_t(double(k) * 1.25) + 1024;
       void* fresh = nullptr;
       size_t fresh_bytes = 0;
-      TRY(grow(&fresh, &fresh_bytes, bs_bin_workspace_bytes(c->bin_n, W, H, pw, ph, c->bin_k)));
+      TRY(grow(&fresh, &fresh_bytes, bs_bin_workspace_bytes(c->bin_n, W, H, bpw, bph, c->bin_k)));
       if (c->bin_ws) cudaFree(c->bin_ws);
       c->bin_ws = fresh;
       c->bin_ws_bytes = fresh_bytes;
@@ -400,7 +433,8 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
     mark(3);
     if (k > c->pl_cap) TRY(grow_pl_async(c, int64_t(double(std::max<int64_t>(k, 1)) * 1.25), st));
     TRY(grow_n(&c->ranges, &c->ranges_cap, 2 * T));
-    TRY(bs_bin_sort(sp, n, c->n_visible, W, H, pw, ph, k, c->point_list, c->ranges, c->bin_ws, c->bin_ws_bytes, st));
+    TRY(bs_bin_sort(sp, n, c->n_visible, W, H, bpw, bph, k, c->point_list, c->ranges, c->bin_ws, c->bin_ws_bytes,
+                    st));
     c->last_k = k;
   }
   mark(4);
@@ -408,10 +442,11 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   // P6 + selection
   TRY(grow(&c->stats_ws, &c->stats_ws_bytes, bs_tile_stats_workspace_bytes(int32_t(T))));
   TRY(grow_n(&c->order, &c->order_cap, T));
+  const uint32_t* tranges = super ? c->ranges16 : c->ranges;  // pw x ph list lengths
   if (T <= 32768)  // LPT order at eighth-octave granularity + the selector's inputs, one launch
-    TRY(bs_tile_order(c->ranges, int32_t(T), c->stats_dev, c->order, st));
+    TRY(bs_tile_order(tranges, int32_t(T), c->stats_dev, c->order, st));
   else
-    TRY(bs_tile_stats(c->ranges, int32_t(T), c->stats_dev, nullptr, c->order, c->stats_ws, c->stats_ws_bytes, st));
+    TRY(bs_tile_stats(tranges, int32_t(T), c->stats_dev, nullptr, c->order, c->stats_ws, c->stats_ws_bytes, st));
   if (variant < 0) TRY(bs_select_variant_device(c->stats_dev, W, H, pw, ph, c->sm_count, c->variant_dev, st));
   mark(5);
 
@@ -436,7 +471,11 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
     fo = bs_frame_out{c->planes[0], c->planes[1], c->planes[2], c->planes[3], c->iplanes[0], c->iplanes[1]};
   }
   TRY(grow(&c->render_ws, &c->render_ws_bytes, bs_render_workspace_bytes(W, H)));
-  if (variant < 0)
+  if (super) {
+    TRY(bs_super_tile_ranges(c->ranges, W, H, pw, ph, c->ranges_t, st));
+    TRY(bs_render_forward_super(variant, c->variant_dev, c->alpha_mode, sp, c->point_list, c->ranges_t, c->order, W,
+                                H, pw, ph, bg, fo, c->render_ws, c->render_ws_bytes, st));
+  } else if (variant < 0)
     TRY(bs_render_forward_auto(c->variant_dev, c->alpha_mode, sp, c->point_list, c->ranges, c->order, W, H, pw, ph,
                                bg, fo, c->render_ws, c->render_ws_bytes, st));
   else
@@ -522,11 +561,12 @@ int verify_pending(bs_context* c, cudaStream_t st, int keep = 0) {
 int fill_info(bs_context* c, cudaStream_t st, bs_frame_info* info) {
   TRY(verify_pending(c, st));
   if (!c->last_out.term) return BS_ERR_INVALID_ARGUMENT;
-  TRY(bs_frame_work(c->last_out.term, c->last_out.contrib, c->ranges, c->last_W, c->last_H, c->last_pw, c->last_ph,
+  const uint32_t* tranges = c->last_super ? c->ranges16 : c->ranges;  // pw x ph list lengths
+  TRY(bs_frame_work(c->last_out.term, c->last_out.contrib, tranges, c->last_W, c->last_H, c->last_pw, c->last_ph,
                     c->work_dev, st));
   // full tile_load_histogram (order statistics too) on request only
   const int32_t T = int32_t(((c->last_W + c->last_pw - 1) / c->last_pw) * ((c->last_H + c->last_ph - 1) / c->last_ph));
-  TRY(bs_tile_stats(c->ranges, T, c->stats_dev, nullptr, nullptr, c->stats_ws, c->stats_ws_bytes, st));
+  TRY(bs_tile_stats(tranges, T, c->stats_dev, nullptr, nullptr, c->stats_ws, c->stats_ws_bytes, st));
   CUTRY(cudaMemcpyAsync(c->stats_host, c->stats_dev, sizeof(bs_tile_histogram), cudaMemcpyDeviceToHost, st));
   CUTRY(cudaMemcpyAsync(c->work_host, c->work_dev, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   if (c->last_variant < 0)
@@ -538,7 +578,7 @@ int fill_info(bs_context* c, cudaStream_t st, bs_frame_info* info) {
   nv = c->variant_host[1];
   info->variant = c->last_variant < 0 ? c->variant_host[0] : c->last_variant;
   info->n_visible = nv;
-  info->k = c->last_k;
+  info->k = c->last_super ? int64_t(c->stats_host->total) : c->last_k;  // pw x ph instances (not super-tile ones)
   info->stats = *c->stats_host;
   info->evaluated = c->work_host[0];
   info->committed = c->work_host[1];
@@ -860,5 +900,13 @@ extern "C" int bs_render_views(bs_context* const* ctxs, int32_t nctx, const bs_g
 extern "C" int bs_context_frame(bs_context* c, bs_frame_out* out) {
   if (!c || !out) return BS_ERR_INVALID_ARGUMENT;
   *out = bs_frame_out{c->planes[0], c->planes[1], c->planes[2], c->planes[3], c->iplanes[0], c->iplanes[1]};
+  return BS_OK;
+}
+
+// 1 when the context's last frame used super-tile lists (2pw x 2ph binning,
+// bs_render_forward_super), 0 for pw x ph lists.
+extern "C" int bs_context_list_mode(bs_context* c, int32_t* super_lists) {
+  if (!c || !super_lists) return BS_ERR_INVALID_ARGUMENT;
+  *super_lists = c->last_super ? 1 : 0;
   return BS_OK;
 }

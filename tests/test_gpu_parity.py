@@ -160,6 +160,63 @@ def test_fused_project_bin_matches_reference(W, H, f, n, bgfrac):
     assert api.splats_to_g2d(sv).tobytes() == g2d.tobytes()
 
 
+@pytest.mark.parametrize("W,H,pw,ph,n", [(250, 130, 16, 16, 5000), (960, 540, 16, 16, 60000), (200, 120, 8, 8, 3000),
+                                         (300, 170, 16, 8, 8000)])
+@pytest.mark.parametrize("variant", [3, 4])
+def test_super_tile_lists_render_exact(W, H, pw, ph, n, variant):
+    """The frame pipeline's super-tile path through the C-ABI: projection +
+    counting at 2pw x 2ph (bs_preprocess_bin_count_super), lists sorted at
+    2pw x 2ph, per-tile super ranges, and bs_render_forward_super keeping each
+    tile's members — equal to the oracle's render of the pw x ph lists
+    (contrib / term / T exact; the pw x ph lengths equal bin_tiles')."""
+    g3d, cam = scene(n, W, H, float(W), bgfrac=0.3)
+    g2d = O.project_all(g3d, cam)
+    pl, rg = O.bin_tiles(g2d, W, H, pw, ph)
+    bg = (0.1, 0.2, 0.3)
+    ref = O.render(variant, pl, rg, g2d, W, H, pw, ph, bg, lazy=True, threads=0)
+    d = api.g3d_to_device(g3d)
+    s = api.DeviceSplats.empty(n, DEV)
+    counts = torch.zeros(2, dtype=torch.int32, device=DEV)
+    b = api.Binner(W, H, 2 * pw, 2 * ph, DEV)
+    T = ((W + pw - 1) // pw) * ((H + ph - 1) // ph)
+    r16 = torch.empty(2 * T, dtype=torch.int32, device=DEV)
+    aux = torch.empty(N.lib().bs_super_aux_bytes(W, H, pw, ph), dtype=torch.uint8, device=DEV)
+    c = ncam(cam)
+    st = api._stream(DEV)
+
+    def count():
+        N.call("bs_preprocess_bin_count_super", d.data_ptr(), n, C.byref(c), None, s.c(), counts.data_ptr(), W, H, pw,
+               ph, b.k_dev.data_ptr(), b.ws.data_ptr(), b.ws.numel(), r16.data_ptr(), aux.data_ptr(), aux.numel(), st)
+
+    b._ensure_ws(n, 0)
+    count()
+    k = b.read_k()
+    b._ensure_ws(n, int(k * 1.25) + 1024)
+    count()
+    pl2 = torch.empty(max(k, 1), dtype=torch.int32, device=DEV)
+    N.call("bs_bin_sort", s.c(), n, counts.data_ptr(), W, H, 2 * pw, 2 * ph, k, pl2.data_ptr(),
+           b.tile_ranges.data_ptr(), b.ws.data_ptr(), b.ws.numel(), st)
+    lens = r16.cpu().numpy().view(np.uint32)
+    assert np.array_equal(lens[1::2] - lens[0::2], rg[1::2] - rg[0::2])  # pw x ph list lengths
+    rt = torch.empty(2 * T, dtype=torch.int32, device=DEV)
+    N.call("bs_super_tile_ranges", b.tile_ranges.data_ptr(), W, H, pw, ph, rt.data_ptr(), st)
+    frame = api.DeviceFrame.empty(W, H, DEV)
+    ws = torch.zeros(N.lib().bs_render_workspace_bytes(W, H), dtype=torch.uint8, device=DEV)
+    bgc = (C.c_float * 3)(*bg)
+    N.call("bs_render_forward_super", variant, None, N.ALPHA_EXACT, s.c(), pl2.data_ptr(), rt.data_ptr(), None, W, H,
+           pw, ph, bgc, frame.c(), ws.data_ptr(), ws.numel(), st)
+    torch.cuda.synchronize()
+    got = frame.to_numpy()
+    for key in ("contrib", "term"):
+        assert np.array_equal(got[key], ref[key]), key
+    for key in ("final_t", "alpha"):
+        assert np.array_equal(got[key].view(np.uint32), ref[key].view(np.uint32)), key
+    if variant == 4:  # SharedMemOpt: serial double sums, bit-exact
+        assert np.array_equal(got["color"].view(np.uint32), ref["color"].view(np.uint32))
+    else:
+        assert np.max(np.abs(got["color"] - ref["color"])) <= 1e-6
+
+
 def test_binning_radix_path_bit_exact():
     """BS_BIN_RADIX=1 (expand + stable tile radix sort) stays bit-exact too."""
     import os
@@ -440,10 +497,12 @@ def test_frame_pipeline_async_overflow_rerun():
     frames need no re-render."""
     W = H = 512
     n = 300
-    g3d, cam = scene(n, W, H, 2048.0, bgfrac=1.0)
+    g3d, cam = scene(n, W, H, 4096.0, bgfrac=1.0)
     g2d = O.project_all(g3d, cam)
     pl, rg = O.bin_tiles(g2d, W, H, 16, 16)
-    assert len(pl) > 64 * n  # the initial capacity overflows
+    # the initial capacity overflows, with 16x16 lists and with the frame
+    # pipeline's 32x32 super-tile lists alike
+    assert len(pl) > 64 * n and len(O.bin_tiles(g2d, W, H, 32, 32)[0]) > 64 * n
     fp = api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT, async_mode=True)
     d = api.g3d_to_device(g3d)
     fp.forward(d, n, ncam(cam), variant=BS_FG, bg=(0.1, 0.2, 0.3))
@@ -631,6 +690,38 @@ def test_render_views_batch_matches():
     assert sum(q.graph_launches() for q in fps) > 0
     for q in fps:
         q.close()
+
+
+def test_frame_pipeline_super_lists_match_tile_lists():
+    """Frames >= 1 Mpixel take the super-tile path (lists at 32x32, members
+    kept per 16x16 tile); with graphs and async frames they equal the
+    stage-by-stage pipeline on 16x16 lists."""
+    import bench
+    W, H, f, n = 1280, 832, 700.0, 150_000
+    cams = [N.make_camera(bench.orbit_view(k * 13), (f, f), W, H) for k in range(5)]
+    g3d = api.gen_clustered_scene(n, cams[0])
+    d = api.g3d_to_device(g3d)
+    pipe = api.Pipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT)
+    ref = []
+    for cam in cams:
+        fr, _ = pipe.forward(d, n, cam, variant=BS_FG)
+        torch.cuda.synchronize()
+        ref.append(fr.to_numpy())
+    fp = api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT, async_mode=True, graphs=True)
+    for i, cam in enumerate(cams):
+        fp.forward(d, n, cam, variant=BS_FG)
+        fp.sync()
+        got = fp.frame.to_numpy()
+        for k in ("contrib", "term"):
+            assert np.array_equal(got[k], ref[i][k]), (i, k)
+        for k in ("final_t", "alpha"):
+            assert np.array_equal(got[k].view(np.uint32), ref[i][k].view(np.uint32)), (i, k)
+        assert np.max(np.abs(got["color"] - ref[i]["color"])) <= 1e-6
+        assert np.max(np.abs(got["depth"] - ref[i]["depth"]) / np.maximum(1, np.abs(ref[i]["depth"]))) <= 1e-6
+    _, fi = fp.forward(d, n, cams[0], variant=BS_FG, info=True)
+    pipe.forward(d, n, cams[0], variant=BS_FG)
+    assert fi.k == pipe.last_binning.k  # info reports the 16x16 instance count
+    fp.close()
 
 
 def test_host_async_pipeline_matches():

@@ -14,6 +14,10 @@ for c in c1 c4; do
   [ -f "$IN/render_fine_full_$c.ncu-rep" ] && \
     python tools/ncu_summary.py "$IN/render_fine_full_$c.ncu-rep" > $P/r1_ncu_full_render_fine_exact_$c.txt
 done
+for c in c2 c4; do
+  [ -f "$IN/render_fine_super_$c.ncu-rep" ] && \
+    python tools/ncu_summary.py "$IN/render_fine_super_$c.ncu-rep" > $P/r1_ncu_full_render_fine_super_$c.txt
+done
 python tools/ncu_traffic.py $P > $P/ncu_traffic.json
 python tools/ncu_summary.py "$IN/chunk_scatter_full.ncu-rep" > $P/r1_ncu_chunk_scatter.txt
 cp "$IN/c3_sweep.jsonl" $P/r1_c3_sweep.jsonl

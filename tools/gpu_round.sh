@@ -19,6 +19,11 @@ timeout 900 python bench.py --config c4 --steps 20 --warmup 3 --no-cpu-baseline 
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > "$OUT/bench_reference.json" 2>> "$OUT/bench.err"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" \
   python bench.py --steps 2 --warmup 4 --no-extras > "$OUT/launches_bench.log" 2>&1
+for c in c2 c4; do  # the frame pipeline's render (super-tile lists at >= 1 Mpixel)
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_render_fine -c 1 \
+    -o "$OUT/render_fine_super_$c" -f python tools/profile_render.py --config $c --variant FineGrainedCombined \
+    --alpha exact --reps 1 --frame-pipeline > "$OUT/ncu_super_$c.log" 2>&1
+done
 for c in c2 c1 c4; do
   sfx=$([ $c = c2 ] && echo "" || echo "_$c")
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_render_fine -c 1 \

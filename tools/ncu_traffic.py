@@ -22,11 +22,14 @@ def dram_bytes(path):
 
 d = sys.argv[1]
 out = {}
-for cfg, name in (("c2", "r1_ncu_full_render_fine_exact.txt"), ("c1", "r1_ncu_full_render_fine_exact_c1.txt"),
-                  ("c4", "r1_ncu_full_render_fine_exact_c4.txt")):
+for key, name in (("c2", "r1_ncu_full_render_fine_exact.txt"), ("c1", "r1_ncu_full_render_fine_exact_c1.txt"),
+                  ("c4", "r1_ncu_full_render_fine_exact_c4.txt"),
+                  ("c2_super", "r1_ncu_full_render_fine_super_c2.txt"),
+                  ("c4_super", "r1_ncu_full_render_fine_super_c4.txt")):
     p = os.path.join(d, name)
     if os.path.exists(p):
-        out[f"{cfg}_FineGrainedCombined_exact"] = dram_bytes(p)
-        out[f"_source_{cfg}"] = (f"profiles/{name}: dram__bytes_read.sum + dram__bytes_write.sum, one {cfg} launch "
+        cfg, _, sup = key.partition("_")
+        out[f"{cfg}_FineGrainedCombined_exact" + ("_super" if sup else "")] = dram_bytes(p)
+        out[f"_source_{key}"] = (f"profiles/{name}: dram__bytes_read.sum + dram__bytes_write.sum, one {cfg} launch "
                                  "of bench's first view (ncu --set full, cold cache)")
 print(json.dumps(out, indent=1))

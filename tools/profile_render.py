@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--f", type=float, default=1000.0)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--config", default=None, help="c1/c2/c4: bench.py's scene and first view (overrides n/W/H/f/sigma)")
+    ap.add_argument("--frame-pipeline", action="store_true",
+                    help="render through the frame pipeline (super-tile lists on >= 1 Mpixel frames)")
     a = ap.parse_args()
     if a.config:
         import bench
@@ -38,11 +40,17 @@ def main():
         g3d = api.gen_clustered_scene(a.n, cam, cluster_sigma=a.sigma)
     g3d["opacity"] *= a.opacity_scale
     mode = 0 if a.alpha == "exact" else 1
-    pipe = api.Pipeline(a.W, a.H, 16, 16, "cuda", mode)
     d = api.g3d_to_device(g3d)
     v = api.variant_from_name(a.variant)
-    for _ in range(a.reps):
-        pipe.forward(d, a.n, cam, variant=v)
+    if a.frame_pipeline:
+        fp = api.FramePipeline(a.W, a.H, 16, 16, "cuda", mode)
+        for _ in range(a.reps):
+            fp.forward(d, a.n, cam, variant=v)
+        fp.sync()
+    else:
+        pipe = api.Pipeline(a.W, a.H, 16, 16, "cuda", mode)
+        for _ in range(a.reps):
+            pipe.forward(d, a.n, cam, variant=v)
     torch.cuda.synchronize()
 
 
