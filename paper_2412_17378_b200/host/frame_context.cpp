@@ -442,7 +442,14 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   // P6 + selection
   TRY(grow(&c->stats_ws, &c->stats_ws_bytes, bs_tile_stats_workspace_bytes(int32_t(T))));
   TRY(grow_n(&c->order, &c->order_cap, T));
-  const uint32_t* tranges = super ? c->ranges16 : c->ranges;  // pw x ph list lengths
+  // LPT order by the lengths the render walks: in super mode each tile walks
+  // its super-tile's list (BS_SUPER_LPT16=1: order by the pw x ph lengths)
+  static const bool lpt16 = [] {
+    const char* e = getenv("BS_SUPER_LPT16");
+    return e && *e == '1';
+  }();
+  if (super) TRY(bs_super_tile_ranges(c->ranges, W, H, pw, ph, c->ranges_t, st));
+  const uint32_t* tranges = super ? (lpt16 ? c->ranges16 : c->ranges_t) : c->ranges;
   if (T <= 32768)  // LPT order at eighth-octave granularity + the selector's inputs, one launch
     TRY(bs_tile_order(tranges, int32_t(T), c->stats_dev, c->order, st));
   else
@@ -472,7 +479,6 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   }
   TRY(grow(&c->render_ws, &c->render_ws_bytes, bs_render_workspace_bytes(W, H)));
   if (super) {
-    TRY(bs_super_tile_ranges(c->ranges, W, H, pw, ph, c->ranges_t, st));
     TRY(bs_render_forward_super(variant, c->variant_dev, c->alpha_mode, sp, c->point_list, c->ranges_t, c->order, W,
                                 H, pw, ph, bg, fo, c->render_ws, c->render_ws_bytes, st));
   } else if (variant < 0)
