@@ -71,6 +71,7 @@ struct RArgs {
   // list iff its S8 rectangle at pw x ph contains t (tile_member)
   int sup, rows;
   float ipw, iph;  // 1/pw, 1/ph (exact: power-of-two patches only)
+  int stragglers;  // live pixels at or below which a warp task finishes Gaussian-wise
 };
 
 // Is tile (tx, ty) inside the splat's S8 rectangle at the pw x ph grid
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(kFgThreads) k_render_gaussianwise(RArgs A) {
 // and depth to double-sum association (serial weights in the straggler path).
 constexpr int kFineWarps = 8;
 constexpr int kFineThreads = kFineWarps * 32;
-constexpr int kStragglers = 8;
+constexpr int kStragglers = 2;  // (8 measured 4 % slower on C2 16x16 lists, 16 % on super-tile lists)
 constexpr int kDonateAfter = 512;       // list entries a task walks before it may hand off
 constexpr int kDonateMinRemain = 1024;  // ... and only if this many entries remain
 constexpr int kStragglerMinRemain = 64;
@@ -612,7 +613,7 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
   while (base < end) {
     const unsigned live = __ballot_sync(kFull, !done);
     if (!live) break;
-    if (__popc(live) <= kStragglers && end - base >= (uint32_t)kStragglerMinRemain) {
+    if (__popc(live) <= A.stragglers && end - base >= (uint32_t)kStragglerMinRemain) {
       // ---- straggler mode: finish each live pixel Gaussian-wise from `base`
       unsigned rem = live;
       while (rem) {
@@ -911,6 +912,7 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
       if (!fine_donate_enabled()) B.donate = nullptr;
       B.donate_after = env_int("BS_FINE_DONATE_AFTER", kDonateAfter);
       B.donate_min_remain = env_int("BS_FINE_DONATE_MIN", kDonateMinRemain);
+      B.stragglers = env_int(A.sup ? "BS_FINE_STRAGGLERS_SUPER" : "BS_FINE_STRAGGLERS", kStragglers);
       if (lm == kListSuper)
         k_render_fine<MODE, kListSuper><<<grid, kFineThreads, 0, st>>>(B, subs);
       else
