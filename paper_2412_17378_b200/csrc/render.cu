@@ -91,6 +91,35 @@ __device__ __forceinline__ bool tile_member(const RArgs& A, float x, float y, fl
   return tx0 <= tx && tx <= tx1 && ty0 <= ty && ty <= ty1;
 }
 
+// The same test on the fast path.  An entry of tile t's super-tile list
+// already satisfies tile_member on one side of each axis: for an even tile
+// column (t is its super-tile's left column) the splat's right edge reaches
+// t, so t is a member unless the left edge tx0 == tx + 1; for an odd column
+// unless the right edge tx1 == tx - 1 (the clamps cannot produce those
+// values).  floor(v) == k is k <= v < k + 1, so one product and two compares
+// per axis decide it.  Exact whenever every edge / pw stays in int range —
+// guaranteed for ceil(radius) < 1e9 (else the full test).
+struct TileSide {
+  float xl, yl;  // tx + 1 or tx - 1, ty + 1 or ty - 1
+  bool qx, qy;   // odd column / row inside the super-tile
+};
+__device__ __forceinline__ TileSide tile_side(int tx, int ty) {
+  TileSide m;
+  m.qx = tx & 1;
+  m.qy = ty & 1;
+  m.xl = (float)(m.qx ? tx - 1 : tx + 1);
+  m.yl = (float)(m.qy ? ty - 1 : ty + 1);
+  return m;
+}
+__device__ __forceinline__ bool tile_member_fast(const RArgs& A, const TileSide& m, float x, float y, float radius,
+                                                 int tx, int ty) {
+  const float rr = ceilf(radius);
+  if (!(rr < 1e9f)) return tile_member(A, x, y, radius, tx, ty);
+  const float xv = __fmul_rn(m.qx ? __fadd_rn(x, rr) : __fsub_rn(x, rr), A.ipw);
+  const float yv = __fmul_rn(m.qy ? __fadd_rn(y, rr) : __fsub_rn(y, rr), A.iph);
+  return !(xv >= m.xl && xv < m.xl + 1.0f) && !(yv >= m.yl && yv < m.yl + 1.0f);
+}
+
 // FineGrainedCombined list mode: pw x ph lists, or super-tile lists
 // filtered by tile_member (a template parameter: the pw x ph kernel keeps
 // its register budget)
@@ -260,7 +289,7 @@ __device__ __forceinline__ void pixelwise_tile(const RArgs& A, int tile, float4*
       else s_id[tid] = id;
       mem = true;
       if (A.sup) {
-        mem = tile_member(A, s_xyab[tid].x, s_xyab[tid].y, __ldg(&A.rgbr[id].w), tx, ty);
+        mem = tile_member_fast(A, tile_side(tx, ty), s_xyab[tid].x, s_xyab[tid].y, __ldg(&A.rgbr[id].w), tx, ty);
         s_mem[tid] = mem;
       }
     }
@@ -497,7 +526,9 @@ __device__ __forceinline__ void load_rec(const RArgs& A, uint32_t k, float4& a, 
 }
 template <int LM>
 __device__ __forceinline__ bool is_member(const RArgs& A, const float4& a, const float4& r, int tx, int ty) {
-  return LM == kListTile || tile_member(A, a.x, a.y, r.w, tx, ty);
+  // (the side is recomputed per call: holding it costs registers the
+  // 64-register budget does not have)
+  return LM == kListTile || tile_member_fast(A, tile_side(tx, ty), a.x, a.y, r.w, tx, ty);
 }
 
 // Conservative sub-tile cull: true only if alpha < 1/255 at every pixel centre
@@ -783,7 +814,8 @@ __global__ void __launch_bounds__(kFineThreads) k_render_donated(RArgs A) {
         if (__syncthreads_count(!done) == 0) break;
         if (base + tid < end) {
           load_rec(A, base + tid, s_xyab[tid], s_cop[tid], s_rgb[tid]);
-          s_mem[tid] = !A.sup || tile_member(A, s_xyab[tid].x, s_xyab[tid].y, s_rgb[tid].w, ttx, tty);
+          s_mem[tid] = !A.sup || tile_member_fast(A, tile_side(ttx, tty), s_xyab[tid].x, s_xyab[tid].y, s_rgb[tid].w,
+                                                  ttx, tty);
         }
         __syncthreads();
         if (done) continue;

@@ -217,6 +217,50 @@ def test_super_tile_lists_render_exact(W, H, pw, ph, n, variant):
         assert np.max(np.abs(got["color"] - ref["color"])) <= 1e-6
 
 
+@pytest.mark.parametrize("W,H", [(250, 130), (96, 80)])
+def test_super_tile_membership_crafted(W, H):
+    """bs_render_forward_super on crafted splats: lists binned at 32x32 from
+    the same splats (bs_bin_count / bs_bin_sort at 2pw x 2ph), members kept by
+    the 16x16 rectangle test — including splats whose rectangle edges sit on
+    every parity of the super-tile grid and huge radii (the fast test's
+    fallback at ceil(radius) >= 1e9, and edges beyond int range)."""
+    rng = np.random.default_rng(7)
+    m = 3000
+    g = np.zeros(m, dtype=O.G2D_DTYPE)
+    g["x"] = rng.uniform(-40, W + 40, m)
+    g["y"] = rng.uniform(-40, H + 40, m)
+    g["radius"] = np.where(rng.uniform(size=m) < 0.5, rng.integers(1, 40, m) - 0.5, rng.uniform(0.1, 60, m))
+    g["radius"][:6] = [1e8, 3e9, 5e10, 2.5e9, 1e12, 7.0]
+    g["x"][:6] = [10.0, -1e9, 50.0, W / 2, -3e11, 15.9]
+    g["conic_a"] = rng.uniform(0.001, 0.05, m)
+    g["conic_c"] = rng.uniform(0.001, 0.05, m)
+    g["conic_b"] = rng.uniform(-0.0005, 0.0005, m)
+    g["opacity"] = rng.uniform(0.05, 0.9, m)
+    g["color"] = rng.uniform(0, 1, (m, 3))
+    g["depth"] = rng.uniform(1, 10, m)
+    pl, rg = O.bin_tiles(g, W, H, 16, 16)
+    bg = (0.1, 0.2, 0.3)
+    s = to_dev_splats(g)
+    b2 = api.bin_tiles(s, W, H, 32, 32)
+    T = ((W + 15) // 16) * ((H + 15) // 16)
+    rt = torch.empty(2 * T, dtype=torch.int32, device=DEV)
+    st = api._stream(DEV)
+    N.call("bs_super_tile_ranges", b2.tile_ranges.data_ptr(), W, H, 16, 16, rt.data_ptr(), st)
+    bgc = (C.c_float * 3)(*bg)
+    for variant in (3, 4):
+        ref = O.render(variant, pl, rg, g, W, H, 16, 16, bg, lazy=True, threads=0)
+        frame = api.DeviceFrame.empty(W, H, DEV)
+        ws = torch.zeros(N.lib().bs_render_workspace_bytes(W, H), dtype=torch.uint8, device=DEV)
+        N.call("bs_render_forward_super", variant, None, N.ALPHA_EXACT, s.c(), b2.point_list.data_ptr(),
+               rt.data_ptr(), None, W, H, 16, 16, bgc, frame.c(), ws.data_ptr(), ws.numel(), st)
+        torch.cuda.synchronize()
+        got = frame.to_numpy()
+        for key in ("contrib", "term"):
+            assert np.array_equal(got[key], ref[key]), (variant, key)
+        assert np.array_equal(got["final_t"].view(np.uint32), ref["final_t"].view(np.uint32)), variant
+        assert np.max(np.abs(got["color"] - ref["color"])) <= 1e-6
+
+
 def test_binning_radix_path_bit_exact():
     """BS_BIN_RADIX=1 (expand + stable tile radix sort) stays bit-exact too."""
     import os
