@@ -641,6 +641,9 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
   uint32_t base = start;
   float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pc = pa, pr = pa;
   if (base + lane < end) load_rec(A, base + lane, pa, pc, pr);
+  // the ids run one batch further ahead than the records: the record loads
+  // of the next batch then depend on no in-flight load
+  uint32_t nid = base + 32 + lane < end ? __ldg(A.point_list + base + 32 + lane) : 0u;
   while (base < end) {
     const unsigned live = __ballot_sync(kFull, !done);
     if (!live) break;
@@ -713,7 +716,12 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
     }
     __syncwarp();
     const uint32_t nb = base + 32;
-    if (nb + lane < end) load_rec(A, nb + lane, pa, pc, pr);
+    if (nb + lane < end) {
+      pa = __ldg(A.xyab + nid);
+      pc = __ldg(A.cop + nid);
+      pr = __ldg(A.rgbr + nid);
+    }
+    nid = nb + 32 + lane < end ? __ldg(A.point_list + nb + 32 + lane) : 0u;
     // queue poll every 8th batch; the value is consumed 8 batches later, so
     // the L2 round trip never stalls the blend loop
     const bool poll_point = A.donate && ((nb - start) & (8u * 32u - 1u)) == 0;
