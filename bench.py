@@ -186,7 +186,8 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def cpu_sample_estimate(g3d, cam_o, g2d, pl, ranges, W, H, pw, ph, threads: int, budget_s: float, seed: int = 0):
+def cpu_sample_estimate(g3d, cam_o, g2d, pl, ranges, W, H, pw, ph, threads: int, budget_s: float, seed: int = 0,
+                        bin_cache: dict | None = None, ideal_threads: bool = False):
     """Time the CPU oracle (the reference's algorithm, restated) on bounded
     samples of one frame and extrapolate to the full frame:
       project_all on 1/8 of the Gaussians      x8 (linear)
@@ -199,20 +200,28 @@ def cpu_sample_estimate(g3d, cam_o, g2d, pl, ranges, W, H, pw, ph, threads: int,
 
     rng = np.random.default_rng(seed)
     n = len(g3d)
-    sub = np.sort(rng.choice(n, size=max(1, n // 8), replace=False))
+    div = 8
+    sub = np.sort(rng.choice(n, size=max(1, n // div), replace=False))
     g3s = np.ascontiguousarray(g3d[sub])
     t0 = time.perf_counter()
     O.project_all(g3s, cam_o)
     t_proj = (time.perf_counter() - t0) * (n / len(sub))
 
     m = len(g2d)
-    sub2 = np.sort(rng.choice(m, size=max(1, m // 8), replace=False))
-    g2s = np.ascontiguousarray(g2d[sub2])
-    t0 = time.perf_counter()
-    pl_s, _ = O.bin_tiles(g2s, W, H, pw, ph)
-    t_bin_s = time.perf_counter() - t0
-    K, Ks = max(len(pl), 2), max(len(pl_s), 2)
-    t_bin = t_bin_s * (K * math.log(K)) / (Ks * math.log(Ks))
+    sub2 = np.sort(rng.choice(m, size=max(1, m // div), replace=False))
+    if bin_cache is not None and "t_bin" in bin_cache:
+        # many-step runs (the reference arm): the bin_tiles sample (the single
+        # -threaded sort, ~1 s) is timed on the first step and reused
+        t_bin = bin_cache["t_bin"]
+    else:
+        g2s = np.ascontiguousarray(g2d[sub2])
+        t0 = time.perf_counter()
+        pl_s, _ = O.bin_tiles(g2s, W, H, pw, ph)
+        t_bin_s = time.perf_counter() - t0
+        K, Ks = max(len(pl), 2), max(len(pl_s), 2)
+        t_bin = t_bin_s * (K * math.log(K)) / (Ks * math.log(Ks))
+        if bin_cache is not None:
+            bin_cache["t_bin"] = t_bin
 
     cols, rows = (W + pw - 1) // pw, (H + ph - 1) // ph
     lens = (ranges[1::2].astype(np.int64) - ranges[0::2].astype(np.int64))
@@ -220,20 +229,27 @@ def cpu_sample_estimate(g3d, cam_o, g2d, pl, ranges, W, H, pw, ph, threads: int,
     pix = (np.minimum(W, (tx + 1) * pw) - tx * pw) * (np.minimum(H, (ty + 1) * ph) - ty * ph)
     work = pix * lens
     total_work = int(work.sum())
-    # ~8 ns per evaluated pair per thread (measured order of magnitude); fill the budget
-    target = budget_s / 8e-9 * max(1, threads)
+    # ~8 ns per evaluated pair per thread (measured order of magnitude); fill
+    # most of the budget (the project / bin samples take the rest).
+    # ideal_threads: a short sample on many threads is dominated by its
+    # heaviest tiles, so it runs on one thread and is credited with perfect
+    # scaling over `threads` (favours the CPU baseline)
+    rthreads = 1 if ideal_threads else max(1, threads)
+    target = 0.6 * budget_s / 8e-9 * rthreads
     order = rng.permutation(cols * rows)
     csum = np.cumsum(work[order])
     cut = int(np.searchsorted(csum, min(target, total_work))) + 1
     tiles = np.sort(order[:cut]).astype(np.int32)
     t0 = time.perf_counter()
-    O.render(0, pl, ranges, g2d, W, H, pw, ph, (0, 0, 0), lazy=False, threads=threads, tiles=tiles)
+    O.render(0, pl, ranges, g2d, W, H, pw, ph, (0, 0, 0), lazy=False, threads=rthreads, tiles=tiles)
     t_r_s = time.perf_counter() - t0
     sw = max(1, int(work[tiles].sum()))
-    t_render = t_r_s * total_work / sw
+    t_render = t_r_s * total_work / sw / (max(1, threads) if ideal_threads else 1)
     desc = (f"project_all on {len(sub)}/{n} Gaussians (x{n / len(sub):.1f}); bin_tiles on {len(sub2)}/{m} splats "
-            f"(x K log K); render_reference faithful on {len(tiles)}/{cols * rows} random tiles "
-            f"({sw / total_work * 100:.2f}% of pixel*list work, extrapolated); threads={threads}")
+            f"(x K log K{'; timed on the first step' if bin_cache is not None else ''}); render_reference faithful "
+            f"on {len(tiles)}/{cols * rows} random tiles "
+            f"({sw / total_work * 100:.2f}% of pixel*list work, extrapolated"
+            f"{'; one thread, credited with ideal scaling' if ideal_threads else ''}); threads={threads}")
     return t_proj + t_bin + t_render, {"project_s": t_proj, "bin_s": t_bin, "render_s": t_render}, desc
 
 
@@ -254,11 +270,13 @@ def run_reference(args) -> None:
     g3d = O.gen_clustered_scene(n, cam, sigma=sig, bgfrac=bgf)
     g2d = O.project_all(g3d, cam)
     pl, ranges = O.bin_tiles(g2d, W, H, pw, ph)
-    budget = max(1.0, 150.0 / max(1, args.steps + args.warmup))
+    budget = max(0.3, 150.0 / max(1, args.steps + args.warmup))  # whole run ~2.5 min + setup
+    bin_cache = {}
     times = []
     desc = ""
     for i in range(args.warmup + args.steps):
-        t, parts, desc = cpu_sample_estimate(g3d, cam, g2d, pl, ranges, W, H, pw, ph, threads, budget, seed=i)
+        t, parts, desc = cpu_sample_estimate(g3d, cam, g2d, pl, ranges, W, H, pw, ph, threads, budget, seed=i,
+                                             bin_cache=bin_cache, ideal_threads=budget < 5.0)
         if i >= args.warmup:
             times.append(t)
     t = float(np.mean(times))
