@@ -563,6 +563,29 @@ def test_frame_pipeline_async_overflow_rerun():
     fp.close()
 
 
+def test_frame_pipeline_super_overflow_rerun():
+    """The async overflow path on a super-tile frame (1024x1024): the first
+    frame's super-tile K exceeds the initial capacity, the frame is rendered
+    again at the sync point, and equals the oracle's 16x16 render."""
+    W = H = 1024
+    n = 300
+    g3d, cam = scene(n, W, H, 4096.0, bgfrac=1.0)
+    g2d = O.project_all(g3d, cam)
+    pl, rg = O.bin_tiles(g2d, W, H, 16, 16)
+    assert len(O.bin_tiles(g2d, W, H, 32, 32)[0]) > 64 * n
+    fp = api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT, async_mode=True)
+    fp.forward(api.g3d_to_device(g3d), n, ncam(cam), variant=BS_FG, bg=(0.1, 0.2, 0.3))
+    assert fp.sync() == 1
+    mode = C.c_int32(0)
+    N.call("bs_context_list_mode", fp.ctx, C.byref(mode))
+    assert mode.value == 1
+    ref = O.render(BS_FG, pl, rg, g2d, W, H, 16, 16, (0.1, 0.2, 0.3), lazy=True, threads=0)
+    got = fp.frame.to_numpy()
+    for k in ("contrib", "term", "final_t"):
+        assert np.array_equal(got[k], ref[k]), k
+    fp.close()
+
+
 def test_frame_pipeline_runs_on_torch_stream():
     """FramePipeline enqueues on torch's current stream: reading the frame on
     that stream right after forward (no explicit sync) sees the finished frame."""
