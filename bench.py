@@ -316,7 +316,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sync-frames", action="store_true", help="wait for K inside each frame (no async mode)")
     ap.add_argument("--no-graphs", action="store_true", help="launch every kernel instead of replaying a CUDA graph")
-    ap.add_argument("--streams", type=int, default=3, help="frame contexts on separate streams (views round-robin)")
+    ap.add_argument("--streams", type=int, default=4, help="frame contexts on separate streams (views round-robin)")
     ap.add_argument("--fine-ctas", type=int, default=3, help="FineGrainedCombined CTAs per SM when streams > 1")
     ap.add_argument("--no-extras", action="store_true", help="skip per-variant sweep / e2e / cpu baseline")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
