@@ -791,6 +791,31 @@ def test_frame_pipeline_super_lists_match_tile_lists():
     fp.close()
 
 
+def test_frame_pipeline_super_lists_fast_mode():
+    """BS_ALPHA_FAST through the super-tile frame path: RGB / T within 1e-4 of
+    the oracle on pixels whose contrib / term match, mismatches rare."""
+    W, H, f, n = 1280, 832, 700.0, 60_000
+    cam = N.make_camera(None, (f, f), W, H)
+    g3d = api.gen_clustered_scene(n, cam)
+    g2d = O.project_all(g3d.view(O.G3D_DTYPE), O.Camera.from_buffer_copy(bytes(cam)))
+    pl, rg = O.bin_tiles(g2d, W, H, 16, 16)
+    bg = (0.1, 0.2, 0.3)
+    ref = O.render(BS_FG, pl, rg, g2d, W, H, 16, 16, bg, lazy=True, threads=0)
+    fp = api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_FAST, async_mode=True)
+    fp.forward(api.g3d_to_device(g3d), n, cam, variant=BS_FG, bg=bg)
+    fp.sync()
+    mode = C.c_int32(0)
+    N.call("bs_context_list_mode", fp.ctx, C.byref(mode))
+    assert mode.value == 1
+    got = fp.frame.to_numpy()
+    match = (got["contrib"] == ref["contrib"]) & (got["term"] == ref["term"])
+    assert 1.0 - match.mean() < 2e-3
+    err = np.abs(got["color"] - ref["color"]).reshape(-1, 3).max(axis=1)
+    assert err[match].max() <= 1e-4
+    assert np.abs(got["final_t"] - ref["final_t"])[match].max() <= 1e-4
+    fp.close()
+
+
 def test_host_async_pipeline_matches():
     """bs_render_frame_host_async: frames uploaded / rendered / downloaded on
     three streams equal the synchronous host-buffer frames."""
