@@ -158,8 +158,9 @@ int bs_splats_to_g2d(bs_splats in, int64_t n, bs_gaussian2d* g2d, void* stream);
 /* ---- P5: binning (bit-exact with src/preprocess.cpp:66-115) ----
  * Two calls so the host can size point_list without a hidden sync:
  *   bs_bin_count: per-splat tile rects, stable depth sort of the visible
- *     splats, exclusive scan of tiles-touched.  Writes K to *k_total (device
- *     i64).  Reads the splat count from *n_visible (device) — n_cap bounds it.
+ *     splats, exclusive scan of tiles-touched.  Writes K to *k_total (an i64
+ *     in device memory or in mapped pinned host memory, stored by a kernel).
+ *     Reads the splat count from *n_visible (device) — n_cap bounds it.
  *   bs_bin_sort: duplicates (tile, id) pairs in depth order, stable radix sort
  *     by tile id, tile ranges.  k is K read back by the host.  Must be given
  *     the same workspace the matching bs_bin_count call used.

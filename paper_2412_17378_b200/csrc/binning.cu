@@ -644,8 +644,11 @@ inline void bin_ws_layout(C& c, int64_t n_cap, const Grid& g, int64_t k_cap, Bin
   radix_ws_layout(c, k_cap, &o.rws_k);
 }
 
-__global__ void k_store_k(const uint64_t* __restrict__ total, int64_t* __restrict__ k_total) {
-  *k_total = (int64_t)*total;
+// K to *k_total — device memory, or mapped pinned host memory (the frame
+// pipeline reads K there without a D2H copy); total == null stores 0
+__global__ void k_store_k(const uint64_t* __restrict__ total, int64_t* k_total) {
+  *reinterpret_cast<volatile int64_t*>(k_total) = total ? (int64_t)*total : 0;
+  __threadfence_system();
 }
 
 }  // namespace bs
@@ -686,7 +689,8 @@ static int bin_count_tail(int64_t n_cap, const int32_t* n_visible, const Grid& g
     k_store_k<<<1, 1, 0, st>>>(total, k_total);
     BS_LAUNCH_CHECK();
   } else {
-    BS_CUDA_TRY(cudaMemsetAsync(k_total, 0, sizeof(int64_t), st));
+    k_store_k<<<1, 1, 0, st>>>(nullptr, k_total);
+    BS_LAUNCH_CHECK();
   }
   // tile histogram from the difference grid -> counts, starts, digit counts
   if (smem_diff) {

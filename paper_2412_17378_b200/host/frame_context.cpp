@@ -361,15 +361,21 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
     TRY(grow_n(&c->ranges16, &c->ranges16_cap, 2 * T));
     TRY(grow_n(&c->ranges_t, &c->ranges_t_cap, 2 * T));
   }
+  const bool async = allow_async && c->async_mode && bs_bin_async_supported(W, H, bpw, bph);
+  const int slot = capturing ? capture_slot : (async ? c->next_slot : 0);
+  // K goes straight to its pinned host slot (mapped memory, written by the
+  // count's last kernel): no copy that could queue behind another stream's
+  // download on the copy engine
+  int64_t* k_out = c->k_host + 1 + slot;
   auto count = [&]() -> int {
     if (super)
       return bs_preprocess_bin_count_super(g3d_dev, n, cam_dev ? nullptr : cam, cam_dev, sp, c->n_visible, W, H, pw,
-                                           ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, c->ranges16, c->aux_ws,
+                                           ph, k_out, c->bin_ws, c->bin_ws_bytes, c->ranges16, c->aux_ws,
                                            c->aux_ws_bytes, st);
     if (fused)
       return bs_preprocess_bin_count(g3d_dev, n, cam_dev ? nullptr : cam, cam_dev, sp, c->n_visible, W, H, pw, ph,
-                                     c->k_dev, c->bin_ws, c->bin_ws_bytes, st);
-    return bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, c->k_dev, c->bin_ws, c->bin_ws_bytes, st);
+                                     k_out, c->bin_ws, c->bin_ws_bytes, st);
+    return bs_bin_count(sp, n, c->n_visible, W, H, pw, ph, k_out, c->bin_ws, c->bin_ws_bytes, st);
   };
 
   // P5 count (workspace keyed on n and the tile grid; k part grown below)
@@ -383,11 +389,7 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   }
   TRY(count());
   mark(2);
-  const bool async = allow_async && c->async_mode && bs_bin_async_supported(W, H, bpw, bph);
-  const int slot = capturing ? capture_slot : (async ? c->next_slot : 0);
-  // K -> pinned host slot by a kernel store (a D2H memcpy would wait behind
-  // any large download on the copy engine, e.g. the previous frame's planes)
-  TRY(bs_publish_i64(c->k_dev, c->k_host + 1 + slot, st));
+
   if (async) {
     // no wait: sort into the current capacity; K is checked kDepth calls later
     if (!c->ev_k[slot]) CUTRY(cudaEventCreateWithFlags(&c->ev_k[slot], cudaEventDisableTiming));
