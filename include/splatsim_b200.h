@@ -183,15 +183,18 @@ int bs_preprocess_bin_count(const bs_gaussian3d* g3d, int64_t n, const bs_camera
                             int64_t* k_total, void* ws, size_t ws_bytes, void* stream);
 /* Super-tile form for the frame pipeline (power-of-two pw, ph): the lists
  * are binned at 2pw x 2ph (bs_bin_sort* follow with 2pw, 2ph) and
- * tile_ranges (2 x T, T = pw x ph tiles) receives the pw x ph list
- * lengths (for bs_tile_order / bs_tile_stats / bs_frame_work).  aux:
- * bs_super_aux_bytes(width, height, pw, ph) bytes. */
+ * tile_ranges (2 x T, T = pw x ph tiles; may be NULL) receives the pw x ph
+ * list lengths (for bs_tile_stats / bs_frame_work) — or later, from the same
+ * aux, bs_super_tile_lengths.  aux: bs_super_aux_bytes(width, height, pw, ph)
+ * bytes. */
 size_t bs_super_aux_bytes(int32_t width, int32_t height, int32_t pw, int32_t ph);
 int bs_preprocess_bin_count_super(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam,
                                   const bs_camera* cam_dev, bs_splats out, int32_t* counts, int32_t width,
                                   int32_t height, int32_t pw, int32_t ph, int64_t* k_total, void* ws,
                                   size_t ws_bytes, uint32_t* tile_ranges, void* aux, size_t aux_bytes,
                                   void* stream);
+int bs_super_tile_lengths(void* aux, size_t aux_bytes, int32_t width, int32_t height, int32_t pw, int32_t ph,
+                          uint32_t* tile_ranges, void* stream);
 int bs_bin_sort(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t width, int32_t height, int32_t pw,
                 int32_t ph, int64_t k, uint32_t* point_list, uint32_t* tile_ranges, void* ws, size_t ws_bytes,
                 void* stream);

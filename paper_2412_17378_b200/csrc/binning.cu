@@ -807,6 +807,9 @@ extern "C" size_t bs_super_aux_bytes(int32_t width, int32_t height, int32_t pw, 
   return z.off + 256;
 }
 
+extern "C" int bs_super_tile_lengths(void* aux, size_t aux_bytes, int32_t width, int32_t height, int32_t pw,
+                                     int32_t ph, uint32_t* tile_ranges, void* stream);
+
 extern "C" int bs_preprocess_bin_count_super(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam,
                                              const bs_camera* cam_dev, bs_splats out, int32_t* counts,
                                              int32_t width, int32_t height, int32_t pw, int32_t ph,
@@ -815,7 +818,7 @@ extern "C" int bs_preprocess_bin_count_super(const bs_gaussian3d* g3d, int64_t n
   if (!pow2i(pw) || !pow2i(ph) || pw > 16384 || ph > 16384) return BS_ERR_UNSUPPORTED;
   int s = check_grid(width, height, 2 * pw, 2 * ph);
   if (s) return s;
-  if (n < 0 || (!cam && !cam_dev) || !counts || !k_total || !tile_ranges ||
+  if (n < 0 || (!cam && !cam_dev) || !counts || !k_total ||
       (n > 0 && (!g3d || !out.xyab || !out.cop || !out.rgbr)))
     return BS_ERR_INVALID_ARGUMENT;
   if (n >= (int64_t)1 << 30) return BS_ERR_CAPACITY;
@@ -850,8 +853,34 @@ extern "C" int bs_preprocess_bin_count_super(const bs_gaussian3d* g3d, int64_t n
                                    w.rects, w.dk0, w.dv0, w.diff, diff_bytes, smem_diff, counts, st, &gt, diff2));
   s = bin_count_tail(n, counts, gs, w, smem_diff, diff_bytes, k_total, st);
   if (s) return s;
-  // the pw x ph list lengths -> tile_ranges (lengths exact; starts are the
-  // lists' offsets had they been materialised)
+  (void)counts2;
+  (void)starts2;
+  (void)partials2;
+  return tile_ranges ? bs_super_tile_lengths(aux, aux_bytes, width, height, pw, ph, tile_ranges, stream) : BS_OK;
+}
+
+// The pw x ph list lengths of the last bs_preprocess_bin_count_super on this
+// aux workspace -> tile_ranges (lengths exact; starts are the lists' offsets
+// had they been materialised).  Call once per count (the difference grid is
+// prefix-summed in place when it exceeds shared memory).
+extern "C" int bs_super_tile_lengths(void* aux, size_t aux_bytes, int32_t width, int32_t height, int32_t pw,
+                                     int32_t ph, uint32_t* tile_ranges, void* stream) {
+  if (!aux || !tile_ranges || width <= 0 || height <= 0 || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
+  if (aux_bytes < bs_super_aux_bytes(width, height, pw, ph)) return BS_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Grid gt = make_grid(width, height, pw, ph);
+  const int64_t T = (int64_t)gt.cols * gt.rows;
+  WsCarver ca(aux, aux_bytes);
+  int* diff2 = ca.take<int>((size_t)(gt.cols + 1) * (gt.rows + 1));
+  uint32_t* counts2 = ca.take<uint32_t>((size_t)T);
+  uint32_t* starts2 = ca.take<uint32_t>((size_t)T);
+  uint32_t* partials2 = ca.take<uint32_t>((size_t)scan_num_blocks(T) + 1);
+  const size_t diff2_bytes = sizeof(int) * (size_t)(gt.cols + 1) * (gt.rows + 1);
+  if (!g_diff_attr_set) {
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_bin_rect<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDiffSmem));
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_diff_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDiffSmem));
+    g_diff_attr_set = true;
+  }
   if (diff2_bytes <= kMaxDiffSmem) {
     k_diff_scan<<<1, 1024, diff2_bytes, st>>>(diff2, gt, counts2);
     BS_LAUNCH_CHECK();
