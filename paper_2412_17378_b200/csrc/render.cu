@@ -332,7 +332,11 @@ __global__ void __launch_bounds__(BLOCK) k_render_pixelwise(RArgs A) {
   __shared__ unsigned long long s_tab[32];
   load_tab(s_tab);
   __syncthreads();
-  pixelwise_tile<MODE, STAGE_COLOR, BLOCK>(A, blockIdx.x, s_xyab, s_cop, s_rgb, s_id, s_mem, make_expk(s_tab));
+  // one tile per CTA, or (a gated auto-mode candidate, launched with fewer
+  // CTAs so that not being selected costs little) tiles in grid stride —
+  // the next tile's first chunk barrier orders the shared-memory reuse
+  for (int tile = blockIdx.x; tile < A.T; tile += gridDim.x)
+    pixelwise_tile<MODE, STAGE_COLOR, BLOCK>(A, tile, s_xyab, s_cop, s_rgb, s_id, s_mem, make_expk(s_tab));
 }
 
 // Paper Alg. 1 (with the exit test fixed to >=).
@@ -902,10 +906,17 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
     case BS_NAIVE:
     case BS_SHARED_MEM_OPT: {
       const bool smem = variant == BS_SHARED_MEM_OPT;
+      int grid = T;
+      if (A.gate) {  // auto-mode candidate: at most 8 CTAs per SM, tiles in grid stride
+        int dev = 0, sms = 148;
+        BS_CUDA_TRY(cudaGetDevice(&dev));
+        BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        grid = max(1, min(T, sms * 8));
+      }
 #define BS_PW_CASE(B)                                                                   \
   if (block_pixels <= B) {                                                              \
-    if (smem) k_render_pixelwise<MODE, true, B><<<T, B, 0, st>>>(A);                    \
-    else k_render_pixelwise<MODE, false, B><<<T, B, 0, st>>>(A);                        \
+    if (smem) k_render_pixelwise<MODE, true, B><<<grid, B, 0, st>>>(A);                 \
+    else k_render_pixelwise<MODE, false, B><<<grid, B, 0, st>>>(A);                     \
     break;                                                                              \
   }
       BS_PW_CASE(64) BS_PW_CASE(128) BS_PW_CASE(256) BS_PW_CASE(512) BS_PW_CASE(1024)
