@@ -16,6 +16,12 @@
 //                      pixel-wise batches, Gaussian-wise stragglers
 //                                          (paper Alg. 3, re-cut for B200)
 //
+// Super-tile lists (bs_render_forward_super, the frame pipeline's >= 1 Mpixel
+// frames): FineGrainedCombined and SharedMemOpt (the auto-mode candidates)
+// also render from lists binned at 2pw x 2ph, keeping per tile exactly the
+// entries of its pw x ph list (tile_member / tile_member_fast) and counting
+// term positions over them.
+//
 // Semantics: pixel-wise variants == render_reference
 // (src/blend.cpp:55-107); Gaussian-wise variants == render_gaussianwise
 // (src/kernels.cpp:57-155).  In BS_ALPHA_EXACT mode every float op that the
@@ -26,9 +32,8 @@
 // are bit-identical (colour/depth differ only by double-sum association).
 // BS_ALPHA_FAST trades that for ex2.approx + float accumulators.
 //
-// No tensor-core path: blending is a dependent scan, not a contraction.  The
-// kernel is bound by FP32/MUFU/FP64 issue for long lists and by L2 for short
-// ones.
+// No tensor-core path: blending is a dependent scan, not a contraction.  All
+// five kernels are instruction-issue-bound (profiles/r1_ncu_variants.txt).
 #include <math.h>
 #include <stdlib.h>
 
