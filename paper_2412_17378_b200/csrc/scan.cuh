@@ -1,4 +1,4 @@
-// scan.cuh — device-wide exclusive prefix sum (reduce-then-scan, 3 kernels).
+// scan.cuh — device-wide exclusive prefix sum (reduce-then-scan, 2 kernels).
 // Used for compaction offsets, tiles-touched offsets, radix-sort digit
 // offsets and tile ranges.  Items at index >= *d_count (when d_count is given)
 // count as zero, so counts that live on the device need no host sync.
@@ -76,32 +76,21 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const TIn* __restr
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
-// Single block: exclusive scan of partials in place, writes grand total.
-template <typename TOut>
-__global__ void __launch_bounds__(1024) k_scan_partials(TOut* __restrict__ partials, int64_t nb,
-                                                        TOut* __restrict__ total_out) {
-  __shared__ TOut carry_s;
-  if (threadIdx.x == 0) carry_s = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < nb; base += blockDim.x) {
-    const int64_t k = base + threadIdx.x;
-    TOut v = k < nb ? partials[k] : TOut(0);
-    TOut tot;
-    TOut ex = block_exclusive_scan(v, &tot);
-    const TOut carry = carry_s;
-    if (k < nb) partials[k] = carry + ex;
-    __syncthreads();
-    if (threadIdx.x == 0) carry_s = carry + tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0 && total_out) *total_out = carry_s;
-}
-
+// partials[] holds each block's raw sum (k_scan_reduce); every block adds up
+// the sums before it itself (at most a few hundred L2 reads — cheaper than a
+// third, single-CTA launch), and the last block writes the grand total.
 template <typename TIn, typename TOut>
 __global__ void __launch_bounds__(kScanThreads) k_scan_downsweep(const TIn* __restrict__ in, int64_t n_cap,
                                                                  const int32_t* __restrict__ d_count,
                                                                  const TOut* __restrict__ partials,
-                                                                 TOut* __restrict__ out) {
+                                                                 TOut* __restrict__ out, TOut* __restrict__ total_out) {
+  __shared__ TOut s_prefix;
+  {
+    TOut p = 0;
+    for (int64_t i = threadIdx.x; i < (int64_t)blockIdx.x; i += kScanThreads) p += partials[i];
+    p = block_reduce_sum(p);
+    if (threadIdx.x == 0) s_prefix = p;
+  }
   const int64_t n = d_count ? (int64_t)*d_count : n_cap;
   const int64_t base = (int64_t)blockIdx.x * kScanTile;
   // blocked arrangement: thread t owns items [t*8, t*8+8) of the tile
@@ -114,13 +103,15 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_downsweep(const TIn* __re
     local += v[i];
   }
   TOut tot;
-  TOut run = block_exclusive_scan(local, &tot) + partials[blockIdx.x];
+  const TOut ex = block_exclusive_scan(local, &tot);  // (its barriers also publish s_prefix)
+  TOut run = ex + s_prefix;
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     const int64_t k = base + (int64_t)threadIdx.x * kScanItems + i;
     if (k < n_cap) out[k] = run;
     run += v[i];
   }
+  if (total_out && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *total_out = s_prefix + tot;
 }
 
 inline int64_t scan_num_blocks(int64_t n_cap) { return (n_cap + kScanTile - 1) / kScanTile; }
@@ -164,9 +155,8 @@ inline cudaError_t exclusive_scan(const TIn* in, TOut* out, int64_t n_cap, const
     return cudaPeekAtLastError();
   }
   k_scan_reduce<TIn, TOut><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_cap, d_count, partials);
-  k_scan_partials<TOut><<<1, 1024, 0, st>>>(partials, nb, total);
-  k_scan_downsweep<TIn, TOut><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_cap, d_count, partials, out);
-  count_launches(3);
+  k_scan_downsweep<TIn, TOut><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_cap, d_count, partials, out, total);
+  count_launches(2);
   return cudaPeekAtLastError();
 }
 
