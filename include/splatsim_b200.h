@@ -225,6 +225,11 @@ int bs_tile_stats(const uint32_t* tile_ranges, int32_t tiles, bs_tile_histogram*
  * fine-grained queue without a full sort). */
 int bs_tile_order(const uint32_t* tile_ranges, int32_t tiles, bs_tile_histogram* stats, uint32_t* task_order,
                   void* stream);
+/* bs_tile_order + bs_select_variant_device in one launch: *variant (device)
+ * <- the selector's choice (select_variant_formula) on the same statistics. */
+int bs_tile_order_select(const uint32_t* tile_ranges, int32_t tiles, bs_tile_histogram* stats,
+                         uint32_t* task_order, int32_t width, int32_t height, int32_t pw, int32_t ph,
+                         int32_t sm_count, int32_t* variant, void* stream);
 
 /* ---- R1-R8: forward render ----
  * variant: bs_variant (not AUTO).  task_order: LPT tile order from

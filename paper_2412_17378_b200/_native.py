@@ -105,6 +105,7 @@ SIGNATURES = {
                                           _f32p, FrameOut, _vp, _sz, _vp]),
     "bs_super_tile_ranges": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "bs_super_tile_lengths": (C.c_int, [_vp, _sz, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "bs_tile_order_select": (C.c_int, [_vp, _i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "bs_context_list_mode": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
     "bs_render_views": (C.c_int, [C.POINTER(C.c_void_p), _i32, _vp, _i64, C.POINTER(Camera), C.POINTER(C.c_int32),
                                   _i32, _i32, _i32, _i32, _f32p, C.POINTER(C.c_void_p), _sz]),

@@ -75,9 +75,14 @@ __device__ __forceinline__ uint32_t len_bucket(uint32_t c) {
   return e < 3u ? v : min(8u * e + ((v >> (e - 3u)) & 7u), (uint32_t)kOrderBuckets - 1u);
 }
 
+struct SelectOut {  // optional: the per-frame variant choice from the same statistics
+  int32_t* variant;
+  int pw, ph, sm_count;
+};
+
 __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t* __restrict__ ranges, int T,
                                                      uint32_t* __restrict__ order_out,
-                                                     bs_tile_histogram* __restrict__ out) {
+                                                     bs_tile_histogram* __restrict__ out, SelectOut sel) {
   __shared__ uint32_t s_cnt[32][kOrderBuckets];  // (warp, bucket) counts, then bases
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < 32 * kOrderBuckets; i += 1024) (&s_cnt[0][0])[i] = 0;
@@ -111,6 +116,7 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t* __restrict_
       s.min = s.p50 = s.p99 = 0;  // order statistics: bs_tile_stats
       s.mean = T ? (double)sum / (double)T : 0.0;
       *out = s;
+      if (sel.variant) *sel.variant = select_variant_formula(sum, m, sel.pw, sel.ph, sel.sm_count);
     }
   }
   // bases: buckets descending, warps ascending inside a bucket
@@ -202,7 +208,22 @@ extern "C" int bs_tile_order(const uint32_t* tile_ranges, int32_t tiles, bs_tile
                              uint32_t* task_order, void* stream) {
   if (tiles < 0 || !stats || !task_order || (tiles > 0 && !tile_ranges)) return BS_ERR_INVALID_ARGUMENT;
   if (tiles > kOrderMaxTiles) return BS_ERR_UNSUPPORTED;
-  k_tile_order<<<1, 1024, 0, (cudaStream_t)stream>>>(tile_ranges, tiles, task_order, stats);
+  k_tile_order<<<1, 1024, 0, (cudaStream_t)stream>>>(tile_ranges, tiles, task_order, stats,
+                                                     SelectOut{nullptr, 0, 0, 0});
+  BS_LAUNCH_CHECK();
+  return BS_OK;
+}
+
+// bs_tile_order + bs_select_variant_device in one launch (the frame
+// pipeline's auto mode): *variant <- the selector's choice on these stats.
+extern "C" int bs_tile_order_select(const uint32_t* tile_ranges, int32_t tiles, bs_tile_histogram* stats,
+                                    uint32_t* task_order, int32_t width, int32_t height, int32_t pw, int32_t ph,
+                                    int32_t sm_count, int32_t* variant, void* stream) {
+  if (tiles < 0 || !stats || !task_order || !variant || (tiles > 0 && !tile_ranges)) return BS_ERR_INVALID_ARGUMENT;
+  if (width <= 0 || height <= 0 || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
+  if (tiles > kOrderMaxTiles) return BS_ERR_UNSUPPORTED;
+  k_tile_order<<<1, 1024, 0, (cudaStream_t)stream>>>(tile_ranges, tiles, task_order, stats,
+                                                     SelectOut{variant, pw, ph, sm_count});
   BS_LAUNCH_CHECK();
   return BS_OK;
 }

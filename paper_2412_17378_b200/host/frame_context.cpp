@@ -451,11 +451,15 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
   if (super) TRY(bs_super_tile_ranges(c->ranges, W, H, pw, ph, c->ranges_t, st));
   c->lengths16_done = false;
   const uint32_t* tranges = super ? c->ranges_t : c->ranges;
-  if (T <= 32768)  // LPT order at eighth-octave granularity + the selector's inputs, one launch
+  if (T <= 32768 && variant < 0)  // LPT order + stats + the device selector, one launch
+    TRY(bs_tile_order_select(tranges, int32_t(T), c->stats_dev, c->order, W, H, pw, ph, c->sm_count,
+                             c->variant_dev, st));
+  else if (T <= 32768)  // LPT order at eighth-octave granularity + the selector's inputs, one launch
     TRY(bs_tile_order(tranges, int32_t(T), c->stats_dev, c->order, st));
   else
     TRY(bs_tile_stats(tranges, int32_t(T), c->stats_dev, nullptr, c->order, c->stats_ws, c->stats_ws_bytes, st));
-  if (variant < 0) TRY(bs_select_variant_device(c->stats_dev, W, H, pw, ph, c->sm_count, c->variant_dev, st));
+  if (variant < 0 && T > 32768)
+    TRY(bs_select_variant_device(c->stats_dev, W, H, pw, ph, c->sm_count, c->variant_dev, st));
   mark(5);
 
   // R
