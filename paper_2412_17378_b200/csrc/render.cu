@@ -520,6 +520,12 @@ __global__ void __launch_bounds__(kFgThreads) k_render_gaussianwise(RArgs A) {
 //     SIMT would otherwise pay for with 31 idle lanes.
 // EXACT output == render_reference on contrib/term/T/alpha bit for bit, colour
 // and depth to double-sum association (serial weights in the straggler path).
+#ifndef BS_SUBW
+#define BS_SUBW 8
+#endif
+// a warp task's sub-tile, one pixel per lane: 8x4 (4x8 measured equal on C2,
+// 16x2 9 % slower; build with EXTRA_NVFLAGS=-DBS_SUBW=4|16 to compare)
+constexpr int kSubW = BS_SUBW, kSubH = 32 / BS_SUBW;
 constexpr int kFineWarps = 8;
 constexpr int kFineThreads = kFineWarps * 32;
 constexpr int kStragglers = 2;  // (8 measured 4 % slower on C2 16x16 lists, 16 % on super-tile lists)
@@ -631,13 +637,14 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
   const int lane = threadIdx.x & 31;
   const int tx = tile % A.cols, ty = tile / A.cols;
   // 8x4-pixel sub-tiles tile the pw x ph patch row-major
-  const int nsx = (A.pw + 7) >> 3;
-  const int ox = tx * A.pw + (sub % nsx) * 8, oy = ty * A.ph + (sub / nsx) * 4;
-  const int lx = (sub % nsx) * 8 + (lane & 7), ly = (sub / nsx) * 4 + (lane >> 3);
-  const int px = ox + (lane & 7), py = oy + (lane >> 3);
+  const int nsx = (A.pw + kSubW - 1) / kSubW;
+  const int ox = tx * A.pw + (sub % nsx) * kSubW, oy = ty * A.ph + (sub / nsx) * kSubH;
+  const int lx = (sub % nsx) * kSubW + (lane % kSubW), ly = (sub / nsx) * kSubH + (lane / kSubW);
+  const int px = ox + (lane % kSubW), py = oy + (lane / kSubW);
   const bool inside = lx < A.pw && ly < A.ph && px < A.W && py < A.H;
   const float sx = __fadd_rn((float)px, 0.5f), sy = __fadd_rn((float)py, 0.5f);
-  const float rx0 = (float)ox + 0.5f, rx1 = (float)ox + 7.5f, ry0 = (float)oy + 0.5f, ry1 = (float)oy + 3.5f;
+  const float rx0 = (float)ox + 0.5f, rx1 = (float)ox + (kSubW - 0.5f), ry0 = (float)oy + 0.5f,
+              ry1 = (float)oy + (kSubH - 0.5f);
   const uint32_t start = A.ranges[2 * tile], end = A.ranges[2 * tile + 1];
 
   bool done = !inside, donated = false, donate_now = false;
@@ -958,7 +965,7 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
       // CTAs leave SM room for another frame context's kernels
       const int cap = g_fine_ctas_per_sm > 0 ? g_fine_ctas_per_sm : env_int("BS_FINE_CTAS_PER_SM", per_sm);
       per_sm = max(1, min(per_sm, cap));
-      const int subs = ((A.pw + 7) / 8) * ((A.ph + 3) / 4);  // 8x4 sub-tiles per tile
+      const int subs = ((A.pw + kSubW - 1) / kSubW) * ((A.ph + kSubH - 1) / kSubH);  // sub-tiles per tile
       const int64_t total = (int64_t)T * subs;
       if (total > 0x7fffffff) return BS_ERR_UNSUPPORTED;
       const int64_t ctas = (total + kFineWarps - 1) / kFineWarps;
