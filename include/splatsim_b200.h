@@ -181,7 +181,9 @@ int bs_bin_count(bs_splats g, int64_t n_cap, const int32_t* n_visible, int32_t w
 int bs_preprocess_bin_count(const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam, const bs_camera* cam_dev,
                             bs_splats out, int32_t* counts, int32_t width, int32_t height, int32_t pw, int32_t ph,
                             int64_t* k_total, void* ws, size_t ws_bytes, void* stream);
-/* Super-tile form for the frame pipeline (power-of-two pw, ph): the lists
+/* Super-tile form for the frame pipeline (power-of-two pw, ph; replaces
+ * project_all + bin_tiles' counting, src/preprocess.cpp:57-92, inside a
+ * frame — the reference's own lists stay available via bs_bin_sort): the lists
  * are binned at 2pw x 2ph (bs_bin_sort* follow with 2pw, 2ph) and
  * tile_ranges (2 x T, T = pw x ph tiles; may be NULL) receives the pw x ph
  * list lengths (for bs_tile_stats / bs_frame_work) — or later, from the same
@@ -226,7 +228,9 @@ int bs_tile_stats(const uint32_t* tile_ranges, int32_t tiles, bs_tile_histogram*
 int bs_tile_order(const uint32_t* tile_ranges, int32_t tiles, bs_tile_histogram* stats, uint32_t* task_order,
                   void* stream);
 /* bs_tile_order + bs_select_variant_device in one launch: *variant (device)
- * <- the selector's choice (select_variant_formula) on the same statistics. */
+ * <- the selector's choice (select_variant_formula) on the same statistics
+ * (tile_load_histogram, src/preprocess.cpp:117-136, feeding the per-frame
+ * predictor of the balanced/baseline choice, src/adaptive.cpp:16-32). */
 int bs_tile_order_select(const uint32_t* tile_ranges, int32_t tiles, bs_tile_histogram* stats,
                          uint32_t* task_order, int32_t width, int32_t height, int32_t pw, int32_t ph,
                          int32_t sm_count, int32_t* variant, void* stream);
@@ -358,7 +362,8 @@ int bs_render_frame_device(bs_context* ctx, const bs_gaussian3d* g3d_dev, int64_
 /* Stream for the following frames: NULL = the legacy default stream; the
  * context's own stream is the value bs_context_stream() returned before. */
 int bs_context_set_stream(bs_context* ctx, void* stream);
-/* A batch of views over several contexts from one native loop: view i
+/* A batch of views over several contexts from one native loop (the
+ * reference renders one view per run_kernel call, src/kernels.cpp:268-301): view i
  * renders cams[view_ids[i]] with ctxs[i % nctx] (into that context's own
  * planes); flush_bufs (nctx device buffers, may be NULL) are zeroed, flush_bytes
  * each, on the view's stream before it (an L2 flush when larger than L2). */
@@ -368,7 +373,9 @@ int bs_render_views(bs_context* const* ctxs, int32_t nctx, const bs_gaussian3d* 
 /* The context-owned planes frames with an empty bs_frame_out render into
  * (device pointers, valid until the next such frame or the context's destroy). */
 int bs_context_frame(bs_context* ctx, bs_frame_out* out);
-/* Render from super-tile lists (binned at 2pw x 2ph): tile_ranges holds, per
+/* Render from super-tile lists (binned at 2pw x 2ph; same outputs as
+ * run_kernel / render_reference on the pw x ph lists, src/kernels.cpp:268-301,
+ * src/blend.cpp:55-107): tile_ranges holds, per
  * pw x ph tile, its super-tile's range (bs_super_tile_ranges); the render
  * keeps the entries whose pw x ph rectangle contains the tile — exactly the
  * tile's list, term counted over it.  variant: FineGrainedCombined,
