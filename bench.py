@@ -283,7 +283,7 @@ def run_reference(args) -> None:
     value = 1.0 / t
     out = {"impl": "reference", "metric": metric_name(args.config), "value": value, "unit": "views/s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulators)",
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64 (f32 alpha/T, f64 colour/depth accumulators)",
            "data": "synthetic: gen_clustered_scene seed 42",
            "config": config_desc(args.config, W, H, n, pw, ph),
            "cpu_baseline": {"value": value, "unit": "views/s", "cores": threads, "kind": "port",
@@ -463,7 +463,7 @@ def main():
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32 alpha/T, f64 colour+depth accumulators (exact mode)" if mode == N.ALPHA_EXACT else "f32",
+        "dtype": "f32+f64 (f32 alpha/T, f64 colour/depth accumulators)" if mode == N.ALPHA_EXACT else "f32",
         "data": "synthetic: gen_clustered_scene seed 42 (no dataset)",
         "config": dict(config_desc(args.config, W, H, n, pw, ph), alpha_mode=args.alpha, variant=args.variant,
                        variants_used={api.variant_name(k): c for k, c in used.items()},
