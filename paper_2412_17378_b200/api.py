@@ -244,22 +244,28 @@ def select_variant(stats: TileStats, width: int, height: int, pw: int, ph: int, 
     return v
 
 
-_render_ws = {}
+def render_workspace(width: int, height: int, device) -> torch.Tensor:
+    """The render's workspace (work-queue counters + FineGrainedCombined tail
+    hand-off slots).  A workspace belongs to ONE stream at a time: two renders
+    sharing one concurrently would race on the queue."""
+    return _ws(N.lib().bs_render_workspace_bytes(width, height), device)
 
 
 def render_forward(variant: int, s: DeviceSplats, b: DeviceBinning, width: int, height: int, pw: int, ph: int,
                    bg=(0.0, 0.0, 0.0), alpha_mode: int = ALPHA_EXACT, task_order: torch.Tensor | None = None,
-                   out: DeviceFrame | None = None) -> DeviceFrame:
-    """run_kernel(variant, ...) output (src/kernels.cpp:268-301) on the device."""
+                   out: DeviceFrame | None = None, ws: torch.Tensor | None = None) -> DeviceFrame:
+    """run_kernel(variant, ...) output (src/kernels.cpp:268-301) on the device.
+
+    ``ws``: a caller-owned render workspace (``render_workspace``), reused
+    across calls on one stream; without it each call takes a fresh one from
+    torch's stream-aware caching allocator."""
     dev = s.xyab.device
     if b.tile_cols != (width + pw - 1) // pw or b.tile_rows != (height + ph - 1) // ph:
         raise ValueError("run_kernel: binning grid does not match image dims")
     out = out or DeviceFrame.empty(width, height, dev)
-    key = str(dev)
     need = N.lib().bs_render_workspace_bytes(width, height)
-    if key not in _render_ws or _render_ws[key].numel() < need:
-        _render_ws[key] = _ws(need, dev)
-    ws = _render_ws[key]
+    if ws is None or ws.numel() < need:
+        ws = _ws(need, dev)
     bgc = (C.c_float * 3)(*[float(x) for x in bg])
     N.call("bs_render_forward", int(variant), int(alpha_mode), s.c(), _ptr(b.point_list) if b.k else None,
            _ptr(b.tile_ranges), _ptr(task_order), width, height, pw, ph, bgc, out.c(), _ptr(ws), ws.numel(),
@@ -301,6 +307,7 @@ class Pipeline:
     frame: DeviceFrame | None = None
     pre_ws: torch.Tensor | None = None
     stats_ws: torch.Tensor | None = None
+    render_ws: torch.Tensor | None = None  # this pipeline's own (queue counters are per render stream)
     last_variant: int = -1
     last_k: int = 0
     last_stats: TileStats | None = field(default=None, repr=False)
@@ -309,6 +316,7 @@ class Pipeline:
     def __post_init__(self):
         self.binner = Binner(self.width, self.height, self.pw, self.ph, self.device)
         self.frame = DeviceFrame.empty(self.width, self.height, self.device)
+        self.render_ws = render_workspace(self.width, self.height, self.device)
 
     def forward(self, g3d_dev: torch.Tensor, n: int, cam: N.Camera, variant="auto", bg=(0.0, 0.0, 0.0),
                 stage_events: list | None = None):
@@ -343,7 +351,7 @@ class Pipeline:
             v = variant if isinstance(variant, int) else variant_from_name(variant)
         mark("stats_select")
         render_forward(v, self.splats, b, self.width, self.height, self.pw, self.ph, bg, self.alpha_mode,
-                       st.task_order, self.frame)
+                       st.task_order, self.frame, self.render_ws)
         mark("render")
         self.last_variant, self.last_k, self.last_stats, self.last_binning = v, b.k, st, b
         return self.frame, v

@@ -96,6 +96,10 @@ struct bs_context {
     float bg[3] = {0, 0, 0};
     bs_frame_out out{};
     int slot = 0;
+    // the point_list capacity the frame was sorted into (for a graph replay:
+    // the one baked in at capture) — its K is checked against this, not
+    // against a capacity grown since
+    int64_t cap = 0;
     // host-buffer pipeline (bs_render_frame_host_async): host planes the
     // frame's outputs go to (a re-render copies them again); io = -1 otherwise
     int io = -1;
@@ -121,6 +125,7 @@ struct bs_context {
   } gkey;
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
   uint64_t gkernels[2] = {0, 0};  // kernel launches recorded in each graph
+  int64_t gcap[2] = {0, 0};       // point_list capacity baked into each graph
   cudaStream_t cap_stream = nullptr;
   bs_camera* cam_dev = nullptr;
   bs_camera* cam_ring = nullptr;  // pinned, 4 slots
@@ -363,7 +368,10 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
     TRY(grow_n(&c->ranges_t, &c->ranges_t_cap, 2 * T));
   }
   const bool async = allow_async && c->async_mode && bs_bin_async_supported(W, H, bpw, bph);
-  const int slot = capturing ? capture_slot : (async ? c->next_slot : 0);
+  // K slots: 0..kDepth-1 for async frames (checked later), kDepth for a
+  // synchronous frame (read at once) — a synchronous frame never overwrites
+  // the K of an async frame still pending
+  const int slot = capturing ? capture_slot : (async ? c->next_slot : bs_context::kDepth);
   // K goes straight to its pinned host slot (mapped memory, written by the
   // count's last kernel): no copy that could queue behind another stream's
   // download on the copy engine
@@ -403,8 +411,10 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
     mark(3);
     if (!c->point_list) TRY(grow_pl_async(c, std::max<int64_t>(n, 1) * 64, st));  // 64 tiles / splat to start
     TRY(grow_n(&c->ranges, &c->ranges_cap, 2 * T));
-    TRY(bs_bin_sort_async(sp, n, c->n_visible, W, H, bpw, bph, std::min<int64_t>(c->pl_cap, (int64_t(1) << 30) - 1),
-                          c->point_list, c->ranges, c->bin_ws, c->bin_ws_bytes, st));
+    const int64_t kcap = std::min<int64_t>(c->pl_cap, (int64_t(1) << 30) - 1);
+    TRY(bs_bin_sort_async(sp, n, c->n_visible, W, H, bpw, bph, kcap, c->point_list, c->ranges, c->bin_ws,
+                          c->bin_ws_bytes, st));
+    if (capturing) c->gcap[slot] = kcap;
     if (!capturing) {
     bs_context::Pending& q = c->pending[c->n_pending++];
     q.g3d = g3d_dev;
@@ -416,12 +426,13 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
     std::copy(bg, bg + 3, q.bg);
     q.out = fo_in;
     q.slot = slot;
+    q.cap = kcap;
     q.io = -1;
     c->next_slot = (slot + 1) % bs_context::kDepth;
     }
   } else {
     CUTRY(cudaStreamSynchronize(st));
-    const int64_t k = c->k_host[1];
+    const int64_t k = c->k_host[1 + bs_context::kDepth];
     if (k > c->bin_k && bs_bin_workspace_bytes(c->bin_n, W, H, bpw, bph, k) > c->bin_ws_bytes) {
       // the count state lives in the workspace: grow, then count again
       c->bin_k = int64_t(double(k) * 1.25) + 1024;
@@ -538,7 +549,7 @@ int verify_pending(bs_context* c, cudaStream_t st, int keep = 0) {
     CUTRY(cudaEventSynchronize(c->ev_k[p0.slot]));
     const int64_t k = c->k_host[1 + p0.slot];
     c->last_k = k;
-    if (k <= c->pl_cap) {
+    if (k <= p0.cap) {  // (p0.cap <= pl_cap: the capacity only grows)
       // keep >= 50 % headroom over every K seen, growing to 3x: a regrowth
       // maps new memory (a multi-ms stall), so it must be rare — HBM is not
       // (the first checked frame calibrates the capacity to 3x its K at once)
@@ -681,9 +692,11 @@ int frame_graph(bs_context* c, const bs_gaussian3d* g3d, int64_t n, const bs_cam
   std::copy(bg, bg + 3, q.bg);
   q.out = out;
   q.slot = slot;
+  q.cap = c->gcap[slot];
   q.io = -1;
   c->next_slot = (slot + 1) % bs_context::kDepth;
   c->last_variant = variant;
+  c->lengths16_done = false;  // the replayed frame's pw x ph lengths are not computed yet
   return BS_OK;
 }
 

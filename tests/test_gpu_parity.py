@@ -586,6 +586,68 @@ def test_frame_pipeline_super_overflow_rerun():
     fp.close()
 
 
+def test_frame_pipeline_async_two_in_flight_capacity_growth():
+    """Two async frames in flight: checking the first one grows the capacity
+    (first-frame calibration to 3x its K), and the second one had overflowed
+    the capacity it was SORTED with.  Its K must be checked against that
+    capacity, not the grown one, so it is rendered again."""
+    W = H = 512
+    n = 300
+    g3d = O.gen_clustered_scene(n, O.make_camera(focal=(1500, 1500), width=W, height=H), bgfrac=1.0)
+    cams = [O.make_camera(focal=(f, f), width=W, height=H) for f in (1000.0, 1500.0)]
+    refs, ks = [], []
+    for cam in cams:
+        g2d = O.project_all(g3d, cam)
+        pl, rg = O.bin_tiles(g2d, W, H, 16, 16)
+        ks.append(len(pl))
+        refs.append(O.render(BS_FG, pl, rg, g2d, W, H, 16, 16, (0.1, 0.2, 0.3), lazy=True, threads=0))
+    # frame 0 fits the initial capacity (64 per Gaussian), frame 1 does not,
+    # but it fits the capacity frame 0's check grows to (3 K0)
+    assert ks[0] < 64 * n < ks[1] <= 3 * ks[0]
+    fp = api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT, async_mode=True)
+    d = api.g3d_to_device(g3d)
+    frames = [api.DeviceFrame.empty(W, H, DEV) for _ in range(3)]
+    for i, cam in enumerate([cams[0], cams[1], cams[0]]):
+        fp.frame = frames[i]
+        fp.forward(d, n, ncam(cam), variant=BS_FG, bg=(0.1, 0.2, 0.3))
+    assert fp.sync() >= 1
+    for i, ref in ((0, refs[0]), (1, refs[1]), (2, refs[0])):
+        got = frames[i].to_numpy()
+        for k in ("contrib", "term", "final_t"):
+            assert np.array_equal(got[k], ref[k]), (i, k)
+    fp.close()
+
+
+def test_frame_pipeline_sync_frame_keeps_pending_k():
+    """A synchronous frame (a grid the async path does not take) while an
+    async frame is pending uses its own K slot: the pending frame's K check
+    still reads its own count."""
+    W = H = 512
+    n = 300
+    g3d = O.gen_clustered_scene(n, O.make_camera(focal=(1500, 1500), width=W, height=H), bgfrac=1.0)
+    cam = O.make_camera(focal=(1500.0, 1500.0), width=W, height=H)
+    g2d = O.project_all(g3d, cam)
+    pl, rg = O.bin_tiles(g2d, W, H, 16, 16)
+    assert len(pl) > 64 * n  # the async frame overflows the initial capacity
+    ref = O.render(BS_FG, pl, rg, g2d, W, H, 16, 16, (0.1, 0.2, 0.3), lazy=True, threads=0)
+    fp = api.FramePipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT, async_mode=True)
+    d = api.g3d_to_device(g3d)
+    fa = api.DeviceFrame.empty(W, H, DEV)
+    fp.frame = fa
+    fp.forward(d, n, ncam(cam), variant=BS_FG, bg=(0.1, 0.2, 0.3))
+    # a frame in between through the same context on a 131,072-tile grid
+    # (beyond the chunked scatter: the synchronous body), few instances
+    big = O.make_camera(focal=(10.0, 10.0), width=8192, height=4096)
+    assert not N.lib().bs_bin_async_supported(8192, 4096, 16, 16)
+    fp.frame = api.DeviceFrame.empty(8192, 4096, DEV)
+    fp.forward(d, n, ncam(big), variant=BS_FG, bg=(0.1, 0.2, 0.3), info=True)
+    fp.sync()
+    got = fa.to_numpy()
+    for k in ("contrib", "term", "final_t"):
+        assert np.array_equal(got[k], ref[k]), k
+    fp.close()
+
+
 def test_frame_pipeline_runs_on_torch_stream():
     """FramePipeline enqueues on torch's current stream: reading the frame on
     that stream right after forward (no explicit sync) sees the finished frame."""
