@@ -20,21 +20,25 @@
 //   Rng / fnv1a64            include/splatsim/rng.hpp:11-69
 //   gen_clustered_scene      src/workload.cpp:198-246
 //
-// Pinning status (see DESIGN.md §Oracle):
-//   * The reference is NOT buildable here (Eigen3 and nlohmann/json absent,
-//     src/experiment.cpp missing), so there is no oracle/_ref.
-//   * The reference ships no golden vectors; the oracle is pinned against
-//     every SPEC.md known-answer test (tests/test_oracle_kat.py).
+// Pinning status (see DESIGN.md §4):
+//   * PINNED TO THE REFERENCE ITSELF: oracle/_ref (make -C oracle ref) builds
+//     /root/reference/proj/core/src/*.cpp unmodified against an Eigen-subset
+//     shim (oracle/ref_shim) and the image's nlohmann/json header;
+//     tests/test_ref_oracle.py checks this restatement against it bit for
+//     bit (scene generator, P1-P6, every render variant on C1, the golden
+//     fixtures, the blend KATs) and tests/test_ref_host.py the product's host
+//     bookkeeping.  The reference ships no golden vectors of its own.
 //   * expf: the oracle calls libm expf exactly as the reference does
 //     (std::exp(float), src/blend.cpp:12).  The third-party dependency is
 //     glibc 2.39 libm (x86-64 ifunc __expf_fma).
-//   * Eigen 3.x fixed-size products (unpinned version): the evaluation order
-//     below is the one Eigen 3.4 uses on x86-64 with SSE2.  Products that are
+//   * Eigen 3.x fixed-size products (unpinned version, absent here): the
+//     evaluation order below — and the shim's — is the one Eigen 3.4 uses on
+//     x86-64 with SSE2 (the reference's flags: no -march).  Products that are
 //     vectorised (Lhs rows a multiple of the packet size: 2x3 double products)
 //     sum left-to-right; scalar coefficient-based products (3x3 float) reduce
-//     as a0 + (a1 + a2) (redux_novec_unroller).  Bit-level parity of P1-P3 with
-//     a real Eigen build is therefore "unpinned"; parity of the GPU with this
-//     oracle is bit-exact by construction and by test.
+//     as a0 + (a1 + a2) (redux_novec_unroller).  P1-P3 bits therefore rest on
+//     that documented order; everything else is pinned by executing the
+//     reference's code.
 //
 // Compiled with -ffp-contract=off, as proj/CMakeLists.txt:11-12 does.
 #pragma once
