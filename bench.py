@@ -32,7 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-NCU_TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+NCU_COUNTERS_PATH = os.path.join(ROOT, "profiles", "ncu_counters.json")
 
 CONFIGS = {
     # name: (W, H, focal, N gaussians, bg fraction, cluster sigma)
@@ -40,21 +40,19 @@ CONFIGS = {
     "c1": (256, 256, 256.0, 10_000, 1.0, 0.035),
     "c4": (3840, 2160, 2000.0, 3_000_000, 0.12, 0.035),
 }
-N_VIEWS = 64
-PIVOT_Z = 5.5
+# the view schedule and the orbit are the product's (paper_2412_17378_b200/
+# sharding.py; tests/test_sharding_gloo.py covers them with world-size-2 gloo)
+from paper_2412_17378_b200.sharding import N_VIEWS, batch_view_ids, orbit_view, views_for_rank  # noqa: E402
 
 
-def orbit_view(k: int, n_views: int = N_VIEWS) -> np.ndarray:
-    """World->camera of view k: yaw about the y axis through (0, 0, PIVOT_Z)."""
-    yaw = math.radians(-15.0 + 30.0 * k / max(1, n_views - 1))
-    c, s = math.cos(yaw), math.sin(yaw)
-    R = np.array([[c, 0.0, s], [0.0, 1.0, 0.0], [-s, 0.0, c]])
-    piv = np.array([0.0, 0.0, PIVOT_Z])
-    t = piv - R @ piv
-    V = np.eye(4)
-    V[:3, :3] = R
-    V[:3, 3] = t
-    return V.astype(np.float32)
+def load_counters() -> dict:
+    """Per-kernel ncu counters (one --set full capture of each render kernel
+    on each config, tools/ncu_counters.py -> profiles/ncu_counters.json)."""
+    try:
+        with open(NCU_COUNTERS_PATH) as f:
+            return json.load(f)
+    except Exception:
+        return {}
 
 
 def load_peaks() -> dict:
@@ -186,108 +184,137 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def cpu_sample_estimate(g3d, cam_o, g2d, pl, ranges, W, H, pw, ph, threads: int, budget_s: float, seed: int = 0,
-                        bin_cache: dict | None = None, ideal_threads: bool = False):
-    """Time the CPU oracle (the reference's algorithm, restated) on bounded
-    samples of one frame and extrapolate to the full frame:
-      project_all on 1/8 of the Gaussians      x8 (linear)
-      bin_tiles on 1/8 of the projected splats  x K log K ratio
-      render_reference (faithful: evaluates the whole tile list per pixel,
-        src/blend.cpp:85-92) on random tiles   x (sum pixels*len) ratio
-    Returns seconds for one full frame + a description."""
+def cpu_libs():
+    """(oracle port, reference library or None, kind).  The reference itself
+    (oracle/_ref: /root/reference's own sources built here against the
+    Eigen-subset shim; the built .so travels to the GPU box) when present,
+    else the oracle restatement.  Test / baseline infrastructure only."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib as O
+    try:
+        import ref_lib as R
+        if os.path.exists(R.REF_LIB):
+            R.lib()
+            return O, R, "reference"
+    except Exception:
+        pass
+    return O, None, "port"
 
+
+def cpu_full_frame(O, R, g3d, cam, W, H, pw, ph, variant: int, threads: int) -> dict:
+    """One COMPLETE frame on the host: project_all -> bin_tiles -> run_kernel,
+    the reference's own functions when R is given (project_all split over
+    `threads` contiguous chunks — an order-preserving map; bin_tiles is the
+    reference's single-threaded sort; run_kernel over tile sets dealt to
+    `threads` threads — tiles are independent, the result is one call's),
+    else the oracle port.  Returns per-stage seconds."""
+    t0 = time.perf_counter()
+    g2d = R.project_all(g3d, cam, threads) if R else O.project_all(g3d, cam)
+    t1 = time.perf_counter()
+    pl, rg = (R or O).bin_tiles(g2d, W, H, pw, ph)
+    t2 = time.perf_counter()
+    if R:
+        R.run_kernel(variant, pl, rg, g2d, W, H, pw, ph, (0, 0, 0), threads=threads)
+    else:
+        O.render(variant, pl, rg, g2d, W, H, pw, ph, (0, 0, 0), lazy=False, threads=threads)
+    t3 = time.perf_counter()
+    return {"project_s": t1 - t0, "bin_s": t2 - t1, "render_s": t3 - t2, "frame_s": t3 - t0,
+            "K": int(len(pl)), "n_visible": int(len(g2d))}
+
+
+def cpu_sample_estimate(O, R, g3d, cam_o, g2d, pl, ranges, W, H, pw, ph, budget_s: float, variant: int = 0,
+                        seed: int = 0):
+    """Bounded sample of one frame on ONE host thread (the reference has no
+    threads), extrapolated to the full frame:
+      project_all on 1/8 of the Gaussians        x8 (linear)
+      bin_tiles on 1/8 of the projected splats    x K log K ratio
+      run_kernel (faithful: evaluates the whole tile list per pixel,
+        src/blend.cpp:85-92) on random tiles     x (sum pixels*len) ratio
+    through the reference's own code (R) when built, else the oracle port."""
     rng = np.random.default_rng(seed)
+    lib = R or O
     n = len(g3d)
     div = 8
     sub = np.sort(rng.choice(n, size=max(1, n // div), replace=False))
     g3s = np.ascontiguousarray(g3d[sub])
     t0 = time.perf_counter()
-    O.project_all(g3s, cam_o)
+    R.project_all(g3s, cam_o, 1) if R else O.project_all(g3s, cam_o)
     t_proj = (time.perf_counter() - t0) * (n / len(sub))
-
     m = len(g2d)
     sub2 = np.sort(rng.choice(m, size=max(1, m // div), replace=False))
-    if bin_cache is not None and "t_bin" in bin_cache:
-        # many-step runs (the reference arm): the bin_tiles sample (the single
-        # -threaded sort, ~1 s) is timed on the first step and reused
-        t_bin = bin_cache["t_bin"]
-    else:
-        g2s = np.ascontiguousarray(g2d[sub2])
-        t0 = time.perf_counter()
-        pl_s, _ = O.bin_tiles(g2s, W, H, pw, ph)
-        t_bin_s = time.perf_counter() - t0
-        K, Ks = max(len(pl), 2), max(len(pl_s), 2)
-        t_bin = t_bin_s * (K * math.log(K)) / (Ks * math.log(Ks))
-        if bin_cache is not None:
-            bin_cache["t_bin"] = t_bin
-
+    g2s = np.ascontiguousarray(g2d[sub2])
+    t0 = time.perf_counter()
+    pl_s, _ = lib.bin_tiles(g2s, W, H, pw, ph)
+    t_bin_s = time.perf_counter() - t0
+    K, Ks = max(len(pl), 2), max(len(pl_s), 2)
+    t_bin = t_bin_s * (K * math.log(K)) / (Ks * math.log(Ks))
     cols, rows = (W + pw - 1) // pw, (H + ph - 1) // ph
     lens = (ranges[1::2].astype(np.int64) - ranges[0::2].astype(np.int64))
     tx, ty = np.arange(cols * rows) % cols, np.arange(cols * rows) // cols
     pix = (np.minimum(W, (tx + 1) * pw) - tx * pw) * (np.minimum(H, (ty + 1) * ph) - ty * ph)
     work = pix * lens
     total_work = int(work.sum())
-    # ~8 ns per evaluated pair per thread (measured order of magnitude); fill
-    # most of the budget (the project / bin samples take the rest).
-    # ideal_threads: a short sample on many threads is dominated by its
-    # heaviest tiles, so it runs on one thread and is credited with perfect
-    # scaling over `threads` (favours the CPU baseline)
-    rthreads = 1 if ideal_threads else max(1, threads)
-    target = 0.6 * budget_s / 8e-9 * rthreads
+    target = 0.6 * budget_s / 8e-9  # ~8 ns per evaluated pair (order of magnitude)
     order = rng.permutation(cols * rows)
     csum = np.cumsum(work[order])
     cut = int(np.searchsorted(csum, min(target, total_work))) + 1
     tiles = np.sort(order[:cut]).astype(np.int32)
     t0 = time.perf_counter()
-    O.render(0, pl, ranges, g2d, W, H, pw, ph, (0, 0, 0), lazy=False, threads=rthreads, tiles=tiles)
+    if R:  # the sampled tiles' lists, every other tile empty
+        sr = np.zeros_like(ranges)
+        sr[2 * tiles], sr[2 * tiles + 1] = ranges[2 * tiles], ranges[2 * tiles + 1]
+        R.run_kernel(variant, pl, sr, g2d, W, H, pw, ph, (0, 0, 0), threads=1)
+    else:
+        O.render(variant, pl, ranges, g2d, W, H, pw, ph, (0, 0, 0), lazy=False, threads=1, tiles=tiles)
     t_r_s = time.perf_counter() - t0
     sw = max(1, int(work[tiles].sum()))
-    t_render = t_r_s * total_work / sw / (max(1, threads) if ideal_threads else 1)
-    desc = (f"project_all on {len(sub)}/{n} Gaussians (x{n / len(sub):.1f}); bin_tiles on {len(sub2)}/{m} splats "
-            f"(x K log K{'; timed on the first step' if bin_cache is not None else ''}); render_reference faithful "
-            f"on {len(tiles)}/{cols * rows} random tiles "
-            f"({sw / total_work * 100:.2f}% of pixel*list work, extrapolated"
-            f"{'; one thread, credited with ideal scaling' if ideal_threads else ''}); threads={threads}")
+    t_render = t_r_s * total_work / sw
+    desc = (f"{'reference (oracle/_ref)' if R else 'oracle port'}, 1 thread: project_all on {len(sub)}/{n} Gaussians "
+            f"(x{n / len(sub):.1f}); bin_tiles on {len(sub2)}/{m} splats (x K log K); run_kernel faithful on "
+            f"{len(tiles)}/{cols * rows} random tiles ({sw / total_work * 100:.2f}% of pixel*list work, extrapolated)")
     return t_proj + t_bin + t_render, {"project_s": t_proj, "bin_s": t_bin, "render_s": t_render}, desc
 
 
 # ---------------------------------------------------------------------------
 def run_reference(args) -> None:
-    """--impl reference: the reference's CPU implementation (oracle port —
-    the reference itself is unbuildable here) on the host cores."""
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref when built, else the oracle port) on the host cores, on
+    this arm's workload: every timed step is one COMPLETE view of the C2
+    orbit (project_all -> bin_tiles -> run_kernel(FineGrainedCombined), the
+    variant our arm's selector runs), all host threads where the reference's
+    functions allow it.  Warm-up steps run project_all only (a CPU has no
+    JIT or clock ramp to warm; a full warm-up frame would add ~15 s each)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import oracle_lib as O
-
+    O, R, kind = cpu_libs()
     W, H, f, n, bgf, sig = CONFIGS[args.config]
     pw = ph = 16
     threads = os.cpu_count() or 1
-    cam = O.make_camera(orbit_view(0), (f, f), W, H)
-    g3d = O.gen_clustered_scene(n, cam, sigma=sig, bgfrac=bgf)
-    g2d = O.project_all(g3d, cam)
-    pl, ranges = O.bin_tiles(g2d, W, H, pw, ph)
-    budget = max(0.3, 150.0 / max(1, args.steps + args.warmup))  # whole run ~2.5 min + setup
-    bin_cache = {}
-    times = []
-    desc = ""
-    for i in range(args.warmup + args.steps):
-        t, parts, desc = cpu_sample_estimate(g3d, cam, g2d, pl, ranges, W, H, pw, ph, threads, budget, seed=i,
-                                             bin_cache=bin_cache, ideal_threads=budget < 5.0)
-        if i >= args.warmup:
-            times.append(t)
-    t = float(np.mean(times))
-    value = 1.0 / t
+    cam0 = O.make_camera(orbit_view(0), (f, f), W, H)
+    g3d = (R or O).gen_clustered_scene(n, cam0, sigma=sig, bgfrac=bgf)
+    cams = [O.make_camera(orbit_view(k), (f, f), W, H) for k in range(N_VIEWS)]
+    for i in range(args.warmup):
+        R.project_all(g3d, cams[i % N_VIEWS], threads) if R else O.project_all(g3d, cams[i % N_VIEWS])
+    stages = []
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        stages.append(cpu_full_frame(O, R, g3d, cams[i % N_VIEWS], W, H, pw, ph, 3, threads))
+    wall = time.perf_counter() - t0
+    value = args.steps / wall
+    mean = {k: float(np.mean([s[k] for s in stages])) for k in ("project_s", "bin_s", "render_s", "frame_s")}
+    sample = (f"{args.steps} complete C2 views (views 0..{args.steps - 1} of the orbit): "
+              f"{'the reference itself (oracle/_ref: /root/reference/proj/core/src built against the Eigen-subset shim)' if R else 'oracle port'}"
+              f"; project_all on {threads} threads (contiguous chunks), bin_tiles single-threaded (the reference's sort), "
+              f"run_kernel(FineGrainedCombined) over tile sets on {threads} threads")
     out = {"impl": "reference", "metric": metric_name(args.config), "value": value, "unit": "views/s",
-           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64 (f32 alpha/T, f64 colour/depth accumulators)",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "f32+f64 (f32 alpha/T, f64 colour/depth accumulators)",
            "data": "synthetic: gen_clustered_scene seed 42",
            "config": config_desc(args.config, W, H, n, pw, ph),
-           "cpu_baseline": {"value": value, "unit": "views/s", "cores": threads, "kind": "port",
-                            "sample": desc, "stage_s": parts},
+           "cpu_baseline": {"value": value, "unit": "views/s", "cores": threads, "kind": kind, "sample": sample,
+                            "stage_s": mean, "K_mean": float(np.mean([s["K"] for s in stages]))},
            "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -319,7 +346,11 @@ def main():
     ap.add_argument("--streams", type=int, default=4, help="frame contexts on separate streams (views round-robin)")
     ap.add_argument("--fine-ctas", type=int, default=3, help="FineGrainedCombined CTAs per SM when streams > 1")
     ap.add_argument("--no-extras", action="store_true", help="skip per-variant sweep / e2e / cpu baseline")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 imbalance sweep in the extras")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--batch", type=int, default=N_VIEWS,
+                    help="views per step: the fixed batch of the first B orbit views, split contiguously over the "
+                         "ranks (SURVEY 8e, strong scaling); 0 = one view per rank per step (weak scaling)")
     args = ap.parse_args()
 
     if args.impl == "reference":
@@ -375,8 +406,16 @@ def main():
     # INSIDE the timed region (conservative: its time counts)
     flushes = [torch.empty(256 << 20, dtype=torch.uint8, device=dev) for _ in range(ns)]
 
-    def view_of(i):
-        return (rank + world * i) % N_VIEWS
+    # every step renders the same fixed batch of args.batch views,
+    # split contiguously over the ranks (sharding.batch_view_ids); --batch 0:
+    # one view per rank per step, round-robin over the orbit (views_for_rank)
+    batch = max(0, args.batch)
+    per_step = len(batch_view_ids(rank, world, 1, batch)) if batch else 1
+
+    def view_ids(first_step, steps):
+        if batch:
+            return batch_view_ids(rank, world, steps, batch)
+        return views_for_rank(rank, world, first_step + steps)[first_step:]
 
     # the whole batch of views is enqueued by one native call
     # (bs_render_views: view i on context i % ns, its L2 flush first), so the
@@ -387,16 +426,19 @@ def main():
     v_int = -1 if variant == "auto" else int(variant)
     bg_arr = (C.c_float * 3)(0.0, 0.0, 0.0)
 
-    def run_views(first, count, flush=True):
-        ids = (C.c_int32 * count)(*[view_of(first + j) for j in range(count)])
-        N.call("bs_render_views", ctx_arr, ns, C.c_void_p(g3d_dev.data_ptr()), int(n), cam_arr, ids, count, pw, ph,
+    def run_views(first_step, steps, flush=True):
+        vids = view_ids(first_step, steps)
+        ids = (C.c_int32 * max(1, len(vids)))(*vids)
+        N.call("bs_render_views", ctx_arr, ns, C.c_void_p(g3d_dev.data_ptr()), int(n), cam_arr, ids, len(vids), pw, ph,
                v_int, bg_arr, flush_arr if flush else None, (256 << 20) if flush else 0)
+        return vids
 
     def sync_all() -> int:
         return sum(f.sync() for f in fps)
 
     clk = make_clock_sampler(gpu)  # sampling spans warm-up + timed region (the timed region alone is < 1 s)
-    run_views(0, max(args.warmup, 2 * ns), flush=False)  # >= 2 frames per context: capacity calibrated, graphs captured
+    # >= 2 frames per context: capacity calibrated, graphs captured
+    run_views(0, max(args.warmup, -(-2 * ns // per_step)), flush=False)
     sync_all()
     torch.cuda.synchronize()
 
@@ -414,7 +456,7 @@ def main():
     t_start.record(main)
     for s_ in streams:
         s_.wait_stream(main)
-    run_views(args.warmup, args.steps)
+    timed_views = run_views(args.warmup, args.steps)
     for s_ in streams:  # join: the end event follows every context's last frame
         main.wait_stream(s_)
     t_end.record(main)
@@ -426,22 +468,23 @@ def main():
     graph_replays = sum(f.graph_launches() for f in fps) - glaunch0
     N.call("bs_render_set_fine_occupancy", 0)  # kernel-level timings below: full occupancy
     # which variant the on-device selector picked for each timed view (replayed untimed)
-    for i in range(args.steps):
-        _, fi = fp.forward(g3d_dev, n, cams[view_of(args.warmup + i)], variant=variant, info=True)
+    for vid in sorted(set(timed_views)):
+        _, fi = fp.forward(g3d_dev, n, cams[vid], variant=variant, info=True)
         used[fi.variant] = used.get(fi.variant, 0) + 1
     if world > 1:
         dist.barrier()
     clocks = clk.stop()
     total_ms = t_start.elapsed_time(t_end)
     if reruns:  # re-renders were enqueued after t_end: time them into the run
-        total_ms *= 1.0 + reruns / args.steps
+        total_ms *= 1.0 + reruns / max(1, len(timed_views))
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         if shared:
             t = t.cpu()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    value = world * args.steps / (max_ms / 1e3)
+    views_per_step = batch if batch else world  # all ranks
+    value = views_per_step * args.steps / (max_ms / 1e3)
 
     extras = {}
     if rank == 0 and not args.no_extras:
@@ -461,13 +504,18 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": max_ms / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if batch else "weak",
         "vs_baseline": None,
+        "views_per_step": views_per_step,
         "dtype": "f32+f64 (f32 alpha/T, f64 colour/depth accumulators)" if mode == N.ALPHA_EXACT else "f32",
         "data": "synthetic: gen_clustered_scene seed 42 (no dataset)",
         "config": dict(config_desc(args.config, W, H, n, pw, ph), alpha_mode=args.alpha, variant=args.variant,
                        variants_used={api.variant_name(k): c for k, c in used.items()},
-                       parallelism=f"view-sharded x{world} (scene replicated, no data-path collective)",
+                       parallelism=(f"view-sharded x{world}: each step is the fixed batch of orbit views 0..{batch - 1}, "
+                                    f"split contiguously ({per_step} per rank); scene replicated, no data-path "
+                                    f"collective" if batch else
+                                    f"view-sharded x{world}: one view per rank per step, round-robin over the "
+                                    f"orbit; scene replicated, no data-path collective"),
                        l2="flushed before every step (256 MiB write on the step's stream, inside the timed region)",
                        streams=ns, fine_ctas_per_sm=args.fine_ctas if ns > 1 else "max"),
         "gpu_launches": launches,
@@ -478,6 +526,53 @@ def main():
     }
     out.update(extras)
     print(json.dumps(out), flush=True)
+
+
+C3_POINTS = [(1.0, 0.035), (0.8, 0.032), (0.6, 0.03), (0.4, 0.027), (0.25, 0.025), (0.12, 0.022), (0.05, 0.02)]
+
+
+def c3_sweep(api, N, torch, W, H, pw, ph, n, f, mode, dev) -> dict:
+    """SURVEY 8d C3 on the C2 geometry: background_fraction 1.0 -> 0.05 with
+    cluster_sigma 0.035 -> 0.02 (uniform -> clustered).  Per point: warm
+    render times (CUDA events, median of 5) of every variant on the point's
+    16x16 TileBinning, the balanced kernels' ratio to the pixel-wise
+    baseline, the device selector's choice and its regret
+    t(chosen) / min_v t(v) - 1."""
+    out = {"points": []}
+    stream = torch.cuda.current_stream()
+    cam = api.camera(np.eye(4, dtype=np.float32), (f, f), W, H)
+    for bgf, sig in C3_POINTS:
+        g3d = api.gen_clustered_scene(n, cam, cluster_sigma=sig, background_fraction=bgf)
+        pipe = api.Pipeline(W, H, pw, ph, dev, mode)
+        frame, v_auto = pipe.forward(api.g3d_to_device(g3d, dev), n, cam, variant="auto")
+        s, b, st = pipe.splats, pipe.last_binning, pipe.last_stats
+        ms = {}
+        for v in range(5):
+            api.render_forward(v, s, b, W, H, pw, ph, (0, 0, 0), mode, st.task_order, frame, pipe.render_ws)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
+            for a, e in ev:
+                a.record(stream)
+                api.render_forward(v, s, b, W, H, pw, ph, (0, 0, 0), mode, st.task_order, frame, pipe.render_ws)
+                e.record(stream)
+            torch.cuda.synchronize()
+            ms[api.variant_name(v)] = round(float(np.median([a.elapsed_time(e) for a, e in ev])), 4)
+        summ = st.summary()
+        best = min(ms.values())
+        out["points"].append({
+            "background_fraction": bgf, "cluster_sigma": sig, "K": b.k, "tile_max": summ["max"],
+            "tile_mean": round(summ["mean"], 1), "render_ms": ms,
+            "fg_over_naive": round(ms["Naive"] / ms["FineGrainedCombined"], 3),
+            "gw_over_naive": round(ms["Naive"] / ms["GaussianWise"], 3),
+            "selected": api.variant_name(v_auto), "regret": round(ms[api.variant_name(v_auto)] / best - 1.0, 4)})
+        del pipe, frame, s, b, st
+        torch.cuda.empty_cache()
+    ext = max(out["points"], key=lambda p: p["tile_max"] / max(1.0, p["tile_mean"]))
+    out["most_imbalanced"] = {"background_fraction": ext["background_fraction"], "cluster_sigma": ext["cluster_sigma"],
+                              "fg_over_naive": ext["fg_over_naive"], "gw_over_naive": ext["gw_over_naive"],
+                              "north_star_target": 3.0}
+    out["def"] = ("render-kernel times on each point's 16x16 TileBinning (bs_render_forward), warm, one identity view "
+                  "of the C2 geometry; most_imbalanced = the point with the largest max/mean tile list length")
+    return out
 
 
 def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, mode, dev, world) -> dict:
@@ -504,10 +599,10 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
 
     def time_render(variant, m, reps=5):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
-        api.render_forward(variant, s, b, W, H, pw, ph, (0, 0, 0), m, st.task_order, frame)
+        api.render_forward(variant, s, b, W, H, pw, ph, (0, 0, 0), m, st.task_order, frame, pipe.render_ws)
         for a, e in ev:
             a.record(stream)
-            api.render_forward(variant, s, b, W, H, pw, ph, (0, 0, 0), m, st.task_order, frame)
+            api.render_forward(variant, s, b, W, H, pw, ph, (0, 0, 0), m, st.task_order, frame, pipe.render_ws)
             e.record(stream)
         torch.cuda.synchronize()
         return float(np.mean([a.elapsed_time(e) for a, e in ev]))
@@ -518,7 +613,7 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     mname = "exact" if mode == N.ALPHA_EXACT else "fast"
     vsel = v_auto if args.variant == "auto" else api.variant_from_name(args.variant)
     t_render = time_render(vsel, mode, reps=10)
-    api.render_forward(vsel, s, b, W, H, pw, ph, (0, 0, 0), mode, st.task_order, frame)
+    api.render_forward(vsel, s, b, W, H, pw, ph, (0, 0, 0), mode, st.task_order, frame, pipe.render_ws)
     E, Cc = api.frame_work(frame, b, pw, ph)
     K, P = b.k, W * H
     ops = 16 * E + 8 * Cc
@@ -530,12 +625,7 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     bytes_alg = 44 * K + 32 * P
     t_s = t_render / 1e3
     t_roof = max(ops / fp32_peak, E / mufu_peak, bytes_alg / hbm_peak)
-    traffic = None
-    try:
-        with open(NCU_TRAFFIC_PATH) as fh:
-            traffic = json.load(fh).get(f"{args.config}_{api.variant_name(vsel)}_{mname}")  # per config
-    except Exception:
-        pass
+    traffic = (load_counters().get(f"{args.config}_{api.variant_name(vsel)}_{mname}") or {}).get("dram_bytes")
     res["fwd_render_ms_per_frame"] = t_render
     res["blends_per_s"] = E / t_s
     res["frame_work"] = {"evaluated_pairs_E": E, "committed_pairs_C": Cc, "tile_instances_K": K, "pixels": P,
@@ -543,9 +633,6 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     res["render_ms_by_variant"] = per_variant
     naive = per_variant[mname]["Naive"]
     res["speedup_vs_naive"] = {k: round(naive / v, 3) for k, v in per_variant[mname].items()}
-    # SURVEY §8d roofline: t_roof = max(ops/FP32, E/MUFU, bytes/HBM); for this
-    # frame the HBM term (44 B per tile instance + 32 B per pixel) is the max,
-    # so the contract's "hbm" view is the headline and the issue view rides along
     # list entries any pixel of a tile still reads under the serial semantics:
     # the tile's longest consumed prefix (max over its pixels of term, or the
     # whole list) — K*44 over-counts lists whose tail lies past every stop
@@ -577,31 +664,76 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
                           "(bs_render_forward, the API path)", "t_ms": t_api_s * 1e3,
                 "frac": bytes_alg / t_api_s / hbm_peak, "t_roof_frac": t_roof / t_api_s, "traffic": traffic}
     if sup.value:
-        traffic = None
-        try:
-            with open(NCU_TRAFFIC_PATH) as fh:
-                traffic = json.load(fh).get(f"{args.config}_{api.variant_name(vsel)}_{mname}_super")
-        except Exception:
-            pass
+        traffic = (load_counters().get(f"{args.config}_{api.variant_name(vsel)}_{mname}_super") or {}).get(
+            "dram_bytes")
     res["fwd_render_ms_per_frame_pipeline"] = t_s * 1e3
     kname = (f"render {api.variant_name(vsel)} ({mname}) on super-tile lists (frame pipeline: the timed frames' "
              "render stage)") if sup.value else f"render {api.variant_name(vsel)} ({mname})"
-    res["roofline"] = {
-        "bound": "hbm", "kernel": kname, "t_ms": t_s * 1e3,
-        "achieved": bytes_alg / t_s / 1e9, "peak": hbm_peak / 1e9, "unit": "GB/s",
-        "frac": bytes_alg / t_s / hbm_peak, "traffic": traffic, "algorithmic_bytes": bytes_alg,
-        "api_kernel_view": api_view,
-        "bytes_def": "SURVEY 8d: 44 B per tile instance (u32 index + 40 B attributes) + 32 B per output pixel",
-        "peak_source": hbm_src,
-        "t_roof_ms": t_roof * 1e3, "t_roof_frac": t_roof / t_s,
-        "consumed_prefix_view": {
-            "bytes": bytes_prefix, "frac": bytes_prefix / t_s / hbm_peak,
+    # The bound is chosen from MEASURED counters of this kernel (one ncu
+    # --set full capture per change, profiles/ncu_counters.json, written by
+    # tools/ncu_counters.py): the time its measured warp instructions need at
+    # one issue per scheduler per clock (148 SMs x 4) vs the time its
+    # consumed-prefix bytes (what tile-serial blending must read) and its
+    # measured DRAM bytes need at the HBM peak.  The headline achieved / peak
+    # / frac is then the ALGORITHMIC work of that resource (SURVEY 8d:
+    # 16E + 8C FP32-pipe instructions, or 44K + 32P bytes) per launch over the
+    # measured launch time.
+    ckey = f"{args.config}_{api.variant_name(vsel)}_{mname}" + ("_super" if sup.value else "")
+    cnt = load_counters().get(ckey)
+    clk_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    issue_peak = 148 * 4 * clk_hz  # warp instructions / s
+    measured = {}
+    if cnt:
+        measured = {"counters_key": ckey, "source": cnt.get("source"),
+                    "warp_instructions": cnt.get("inst_executed"), "dram_bytes": cnt.get("dram_bytes"),
+                    "issue_slot_util_ncu": cnt.get("issue_active_pct")}
+        if cnt.get("inst_executed"):
+            measured["t_issue_ms"] = cnt["inst_executed"] / issue_peak * 1e3
+            measured["issue_util"] = cnt["inst_executed"] / issue_peak / t_s
+            measured["thread_instr_per_evaluated_pair"] = (cnt["inst_executed"] * cnt.get("avg_active_lanes", 32.0)
+                                                           / max(1, E))
+        if cnt.get("dram_bytes") is not None:
+            measured["dram_util"] = cnt["dram_bytes"] / t_s / hbm_peak
+    prefix_util = bytes_prefix / t_s / hbm_peak
+    mem_util = max(prefix_util, measured.get("dram_util", 0.0))
+    issue_util = measured.get("issue_util", ops / t_s / fp32_peak)
+    bound = "issue" if issue_util >= mem_util else "hbm"
+    if bound == "issue":
+        head = {"achieved": ops / t_s / 1e9, "peak": fp32_peak / 1e9, "unit": "Ginstr/s (FP32 lanes)",
+                "frac": ops / t_s / fp32_peak,
+                "work_def": "SURVEY 8d: 16 FP32-pipe instructions per evaluated pair E + 8 per committed pair C",
+                "algorithmic_work": ops}
+    else:
+        head = {"achieved": bytes_alg / t_s / 1e9, "peak": hbm_peak / 1e9, "unit": "GB/s",
+                "frac": bytes_alg / t_s / hbm_peak,
+                "work_def": "SURVEY 8d: 44 B per tile instance + 32 B per output pixel", "algorithmic_work": bytes_alg}
+    res["roofline"] = dict(
+        {"bound": bound, "bound_basis": ("measured: issue_util (ncu warp instructions / (148 SMs x 4 x clock x t)) "
+                                         f"{issue_util:.3f} vs memory util (max of consumed-prefix bytes and ncu DRAM "
+                                         f"bytes / (HBM peak x t)) {mem_util:.3f}"),
+         "kernel": kname, "t_ms": t_s * 1e3},
+        **head,
+        traffic=measured.get("dram_bytes", traffic), measured=measured,
+        t_roof_ms=t_roof * 1e3, t_roof_frac=t_roof / t_s,
+        t_roof_def="SURVEY 8d: max(16E+8C / FP32 peak, E / MUFU peak, (44K+32P) / HBM peak)",
+        api_kernel_view=api_view, peak_source=hbm_src,
+        hbm_view={"achieved": bytes_alg / t_s / 1e9, "peak": hbm_peak / 1e9, "unit": "GB/s",
+                  "frac": bytes_alg / t_s / hbm_peak, "algorithmic_bytes": bytes_alg},
+        consumed_prefix_view={
+            "bytes": bytes_prefix, "frac": prefix_util,
             "def": "44 B per entry of each tile's longest consumed list prefix + 32 B per pixel: what tile-serial "
-                   "blending must read; K*44 exceeds it when list tails lie past every pixel's stop (C4)"},
-        "issue_view": {"achieved_ginstr_s": ops / t_s / 1e9, "peak_ginstr_s": fp32_peak / 1e9,
-                       "frac": (ops / t_s) / fp32_peak, "ops": ops,
-                       "def": "FP32-pipe instructions 16E+8C (SURVEY 8d), peak 148 SMs x 128 lanes x sm_max_mhz"},
-        "mufu_view": {"frac": (E / t_s) / mufu_peak}}
+                   "blending must read; K*44 exceeds it when list tails lie past every pixel's stop"},
+        issue_view={"achieved_ginstr_s": ops / t_s / 1e9, "peak_ginstr_s": fp32_peak / 1e9,
+                    "frac": (ops / t_s) / fp32_peak, "ops": ops,
+                    "def": "FP32-pipe instructions 16E+8C (SURVEY 8d), peak 148 SMs x 128 lanes x sm_max_mhz"},
+        mufu_view={"frac": (E / t_s) / mufu_peak})
+
+    # C3: the imbalance sweep on the C2 geometry — render time of
+    # the pixel-wise baseline vs the balanced kernels at every point, the
+    # north-star ratio FG / Naive on the most imbalanced scene, and the
+    # per-frame selector's choice and regret
+    if not args.no_c3:
+        res["c3_sweep"] = c3_sweep(api, N, torch, W, H, pw, ph, n, cams[0].focal[0], mode, dev)
 
     # e2e: host buffers through the pipelined C-ABI host frame API — every
     # step uploads the scene from pinned host memory and downloads all six
@@ -663,12 +795,11 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
         g2d = api.splats_to_g2d(s)
         pl = b.point_list.cpu().numpy().view(np.uint32)
         ranges = b.tile_ranges.cpu().numpy().view(np.uint32)
-        sys.path.insert(0, os.path.join(ROOT, "tests"))
-        import oracle_lib as O
+        O, R, kind = cpu_libs()
         ocam = O.Camera.from_buffer_copy(bytes(cam_id))
-        tcpu, parts, desc = cpu_sample_estimate(g3d.view(O.G3D_DTYPE), ocam, g2d.view(O.G2D_DTYPE), pl, ranges, W, H,
-                                                pw, ph, 1, args.cpu_budget)
-        res["cpu_baseline"] = {"value": 1.0 / tcpu, "unit": "views/s", "cores": 1, "kind": "port", "sample": desc,
+        tcpu, parts, desc = cpu_sample_estimate(O, R, g3d.view(O.G3D_DTYPE), ocam, g2d.view(O.G2D_DTYPE), pl, ranges,
+                                                W, H, pw, ph, args.cpu_budget, variant=3)
+        res["cpu_baseline"] = {"value": 1.0 / tcpu, "unit": "views/s", "cores": 1, "kind": kind, "sample": desc,
                                "stage_s": parts, "host_cpu": os.cpu_count()}
     return res
 

@@ -285,9 +285,13 @@ int bs_select_variant_device(const bs_tile_histogram* stats, int32_t width, int3
 
 /* ---- diagnostics ----
  * y[i] = the device exp the render kernels use in alpha_mode (EXACT: the
- * glibc-identical expf; FAST: ex2.approx).  Used by the parity tests to pin
- * the exact path against the host libm. */
+ * glibc-identical expf, through the same in-range function and shared-memory
+ * table the render's eval_step calls on [-0x1.9fe368p6, 0], the general one
+ * elsewhere; FAST: ex2.approx).  Used by the parity tests to pin the exact
+ * path against the host libm.  _range: x = the float with bit pattern
+ * first_bits + i (exhaustive sweeps without an input array). */
 int bs_test_expf(const float* x, float* y, int64_t n, int alpha_mode, void* stream);
+int bs_test_expf_range(uint32_t first_bits, int64_t n, float* y, int alpha_mode, void* stream);
 
 /* ---- host-side helpers (implemented in the C++ host layer) ----
  * gen_clustered_scene (src/workload.cpp:198-246, include/splatsim/workload.hpp:68-76):

@@ -272,6 +272,29 @@ int64_t orc_expf_exhaustive_check(float lo, float hi, float* bad_x, int max_bad)
   return bad;
 }
 
+// Count of i in [0, n) with y[i] != libm expf(float with bits first_bits + i),
+// over all host threads (exhaustive sweeps of the device exp).
+int64_t orc_expf_compare_range(uint32_t first_bits, int64_t n, const float* y) {
+  const unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+  std::vector<int64_t> bad(nt, 0);
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < nt; ++t)
+    pool.emplace_back([&, t]() {
+      const int64_t b = n * int64_t(t) / int64_t(nt), e = n * int64_t(t + 1) / int64_t(nt);
+      for (int64_t i = b; i < e; ++i) {
+        const uint32_t u = first_bits + uint32_t(i);
+        float x;
+        std::memcpy(&x, &u, 4);
+        const float a = std::exp(x);
+        if (std::memcmp(&a, &y[i], 4) != 0) ++bad[t];
+      }
+    });
+  for (auto& th : pool) th.join();
+  int64_t s = 0;
+  for (int64_t b : bad) s += b;
+  return s;
+}
+
 // Count of i with y[i] != libm expf(x[i]) bitwise.
 int64_t orc_expf_compare_batch(const float* x, const float* y, int64_t n) {
   int64_t bad = 0;

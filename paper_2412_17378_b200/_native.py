@@ -86,6 +86,7 @@ SIGNATURES = {
     "bs_render_set_fine_occupancy": (C.c_int, [_i32]),
     "bs_select_variant": (C.c_int, [C.POINTER(TileHistogram), _i32, _i32, _i32, _i32, _i32]),
     "bs_test_expf": (C.c_int, [_vp, _vp, _i64, C.c_int, _vp]),
+    "bs_test_expf_range": (C.c_int, [C.c_uint32, _i64, _vp, C.c_int, _vp]),
     "bs_context_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
     "bs_context_destroy": (C.c_int, [_vp]),
     "bs_context_stream": (_vp, [_vp]),

@@ -170,13 +170,19 @@ struct Accum<BS_ALPHA_EXACT> {
     b = __dadd_rn(b, __dmul_rn((double)col.z, w));
     d = __dadd_rn(d, __dmul_rn((double)dep, w));
   }
-  // colour/depth already widened to double (rg = (r, g), bd = (b, depth))
+  // colour/depth already widened to double (rg = (r, g), bd = (b, depth));
+  // FineGrainedCombined's batch loop: the exact weight w = alpha * t (a
+  // 24 x 24-bit product, exact in double) and one fused multiply-add per
+  // channel — the reference rounds the product and the sum separately
+  // (src/blend.cpp:28-32), so the double sums may differ in their last bit
+  // (the Gaussian-wise variants' colour bar: 1e-6; the float outputs are
+  // almost always identical)
   __device__ __forceinline__ void add_wide(float alpha, float t, double2 rg, double2 bd) {
     const double w = __dmul_rn((double)alpha, (double)t);
-    r = __dadd_rn(r, __dmul_rn(rg.x, w));
-    g = __dadd_rn(g, __dmul_rn(rg.y, w));
-    b = __dadd_rn(b, __dmul_rn(bd.x, w));
-    d = __dadd_rn(d, __dmul_rn(bd.y, w));
+    r = __fma_rn(rg.x, w, r);
+    g = __fma_rn(rg.y, w, g);
+    b = __fma_rn(bd.x, w, b);
+    d = __fma_rn(bd.y, w, d);
   }
   __device__ __forceinline__ void store(double* o) const { o[0] = r; o[1] = g; o[2] = b; o[3] = d; }
   __device__ __forceinline__ void load(const double* o) { r = o[0]; g = o[1]; b = o[2]; d = o[3]; }
@@ -772,8 +778,13 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
   if (inside && !donated) acc.finish(A, (size_t)py * A.W + px, t, contrib, term);
 }
 
-template <int MODE, int LM>
-__global__ void __launch_bounds__(kFineThreads, 4) k_render_fine(RArgs A, int subs) {
+// MINB: resident CTAs per SM the register budget is sized for — 4 (64
+// registers) when the kernel has the SMs to itself, 3 (80 registers: the
+// exp's constants and table base stay in registers instead of being
+// re-loaded every list entry) when it is capped at 3 CTAs per SM to share the
+// SMs with other frame contexts (bs_render_set_fine_occupancy)
+template <int MODE, int LM, int MINB>
+__global__ void __launch_bounds__(kFineThreads, MINB) k_render_fine(RArgs A, int subs) {
   __shared__ float4 s_rec[kFineWarps][4][32];
   __shared__ int s_k[kFineWarps][32];
   __shared__ unsigned long long s_tab[32];
@@ -959,12 +970,13 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
       BS_CUDA_TRY(cudaGetDevice(&dev));
       BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       const int lm = A.sup ? kListSuper : kListTile;
-      BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_fine<MODE, kListTile>, kFineThreads,
-                                                                0));
+      BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_fine<MODE, kListTile, 4>,
+                                                                kFineThreads, 0));
       // bs_render_set_fine_occupancy / BS_FINE_CTAS_PER_SM: fewer resident
       // CTAs leave SM room for another frame context's kernels
       const int cap = g_fine_ctas_per_sm > 0 ? g_fine_ctas_per_sm : env_int("BS_FINE_CTAS_PER_SM", per_sm);
       per_sm = max(1, min(per_sm, cap));
+      const bool wide = per_sm <= 3 && env_int("BS_FINE_WIDE", 1) != 0;  // the 80-register build
       const int subs = ((A.pw + kSubW - 1) / kSubW) * ((A.ph + kSubH - 1) / kSubH);  // sub-tiles per tile
       const int64_t total = (int64_t)T * subs;
       if (total > 0x7fffffff) return BS_ERR_UNSUPPORTED;
@@ -976,10 +988,13 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
       B.donate_after = env_int("BS_FINE_DONATE_AFTER", kDonateAfter);
       B.donate_min_remain = env_int("BS_FINE_DONATE_MIN", kDonateMinRemain);
       B.stragglers = env_int(A.sup ? "BS_FINE_STRAGGLERS_SUPER" : "BS_FINE_STRAGGLERS", kStragglers);
-      if (lm == kListSuper)
-        k_render_fine<MODE, kListSuper><<<grid, kFineThreads, 0, st>>>(B, subs);
-      else
-        k_render_fine<MODE, kListTile><<<grid, kFineThreads, 0, st>>>(B, subs);
+      if (lm == kListSuper) {
+        if (wide) k_render_fine<MODE, kListSuper, 3><<<grid, kFineThreads, 0, st>>>(B, subs);
+        else k_render_fine<MODE, kListSuper, 4><<<grid, kFineThreads, 0, st>>>(B, subs);
+      } else {
+        if (wide) k_render_fine<MODE, kListTile, 3><<<grid, kFineThreads, 0, st>>>(B, subs);
+        else k_render_fine<MODE, kListTile, 4><<<grid, kFineThreads, 0, st>>>(B, subs);
+      }
       BS_LAUNCH_CHECK();
       if (B.donate) {
         int per_sm2 = 0;
@@ -1119,20 +1134,39 @@ extern "C" int bs_super_tile_ranges(const uint32_t* super_ranges, int32_t width,
 }
 
 namespace bs {
+// The render's exp, exactly as eval_step calls it: EXACT mode ->
+// glibc_expf_fast (valid on [-0x1.9fe368p6, 0], the range power_cut and the
+// power > 0 skip leave it) with the table in shared memory through ExpK;
+// inputs outside that range take the general glibc_expf.  FAST mode -> the
+// ex2.approx path.
+__device__ __forceinline__ float render_expf(float x, int mode, const ExpK& ek, const unsigned long long* s_tab) {
+  float e;
+  if (mode == BS_ALPHA_EXACT) {
+    e = (x >= -0x1.9fe368p6f && x <= 0.0f) ? glibc_expf_fast(x, ek) : glibc_expf(x, s_tab);
+  } else {
+    const float p2 = x * 1.4426950408889634f;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(p2));
+  }
+  return e;
+}
+
 __global__ void k_test_expf(const float* __restrict__ x, float* __restrict__ y, int64_t n, int mode) {
   __shared__ unsigned long long s_tab[32];
   load_tab(s_tab);
   __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float e;
-    if (mode == BS_ALPHA_EXACT) {
-      e = glibc_expf(x[i], s_tab);
-    } else {
-      const float p2 = x[i] * 1.4426950408889634f;
-      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(p2));
-    }
-    y[i] = e;
-  }
+  const ExpK ek = make_expk(s_tab);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = render_expf(x[i], mode, ek, s_tab);
+}
+
+// y[i] = exp(float with bit pattern first_bits + i)
+__global__ void k_test_expf_range(uint32_t first_bits, float* __restrict__ y, int64_t n, int mode) {
+  __shared__ unsigned long long s_tab[32];
+  load_tab(s_tab);
+  __syncthreads();
+  const ExpK ek = make_expk(s_tab);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = render_expf(__uint_as_float(first_bits + (uint32_t)i), mode, ek, s_tab);
 }
 }  // namespace bs
 
@@ -1141,6 +1175,15 @@ extern "C" int bs_test_expf(const float* x, float* y, int64_t n, int alpha_mode,
   if (n == 0) return BS_OK;
   const int64_t blocks = min((n + 255) / 256, (int64_t)148 * 16);
   k_test_expf<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, y, n, alpha_mode);
+  BS_LAUNCH_CHECK();
+  return BS_OK;
+}
+
+extern "C" int bs_test_expf_range(uint32_t first_bits, int64_t n, float* y, int alpha_mode, void* stream) {
+  if (n < 0 || (n > 0 && !y) || (uint64_t)first_bits + (uint64_t)n > 0x100000000ull) return BS_ERR_INVALID_ARGUMENT;
+  if (n == 0) return BS_OK;
+  const int64_t blocks = min((n + 255) / 256, (int64_t)148 * 16);
+  k_test_expf_range<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(first_bits, y, n, alpha_mode);
   BS_LAUNCH_CHECK();
   return BS_OK;
 }

@@ -28,6 +28,15 @@ def contiguous_shard(n_views: int, rank: int, world: int) -> range:
     return range(lo, lo + base + (1 if rank < extra else 0))
 
 
+def batch_view_ids(rank: int, world: int, steps: int, batch: int = N_VIEWS) -> list[int]:
+    """View ids rank `rank` renders over `steps` steps of the §8(e) batch
+    schedule: every step is the same fixed batch of `batch` views
+    (0..batch-1 of the orbit), split contiguously over the ranks
+    (contiguous_shard) — the total work per step is fixed (strong scaling)."""
+    mine = list(contiguous_shard(batch, rank, world))
+    return mine * steps
+
+
 def orbit_view(k: int, n_views: int = N_VIEWS, pivot_z: float = PIVOT_Z) -> np.ndarray:
     """World->camera 4x4 of view k: yaw -15..+15 deg about the y axis through
     (0, 0, pivot_z); the rotation block is orthonormal (src/scene.cpp:45-47)."""

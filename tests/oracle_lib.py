@@ -76,6 +76,8 @@ def lib() -> C.CDLL:
         L.orc_expf_exhaustive_check.restype = i64
         L.orc_expf_compare_batch.argtypes = [vp, vp, i64]
         L.orc_expf_compare_batch.restype = i64
+        L.orc_expf_compare_range.argtypes = [C.c_uint32, i64, vp]
+        L.orc_expf_compare_range.restype = i64
         _lib = L
     return _lib
 

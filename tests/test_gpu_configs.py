@@ -1,0 +1,209 @@
+"""GPU parity on BASELINE.json's own configurations, vs
+the CPU oracle on the same seeded inputs:
+
+  C2  1920x1080, 1M clustered Gaussians, seed 42 — FULL FRAME: the GPU
+      binning bit-exact; every variant through the C-ABI (bs_render_forward)
+      on the reference's 16x16 TileBinning; the frame pipeline (fused
+      projection + super-tile lists + device-selected variant, async, CUDA
+      graphs) — all against O.render on every pixel.
+  C5  views {0, 31, 63} of the 64-view orbit (sharding.orbit_view, the
+      bench's view schedule), full frames through the frame pipeline + the
+      Naive API path.
+  C3  the imbalance sweep's 7 geometric points, every variant on sampled
+      tiles (the 32 longest + 1 % random, seed 42; tiles are independent).
+  SPEC acceptance #1: 100 seeded random scenes (<= 5k
+      Gaussians, 128x128, random patch / background / opacity), all 5
+      variants.
+
+Bars: contrib / term / final_t / alpha bit-exact for every variant;
+colour / depth bit-exact for the pixel-wise variants and within 1e-6 (abs;
+depth relative to max(1, |ref|)) for the Gaussian-wise ones.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from paper_2412_17378_b200 import _native as N  # noqa: E402
+from paper_2412_17378_b200 import api  # noqa: E402
+from paper_2412_17378_b200 import sharding  # noqa: E402
+
+DEV = "cuda"
+W2, H2, F2, N2 = 1920, 1080, 1000.0, 1_000_000
+BG = (0.1, 0.2, 0.3)
+PIXELWISE = (0, 1, 4)
+
+
+def ncam(o_cam):
+    return N.Camera.from_buffer_copy(bytes(o_cam))
+
+
+def assert_frame(got: dict, ref: dict, variant: int, pixels=None, tag=""):
+    sel = (lambda a: a) if pixels is None else (lambda a: a[pixels])
+    csel = (lambda a: a) if pixels is None else (lambda a: a.reshape(-1, 3)[pixels])
+    for k in ("contrib", "term"):
+        assert np.array_equal(sel(got[k]), sel(ref[k])), (tag, variant, k)
+    for k in ("final_t", "alpha"):
+        assert np.array_equal(sel(got[k]).view(np.uint32), sel(ref[k]).view(np.uint32)), (tag, variant, k)
+    if variant in PIXELWISE:
+        assert np.array_equal(csel(got["color"]).view(np.uint32), csel(ref["color"]).view(np.uint32)), (tag, variant)
+        assert np.array_equal(sel(got["depth"]).view(np.uint32), sel(ref["depth"]).view(np.uint32)), (tag, variant)
+    else:
+        assert float(np.abs(csel(got["color"]) - csel(ref["color"])).max(initial=0.0)) <= 1e-6, (tag, variant)
+        rel = np.abs(sel(got["depth"]) - sel(ref["depth"])) / np.maximum(1.0, np.abs(sel(ref["depth"])))
+        assert float(rel.max(initial=0.0)) <= 1e-6, (tag, variant)
+
+
+def gpu_binning(g2d, W, H, pw=16, ph=16):
+    s = api.splats_from_g2d(g2d, DEV)
+    b = api.bin_tiles(s, W, H, pw, ph)
+    st = api.tile_load_histogram(b)
+    return s, b, st
+
+
+def api_render(v, s, b, st, W, H, mode=N.ALPHA_EXACT, pw=16, ph=16):
+    f = api.render_forward(v, s, b, W, H, pw, ph, BG, mode, st.task_order)
+    torch.cuda.synchronize()
+    return f.to_numpy()
+
+
+@pytest.fixture(scope="module")
+def c2():
+    cam = O.make_camera(focal=(F2, F2), width=W2, height=H2)
+    g3d = O.gen_clustered_scene(N2, cam)
+    g2d = O.project_all(g3d, cam)
+    pl, rg = O.bin_tiles(g2d, W2, H2, 16, 16)
+    refs = {v: O.render(v, pl, rg, g2d, W2, H2, 16, 16, BG, lazy=True, threads=0) for v in (0, 2, 3)}
+    return cam, g3d, g2d, pl, rg, refs
+
+
+def test_c2_binning_full_frame(c2):
+    cam, g3d, g2d, pl, rg, _ = c2
+    assert len(pl) > 40_000_000  # the headline's 43.6 M tile instances
+    s, b, _ = gpu_binning(g2d, W2, H2)
+    assert b.k == len(pl)
+    assert np.array_equal(b.tile_ranges.cpu().numpy().view(np.uint32), rg)
+    assert np.array_equal(b.point_list.cpu().numpy().view(np.uint32), pl)
+    got = api.splats_to_g2d(api.project_all(api.g3d_to_device(g3d), N2, ncam(cam)))
+    assert got.tobytes() == g2d.tobytes()
+
+
+@pytest.mark.parametrize("variant", range(5))
+def test_c2_full_frame_api(c2, variant):
+    """bs_render_forward on the reference's 16x16 TileBinning, every pixel."""
+    cam, g3d, g2d, pl, rg, refs = c2
+    s, b, st = gpu_binning(g2d, W2, H2)
+    got = api_render(variant, s, b, st, W2, H2)
+    ref = refs[0] if variant in PIXELWISE else refs[variant]
+    assert_frame(got, ref, variant, tag="C2")
+    if variant == 3:  # FineGrainedCombined blends with serial weights: == render_reference too
+        assert float(np.abs(got["color"] - refs[0]["color"]).max()) <= 1e-6
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_c2_full_frame_pipeline(c2, graphs):
+    """The bench's path: fused projection + binning at 32x32 super-tiles,
+    device-selected variant, async K checks (+ CUDA-graph replays)."""
+    cam, g3d, g2d, pl, rg, refs = c2
+    fp = api.FramePipeline(W2, H2, 16, 16, DEV, N.ALPHA_EXACT, async_mode=True, graphs=graphs)
+    d = api.g3d_to_device(g3d)
+    for _ in range(3 if graphs else 1):
+        fp.forward(d, N2, ncam(cam), variant="auto", bg=BG)
+    fp.sync()
+    mode = N.C.c_int32(0)
+    N.call("bs_context_list_mode", fp.ctx, N.C.byref(mode))
+    assert mode.value == 1
+    info = fp.last_info()
+    assert info.k == len(pl) and info.n_visible == len(g2d)
+    got = fp.frame.to_numpy()
+    assert_frame(got, refs[0] if info.variant in PIXELWISE else refs[info.variant], info.variant, tag="C2 pipeline")
+    if graphs:
+        assert fp.graph_launches() >= 1
+    fp.close()
+
+
+@pytest.mark.parametrize("k", [0, 31, 63])
+def test_c5_views_full_frame(k):
+    """C5: orbit views 0, 31, 63 of the C2 scene, every pixel, through the
+    frame pipeline (auto) and the Naive API path; GPU binning bit-exact."""
+    cam0 = O.make_camera(focal=(F2, F2), width=W2, height=H2)
+    g3d = O.gen_clustered_scene(N2, cam0)
+    cam = O.make_camera(view=sharding.orbit_view(k), focal=(F2, F2), width=W2, height=H2)
+    g2d = O.project_all(g3d, cam)
+    pl, rg = O.bin_tiles(g2d, W2, H2, 16, 16)
+    ref = O.render(0, pl, rg, g2d, W2, H2, 16, 16, BG, lazy=True, threads=0)
+    fp = api.FramePipeline(W2, H2, 16, 16, DEV, N.ALPHA_EXACT, async_mode=True)
+    fp.forward(api.g3d_to_device(g3d), N2, ncam(cam), variant="auto", bg=BG)
+    fp.sync()
+    info = fp.last_info()
+    assert info.k == len(pl)
+    assert_frame(fp.frame.to_numpy(), ref, 0 if info.variant in PIXELWISE else 3, tag=f"C5 view {k}")
+    fp.close()
+    s, b, st = gpu_binning(g2d, W2, H2)
+    assert np.array_equal(b.point_list.cpu().numpy().view(np.uint32), pl)
+    assert_frame(api_render(0, s, b, st, W2, H2), ref, 0, tag=f"C5 view {k} Naive")
+
+
+C3_POINTS = [(1.0, 0.035), (0.8, 0.032), (0.6, 0.03), (0.4, 0.027), (0.25, 0.025), (0.12, 0.022), (0.05, 0.02)]
+
+
+@pytest.mark.parametrize("bgf,sigma", C3_POINTS)
+def test_c3_sweep_sampled_tiles(bgf, sigma):
+    """C3 point: every variant renders the full frame on the GPU; the oracle
+    renders the 32 longest tiles + 1 % random tiles; those pixels compared."""
+    cam = O.make_camera(focal=(F2, F2), width=W2, height=H2)
+    g3d = O.gen_clustered_scene(N2, cam, sigma=sigma, bgfrac=bgf)
+    g2d = O.project_all(g3d, cam)
+    pl, rg = O.bin_tiles(g2d, W2, H2, 16, 16)
+    cols, rows = (W2 + 15) // 16, (H2 + 15) // 16
+    lens = (rg[1::2] - rg[0::2]).astype(np.int64)
+    rng = np.random.default_rng(42)
+    tiles = np.unique(np.concatenate([np.argsort(-lens, kind="stable")[:32],
+                                      rng.choice(cols * rows, size=(cols * rows) // 100, replace=False)]))
+    ty, tx = np.divmod(tiles, cols)
+    yy, xx = np.meshgrid(np.arange(16), np.arange(16), indexing="ij")
+    px = (tx[:, None, None] * 16 + xx[None]).reshape(-1)
+    py = (ty[:, None, None] * 16 + yy[None]).reshape(-1)
+    keep = (px < W2) & (py < H2)
+    pixels = py[keep] * W2 + px[keep]
+    refs = {v: O.render(v, pl, rg, g2d, W2, H2, 16, 16, BG, lazy=True, threads=0, tiles=tiles) for v in (0, 2)}
+    s, b, st = gpu_binning(g2d, W2, H2)
+    assert np.array_equal(b.tile_ranges.cpu().numpy().view(np.uint32), rg)
+    for v in range(5):
+        got = api_render(v, s, b, st, W2, H2)
+        assert_frame(got, refs[2] if v == 2 else refs[0], v, pixels=pixels, tag=f"C3 {bgf}")
+
+
+def test_spec_acceptance_100_random_scenes():
+    """100 seeded random scenes, every variant (GPU, exact
+    mode) equals the oracle: contrib / term / T / alpha exact; colour and
+    depth bit-exact pixel-wise, within 1e-6 Gaussian-wise."""
+    rng = np.random.default_rng(619)
+    W = H = 128
+    for i in range(100):
+        n = int(rng.integers(0, 5001))
+        pw, ph = [(16, 16), (16, 8), (8, 8), (32, 16), (8, 16)][i % 5]
+        f = float(rng.uniform(60.0, 400.0))
+        cam = O.make_camera(focal=(f, f), width=W, height=H)
+        g3d = O.gen_clustered_scene(n, cam, n_clusters=int(rng.integers(1, 6)), seed=1000 + i,
+                                    sigma=float(rng.uniform(0.01, 0.08)), bgfrac=float(rng.uniform(0.0, 1.0)))
+        if n:
+            g3d["opacity"] *= np.float32(rng.uniform(0.05, 1.0))
+        bg = tuple(float(x) for x in rng.uniform(0, 1, 3))
+        g2d = O.project_all(g3d, cam)
+        pl, rg = O.bin_tiles(g2d, W, H, pw, ph)
+        refs = {v: O.render(v, pl, rg, g2d, W, H, pw, ph, bg, lazy=True, threads=0) for v in (0, 2)}
+        s = api.splats_from_g2d(g2d, DEV)
+        b = api.bin_tiles(s, W, H, pw, ph)
+        assert b.k == len(pl)
+        st = api.tile_load_histogram(b)
+        for v in range(5):
+            f_ = api.render_forward(v, s, b, W, H, pw, ph, bg, N.ALPHA_EXACT, st.task_order)
+            torch.cuda.synchronize()
+            assert_frame(f_.to_numpy(), refs[2] if v == 2 else refs[0], v, tag=f"scene {i}")

@@ -48,16 +48,35 @@ def test_library_loads_and_device():
 
 
 def test_exact_expf_matches_libm():
-    # every float in [-6, 0] at stride 7 (~1.5e8 values), plus the glibc special case
-    lo = np.float32(-6.0).view(np.uint32)
-    bits = np.arange(0x80000000, int(lo) + 1, 7, dtype=np.uint64).astype(np.uint32)
-    x = np.concatenate([bits.view(np.float32), np.array([float.fromhex("-0x1.f8cbb2p+5"), -50.0, -103.0, -104.5], np.float32)])
+    """The render's own exp (glibc_expf_fast through the shared-memory table,
+    as eval_step calls it) on EVERY float of its input range
+    [-0x1.9fe368p6, 0] (~1.12e9 values, +0 and -0 included) against the host
+    libm expf the reference calls (src/blend.cpp:12): bit for bit."""
+    lo_bits = int(np.float32(float.fromhex("-0x1.9fe368p6")).view(np.uint32))
+    first, last = 0x80000000, lo_bits  # -0.0 .. -103.97 (negative floats grow in bits)
+    chunk = 1 << 27
+    y = torch.empty(chunk, dtype=torch.float32, device=DEV)
+    yh = torch.empty(chunk, dtype=torch.float32, pin_memory=True)
+    bad = total = 0
+    b = first
+    while b <= last:
+        n = min(chunk, last - b + 1)
+        N.call("bs_test_expf_range", b, n, y.data_ptr(), N.ALPHA_EXACT, api._stream(DEV))
+        yh[:n].copy_(y[:n])
+        bad += O.lib().orc_expf_compare_range(b, n, yh.data_ptr())
+        total += n
+        b += n
+    N.call("bs_test_expf_range", 0, 1, y.data_ptr(), N.ALPHA_EXACT, api._stream(DEV))  # +0.0
+    yh[:1].copy_(y[:1])
+    bad += O.lib().orc_expf_compare_range(0, 1, yh.data_ptr())
+    assert total == last - first + 1 > 1_100_000_000
+    assert bad == 0
+    # the array form on a few values outside the render's range (general path)
+    x = np.array([float.fromhex("-0x1.f8cbb2p+5"), -50.0, -103.0, -104.5, 1.5, 80.0], np.float32)
     xd = torch.from_numpy(x).to(DEV)
     yd = torch.empty_like(xd)
     N.call("bs_test_expf", xd.data_ptr(), yd.data_ptr(), x.size, N.ALPHA_EXACT, api._stream(DEV))
-    y = yd.cpu().numpy()
-    bad = O.lib().orc_expf_compare_batch(O.p(x), O.p(y), x.size)
-    assert bad == 0
+    assert O.lib().orc_expf_compare_batch(O.p(x), O.p(yd.cpu().numpy()), x.size) == 0
 
 
 def test_preprocess_bit_exact():
@@ -915,3 +934,27 @@ def test_host_async_pipeline_matches():
     for i, (a, r) in enumerate(zip(outs, ref)):
         for k in range(6):
             assert torch.equal(a[k], r[k]), (i, k)
+
+
+def test_two_pipelines_on_two_streams():
+    """Two Pipelines rendering FineGrainedCombined concurrently on two torch
+    streams: each owns its render workspace (work-queue counters, tail
+    hand-off slots), so neither frame is corrupted."""
+    W, H = 480, 320
+    scenes = []
+    for seed, bgf in ((1, 0.12), (2, 0.6)):
+        g3d, cam = scene(40000, W, H, 480.0, bgfrac=bgf, seed=seed)
+        g2d = O.project_all(g3d, cam)
+        scenes.append((g3d, cam, _oracle_render(3, g2d, W, H, 16, 16, (0.1, 0.2, 0.3))))
+    pipes = [api.Pipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT) for _ in scenes]
+    streams = [torch.cuda.Stream() for _ in scenes]
+    devs = [api.g3d_to_device(g) for g, _, _ in scenes]
+    for _ in range(4):
+        for p, st, d, (g3d, cam, _) in zip(pipes, streams, devs, scenes):
+            with torch.cuda.stream(st):
+                p.forward(d, len(g3d), ncam(cam), variant="FineGrainedCombined", bg=(0.1, 0.2, 0.3))
+        torch.cuda.synchronize()
+        for p, (_, _, ref) in zip(pipes, scenes):
+            got = p.frame.to_numpy()
+            assert np.array_equal(got["contrib"], ref["contrib"]) and np.array_equal(got["term"], ref["term"])
+            assert np.array_equal(got["final_t"], ref["final_t"])

@@ -10,10 +10,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2412_17378_b200 import _native as N  # noqa: E402
 from paper_2412_17378_b200 import api  # noqa: E402
+from paper_2412_17378_b200 import sharding  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 W, H, f, n, bgf, sig = bench.CONFIGS[cfg]
-cams = [api.camera(bench.orbit_view(k), (f, f), W, H) for k in range(64)]
+cams = [api.camera(sharding.orbit_view(k), (f, f), W, H) for k in range(64)]
 g3d = api.gen_clustered_scene(n, cams[0], cluster_sigma=sig, background_fraction=bgf)
 d = api.g3d_to_device(g3d, "cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
