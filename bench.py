@@ -325,8 +325,10 @@ def metric_name(cfg: str) -> str:
 
 
 def config_desc(cfg, W, H, n, pw, ph) -> dict:
-    return {"workload": f"{cfg.upper()}: {W}x{H}, {n} clustered Gaussians (4 clusters, sigma 0.035, 12% background), "
-                        f"{pw}x{ph} tiles, views from a 64-view +-15 deg yaw orbit",
+    _, _, f, _, bgf, sig = CONFIGS[cfg]
+    return {"workload": f"{cfg.upper()}: {W}x{H}, focal {f:g}, {n} Gaussians from gen_clustered_scene (4 clusters, "
+                        f"sigma {sig:g}, background fraction {bgf:g}), {pw}x{ph} tiles, views from the 64-view "
+                        "+-15 deg yaw orbit",
             "global_batch": None, "seq_len": None}
 
 

@@ -88,11 +88,19 @@ __device__ __forceinline__ float glibc_expf_inrange(float x, const unsigned long
 __constant__ double c_expf_k[4] = {0x1.71547652b82fep+0 * 32.0, 0x1.c6af84b912394p-5 / 32.0 / 32.0 / 32.0,
                                    0x1.ebfce50fac4f3p-3 / 32.0 / 32.0, 0x1.62e42ff0c52d6p-1 / 32.0};
 
+// The table's address is held as a 32-bit shared-window address in an
+// ordinary register (opaque to the compiler: a generic pointer to shared
+// memory was re-derived from SR_CgaCtaId with four uniform instructions on
+// every list entry).
 struct ExpK {
-  const unsigned long long* tab;
+  uint32_t tab;
 };
 
-__device__ __forceinline__ ExpK make_expk(const unsigned long long* s_tab) { return ExpK{s_tab}; }
+__device__ __forceinline__ ExpK make_expk(const unsigned long long* s_tab) {
+  uint32_t a;
+  asm volatile("mov.u32 %0, %1;" : "=r"(a) : "r"((uint32_t)__cvta_generic_to_shared(s_tab)));
+  return ExpK{a};
+}
 
 // glibc_expf_inrange with constant-bank operands (same operations, same bits).
 __device__ __forceinline__ float glibc_expf_fast(float x, const ExpK& k) {
@@ -101,8 +109,9 @@ __device__ __forceinline__ float glibc_expf_fast(float x, const ExpK& k) {
   const double kds = __dadd_rn(z, kShift);
   const unsigned lo = (unsigned)__double2loint(kds);
   const double r = __dsub_rn(z, __dsub_rn(kds, kShift));
-  const unsigned long long tv = k.tab[lo & 31u];
-  const double s = __hiloint2double((int)((unsigned)(tv >> 32) + (lo << 15)), (int)(unsigned)tv);
+  unsigned tlo, thi;
+  asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(tlo), "=r"(thi) : "r"(k.tab + ((lo & 31u) << 3)));
+  const double s = __hiloint2double((int)(thi + (lo << 15)), (int)tlo);
   const double zz = __fma_rn(c_expf_k[1], r, c_expf_k[2]);
   const double r2 = __dmul_rn(r, r);
   double y = __fma_rn(c_expf_k[3], r, 1.0);

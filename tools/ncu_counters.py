@@ -20,7 +20,9 @@ import subprocess
 METRICS = {
     "duration_ns": "gpu__time_duration.sum",
     "inst_executed": "smsp__inst_executed.sum",
-    "thread_inst_executed": "smsp__thread_inst_executed.sum",
+    "avg_active_lanes": "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "avg_pred_on_lanes": "smsp__thread_inst_executed_pred_on_per_inst_executed.ratio",
+    "warps_active_per_smsp": "smsp__warps_active.avg.per_cycle_active",
     "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "dram_read": "dram__bytes_read.sum",
     "dram_write": "dram__bytes_write.sum",
@@ -47,11 +49,8 @@ def read(rep: str) -> dict:
                 pass
     if "dram_read" in out and "dram_write" in out:
         out["dram_bytes"] = int(out["dram_read"] + out["dram_write"])
-    if out.get("inst_executed") and out.get("thread_inst_executed"):
-        out["avg_active_lanes"] = out["thread_inst_executed"] / out["inst_executed"]
-    for k in ("inst_executed", "thread_inst_executed"):
-        if k in out:
-            out[k] = int(out[k])
+    if "inst_executed" in out:
+        out["inst_executed"] = int(out["inst_executed"])
     return out
 
 

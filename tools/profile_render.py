@@ -29,7 +29,12 @@ def main():
     ap.add_argument("--config", default=None, help="c1/c2/c4: bench.py's scene and first view (overrides n/W/H/f/sigma)")
     ap.add_argument("--frame-pipeline", action="store_true",
                     help="render through the frame pipeline (super-tile lists on >= 1 Mpixel frames)")
+    ap.add_argument("--fine-ctas", type=int, default=0,
+                    help="FineGrainedCombined CTAs per SM (bs_render_set_fine_occupancy; the bench's timed frames use 3)")
     a = ap.parse_args()
+    if a.fine_ctas:
+        from paper_2412_17378_b200 import _native as N
+        N.call("bs_render_set_fine_occupancy", a.fine_ctas)
     if a.config:
         import bench
         a.W, a.H, a.f, a.n, bgf, a.sigma = bench.CONFIGS[a.config]
