@@ -395,14 +395,13 @@ def main():
     # take the views round-robin, so view i+1's preprocess / binning overlaps
     # view i's render
     ns = max(1, args.streams)
-    if ns > 1:  # leave SM room for the other contexts' kernels during a render
-        N.call("bs_render_set_fine_occupancy", args.fine_ctas)
+    fine_ctas = args.fine_ctas if ns > 1 else 0  # leave SM room for the other contexts' kernels during a render
     streams = [torch.cuda.Stream(device=dev) for _ in range(ns)]
     fps = []
     for s_ in streams:
         with torch.cuda.stream(s_):
             fps.append(api.FramePipeline(W, H, pw, ph, dev, mode, async_mode=not args.sync_frames,
-                                         graphs=not (args.sync_frames or args.no_graphs)))
+                                         graphs=not (args.sync_frames or args.no_graphs), fine_ctas=fine_ctas))
     fp = fps[0]
     # one L2 flush (256 MiB write > 126 MB L2) per step on the step's stream,
     # INSIDE the timed region (conservative: its time counts)
@@ -468,7 +467,6 @@ def main():
     launches = int(N.lib().bs_kernel_launches() - launches0)
     grows = sum(f.capacity()[1] for f in fps) - grows_warm
     graph_replays = sum(f.graph_launches() for f in fps) - glaunch0
-    N.call("bs_render_set_fine_occupancy", 0)  # kernel-level timings below: full occupancy
     # which variant the on-device selector picked for each timed view (replayed untimed)
     for vid in sorted(set(timed_views)):
         _, fi = fp.forward(g3d_dev, n, cams[vid], variant=variant, info=True)
@@ -744,13 +742,13 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     # and 3 I/O slots, a ring of 3 pinned output sets per context); wall
     # clock from the first enqueue to the final sync of every context
     nctx = max(1, args.streams)
-    if nctx > 1:
-        N.call("bs_render_set_fine_occupancy", args.fine_ctas)
     ctxs = []
     for _ in range(nctx):
         cx = C.c_void_p()
         N.call("bs_context_create", C.byref(cx), int(mode))
         N.call("bs_context_set_async", cx, 1)
+        if nctx > 1:
+            N.call("bs_context_set_fine_occupancy", cx, args.fine_ctas)
         ctxs.append(cx)
     host_g3d = torch.from_numpy(np.ascontiguousarray(g3d).view(np.uint8).reshape(-1).copy()).pin_memory()
     P3 = P * 3
@@ -785,7 +783,6 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     e2e_s = (time.perf_counter() - t0) / ne
     for cx in ctxs:
         N.call("bs_context_destroy", cx)
-    N.call("bs_render_set_fine_occupancy", 0)
     res["e2e"] = {"value": 1.0 / e2e_s, "unit": "views/s", "h2d_bytes_per_step": int(n * 56),
                   "d2h_bytes_per_step": int(P * 32), "ms_per_step": e2e_s * 1e3, "steps": ne,
                   "reruns": int(r1 - r0), "contexts": nctx,

@@ -242,7 +242,9 @@ int bs_tile_order_select(const uint32_t* tile_ranges, int32_t tiles, bs_tile_his
  * Output equals render_reference (pixel-wise variants) or
  * render_gaussianwise (GaussianWise / FineGrainedCombined).
  * Workspace holds the dynamic-queue counter (reset by the call). */
-/* queue counters + the FineGrainedCombined tail hand-off buffer (48 B/pixel) */
+/* queue counters (256 B) + the FineGrainedCombined tail hand-off slots
+ * (64 B/pixel) + parked-task records (8 B per 4 pixels): ~66 B/pixel, e.g.
+ * 137 MB at 1080p, 548 MB at 4K. */
 size_t bs_render_workspace_bytes(int32_t width, int32_t height);
 int bs_render_forward(int variant, int alpha_mode, bs_splats g, const uint32_t* point_list,
                       const uint32_t* tile_ranges, const uint32_t* task_order, int32_t width, int32_t height,
@@ -263,6 +265,16 @@ int bs_render_forward_auto(const int32_t* variant_dev, int alpha_mode, bs_splats
  * views concurrently, 3 leaves room for the other context's preprocess and
  * binning kernels to overlap the render (process-wide setting). */
 int bs_render_set_fine_occupancy(int32_t ctas_per_sm);
+
+/* The frame context's render entry: bs_render_forward (super_lists = 0) /
+ * bs_render_forward_super (super_lists = 1), variant -1 = the device-selected
+ * one (variant_dev), with a per-call FineGrainedCombined occupancy cap
+ * (fine_ctas_per_sm > 0; 0 = the process default above) — each context keeps
+ * its own (bs_context_set_fine_occupancy). */
+int bs_render_forward_ctx(int variant, const int32_t* variant_dev, int alpha_mode, bs_splats g,
+                          const uint32_t* point_list, const uint32_t* tile_ranges, const uint32_t* task_order,
+                          int32_t width, int32_t height, int32_t pw, int32_t ph, const float bg[3], bs_frame_out out,
+                          int32_t super_lists, int32_t fine_ctas_per_sm, void* ws, size_t ws_bytes, void* stream);
 
 /* Work counters of a rendered frame (src/kernels.cpp:283-298):
  *   evaluated = sum_p consumed(p), consumed = term > 0 ? term : list_len(tile(p))
@@ -416,6 +428,11 @@ int bs_context_sync(bs_context* ctx, int64_t* reruns);
  * ahead of the launch) — one launch instead of ~45.  Off by default.
  * bs_context_graph_launches counts the replays. */
 int bs_context_set_graphs(bs_context* ctx, int32_t on);
+/* This context's FineGrainedCombined resident CTAs per SM (0 = the process
+ * default, bs_render_set_fine_occupancy).  With several contexts streaming
+ * views concurrently, 3 leaves SM room for the other contexts' preprocess and
+ * binning kernels to overlap the render. */
+int bs_context_set_fine_occupancy(bs_context* ctx, int32_t ctas_per_sm);
 int bs_context_graph_launches(bs_context* ctx, int64_t* launches);
 /* Drops pending K checks without waiting (after capturing a frame into a
  * CUDA graph: the captured call's check never ran).  The caller then owns

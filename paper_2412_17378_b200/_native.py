@@ -84,6 +84,8 @@ SIGNATURES = {
                                     FrameOut, _vp, _sz, _vp]),
     "bs_frame_work": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
     "bs_render_set_fine_occupancy": (C.c_int, [_i32]),
+    "bs_render_forward_ctx": (C.c_int, [C.c_int, _vp, C.c_int, Splats, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _f32p,
+                                        FrameOut, _i32, _i32, _vp, _sz, _vp]),
     "bs_select_variant": (C.c_int, [C.POINTER(TileHistogram), _i32, _i32, _i32, _i32, _i32]),
     "bs_test_expf": (C.c_int, [_vp, _vp, _i64, C.c_int, _vp]),
     "bs_test_expf_range": (C.c_int, [C.c_uint32, _i64, _vp, C.c_int, _vp]),
@@ -115,6 +117,7 @@ SIGNATURES = {
     "bs_context_capacity": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "bs_context_drop_pending": (C.c_int, [_vp]),
     "bs_context_set_graphs": (C.c_int, [_vp, _i32]),
+    "bs_context_set_fine_occupancy": (C.c_int, [_vp, _i32]),
     "bs_context_graph_launches": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
     "bs_preprocess_devcam": (C.c_int, [_vp, _i64, _vp, Splats, _vp, _vp, _sz, _vp]),
     "bs_bin_sort_async": (C.c_int, [Splats, _i64, _vp, _i32, _i32, _i32, _i32, _i64, _vp, _vp, _vp, _sz, _vp]),

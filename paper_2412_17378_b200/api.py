@@ -368,7 +368,7 @@ class FramePipeline:
 
     def __init__(self, width: int, height: int, pw: int = 16, ph: int = 16, device="cuda",
                  alpha_mode: int = ALPHA_EXACT, timing: bool = False, async_mode: bool = False,
-                 graphs: bool = False):
+                 graphs: bool = False, fine_ctas: int = 0):
         self.width, self.height, self.pw, self.ph, self.device = width, height, pw, ph, device
         self.ctx = C.c_void_p()
         N.call("bs_context_create", C.byref(self.ctx), int(alpha_mode))
@@ -377,6 +377,8 @@ class FramePipeline:
             N.call("bs_context_set_async", self.ctx, 1)
         if graphs:  # replay a captured CUDA graph of the frame (bs_context_set_graphs)
             N.call("bs_context_set_graphs", self.ctx, 1)
+        if fine_ctas:  # this context's FineGrainedCombined CTAs per SM (bs_context_set_fine_occupancy)
+            N.call("bs_context_set_fine_occupancy", self.ctx, int(fine_ctas))
         if timing:
             N.call("bs_context_enable_timing", self.ctx, 1)
         self.frame = DeviceFrame.empty(width, height, device)

@@ -13,6 +13,12 @@
     if (_e != cudaSuccess) return BS_ERR_CUDA;         \
   } while (0)
 
+#define TRY_BS(expr)                                   \
+  do {                                                 \
+    const int _s = (expr);                             \
+    if (_s != BS_OK) return _s;                        \
+  } while (0)
+
 #define BS_LAUNCH_CHECK()                              \
   do {                                                 \
     bs::count_launches(1);                             \

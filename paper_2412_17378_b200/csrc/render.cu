@@ -908,34 +908,92 @@ __global__ void k_frame_work(const int32_t* __restrict__ term, const int32_t* __
   }
 }
 
-static int g_fine_ctas_per_sm = 0;  // 0 = as many as fit (bs_render_set_fine_occupancy)
+static int g_fine_ctas_per_sm = 0;  // process default (bs_render_set_fine_occupancy); 0 = as many as fit
 
-// Tail hand-off switch (BS_FINE_DONATE=0 disables it, for A/B measurement).
-// Tuning overrides for experiments / tests (defaults are the calibrated ones).
+// Tuning knobs, read from the environment ONCE per process (defaults are the
+// calibrated ones; the variables exist for A/B measurement — DESIGN.md §9).
+struct FineTuning {
+  int ctas_per_sm;  // BS_FINE_CTAS_PER_SM (0 = as many as fit)
+  bool donate;      // BS_FINE_DONATE=0 disables the tail hand-off
+  int donate_after, donate_min_remain, stragglers, stragglers_super;
+  bool wide;        // BS_FINE_WIDE=0: never the 80-register build
+  bool no_lpt;      // BS_FINE_NO_LPT=1: tasks in tile-index order
+};
 static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
 }
-
-static bool fine_donate_enabled() {
-  const char* e = getenv("BS_FINE_DONATE");
-  return !(e && e[0] == '0');
+static const FineTuning& fine_tuning() {
+  static const FineTuning t = [] {
+    FineTuning f;
+    f.ctas_per_sm = env_int("BS_FINE_CTAS_PER_SM", 0);
+    f.donate = env_int("BS_FINE_DONATE", 1) != 0;
+    f.donate_after = env_int("BS_FINE_DONATE_AFTER", kDonateAfter);
+    f.donate_min_remain = env_int("BS_FINE_DONATE_MIN", kDonateMinRemain);
+    f.stragglers = env_int("BS_FINE_STRAGGLERS", kStragglers);
+    f.stragglers_super = env_int("BS_FINE_STRAGGLERS_SUPER", kStragglers);
+    f.wide = env_int("BS_FINE_WIDE", 1) != 0;
+    f.no_lpt = env_int("BS_FINE_NO_LPT", 0) != 0;
+    return f;
+  }();
+  return t;
 }
 
+// Per-device launch facts (SM count, occupancy of the persistent kernels),
+// queried once per device and mode instead of on every launch.
+struct DevFacts {
+  int sms = 0;
+  int fine_per_sm[2] = {0, 0};     // k_render_fine<MODE, kListTile, 4>, by MODE
+  int donated_per_sm[2] = {0, 0};  // k_render_donated<MODE>
+  int dyn_per_sm[2][5] = {};       // k_render_dynamic<MODE, 64 << i>
+};
+constexpr int kMaxDevices = 64;
+static DevFacts g_dev[kMaxDevices];
+
+static int dev_facts(DevFacts** out) {
+  int dev = 0;
+  BS_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return BS_ERR_UNSUPPORTED;
+  DevFacts& f = g_dev[dev];
+  if (f.sms == 0) {  // (a concurrent first call computes the same values)
+    DevFacts n;
+    BS_CUDA_TRY(cudaDeviceGetAttribute(&n.sms, cudaDevAttrMultiProcessorCount, dev));
+    BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n.fine_per_sm[0],
+                                                              k_render_fine<BS_ALPHA_EXACT, kListTile, 4>,
+                                                              kFineThreads, 0));
+    BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n.fine_per_sm[1],
+                                                              k_render_fine<BS_ALPHA_FAST, kListTile, 4>,
+                                                              kFineThreads, 0));
+    BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n.donated_per_sm[0], k_render_donated<BS_ALPHA_EXACT>,
+                                                              kFineThreads, 0));
+    BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n.donated_per_sm[1], k_render_donated<BS_ALPHA_FAST>,
+                                                              kFineThreads, 0));
+#define BS_DYN_OCC(M, I, B) \
+    BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n.dyn_per_sm[M][I], k_render_dynamic<M, B>, B, 0));
+    BS_DYN_OCC(0, 0, 64) BS_DYN_OCC(0, 1, 128) BS_DYN_OCC(0, 2, 256) BS_DYN_OCC(0, 3, 512) BS_DYN_OCC(0, 4, 1024)
+    BS_DYN_OCC(1, 0, 64) BS_DYN_OCC(1, 1, 128) BS_DYN_OCC(1, 2, 256) BS_DYN_OCC(1, 3, 512) BS_DYN_OCC(1, 4, 1024)
+#undef BS_DYN_OCC
+    f = n;
+  }
+  *out = &f;
+  return BS_OK;
+}
+
+// fine_cap: resident FineGrainedCombined CTAs per SM for this launch (> 0),
+// or 0 = the process default (bs_render_set_fine_occupancy, then
+// BS_FINE_CTAS_PER_SM, then as many as fit).
 template <int MODE>
-static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStream_t st) {
+static int launch_variant(int variant, const RArgs& A, int block_pixels, int fine_cap, cudaStream_t st) {
   const int T = A.T;
+  DevFacts* df = nullptr;
+  TRY_BS(dev_facts(&df));
+  const int sms = df->sms;
   switch (variant) {
     case BS_NAIVE:
     case BS_SHARED_MEM_OPT: {
       const bool smem = variant == BS_SHARED_MEM_OPT;
-      int grid = T;
-      if (A.gate) {  // auto-mode candidate: at most 8 CTAs per SM, tiles in grid stride
-        int dev = 0, sms = 148;
-        BS_CUDA_TRY(cudaGetDevice(&dev));
-        BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        grid = max(1, min(T, sms * 8));
-      }
+      // auto-mode candidate: at most 8 CTAs per SM, tiles in grid stride
+      const int grid = A.gate ? max(1, min(T, sms * 8)) : T;
 #define BS_PW_CASE(B)                                                                   \
   if (block_pixels <= B) {                                                              \
     if (smem) k_render_pixelwise<MODE, true, B><<<grid, B, 0, st>>>(A);                 \
@@ -947,18 +1005,13 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
       return BS_ERR_UNSUPPORTED;
     }
     case BS_DYNAMIC_BLOCKS: {
-      int dev = 0, sms = 0;
-      BS_CUDA_TRY(cudaGetDevice(&dev));
-      BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-#define BS_DYN_CASE(B)                                                                                   \
-  if (block_pixels <= B) {                                                                               \
-    int per_sm = 0;                                                                                      \
-    BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_dynamic<MODE, B>, B, 0)); \
-    const int grid = max(1, min(T, sms * max(1, per_sm)));                                               \
-    k_render_dynamic<MODE, B><<<grid, B, 0, st>>>(A);                                                    \
-    break;                                                                                               \
+#define BS_DYN_CASE(I, B)                                                      \
+  if (block_pixels <= B) {                                                     \
+    const int grid = max(1, min(T, sms * max(1, df->dyn_per_sm[MODE][I])));   \
+    k_render_dynamic<MODE, B><<<grid, B, 0, st>>>(A);                          \
+    break;                                                                     \
   }
-      BS_DYN_CASE(64) BS_DYN_CASE(128) BS_DYN_CASE(256) BS_DYN_CASE(512) BS_DYN_CASE(1024)
+      BS_DYN_CASE(0, 64) BS_DYN_CASE(1, 128) BS_DYN_CASE(2, 256) BS_DYN_CASE(3, 512) BS_DYN_CASE(4, 1024)
 #undef BS_DYN_CASE
       return BS_ERR_UNSUPPORTED;
     }
@@ -966,28 +1019,25 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
       k_render_gaussianwise<MODE><<<T, kFgThreads, 0, st>>>(A);
       break;
     case BS_FINE_GRAINED_COMBINED: {
-      int dev = 0, sms = 0, per_sm = 0;
-      BS_CUDA_TRY(cudaGetDevice(&dev));
-      BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const FineTuning& ft = fine_tuning();
       const int lm = A.sup ? kListSuper : kListTile;
-      BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_fine<MODE, kListTile, 4>,
-                                                                kFineThreads, 0));
-      // bs_render_set_fine_occupancy / BS_FINE_CTAS_PER_SM: fewer resident
-      // CTAs leave SM room for another frame context's kernels
-      const int cap = g_fine_ctas_per_sm > 0 ? g_fine_ctas_per_sm : env_int("BS_FINE_CTAS_PER_SM", per_sm);
-      per_sm = max(1, min(per_sm, cap));
-      const bool wide = per_sm <= 3 && env_int("BS_FINE_WIDE", 1) != 0;  // the 80-register build
+      // fewer resident CTAs leave SM room for another frame context's kernels
+      int per_sm = df->fine_per_sm[MODE];
+      const int cap = fine_cap > 0 ? fine_cap : (g_fine_ctas_per_sm > 0 ? g_fine_ctas_per_sm : ft.ctas_per_sm);
+      if (cap > 0) per_sm = min(per_sm, cap);
+      per_sm = max(1, per_sm);
+      const bool wide = per_sm <= 3 && ft.wide;  // the 80-register build
       const int subs = ((A.pw + kSubW - 1) / kSubW) * ((A.ph + kSubH - 1) / kSubH);  // sub-tiles per tile
       const int64_t total = (int64_t)T * subs;
       if (total > 0x7fffffff) return BS_ERR_UNSUPPORTED;
       const int64_t ctas = (total + kFineWarps - 1) / kFineWarps;
-      const int grid = (int)max((int64_t)1, min(ctas, (int64_t)sms * max(1, per_sm)));
+      const int grid = (int)max((int64_t)1, min(ctas, (int64_t)sms * per_sm));
       RArgs B = A;
       B.total_tasks = (int)total;
-      if (!fine_donate_enabled()) B.donate = nullptr;
-      B.donate_after = env_int("BS_FINE_DONATE_AFTER", kDonateAfter);
-      B.donate_min_remain = env_int("BS_FINE_DONATE_MIN", kDonateMinRemain);
-      B.stragglers = env_int(A.sup ? "BS_FINE_STRAGGLERS_SUPER" : "BS_FINE_STRAGGLERS", kStragglers);
+      if (!ft.donate) B.donate = nullptr;
+      B.donate_after = ft.donate_after;
+      B.donate_min_remain = ft.donate_min_remain;
+      B.stragglers = A.sup ? ft.stragglers_super : ft.stragglers;
       if (lm == kListSuper) {
         if (wide) k_render_fine<MODE, kListSuper, 3><<<grid, kFineThreads, 0, st>>>(B, subs);
         else k_render_fine<MODE, kListSuper, 4><<<grid, kFineThreads, 0, st>>>(B, subs);
@@ -996,11 +1046,8 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, cudaStr
         else k_render_fine<MODE, kListTile, 4><<<grid, kFineThreads, 0, st>>>(B, subs);
       }
       BS_LAUNCH_CHECK();
-      if (B.donate) {
-        int per_sm2 = 0;
-        BS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_render_donated<MODE>, kFineThreads, 0));
-        k_render_donated<MODE><<<sms * max(1, per_sm2), kFineThreads, 0, st>>>(B);
-      }
+      if (!B.donate) return BS_OK;
+      k_render_donated<MODE><<<sms * max(1, df->donated_per_sm[MODE]), kFineThreads, 0, st>>>(B);
       break;
     }
     default:
@@ -1026,7 +1073,7 @@ static bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 static int render_impl(int variant, const int32_t* gate, int alpha_mode, bs_splats g, const uint32_t* point_list,
                        const uint32_t* tile_ranges, const uint32_t* task_order, int32_t width, int32_t height,
                        int32_t pw, int32_t ph, const float bg[3], bs_frame_out out, void* ws, size_t ws_bytes,
-                       void* stream, bool sup = false) {
+                       void* stream, bool sup = false, int fine_cap = 0) {
   if (width <= 0 || height <= 0 || pw <= 0 || ph <= 0 || !bg || !tile_ranges) return BS_ERR_INVALID_ARGUMENT;
   if (alpha_mode != BS_ALPHA_EXACT && alpha_mode != BS_ALPHA_FAST) return BS_ERR_INVALID_ARGUMENT;
   if (!out.color || !out.alpha || !out.depth || !out.final_t || !out.contrib || !out.term) return BS_ERR_INVALID_ARGUMENT;
@@ -1039,7 +1086,7 @@ static int render_impl(int variant, const int32_t* gate, int alpha_mode, bs_spla
   A.rgbr = reinterpret_cast<const float4*>(g.rgbr);
   A.point_list = point_list;
   A.ranges = tile_ranges;
-  A.task_order = env_int("BS_FINE_NO_LPT", 0) ? nullptr : task_order;  // A/B: index order
+  A.task_order = fine_tuning().no_lpt ? nullptr : task_order;  // A/B: index order
   A.W = width; A.H = height; A.pw = pw; A.ph = ph;
   A.cols = (width + pw - 1) / pw;
   const int64_t T = (int64_t)A.cols * ((height + ph - 1) / ph);
@@ -1063,8 +1110,8 @@ static int render_impl(int variant, const int32_t* gate, int alpha_mode, bs_spla
     BS_CUDA_TRY(cudaMemsetAsync(ws, 0, 8 * sizeof(unsigned int), st));
   const int block_pixels = pw * ph;
   auto launch = [&](int v) {
-    return alpha_mode == BS_ALPHA_EXACT ? launch_variant<BS_ALPHA_EXACT>(v, A, block_pixels, st)
-                                        : launch_variant<BS_ALPHA_FAST>(v, A, block_pixels, st);
+    return alpha_mode == BS_ALPHA_EXACT ? launch_variant<BS_ALPHA_EXACT>(v, A, block_pixels, fine_cap, st)
+                                        : launch_variant<BS_ALPHA_FAST>(v, A, block_pixels, fine_cap, st);
   };
   if (!gate) return launch(variant);
   // auto: the selector's two candidates (select_variant_formula)
@@ -1200,6 +1247,22 @@ extern "C" int bs_frame_work(const int32_t* term, const int32_t* contrib, const 
                                                             reinterpret_cast<unsigned long long*>(evaluated_committed));
   BS_LAUNCH_CHECK();
   return BS_OK;
+}
+
+// The frame context's render: the pw x ph lists (sup = 0) or super-tile
+// lists (sup = 1), a fixed variant or (variant -1) the device-selected one,
+// and the context's own FineGrainedCombined occupancy cap (0 = process
+// default) — so two contexts in one process never share that setting.
+extern "C" int bs_render_forward_ctx(int variant, const int32_t* variant_dev, int alpha_mode, bs_splats g,
+                                     const uint32_t* point_list, const uint32_t* tile_ranges,
+                                     const uint32_t* task_order, int32_t width, int32_t height, int32_t pw, int32_t ph,
+                                     const float bg[3], bs_frame_out out, int32_t super_lists,
+                                     int32_t fine_ctas_per_sm, void* ws, size_t ws_bytes, void* stream) {
+  if (variant < -1 || variant > 4 || (variant < 0 && !variant_dev) || fine_ctas_per_sm < 0)
+    return BS_ERR_INVALID_ARGUMENT;
+  return render_impl(variant < 0 ? -1 : variant, variant < 0 ? variant_dev : nullptr, alpha_mode, g, point_list,
+                     tile_ranges, task_order, width, height, pw, ph, bg, out, ws, ws_bytes, stream, super_lists != 0,
+                     fine_ctas_per_sm);
 }
 
 extern "C" int bs_render_set_fine_occupancy(int32_t ctas_per_sm) {

@@ -28,6 +28,7 @@ constexpr int kStages = 6;  // preprocess, bin_count, k_readback, bin_sort, stat
 
 struct bs_context {
   int alpha_mode = BS_ALPHA_EXACT;
+  int32_t fine_ctas = 0;  // FineGrainedCombined CTAs per SM for this context (0 = process default)
   cudaStream_t stream = nullptr;
   int sm_count = 148;
   // device buffers
@@ -494,15 +495,9 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
     fo = bs_frame_out{c->planes[0], c->planes[1], c->planes[2], c->planes[3], c->iplanes[0], c->iplanes[1]};
   }
   TRY(grow(&c->render_ws, &c->render_ws_bytes, bs_render_workspace_bytes(W, H)));
-  if (super) {
-    TRY(bs_render_forward_super(variant, c->variant_dev, c->alpha_mode, sp, c->point_list, c->ranges_t, c->order, W,
-                                H, pw, ph, bg, fo, c->render_ws, c->render_ws_bytes, st));
-  } else if (variant < 0)
-    TRY(bs_render_forward_auto(c->variant_dev, c->alpha_mode, sp, c->point_list, c->ranges, c->order, W, H, pw, ph,
-                               bg, fo, c->render_ws, c->render_ws_bytes, st));
-  else
-    TRY(bs_render_forward(variant, c->alpha_mode, sp, c->point_list, c->ranges, c->order, W, H, pw, ph, bg, fo,
-                          c->render_ws, c->render_ws_bytes, st));
+  TRY(bs_render_forward_ctx(variant, c->variant_dev, c->alpha_mode, sp, c->point_list, super ? c->ranges_t : c->ranges,
+                            c->order, W, H, pw, ph, bg, fo, super ? 1 : 0, c->fine_ctas, c->render_ws,
+                            c->render_ws_bytes, st));
   mark(6);
   c->last_variant = variant;
   c->last_W = W;
@@ -725,6 +720,13 @@ extern "C" int bs_render_frame_device(bs_context* c, const bs_gaussian3d* g3d_de
 extern "C" int bs_context_set_graphs(bs_context* c, int32_t on) {
   if (!c) return BS_ERR_INVALID_ARGUMENT;
   c->graphs = on != 0;
+  return BS_OK;
+}
+
+extern "C" int bs_context_set_fine_occupancy(bs_context* c, int32_t ctas_per_sm) {
+  if (!c || ctas_per_sm < 0) return BS_ERR_INVALID_ARGUMENT;
+  if (c->fine_ctas != ctas_per_sm) ++g_alloc_gen;  // captured graphs bake the grid size in
+  c->fine_ctas = ctas_per_sm;
   return BS_OK;
 }
 

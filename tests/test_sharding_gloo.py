@@ -26,6 +26,7 @@ def _worker(rank, world, port, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     views = sharding.views_for_rank(rank, world, steps=32)
     mine = list(sharding.contiguous_shard(64, rank, world))
+    batch = sharding.batch_view_ids(rank, world, steps=3)  # bench.py's default schedule
     t = sharding.max_over_ranks(10.0 + rank, dist, "cpu")
     import torch
 
@@ -33,8 +34,10 @@ def _worker(rank, world, port, out):
     dist.all_gather(gathered, torch.tensor(views, dtype=torch.int64))
     gathered_c = [None] * world
     dist.all_gather_object(gathered_c, mine)
+    gathered_b = [None] * world
+    dist.all_gather_object(gathered_b, batch)
     if rank == 0:
-        out.put((t, [g.tolist() for g in gathered], gathered_c))
+        out.put((t, [g.tolist() for g in gathered], gathered_c, gathered_b))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -46,7 +49,7 @@ def test_two_rank_sharding_and_max():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    t, views, contig = q.get(timeout=120)
+    t, views, contig, batches = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -54,6 +57,9 @@ def test_two_rank_sharding_and_max():
     allv = views[0] + views[1]
     assert sorted(allv) == list(range(64))  # 2 ranks x 32 steps cover the orbit once
     assert set(contig[0]).isdisjoint(contig[1]) and sorted(contig[0] + contig[1]) == list(range(64))
+    # batch mode: each of the 3 steps renders the 64-view batch exactly once over the ranks
+    assert len(batches[0]) == len(batches[1]) == 3 * 32
+    assert sorted(batches[0] + batches[1]) == sorted(list(range(64)) * 3)
 
 
 def test_contiguous_shards_all_sizes():
@@ -69,3 +75,23 @@ def test_orbit_views_orthonormal():
         assert np.abs(R @ R.T - np.eye(3)).max() < 1e-5
         # pivot maps to itself
         assert np.allclose(V[:3, :3] @ [0, 0, 5.5] + V[:3, 3], [0, 0, 5.5], atol=1e-5)
+
+
+def test_reference_arm_two_ranks_cpu():
+    """bench.py --impl reference under torch.distributed.run with 2 ranks on
+    CPU: rank 0 alone times the reference (C1, one complete frame) and
+    prints one JSON line; rank 1 exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2", "--impl", "reference",
+           "--config", "c1", "--steps", "1", "--warmup", "1"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["value"] == d["value"]
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
