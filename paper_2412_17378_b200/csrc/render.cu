@@ -513,6 +513,161 @@ __global__ void __launch_bounds__(kFgThreads) k_render_gaussianwise(RArgs A) {
 }
 
 // ---------------------------------------------------------------------------
+// GaussianWise, B200 form (paper Alg. 2/6 with the reference's serial-exact
+// decisions, src/kernels.cpp:57-107), for patches of <= 256 pixels.
+// CTA = one tile, 8 warps; warp w owns the tile's local pixels
+// [32w, 32w+32), lane = pixel for the per-pixel state.  The CTA stages the
+// tile list ONCE per 256-entry chunk (shared by all 8 warps); each warp then
+// walks the chunk in 32-entry groups, two phases per group:
+//   phase 1, Gaussian-wise (lane = list entry), once per live pixel p:
+//     alpha of the 32 consecutive entries at p, the shfl_up doubling prefix
+//     product of (1 - alpha) started at p's carried t (inc/blend.hpp:69-83)
+//     -> each entry's colour weight t_before; (alpha, t_before) go to the
+//     warp's 32 x 33 scratch (row p);
+//   phase 2, serial (lane = pixel): each live lane walks its row in list
+//     order — skip, stop (t * (1 - alpha) < 1e-4, nothing committed, term =
+//     list position), commit (colour/depth += c * alpha * t_before, separate
+//     double mul / add in list order as the reference).
+// So contrib / term / final_t / alpha AND colour / depth equal
+// render_gaussianwise bit for bit.  The exps of phase 1 run on 32 useful
+// lanes (one pixel, 32 entries) and only for pixels still live; the list is
+// read from L2 once per tile instead of once per 4 pixels.
+constexpr int kGwWarps = 8;
+constexpr int kGwThreads = kGwWarps * 32;
+constexpr int kGwChunk = kGwThreads;  // list entries staged per CTA round
+constexpr size_t kGwDynSmem = sizeof(float) * kGwWarps * 2 * 32 * 33;  // per-warp phase scratch, 67.6 KB
+
+template <int MODE>
+__global__ void __launch_bounds__(kGwThreads) k_render_gw(RArgs A) {
+  __shared__ float4 s_xyab[kGwChunk];
+  __shared__ float4 s_cop[kGwChunk];
+  __shared__ double2 s_rg[kGwChunk];  // (r, g) widened once per staged entry
+  __shared__ double2 s_bd[kGwChunk];  // (b, depth)
+  // dynamic: per warp, alpha of (pixel row, entry) (0 = skipped) and the
+  // prefix-product t_before, 32 x 33 floats each (stride 33: conflict-free
+  // row writes in phase 1 and column reads in phase 2)
+  extern __shared__ float s_gw_dyn[];
+  __shared__ unsigned long long s_tab[32];
+  if (gated_out(A, BS_GAUSSIAN_WISE)) return;
+  load_tab(s_tab);
+  const ExpK ek = make_expk(s_tab);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile = blockIdx.x;
+  const int tx = tile % A.cols, ty = tile / A.cols;
+  const int npix = A.pw * A.ph;
+  // this lane's pixel (phase 2 / state)
+  const int local = warp * 32 + lane;
+  const int lx = local % A.pw, ly = local / A.pw;
+  const int px = tx * A.pw + lx, py = ty * A.ph + ly;
+  const bool inside = local < npix && px < A.W && py < A.H;
+  const uint32_t start = A.ranges[2 * tile], end = A.ranges[2 * tile + 1];
+  float* const sa = s_gw_dyn + warp * (2 * 32 * 33);
+  float* const stb = sa + 32 * 33;
+
+  bool done = !inside;
+  float t = 1.0f;
+  int contrib = 0, term = 0;
+  double ar = 0.0, ag = 0.0, ab = 0.0, ad = 0.0;
+  float fr = 0.0f, fg = 0.0f, fb = 0.0f, fd = 0.0f;
+
+  for (uint32_t base = start; base < end; base += kGwChunk) {
+    if (__syncthreads_count(!done) == 0) break;
+    const uint32_t k = base + tid;
+    if (k < end) {
+      const uint32_t id = __ldg(A.point_list + k);
+      const float4 r = __ldg(A.rgbr + id);
+      s_xyab[tid] = __ldg(A.xyab + id);
+      const float4 c = __ldg(A.cop + id);
+      s_cop[tid] = c;
+      s_rg[tid] = make_double2((double)r.x, (double)r.y);
+      s_bd[tid] = make_double2((double)r.z, (double)c.w);
+    }
+    __syncthreads();
+    const int cnt = (int)min((uint32_t)kGwChunk, end - base);
+    for (int g0 = 0; g0 < cnt && __any_sync(kFull, !done); g0 += 32) {
+      const int gn = min(32, cnt - g0);
+      // ---- phase 1: per live pixel, lanes on 32 consecutive entries
+      unsigned live = __ballot_sync(kFull, !done);
+      const int j = g0 + lane;
+      const bool active = lane < gn;
+      const float4 a = s_xyab[active ? j : g0], c = s_cop[active ? j : g0];
+      while (live) {
+        const int p = __ffs(live) - 1;
+        live &= live - 1;
+        const int pl = warp * 32 + p;
+        const float psx = __fadd_rn((float)(tx * A.pw + pl % A.pw), 0.5f);
+        const float psy = __fadd_rn((float)(ty * A.ph + pl / A.pw), 0.5f);
+        const float ts = __shfl_sync(kFull, t, p);
+        float alpha = 0.0f;
+        const bool ns = active && eval_step<MODE>(a, c, psx, psy, ek, alpha);
+        sa[p * 33 + lane] = ns ? alpha : 0.0f;
+        if (__ballot_sync(kFull, ns) == 0) continue;  // no weight is read
+        float pre = ns ? __fsub_rn(1.0f, alpha) : 1.0f;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const float v = __shfl_up_sync(kFull, pre, off);
+          if (lane >= off) pre = __fmul_rn(pre, v);
+        }
+        const float per_lane = __fmul_rn(ts, pre);
+        const float tb = __shfl_up_sync(kFull, per_lane, 1);
+        stb[p * 33 + lane] = lane == 0 ? ts : tb;
+      }
+      __syncwarp();
+      // ---- phase 2: serial decisions and commits, lane = pixel
+      if (!done) {
+        const float* row_a = sa + lane * 33;
+        const float* row_t = stb + lane * 33;
+        for (int q = 0; q < gn; ++q) {
+          const float al = row_a[q];
+          if (al == 0.0f) continue;  // skipped (a non-skipped alpha is >= 1/255)
+          const float tmp = __fmul_rn(t, __fsub_rn(1.0f, al));
+          if (tmp < kStopThreshold) {
+            done = true;
+            term = (int)(base - start) + g0 + q + 1;
+            break;
+          }
+          if (MODE == BS_ALPHA_EXACT) {
+            const double w = __dmul_rn((double)al, (double)row_t[q]);
+            const double2 rg = s_rg[g0 + q], bd = s_bd[g0 + q];
+            ar = __dadd_rn(ar, __dmul_rn(rg.x, w));
+            ag = __dadd_rn(ag, __dmul_rn(rg.y, w));
+            ab = __dadd_rn(ab, __dmul_rn(bd.x, w));
+            ad = __dadd_rn(ad, __dmul_rn(bd.y, w));
+          } else {  // FAST: float weights and accumulators (the accumulators are widened at the end)
+            const float w = al * row_t[q];
+            const double2 rg = s_rg[g0 + q], bd = s_bd[g0 + q];
+            fr = fmaf((float)rg.x, w, fr);
+            fg = fmaf((float)rg.y, w, fg);
+            fb = fmaf((float)bd.x, w, fb);
+            fd = fmaf((float)bd.y, w, fd);
+          }
+          t = tmp;
+          ++contrib;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (MODE != BS_ALPHA_EXACT) {
+    ar = fr;
+    ag = fg;
+    ab = fb;
+    ad = fd;
+  }
+  if (inside) {
+    const size_t pix = (size_t)py * A.W + px;
+    A.color[3 * pix + 0] = __double2float_rn(__dadd_rn(ar, __dmul_rn((double)A.bg0, (double)t)));
+    A.color[3 * pix + 1] = __double2float_rn(__dadd_rn(ag, __dmul_rn((double)A.bg1, (double)t)));
+    A.color[3 * pix + 2] = __double2float_rn(__dadd_rn(ab, __dmul_rn((double)A.bg2, (double)t)));
+    A.alpha[pix] = __fsub_rn(1.0f, t);
+    A.depth[pix] = __double2float_rn(ad);
+    A.final_t[pix] = t;
+    A.contrib[pix] = contrib;
+    A.term[pix] = term;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // FineGrainedCombined, B200 form (paper Alg. 3 re-cut for 148 SMs):
 //   * persistent CTAs of kFineWarps warps; every WARP claims tasks on its own
 //     from the global atomicAdd queue (no CTA barriers in the loop);
@@ -752,24 +907,44 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
       if (lane == 0) qpoll = ld_relaxed_u32(A.queue);
     }
     const int cnt = __popc(km);
+    // Branch-free steps: after the sub-tile cull almost every step runs the
+    // exp and a commit in some lane (ncu: 98 % / 97 % of steps), so the
+    // divergent branches only cost reconvergence and branch-resolve stalls.
+    // Every lane evaluates every step; skip / stop / commit become
+    // predicates (a non-committing lane adds c * 0 to its sums and keeps t).
+    // Out-of-range or NaN powers are harmless: their exp is never used (the
+    // cut / power > 0 tests reject them, or, for NaN, alpha = 0.99 as the
+    // reference's std::min gives).
 #pragma unroll 2
     for (int j = 0; j < cnt; ++j) {
-      if (done) continue;
-      float alpha;
-      const float4 c = s[1][j];
-      if (!eval_step<MODE>(s[0][j], c, sx, sy, ek, alpha)) continue;
-      const float tmp = __fmul_rn(t, __fsub_rn(1.0f, alpha));
-      if (tmp < kStopThreshold) {
-        done = true;
-        term = s_k[j];
-        continue;
+      const float4 a = s[0][j], c = s[1][j];
+      const float dx = __fsub_rn(sx, a.x);
+      const float dy = __fsub_rn(sy, a.y);
+      const float q = __fadd_rn(__fmul_rn(__fmul_rn(a.z, dx), dx), __fmul_rn(__fmul_rn(c.x, dy), dy));
+      const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(a.w, dx), dy));
+      float e;
+      if (MODE == BS_ALPHA_EXACT) {
+        e = glibc_expf_fast(power, ek);
+      } else {
+        const float p2 = power * 1.4426950408889634f;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(p2));
       }
+      const float x = __fmul_rn(c.y, e);
+      const float alpha = (x < kAlphaClamp) ? x : kAlphaClamp;  // std::min(0.99f, x)
+      // not skipped: power >= power_cut (certain-skip bound), power <= 0, alpha >= 1/255
+      const bool ns = !done && !(power < c.z) && !(power > 0.0f) && !(alpha < kAlphaSkip);
+      const float tmp = __fmul_rn(t, __fsub_rn(1.0f, alpha));
+      const bool stop = ns && tmp < kStopThreshold;
+      const bool commit = ns && !stop;
+      if (stop) term = s_k[j];
+      done = done || stop;
+      const float ac = commit ? alpha : 0.0f;
       if (MODE == BS_ALPHA_EXACT)
-        acc.add_wide(alpha, t, reinterpret_cast<const double2*>(s[2])[j], reinterpret_cast<const double2*>(s[3])[j]);
+        acc.add_wide(ac, t, reinterpret_cast<const double2*>(s[2])[j], reinterpret_cast<const double2*>(s[3])[j]);
       else
-        acc.add(alpha, t, s[2][j], c.w);
-      t = tmp;
-      ++contrib;
+        acc.add(ac, t, s[2][j], c.w);
+      t = commit ? tmp : t;
+      contrib += commit ? 1 : 0;
     }
     __syncwarp();
     if (LM != kListTile) mpos += (uint32_t)__popc(mm);
@@ -973,6 +1148,10 @@ static int dev_facts(DevFacts** out) {
     BS_DYN_OCC(0, 0, 64) BS_DYN_OCC(0, 1, 128) BS_DYN_OCC(0, 2, 256) BS_DYN_OCC(0, 3, 512) BS_DYN_OCC(0, 4, 1024)
     BS_DYN_OCC(1, 0, 64) BS_DYN_OCC(1, 1, 128) BS_DYN_OCC(1, 2, 256) BS_DYN_OCC(1, 3, 512) BS_DYN_OCC(1, 4, 1024)
 #undef BS_DYN_OCC
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_render_gw<BS_ALPHA_EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kGwDynSmem));
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_render_gw<BS_ALPHA_FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kGwDynSmem));
     f = n;
   }
   *out = &f;
@@ -1016,7 +1195,10 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, int fin
       return BS_ERR_UNSUPPORTED;
     }
     case BS_GAUSSIAN_WISE:
-      k_render_gaussianwise<MODE><<<T, kFgThreads, 0, st>>>(A);
+      if (block_pixels <= kGwThreads)  // (dynamic smem opt-in: dev_facts)
+        k_render_gw<MODE><<<T, kGwThreads, kGwDynSmem, st>>>(A);
+      else  // larger patches: 4-warp tasks, 4 pixels at a time
+        k_render_gaussianwise<MODE><<<T, kFgThreads, 0, st>>>(A);
       break;
     case BS_FINE_GRAINED_COMBINED: {
       const FineTuning& ft = fine_tuning();

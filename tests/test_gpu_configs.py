@@ -16,8 +16,10 @@ the CPU oracle on the same seeded inputs:
       variants.
 
 Bars: contrib / term / final_t / alpha bit-exact for every variant;
-colour / depth bit-exact for the pixel-wise variants and within 1e-6 (abs;
-depth relative to max(1, |ref|)) for the Gaussian-wise ones.
+colour / depth bit-exact for the pixel-wise variants and GaussianWise
+(<= 256-pixel patches: serial list-order commits with the prefix weights, as
+render_gaussianwise), within 1e-6 (abs; depth relative to max(1, |ref|)) for
+FineGrainedCombined (fused multiply-add sums).
 """
 from __future__ import annotations
 
@@ -44,14 +46,14 @@ def ncam(o_cam):
     return N.Camera.from_buffer_copy(bytes(o_cam))
 
 
-def assert_frame(got: dict, ref: dict, variant: int, pixels=None, tag=""):
+def assert_frame(got: dict, ref: dict, variant: int, pixels=None, tag="", gw_exact=True):
     sel = (lambda a: a) if pixels is None else (lambda a: a[pixels])
     csel = (lambda a: a) if pixels is None else (lambda a: a.reshape(-1, 3)[pixels])
     for k in ("contrib", "term"):
         assert np.array_equal(sel(got[k]), sel(ref[k])), (tag, variant, k)
     for k in ("final_t", "alpha"):
         assert np.array_equal(sel(got[k]).view(np.uint32), sel(ref[k]).view(np.uint32)), (tag, variant, k)
-    if variant in PIXELWISE:
+    if variant in PIXELWISE or (variant == 2 and gw_exact):
         assert np.array_equal(csel(got["color"]).view(np.uint32), csel(ref["color"]).view(np.uint32)), (tag, variant)
         assert np.array_equal(sel(got["depth"]).view(np.uint32), sel(ref["depth"]).view(np.uint32)), (tag, variant)
     else:
@@ -206,4 +208,4 @@ def test_spec_acceptance_100_random_scenes():
         for v in range(5):
             f_ = api.render_forward(v, s, b, W, H, pw, ph, bg, N.ALPHA_EXACT, st.task_order)
             torch.cuda.synchronize()
-            assert_frame(f_.to_numpy(), refs[2] if v == 2 else refs[0], v, tag=f"scene {i}")
+            assert_frame(f_.to_numpy(), refs[2] if v == 2 else refs[0], v, tag=f"scene {i}", gw_exact=pw * ph <= 256)
