@@ -735,12 +735,15 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     if not args.no_c3:
         res["c3_sweep"] = c3_sweep(api, N, torch, W, H, pw, ph, n, cams[0].focal[0], mode, dev)
 
-    # e2e: host buffers through the pipelined C-ABI host frame API — every
-    # step uploads the scene from pinned host memory and downloads all six
-    # output planes into pinned host buffers.  Frames go round-robin to
-    # --streams contexts (each with its own upload / frame / download streams
-    # and 3 I/O slots, a ring of 3 pinned output sets per context); wall
-    # clock from the first enqueue to the final sync of every context
+    # e2e: the same metric through the C-ABI with HOST buffers, host<->device
+    # copies inside the timed region.  Batch mode (the timed steps' shape):
+    # each step is one bs_render_views_host call — the scene uploaded once
+    # from pinned host memory, the step's 64 views rendered round-robin over
+    # --streams contexts (async frame bodies), every view's six output planes
+    # downloaded into its own pinned host buffers; --batch 0: one
+    # bs_render_frame_host_async call (scene upload + frame + download) per
+    # view.  Wall clock from the first enqueue to bs_context_sync on every
+    # context.
     nctx = max(1, args.streams)
     ctxs = []
     for _ in range(nctx):
@@ -752,17 +755,8 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
         ctxs.append(cx)
     host_g3d = torch.from_numpy(np.ascontiguousarray(g3d).view(np.uint8).reshape(-1).copy()).pin_memory()
     P3 = P * 3
-    rings = [[[torch.empty(P3, dtype=torch.float32).pin_memory()] +
-              [torch.empty(P, dtype=torch.float32).pin_memory() for _ in range(3)] +
-              [torch.empty(P, dtype=torch.int32).pin_memory() for _ in range(2)] for _ in range(3)]
-             for _ in range(nctx)]
     bgc = (C.c_float * 3)(0.0, 0.0, 0.0)
     vv = -1 if args.variant == "auto" else int(vsel)
-
-    def e2e_step(k):
-        c_, j = k % nctx, k // nctx
-        N.call("bs_render_frame_host_async", ctxs[c_], host_g3d.data_ptr(), n, C.byref(cams[k % N_VIEWS]), pw, ph,
-               vv, bgc, *[o.data_ptr() for o in rings[c_][j % 3]])
 
     def e2e_sync():
         tot = 0
@@ -772,10 +766,41 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
             tot += r.value
         return tot
 
-    for k in range(4 * nctx):
+    batch = max(0, args.batch)
+    if batch:
+        # one pinned output set per view of the batch (every view's result lands on the host)
+        outs = [[torch.empty(P3, dtype=torch.float32).pin_memory()] +
+                [torch.empty(P, dtype=torch.float32).pin_memory() for _ in range(3)] +
+                [torch.empty(P, dtype=torch.int32).pin_memory() for _ in range(2)] for _ in range(batch)]
+        out_ptrs = (C.c_void_p * (6 * batch))(*[o.data_ptr() for v in outs for o in v])
+        ctx_arr = (C.c_void_p * nctx)(*[cx.value for cx in ctxs])
+        cam_arr = (N.Camera * N_VIEWS)(*cams)
+        ids = (C.c_int32 * batch)(*[k % N_VIEWS for k in range(batch)])
+
+        def e2e_step(_k):
+            N.call("bs_render_views_host", ctx_arr, nctx, host_g3d.data_ptr(), n, cam_arr, ids, batch, pw, ph, vv,
+                   bgc, out_ptrs)
+        per_step, warm, ne = batch, 2, max(3, min(args.steps, 10))
+        h2d, path = int(n * 56), ("bs_render_views_host (C-ABI; the scene uploaded once per step from pinned host "
+                                  "memory, the step's views round-robin over the contexts, each view's six planes "
+                                  "downloaded into its own pinned host buffers; wall clock to bs_context_sync)")
+    else:
+        rings = [[[torch.empty(P3, dtype=torch.float32).pin_memory()] +
+                  [torch.empty(P, dtype=torch.float32).pin_memory() for _ in range(3)] +
+                  [torch.empty(P, dtype=torch.int32).pin_memory() for _ in range(2)] for _ in range(3)]
+                 for _ in range(nctx)]
+
+        def e2e_step(k):
+            c_, j = k % nctx, k // nctx
+            N.call("bs_render_frame_host_async", ctxs[c_], host_g3d.data_ptr(), n, C.byref(cams[k % N_VIEWS]), pw,
+                   ph, vv, bgc, *[o.data_ptr() for o in rings[c_][j % 3]])
+        per_step, warm, ne = 1, 4 * nctx, max(3, min(args.steps, 100))
+        h2d, path = int(n * 56), ("bs_render_frame_host_async (C-ABI; pinned host buffers; per context upload / "
+                                  "frame / download on three streams, 3 frames in flight; frames round-robin over "
+                                  "the contexts; wall clock to bs_context_sync)")
+    for k in range(warm):
         e2e_step(k)
     r0 = e2e_sync()
-    ne = max(3, min(args.steps, 100))
     t0 = time.perf_counter()
     for k in range(ne):
         e2e_step(k)
@@ -783,12 +808,9 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     e2e_s = (time.perf_counter() - t0) / ne
     for cx in ctxs:
         N.call("bs_context_destroy", cx)
-    res["e2e"] = {"value": 1.0 / e2e_s, "unit": "views/s", "h2d_bytes_per_step": int(n * 56),
-                  "d2h_bytes_per_step": int(P * 32), "ms_per_step": e2e_s * 1e3, "steps": ne,
-                  "reruns": int(r1 - r0), "contexts": nctx,
-                  "path": "bs_render_frame_host_async (C-ABI; pinned host buffers; per context upload / frame / "
-                          "download on three streams, 3 frames in flight; frames round-robin over the contexts; "
-                          "wall clock to bs_context_sync)"}
+    res["e2e"] = {"value": per_step / e2e_s, "unit": "views/s", "h2d_bytes_per_step": h2d,
+                  "d2h_bytes_per_step": int(P * 32) * per_step, "views_per_step": per_step,
+                  "ms_per_step": e2e_s * 1e3, "steps": ne, "reruns": int(r1 - r0), "contexts": nctx, "path": path}
 
     if world == 1 and not args.no_cpu_baseline:
         g2d = api.splats_to_g2d(s)

@@ -386,6 +386,17 @@ int bs_context_set_stream(bs_context* ctx, void* stream);
 int bs_render_views(bs_context* const* ctxs, int32_t nctx, const bs_gaussian3d* g3d_dev, int64_t n,
                     const bs_camera* cams, const int32_t* view_ids, int32_t count, int32_t pw, int32_t ph,
                     int32_t variant, const float bg[3], void* const* flush_bufs, size_t flush_bytes);
+/* A batch of views of ONE scene from HOST memory (the host-buffer form of
+ * bs_render_views): the scene is uploaded once per call (ctxs[0]'s upload
+ * stream), view i = cams[view_ids[i]] renders on ctxs[i % nctx] (async
+ * frame body; every context must be in async mode) and its six planes are
+ * downloaded into host_out[6i .. 6i+5] = color, alpha, depth, final_t,
+ * contrib, term (pinned host memory for full speed; NULL skips a plane).
+ * Outputs are final after bs_context_sync on every context; the host
+ * buffers of one call must stay untouched until then. */
+int bs_render_views_host(bs_context* const* ctxs, int32_t nctx, const bs_gaussian3d* g3d_host, int64_t n,
+                         const bs_camera* cams, const int32_t* view_ids, int32_t count, int32_t pw, int32_t ph,
+                         int32_t variant, const float bg[3], void* const* host_out);
 /* The context-owned planes frames with an empty bs_frame_out render into
  * (device pointers, valid until the next such frame or the context's destroy). */
 int bs_context_frame(bs_context* ctx, bs_frame_out* out);

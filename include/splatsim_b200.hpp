@@ -204,7 +204,8 @@ RenderOutput render_reference(const TileBinning& binning, const std::vector<Gaus
 KernelRun run_kernel(KernelVariant variant, const TileBinning& binning, const std::vector<Gaussian2D>& gaussians,
                      int width, int height, int patch_width, int patch_height,
                      const std::array<float, 3>& background);
-// Device time (ms, CUDA events) of one render of `variant` on this frame.
+// Device time (ms, CUDA events) of one render of `variant` on this frame:
+// the median of `repeats` launches, each from a flushed L2 (256 MiB write).
 double time_kernel_ms(KernelVariant variant, const TileBinning& binning, const std::vector<Gaussian2D>& gaussians,
                       int width, int height, int patch_width, int patch_height, int repeats = 3);
 

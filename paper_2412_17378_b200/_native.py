@@ -110,6 +110,7 @@ SIGNATURES = {
     "bs_super_tile_lengths": (C.c_int, [_vp, _sz, _i32, _i32, _i32, _i32, _vp, _vp]),
     "bs_tile_order_select": (C.c_int, [_vp, _i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "bs_context_list_mode": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
+    "bs_render_views_host": (C.c_int, [_vp, _i32, _vp, _i64, _vp, _vp, _i32, _i32, _i32, _i32, _f32p, _vp]),
     "bs_render_views": (C.c_int, [C.POINTER(C.c_void_p), _i32, _vp, _i64, C.POINTER(Camera), C.POINTER(C.c_int32),
                                   _i32, _i32, _i32, _i32, _f32p, C.POINTER(C.c_void_p), _sz]),
     "bs_context_set_async": (C.c_int, [_vp, _i32]),

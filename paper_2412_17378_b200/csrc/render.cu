@@ -560,6 +560,7 @@ __global__ void __launch_bounds__(kGwThreads) k_render_gw(RArgs A) {
   const int lx = local % A.pw, ly = local / A.pw;
   const int px = tx * A.pw + lx, py = ty * A.ph + ly;
   const bool inside = local < npix && px < A.W && py < A.H;
+  const float my_sx = __fadd_rn((float)px, 0.5f), my_sy = __fadd_rn((float)py, 0.5f);  // S1 sample point
   const uint32_t start = A.ranges[2 * tile], end = A.ranges[2 * tile + 1];
   float* const sa = s_gw_dyn + warp * (2 * 32 * 33);
   float* const stb = sa + 32 * 33;
@@ -591,17 +592,18 @@ __global__ void __launch_bounds__(kGwThreads) k_render_gw(RArgs A) {
       const int j = g0 + lane;
       const bool active = lane < gn;
       const float4 a = s_xyab[active ? j : g0], c = s_cop[active ? j : g0];
+      unsigned gmask = 0;  // entries of the group some live pixel does not skip
       while (live) {
         const int p = __ffs(live) - 1;
         live &= live - 1;
-        const int pl = warp * 32 + p;
-        const float psx = __fadd_rn((float)(tx * A.pw + pl % A.pw), 0.5f);
-        const float psy = __fadd_rn((float)(ty * A.ph + pl / A.pw), 0.5f);
+        const float psx = __shfl_sync(kFull, my_sx, p), psy = __shfl_sync(kFull, my_sy, p);
         const float ts = __shfl_sync(kFull, t, p);
         float alpha = 0.0f;
         const bool ns = active && eval_step<MODE>(a, c, psx, psy, ek, alpha);
         sa[p * 33 + lane] = ns ? alpha : 0.0f;
-        if (__ballot_sync(kFull, ns) == 0) continue;  // no weight is read
+        const unsigned nsm = __ballot_sync(kFull, ns);
+        gmask |= nsm;
+        if (nsm == 0) continue;  // no weight is read
         float pre = ns ? __fsub_rn(1.0f, alpha) : 1.0f;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -617,7 +619,10 @@ __global__ void __launch_bounds__(kGwThreads) k_render_gw(RArgs A) {
       if (!done) {
         const float* row_a = sa + lane * 33;
         const float* row_t = stb + lane * 33;
-        for (int q = 0; q < gn; ++q) {
+        // only the entries some pixel does not skip (the others are skipped
+        // by every pixel: no decision, no commit)
+        for (unsigned m = gmask; m; m &= m - 1) {
+          const int q = __ffs(m) - 1;
           const float al = row_a[q];
           if (al == 0.0f) continue;  // skipped (a non-skipped alpha is >= 1/255)
           const float tmp = __fmul_rn(t, __fsub_rn(1.0f, al));
@@ -907,44 +912,27 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
       if (lane == 0) qpoll = ld_relaxed_u32(A.queue);
     }
     const int cnt = __popc(km);
-    // Branch-free steps: after the sub-tile cull almost every step runs the
-    // exp and a commit in some lane (ncu: 98 % / 97 % of steps), so the
-    // divergent branches only cost reconvergence and branch-resolve stalls.
-    // Every lane evaluates every step; skip / stop / commit become
-    // predicates (a non-committing lane adds c * 0 to its sums and keeps t).
-    // Out-of-range or NaN powers are harmless: their exp is never used (the
-    // cut / power > 0 tests reject them, or, for NaN, alpha = 0.99 as the
-    // reference's std::min gives).
+    // (a branch-free form of these steps — every lane evaluating every step,
+    // skip / stop / commit as predicates — measured 1-3 % slower: the
+    // all-skip steps then pay the exp too)
 #pragma unroll 2
     for (int j = 0; j < cnt; ++j) {
-      const float4 a = s[0][j], c = s[1][j];
-      const float dx = __fsub_rn(sx, a.x);
-      const float dy = __fsub_rn(sy, a.y);
-      const float q = __fadd_rn(__fmul_rn(__fmul_rn(a.z, dx), dx), __fmul_rn(__fmul_rn(c.x, dy), dy));
-      const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(a.w, dx), dy));
-      float e;
-      if (MODE == BS_ALPHA_EXACT) {
-        e = glibc_expf_fast(power, ek);
-      } else {
-        const float p2 = power * 1.4426950408889634f;
-        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(p2));
-      }
-      const float x = __fmul_rn(c.y, e);
-      const float alpha = (x < kAlphaClamp) ? x : kAlphaClamp;  // std::min(0.99f, x)
-      // not skipped: power >= power_cut (certain-skip bound), power <= 0, alpha >= 1/255
-      const bool ns = !done && !(power < c.z) && !(power > 0.0f) && !(alpha < kAlphaSkip);
+      if (done) continue;
+      float alpha;
+      const float4 c = s[1][j];
+      if (!eval_step<MODE>(s[0][j], c, sx, sy, ek, alpha)) continue;
       const float tmp = __fmul_rn(t, __fsub_rn(1.0f, alpha));
-      const bool stop = ns && tmp < kStopThreshold;
-      const bool commit = ns && !stop;
-      if (stop) term = s_k[j];
-      done = done || stop;
-      const float ac = commit ? alpha : 0.0f;
+      if (tmp < kStopThreshold) {
+        done = true;
+        term = s_k[j];
+        continue;
+      }
       if (MODE == BS_ALPHA_EXACT)
-        acc.add_wide(ac, t, reinterpret_cast<const double2*>(s[2])[j], reinterpret_cast<const double2*>(s[3])[j]);
+        acc.add_wide(alpha, t, reinterpret_cast<const double2*>(s[2])[j], reinterpret_cast<const double2*>(s[3])[j]);
       else
-        acc.add(ac, t, s[2][j], c.w);
-      t = commit ? tmp : t;
-      contrib += commit ? 1 : 0;
+        acc.add(alpha, t, s[2][j], c.w);
+      t = tmp;
+      ++contrib;
     }
     __syncwarp();
     if (LM != kListTile) mpos += (uint32_t)__popc(mm);

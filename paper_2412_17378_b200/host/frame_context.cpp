@@ -143,6 +143,13 @@ struct bs_context {
   int64_t io_pixels = 0;
   cudaEvent_t ev_h2d[kIo] = {}, ev_comp[kIo] = {}, ev_d2h[kIo] = {};
   int io_next = 0;
+  // bs_render_views_host (on the batch's first context): the scene's two
+  // alternating device buffers, their upload and "all readers done" events
+  void* batch_g3d[2] = {nullptr, nullptr};
+  size_t batch_g3d_bytes[2] = {0, 0};
+  cudaEvent_t ev_batch[2] = {}, ev_batch_done[2] = {};
+  int batch_next = 0;
+  cudaEvent_t ev_any = nullptr;  // this context's stream position (batch bookkeeping)
   // BS_PIPE_TRACE=1: per-frame H2D / compute / D2H event timeline, printed at sync
   std::vector<std::array<cudaEvent_t, 6>> trace;
   bool pl_calibrated = false;
@@ -271,6 +278,12 @@ extern "C" int bs_context_destroy(bs_context* c) {
     for (cudaEvent_t e : {c->ev_h2d[i], c->ev_comp[i], c->ev_d2h[i]})
       if (e) cudaEventDestroy(e);
   }
+  for (int b = 0; b < 2; ++b) {
+    if (c->batch_g3d[b]) cudaFree(c->batch_g3d[b]);
+    for (cudaEvent_t e : {c->ev_batch[b], c->ev_batch_done[b]})
+      if (e) cudaEventDestroy(e);
+  }
+  if (c->ev_any) cudaEventDestroy(c->ev_any);
   if (c->st_h2d) cudaStreamSynchronize(c->st_h2d), cudaStreamDestroy(c->st_h2d);
   if (c->st_d2h) cudaStreamSynchronize(c->st_d2h), cudaStreamDestroy(c->st_d2h);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
@@ -830,26 +843,27 @@ extern "C" int bs_context_drop_pending(bs_context* c) {
 // Pipelined host-buffer frames: upload (st_h2d), the async frame body
 // (context stream), download (st_d2h), ordered by per-slot events so three
 // frames are in flight.  Outputs are final after bs_context_sync.
-extern "C" int bs_render_frame_host_async(bs_context* c, const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam,
-                                          int32_t pw, int32_t ph, int32_t variant, const float bg[3], float* color,
-                                          float* alpha, float* depth, float* final_t, int32_t* contrib,
-                                          int32_t* term) {
-  if (!c || !cam || !bg || n < 0 || (n > 0 && !g3d) || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
-  if (variant < -1 || variant > 4) return BS_ERR_INVALID_ARGUMENT;
+namespace {
+int ensure_io(bs_context* c) {
+  if (c->st_h2d) return BS_OK;
+  CUTRY(cudaEventCreateWithFlags(&c->ev_any, cudaEventDisableTiming));
+  CUTRY(cudaStreamCreateWithFlags(&c->st_h2d, cudaStreamNonBlocking));
+  CUTRY(cudaStreamCreateWithFlags(&c->st_d2h, cudaStreamNonBlocking));
+  for (int i = 0; i < bs_context::kIo; ++i)
+    for (cudaEvent_t* e : {&c->ev_h2d[i], &c->ev_comp[i], &c->ev_d2h[i]})
+      CUTRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  return BS_OK;
+}
+
+// One pipelined frame.  g3d_dev == NULL: upload g3d_host into the I/O slot
+// first (on st_h2d); else the scene is already on the device and the frame
+// waits for scene_ready (an event on another context's upload stream).
+int host_async_frame(bs_context* c, const bs_gaussian3d* g3d_host, const bs_gaussian3d* g3d_dev,
+                     cudaEvent_t scene_ready, int64_t n, const bs_camera* cam, int32_t pw, int32_t ph,
+                     int32_t variant, const float bg[3], void* const hs[6]) {
   const int32_t W = cam->width, H = cam->height;
-  if (W <= 0 || H <= 0) return BS_ERR_INVALID_ARGUMENT;
-  if (!c->async_mode || !bs_bin_async_supported(W, H, pw, ph)) {  // no pipeline: the synchronous form
-    return bs_render_frame_host(c, g3d, n, cam, pw, ph, variant, bg, color, alpha, depth, final_t, contrib, term,
-                                nullptr);
-  }
   cudaStream_t st = static_cast<cudaStream_t>(bs_context_stream(c));
-  if (!c->st_h2d) {
-    CUTRY(cudaStreamCreateWithFlags(&c->st_h2d, cudaStreamNonBlocking));
-    CUTRY(cudaStreamCreateWithFlags(&c->st_d2h, cudaStreamNonBlocking));
-    for (int i = 0; i < bs_context::kIo; ++i)
-      for (cudaEvent_t* e : {&c->ev_h2d[i], &c->ev_comp[i], &c->ev_d2h[i]})
-        CUTRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-  }
+  TRY(ensure_io(c));
   const int io = c->io_next;
   c->io_next = (io + 1) % bs_context::kIo;
   const int64_t P = int64_t(W) * H;
@@ -863,12 +877,6 @@ extern "C" int bs_render_frame_host_async(bs_context* c, const bs_gaussian3d* g3
     c->io_pixels = P;
     ++g_alloc_gen;
   }
-  // upload into slot io once the frame that last read it is done
-  CUTRY(cudaStreamWaitEvent(c->st_h2d, c->ev_comp[io], 0));
-  if (c->io_g3d_bytes[io] < size_t(std::max<int64_t>(n, 1)) * sizeof(bs_gaussian3d)) {
-    CUTRY(cudaStreamSynchronize(c->st_h2d));
-    TRY(grow(&c->io_g3d[io], &c->io_g3d_bytes[io], size_t(std::max<int64_t>(n, 1)) * sizeof(bs_gaussian3d)));
-  }
   static const bool tracing = [] {
     const char* e = getenv("BS_PIPE_TRACE");
     return e && e[0] == '1';
@@ -876,25 +884,36 @@ extern "C" int bs_render_frame_host_async(bs_context* c, const bs_gaussian3d* g3
   std::array<cudaEvent_t, 6> tev{};
   if (tracing)
     for (auto& e : tev) cudaEventCreate(&e);
-  if (tracing) cudaEventRecord(tev[0], c->st_h2d);
-  if (n > 0)
-    CUTRY(cudaMemcpyAsync(c->io_g3d[io], g3d, size_t(n) * sizeof(bs_gaussian3d), cudaMemcpyHostToDevice, c->st_h2d));
-  if (tracing) cudaEventRecord(tev[1], c->st_h2d);
-  CUTRY(cudaEventRecord(c->ev_h2d[io], c->st_h2d));
-  // compute after the upload and after the slot's previous download
-  CUTRY(cudaStreamWaitEvent(st, c->ev_h2d[io], 0));
+  const bs_gaussian3d* gd = g3d_dev;
+  if (!gd) {
+    // upload into slot io once the frame that last read it is done
+    CUTRY(cudaStreamWaitEvent(c->st_h2d, c->ev_comp[io], 0));
+    if (c->io_g3d_bytes[io] < size_t(std::max<int64_t>(n, 1)) * sizeof(bs_gaussian3d)) {
+      CUTRY(cudaStreamSynchronize(c->st_h2d));
+      TRY(grow(&c->io_g3d[io], &c->io_g3d_bytes[io], size_t(std::max<int64_t>(n, 1)) * sizeof(bs_gaussian3d)));
+    }
+    if (tracing) cudaEventRecord(tev[0], c->st_h2d);
+    if (n > 0)
+      CUTRY(cudaMemcpyAsync(c->io_g3d[io], g3d_host, size_t(n) * sizeof(bs_gaussian3d), cudaMemcpyHostToDevice,
+                            c->st_h2d));
+    if (tracing) cudaEventRecord(tev[1], c->st_h2d);
+    CUTRY(cudaEventRecord(c->ev_h2d[io], c->st_h2d));
+    CUTRY(cudaStreamWaitEvent(st, c->ev_h2d[io], 0));
+    gd = static_cast<const bs_gaussian3d*>(c->io_g3d[io]);
+  } else if (scene_ready) {
+    CUTRY(cudaStreamWaitEvent(st, scene_ready, 0));
+  }
+  // compute after the slot's previous download
   CUTRY(cudaStreamWaitEvent(st, c->ev_d2h[io], 0));
   TRY(verify_pending(c, st, bs_context::kDepth - 1));
   const bs_frame_out fo{static_cast<float*>(c->io_out[io][0]), static_cast<float*>(c->io_out[io][1]),
                         static_cast<float*>(c->io_out[io][2]), static_cast<float*>(c->io_out[io][3]),
                         static_cast<int32_t*>(c->io_out[io][4]), static_cast<int32_t*>(c->io_out[io][5])};
-  const bs_gaussian3d* gd = static_cast<const bs_gaussian3d*>(c->io_g3d[io]);
   if (tracing) cudaEventRecord(tev[2], st);
   TRY(frame_device(c, gd, n, cam, pw, ph, variant, bg, fo, st, true));
   if (tracing) cudaEventRecord(tev[3], st);
   bs_context::Pending& q = c->pending[c->n_pending - 1];  // the entry frame_device just queued
   q.io = io;
-  void* hs[6] = {color, alpha, depth, final_t, contrib, term};
   std::copy(hs, hs + 6, q.host_out);
   CUTRY(cudaEventRecord(c->ev_comp[io], st));
   // download once computed
@@ -904,6 +923,80 @@ extern "C" int bs_render_frame_host_async(bs_context* c, const bs_gaussian3d* g3
   if (tracing) cudaEventRecord(tev[5], c->st_d2h);
   CUTRY(cudaEventRecord(c->ev_d2h[io], c->st_d2h));
   if (tracing) c->trace.push_back(tev);
+  return BS_OK;
+}
+}  // namespace
+
+extern "C" int bs_render_frame_host_async(bs_context* c, const bs_gaussian3d* g3d, int64_t n, const bs_camera* cam,
+                                          int32_t pw, int32_t ph, int32_t variant, const float bg[3], float* color,
+                                          float* alpha, float* depth, float* final_t, int32_t* contrib,
+                                          int32_t* term) {
+  if (!c || !cam || !bg || n < 0 || (n > 0 && !g3d) || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
+  if (variant < -1 || variant > 4) return BS_ERR_INVALID_ARGUMENT;
+  const int32_t W = cam->width, H = cam->height;
+  if (W <= 0 || H <= 0) return BS_ERR_INVALID_ARGUMENT;
+  if (!c->async_mode || !bs_bin_async_supported(W, H, pw, ph)) {  // no pipeline: the synchronous form
+    return bs_render_frame_host(c, g3d, n, cam, pw, ph, variant, bg, color, alpha, depth, final_t, contrib, term,
+                                nullptr);
+  }
+  void* const hs[6] = {color, alpha, depth, final_t, contrib, term};
+  return host_async_frame(c, g3d, nullptr, nullptr, n, cam, pw, ph, variant, bg, hs);
+}
+
+// A batch of views of ONE scene from host memory: the scene is uploaded
+// once (on ctxs[0]'s upload stream, into one of two device buffers that
+// alternate between calls), then view i = cams[view_ids[i]] renders on
+// ctxs[i % nctx] (its async frame body) and its six planes are downloaded
+// into host_out[6 i .. 6 i + 5] (color, alpha, depth, final_t, contrib,
+// term; NULL skips a plane).  Outputs are final after bs_context_sync on
+// every context.  Requires async mode on every context.
+extern "C" int bs_render_views_host(bs_context* const* ctxs, int32_t nctx, const bs_gaussian3d* g3d_host, int64_t n,
+                                    const bs_camera* cams, const int32_t* view_ids, int32_t count, int32_t pw,
+                                    int32_t ph, int32_t variant, const float bg[3], void* const* host_out) {
+  if (!ctxs || nctx <= 0 || !cams || !view_ids || count < 0 || !bg || !host_out || n < 0 || (n > 0 && !g3d_host))
+    return BS_ERR_INVALID_ARGUMENT;
+  if (pw <= 0 || ph <= 0 || variant < -1 || variant > 4) return BS_ERR_INVALID_ARGUMENT;
+  for (int32_t k = 0; k < nctx; ++k)
+    if (!ctxs[k] || !ctxs[k]->async_mode) return BS_ERR_INVALID_ARGUMENT;
+  if (count == 0) return BS_OK;
+  bs_context* c0 = ctxs[0];
+  for (int32_t k = 0; k < nctx; ++k) TRY(ensure_io(ctxs[k]));
+  if (!c0->ev_batch[0])
+    for (auto* e : {&c0->ev_batch[0], &c0->ev_batch[1], &c0->ev_batch_done[0], &c0->ev_batch_done[1]})
+      CUTRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  // Every earlier frame is verified first (a frame whose K overflowed is
+  // rendered again now, reading its batch buffer), then the previous call's
+  // buffer is marked free once all its readers — re-renders included — are
+  // done.  (The host waits here for the previous call's last counts: one
+  // short bubble per batch.)
+  for (int32_t k = 0; k < nctx; ++k) TRY(verify_pending(ctxs[k], static_cast<cudaStream_t>(bs_context_stream(ctxs[k]))));
+  const int b = c0->batch_next;
+  c0->batch_next ^= 1;
+  if (c0->batch_g3d[b ^ 1]) {
+    for (int32_t k = 0; k < nctx; ++k) {
+      CUTRY(cudaEventRecord(ctxs[k]->ev_any, static_cast<cudaStream_t>(bs_context_stream(ctxs[k]))));
+      CUTRY(cudaStreamWaitEvent(c0->st_h2d, ctxs[k]->ev_any, 0));
+    }
+    CUTRY(cudaEventRecord(c0->ev_batch_done[b ^ 1], c0->st_h2d));
+  }
+  const size_t bytes = size_t(std::max<int64_t>(n, 1)) * sizeof(bs_gaussian3d);
+  // the buffer's previous readers (the views of the call before last) are done
+  CUTRY(cudaStreamWaitEvent(c0->st_h2d, c0->ev_batch_done[b], 0));
+  if (c0->batch_g3d_bytes[b] < bytes) {
+    CUTRY(cudaStreamSynchronize(c0->st_h2d));
+    TRY(grow(&c0->batch_g3d[b], &c0->batch_g3d_bytes[b], bytes));
+  }
+  if (n > 0) CUTRY(cudaMemcpyAsync(c0->batch_g3d[b], g3d_host, size_t(n) * sizeof(bs_gaussian3d),
+                                   cudaMemcpyHostToDevice, c0->st_h2d));
+  CUTRY(cudaEventRecord(c0->ev_batch[b], c0->st_h2d));
+  const bs_gaussian3d* gd = static_cast<const bs_gaussian3d*>(c0->batch_g3d[b]);
+  for (int32_t i = 0; i < count; ++i) {
+    bs_context* c = ctxs[i % nctx];
+    const bs_camera& cam = cams[view_ids[i]];
+    if (cam.width <= 0 || cam.height <= 0) return BS_ERR_INVALID_ARGUMENT;
+    if (!bs_bin_async_supported(cam.width, cam.height, pw, ph)) return BS_ERR_UNSUPPORTED;
+    TRY(host_async_frame(c, nullptr, gd, c0->ev_batch[b], n, &cam, pw, ph, variant, bg, host_out + 6 * size_t(i)));
+  }
   return BS_OK;
 }
 

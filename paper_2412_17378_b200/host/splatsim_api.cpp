@@ -65,6 +65,7 @@ struct Ctx {
   cudaStream_t st = nullptr;
   DBuf g3d, xyab, cop, rgbr, nvis, kdev, pre_ws, bin_ws, pl, ranges, stats_ws, order, hist, render_ws, g2d;
   DBuf planes[6];
+  DBuf flush;  // L2 flush buffer for time_kernel_ms (larger than the 126 MB L2)
   Ctx() { cu("cudaStreamCreate", cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)); }
   ~Ctx() {
     if (st) cudaStreamDestroy(st);
@@ -349,24 +350,32 @@ double time_kernel_ms(KernelVariant variant, const TileBinning& binning, const s
   const size_t rwb = bs_render_workspace_bytes(width, height);
   void* rws = c.render_ws.get(rwb);
   const float bg[3] = {0, 0, 0};
-  cudaEvent_t a, b;
-  cu("event", cudaEventCreate(&a));
-  cu("event", cudaEventCreate(&b));
+  // every timed launch starts from a flushed L2 (a 256 MiB write, outside
+  // the timed interval), like the frames of a real view stream: warm-L2
+  // repeats would favour the kernel whose lists happen to stay resident
+  constexpr size_t kFlush = size_t(256) << 20;
+  void* fl = c.flush.get(kFlush);
+  const int reps = std::max(1, repeats);
+  std::vector<cudaEvent_t> ev(2 * size_t(reps));
+  for (auto& e : ev) cu("event", cudaEventCreate(&e));
   auto launch = [&]() {
     ck("time_kernel_ms", bs_render_forward(static_cast<int>(variant), mode_c(), s, d.pl, d.ranges,
                                            static_cast<uint32_t*>(c.order.p), width, height, patch_width,
                                            patch_height, bg, fo, rws, rwb, c.st));
   };
-  launch();  // warm-up
-  cu("event", cudaEventRecord(a, c.st));
-  for (int i = 0; i < std::max(1, repeats); ++i) launch();
-  cu("event", cudaEventRecord(b, c.st));
+  launch();  // warm-up (first-launch costs)
+  for (int i = 0; i < reps; ++i) {
+    cu("flush", cudaMemsetAsync(fl, i & 0xff, kFlush, c.st));
+    cu("event", cudaEventRecord(ev[2 * size_t(i)], c.st));
+    launch();
+    cu("event", cudaEventRecord(ev[2 * size_t(i) + 1], c.st));
+  }
   c.sync();
-  float ms = 0;
-  cu("event", cudaEventElapsedTime(&ms, a, b));
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
-  return double(ms) / std::max(1, repeats);
+  std::vector<float> ms(size_t(reps), 0.0f);
+  for (int i = 0; i < reps; ++i) cu("event", cudaEventElapsedTime(&ms[size_t(i)], ev[2 * size_t(i)], ev[2 * size_t(i) + 1]));
+  for (auto& e : ev) cudaEventDestroy(e);
+  std::sort(ms.begin(), ms.end());
+  return double(ms[size_t(reps) / 2]);  // median
 }
 
 // ---------------------------------------------------------------------------

@@ -23,6 +23,7 @@ torch = pytest.importorskip("torch")
 
 from paper_2412_17378_b200 import _native as N  # noqa: E402
 from paper_2412_17378_b200 import api  # noqa: E402
+from paper_2412_17378_b200 import sharding  # noqa: E402
 
 DEV = "cuda"
 PLANES_F = ("color", "alpha", "depth", "final_t")
@@ -762,9 +763,8 @@ def test_c4_tile_sampled(mode):
 def test_frame_pipeline_graph_replay_matches():
     """CUDA-graph mode: frames replayed from the captured graph (new camera
     each time) equal the same frames rendered launch by launch."""
-    import bench
     W, H, f, n = 960, 540, 500.0, 200_000
-    cams = [N.make_camera(bench.orbit_view(k * 9), (f, f), W, H) for k in range(7)]
+    cams = [N.make_camera(sharding.orbit_view(k * 9), (f, f), W, H) for k in range(7)]
     g3d = api.gen_clustered_scene(n, cams[0])
     d = api.g3d_to_device(g3d)
     ref = []
@@ -798,9 +798,8 @@ def test_render_views_batch_matches():
     native call (with per-view L2 flushes) equal the same views rendered one
     call at a time; checked on each context's last view, over several batches
     so graph capture and replay both run."""
-    import bench
     W, H, f, n = 960, 540, 500.0, 200_000
-    cams = [N.make_camera(bench.orbit_view(k * 11), (f, f), W, H) for k in range(8)]
+    cams = [N.make_camera(sharding.orbit_view(k * 11), (f, f), W, H) for k in range(8)]
     g3d = api.gen_clustered_scene(n, cams[0])
     d = api.g3d_to_device(g3d)
     ref = []
@@ -847,9 +846,8 @@ def test_frame_pipeline_super_lists_match_tile_lists():
     """Frames >= 1 Mpixel take the super-tile path (lists at 32x32, members
     kept per 16x16 tile); with graphs and async frames they equal the
     stage-by-stage pipeline on 16x16 lists."""
-    import bench
     W, H, f, n = 1280, 832, 700.0, 150_000
-    cams = [N.make_camera(bench.orbit_view(k * 13), (f, f), W, H) for k in range(5)]
+    cams = [N.make_camera(sharding.orbit_view(k * 13), (f, f), W, H) for k in range(5)]
     g3d = api.gen_clustered_scene(n, cams[0])
     d = api.g3d_to_device(g3d)
     pipe = api.Pipeline(W, H, 16, 16, DEV, N.ALPHA_EXACT)
@@ -903,9 +901,8 @@ def test_frame_pipeline_super_lists_fast_mode():
 def test_host_async_pipeline_matches():
     """bs_render_frame_host_async: frames uploaded / rendered / downloaded on
     three streams equal the synchronous host-buffer frames."""
-    import bench
     W, H, f, n = 480, 270, 250.0, 40_000
-    cams = [N.make_camera(bench.orbit_view(k * 7), (f, f), W, H) for k in range(6)]
+    cams = [N.make_camera(sharding.orbit_view(k * 7), (f, f), W, H) for k in range(6)]
     g3d = api.gen_clustered_scene(n, cams[0])
     host = torch.from_numpy(np.ascontiguousarray(g3d).view(np.uint8).reshape(-1).copy()).pin_memory()
     P = W * H
@@ -961,3 +958,49 @@ def test_two_pipelines_on_two_streams():
             got = p.frame.to_numpy()
             assert np.array_equal(got["contrib"], ref["contrib"]) and np.array_equal(got["term"], ref["term"])
             assert np.array_equal(got["final_t"], ref["final_t"])
+
+
+def test_render_views_host_batch_matches():
+    """bs_render_views_host: one scene upload per call, views round-robin over
+    two async contexts, every view's planes downloaded to its own host
+    buffers; three calls back to back (the alternating scene buffers), each
+    view equal to the oracle's render of that view."""
+    W, H, f, n = 640, 480, 600.0, 30000
+    g3d, cam0 = scene(n, W, H, f)
+    views = [3, 17, 40, 63, 9]
+    cams = [N.make_camera(sharding.orbit_view(k), (f, f), W, H) for k in range(64)]
+    refs = {}
+    for k in views:
+        oc = O.Camera.from_buffer_copy(bytes(cams[k]))
+        g2d = O.project_all(g3d, oc)
+        pl, rg = O.bin_tiles(g2d, W, H, 16, 16)
+        refs[k] = O.render(0, pl, rg, g2d, W, H, 16, 16, (0.1, 0.2, 0.3), lazy=True, threads=0)
+    ctxs = []
+    for _ in range(2):
+        cx = C.c_void_p()
+        N.call("bs_context_create", C.byref(cx), N.ALPHA_EXACT)
+        N.call("bs_context_set_async", cx, 1)
+        ctxs.append(cx)
+    P = W * H
+    host = np.ascontiguousarray(g3d)
+    ctx_arr = (C.c_void_p * 2)(*[c.value for c in ctxs])
+    cam_arr = (N.Camera * 64)(*cams)
+    ids = (C.c_int32 * len(views))(*views)
+    bgc = (C.c_float * 3)(0.1, 0.2, 0.3)
+    calls = []
+    for _ in range(3):
+        outs = [[np.zeros(3 * P, np.float32)] + [np.zeros(P, np.float32) for _ in range(3)] +
+                [np.zeros(P, np.int32) for _ in range(2)] for _ in views]
+        ptrs = (C.c_void_p * (6 * len(views)))(*[o.ctypes.data for v in outs for o in v])
+        N.call("bs_render_views_host", ctx_arr, 2, host.ctypes.data, n, cam_arr, ids, len(views), 16, 16, -1, bgc,
+               ptrs)
+        calls.append((outs, ptrs))
+    for c in ctxs:
+        N.call("bs_context_sync", c, None)
+        N.call("bs_context_destroy", c)
+    for outs, _ in calls:
+        for k, o in zip(views, outs):
+            ref = refs[k]
+            assert np.array_equal(o[4], ref["contrib"]) and np.array_equal(o[5], ref["term"]), k
+            assert np.array_equal(o[3], ref["final_t"]) and np.array_equal(o[1], ref["alpha"]), k
+            assert float(np.abs(o[0] - ref["color"]).max()) <= 1e-6, k

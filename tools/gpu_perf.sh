@@ -19,3 +19,10 @@ python tools/ncu_counters.py --out "$OUT/ncu_counters.json" --tag "$TAG" \
   c2_FineGrainedCombined_exact_super="$OUT/fine_super_c2.ncu-rep" \
   c2_FineGrainedCombined_exact="$OUT/fine_api_c2.ncu-rep" > "$OUT/counters.log" 2>&1
 tail -c 1500 "$OUT/bench.json"; cat "$OUT/counters.log"
+if [ "${GW:-0}" = 1 ]; then
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_render_gw -c 1 -o "$OUT/gw_c2" -f \
+    python tools/profile_render.py --config c2 --variant GaussianWise --alpha exact --reps 1 > "$OUT/ncu_gw.log" 2>&1
+  python tools/ncu_counters.py --out "$OUT/ncu_counters.json" --tag "$TAG" c2_GaussianWise_exact="$OUT/gw_c2.ncu-rep" \
+    >> "$OUT/counters.log" 2>&1
+  tail -1 "$OUT/counters.log"
+fi
