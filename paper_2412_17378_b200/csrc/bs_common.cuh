@@ -79,7 +79,16 @@ struct WsSizer {
 // FineGrainedCombined when t_static > t_fine, else SharedMemOpt (the
 // selector's fallback, src/adaptive.cpp:27-28).  rho = 0.75 and c0 = 64 list
 // entries are the B200 calibration from the C3 sweep (profiles/r1_c3_*.jsonl).
-__host__ __device__ inline int select_variant_formula(uint64_t total, uint32_t max_len, int pw, int ph, int sm_count) {
+// Short lists: below kShortList entries per tile on average the fine-grained
+// kernel's fixed per-task cost (queue claim, per-batch cull and compaction,
+// 8 tasks per 16x16 tile) outweighs any balance it buys — the r2 selector
+// sweep (profiles/r2_selector_sweep.jsonl) measured SharedMemOpt 10-40 %
+// faster at every point with a mean list of <= 6 entries, FG faster from
+// ~22 up (ties near 14).
+constexpr double kShortList = 12.0;
+__host__ __device__ inline int select_variant_formula(uint64_t total, uint32_t max_len, int32_t tiles, int pw, int ph,
+                                                      int sm_count) {
+  if (tiles > 0 && (double)total < kShortList * (double)tiles) return BS_SHARED_MEM_OPT;
   const double S = sm_count > 0 ? (double)sm_count : 148.0;
   const int pixels = pw * ph;
   const double k = pixels <= 128 ? 12.0 : (pixels <= 256 ? 6.0 : 3.0);  // resident tile CTAs per SM

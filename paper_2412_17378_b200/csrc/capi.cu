@@ -65,13 +65,13 @@ extern "C" int bs_device_sm_count(int32_t* sm_count) {
 extern "C" int bs_select_variant(const bs_tile_histogram* stats, int32_t width, int32_t height, int32_t pw, int32_t ph,
                                  int32_t sm_count) {
   if (!stats || width <= 0 || height <= 0 || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
-  return bs::select_variant_formula(stats->total, stats->max, pw, ph, sm_count);
+  return bs::select_variant_formula(stats->total, stats->max, stats->tiles, pw, ph, sm_count);
 }
 
 namespace bs {
 __global__ void k_select_variant(const bs_tile_histogram* __restrict__ stats, int pw, int ph, int sm_count,
                                  int32_t* __restrict__ variant) {
-  *variant = select_variant_formula(stats->total, stats->max, pw, ph, sm_count);
+  *variant = select_variant_formula(stats->total, stats->max, stats->tiles, pw, ph, sm_count);
 }
 }  // namespace bs
 

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t* __restrict_
       s.min = s.p50 = s.p99 = 0;  // order statistics: bs_tile_stats
       s.mean = T ? (double)sum / (double)T : 0.0;
       *out = s;
-      if (sel.variant) *sel.variant = select_variant_formula(sum, m, sel.pw, sel.ph, sel.sm_count);
+      if (sel.variant) *sel.variant = select_variant_formula(sum, m, T, sel.pw, sel.ph, sel.sm_count);
     }
   }
   // bases: buckets descending, warps ascending inside a bucket

@@ -91,6 +91,12 @@ def test_selector_rule():
     h.total, h.max, h.tiles, h.mean = 200, 2, 8160, 200 / 8160
     assert L.bs_select_variant(C.byref(h), 1920, 1080, 16, 16, 148) == 4
     assert L.bs_select_variant(None, 1920, 1080, 16, 16, 148) == -1
+    # short lists (mean < 12 entries per tile, even with a 30x imbalance):
+    # SharedMemOpt (profiles/r2_selector_sweep.jsonl: 1k-Gaussian 1080p / 4K frames)
+    h.total, h.max, h.tiles, h.mean = 8160 * 5, 163, 8160, 5.0
+    assert L.bs_select_variant(C.byref(h), 1920, 1080, 16, 16, 148) == 4
+    h.total, h.max, h.tiles, h.mean = 8160 * 53, 1493, 8160, 53.0  # 10k clustered: FG
+    assert L.bs_select_variant(C.byref(h), 1920, 1080, 16, 16, 148) == 3
 
 
 @pytest.mark.parametrize("n,W,H,f,bgf", [(3000, 1920, 1080, 1000.0, 0.12), (2000, 256, 256, 256.0, 1.0)])
