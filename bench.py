@@ -346,7 +346,9 @@ def main():
     ap.add_argument("--sync-frames", action="store_true", help="wait for K inside each frame (no async mode)")
     ap.add_argument("--no-graphs", action="store_true", help="launch every kernel instead of replaying a CUDA graph")
     ap.add_argument("--streams", type=int, default=4, help="frame contexts on separate streams (views round-robin)")
-    ap.add_argument("--fine-ctas", type=int, default=3, help="FineGrainedCombined CTAs per SM when streams > 1")
+    ap.add_argument("--fine-ctas", type=int, default=0,
+                    help="FineGrainedCombined CTAs per SM per context when streams > 1 (0 = as many as fit; "
+                         "tools/sweep_occupancy.sh: uncapped is best with the r2 kernels)")
     ap.add_argument("--no-extras", action="store_true", help="skip per-variant sweep / e2e / cpu baseline")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 imbalance sweep in the extras")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
@@ -517,7 +519,7 @@ def main():
                                     f"view-sharded x{world}: one view per rank per step, round-robin over the "
                                     f"orbit; scene replicated, no data-path collective"),
                        l2="flushed before every step (256 MiB write on the step's stream, inside the timed region)",
-                       streams=ns, fine_ctas_per_sm=args.fine_ctas if ns > 1 else "max"),
+                       streams=ns, fine_ctas_per_sm=(args.fine_ctas or "max") if ns > 1 else "max"),
         "gpu_launches": launches,
         "async_reruns": reruns,
         "point_list_grows": grows,

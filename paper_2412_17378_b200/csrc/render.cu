@@ -942,10 +942,11 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
 }
 
 // MINB: resident CTAs per SM the register budget is sized for — 4 (64
-// registers) when the kernel has the SMs to itself, 3 (80 registers: the
-// exp's constants and table base stay in registers instead of being
-// re-loaded every list entry) when it is capped at 3 CTAs per SM to share the
-// SMs with other frame contexts (bs_render_set_fine_occupancy)
+// registers, the default) or, opt-in with BS_FINE_WIDE=1 when the kernel is
+// capped at <= 3 CTAs per SM, 3 (80 registers: the exp's constants stay in
+// registers).  The 80-register build is 1 % faster alone but 1 % slower in
+// the streamed frame pipeline (tools/sweep_occupancy.sh), where the
+// uncapped 64-register kernel is best.
 template <int MODE, int LM, int MINB>
 __global__ void __launch_bounds__(kFineThreads, MINB) k_render_fine(RArgs A, int subs) {
   __shared__ float4 s_rec[kFineWarps][4][32];
@@ -1079,7 +1080,7 @@ struct FineTuning {
   int ctas_per_sm;  // BS_FINE_CTAS_PER_SM (0 = as many as fit)
   bool donate;      // BS_FINE_DONATE=0 disables the tail hand-off
   int donate_after, donate_min_remain, stragglers, stragglers_super;
-  bool wide;        // BS_FINE_WIDE=0: never the 80-register build
+  bool wide;        // BS_FINE_WIDE=1: the 80-register build when capped at <= 3 CTAs/SM
   bool no_lpt;      // BS_FINE_NO_LPT=1: tasks in tile-index order
 };
 static int env_int(const char* name, int dflt) {
@@ -1095,7 +1096,7 @@ static const FineTuning& fine_tuning() {
     f.donate_min_remain = env_int("BS_FINE_DONATE_MIN", kDonateMinRemain);
     f.stragglers = env_int("BS_FINE_STRAGGLERS", kStragglers);
     f.stragglers_super = env_int("BS_FINE_STRAGGLERS_SUPER", kStragglers);
-    f.wide = env_int("BS_FINE_WIDE", 1) != 0;
+    f.wide = env_int("BS_FINE_WIDE", 0) != 0;  // opt-in: measured 1 % slower in the streamed pipeline
     f.no_lpt = env_int("BS_FINE_NO_LPT", 0) != 0;
     return f;
   }();

@@ -191,6 +191,31 @@ int main() {
     CHECK(threw);
   }
 
+  // the regime where the baseline wins on B200 (profiles/r2_selector_sweep.jsonl):
+  // a sparse 1080p frame (1,000 uniform Gaussians, ~5 entries per tile) —
+  // the measured checkpoint (L2-flushed kernel times) switches permanently
+  // to SharedMemOpt and the per-frame predictor picks it too
+  {
+    splatsim::Camera c2;
+    c2.focal = {1000.0f, 1000.0f};
+    c2.width = 1920;
+    c2.height = 1080;
+    splatsim::ClusterSceneParams sp;
+    sp.n_gaussians = 1000;
+    sp.background_fraction = 1.0;
+    const auto gs = splatsim::project_all(splatsim::gen_clustered_scene(sp, c2), c2);
+    const auto bb = splatsim::bin_tiles(gs, 1920, 1080, 16, 16);
+    const double t_fg = splatsim::time_kernel_ms(splatsim::KernelVariant::FineGrainedCombined, bb, gs, 1920, 1080,
+                                                 16, 16, 7);
+    const double t_smo = splatsim::time_kernel_ms(splatsim::KernelVariant::SharedMemOpt, bb, gs, 1920, 1080, 16, 16,
+                                                  7);
+    std::printf("sparse 1080p: FineGrainedCombined %.4f ms, SharedMemOpt %.4f ms\n", t_fg, t_smo);
+    const splatsim::SelectionState st = splatsim::checkpoint(splatsim::SelectionState{}, 0, bb, gs, 1920, 1080, 16, 16);
+    CHECK(st.switched && st.current == splatsim::KernelVariant::SharedMemOpt);
+    CHECK(splatsim::select_variant(splatsim::tile_load_histogram(bb), 1920, 1080, 16, 16) ==
+          splatsim::KernelVariant::SharedMemOpt);
+  }
+
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

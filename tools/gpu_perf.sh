@@ -11,7 +11,7 @@ timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-c3 "$@"
 echo "bench rc=$?" >> "$OUT/bench.err"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_render_fine -c 1 \
   -o "$OUT/fine_super_c2" -f python tools/profile_render.py --config c2 --variant FineGrainedCombined \
-  --alpha exact --reps 1 --frame-pipeline --fine-ctas 3 > "$OUT/ncu_super.log" 2>&1
+  --alpha exact --reps 1 --frame-pipeline > "$OUT/ncu_super.log" 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_render_fine -c 1 \
   -o "$OUT/fine_api_c2" -f python tools/profile_render.py --config c2 --variant FineGrainedCombined \
   --alpha exact --reps 1 > "$OUT/ncu_api.log" 2>&1
