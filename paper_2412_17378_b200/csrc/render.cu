@@ -797,6 +797,146 @@ __device__ __forceinline__ void gw_finish_pixel(const RArgs& A, uint32_t from, u
   part.warp_sum();
 }
 
+// ---------------------------------------------------------------------------
+// GaussianWise with the sub-tile cull (r2): the paper's static schedule (one
+// CTA per tile, Alg. 2) with each warp owning 8x4-pixel sub-tiles of the tile
+// (lane = pixel for the state).  Per 32-entry batch of the tile's list the
+// loading lane culls its entry against the sub-tile (cull_subtile, as the
+// fine-grained kernel) and the survivors are compacted; then, two phases per
+// group of survivors:
+//   phase 1, Gaussian-wise (lane = survivor), once per live pixel: alpha of
+//     the group's entries at the pixel, the shfl_up doubling prefix product
+//     of (1 - alpha) from the pixel's carried t (inc/blend.hpp:69-83) -> each
+//     entry's colour weight t_before; (alpha, t_before) into the warp's
+//     32 x 33 scratch;
+//   phase 2, serial (lane = pixel): skip / stop / commit in list order over
+//     the entries some pixel keeps; contrib, term and the carried t follow
+//     the serial float recurrence (src/kernels.cpp:79-89) bit for bit.
+// Culled entries have alpha < 1/255 at every pixel of the sub-tile (skipped:
+// factor 1), so dropping them changes only how the doubling prefix groups
+// the factors — the colour weights differ from render_gaussianwise's fixed
+// 32-entry windows by float reassociation (<= 1e-6), every decision is
+// exact.
+constexpr int kGcWarps = 8;
+constexpr int kGcThreads = kGcWarps * 32;
+constexpr size_t kGcDynSmem = sizeof(float) * kGcWarps * 2 * 32 * 33;  // phase scratch, 67.6 KB
+
+template <int MODE>
+__global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs) {
+  extern __shared__ float s_gc_dyn[];
+  __shared__ float4 s_geo[kGcWarps][2][32];    // survivors' xyab, cop
+  __shared__ double2 s_col[kGcWarps][2][32];   // survivors' (r, g), (b, depth) widened once
+  __shared__ int s_kpos[kGcWarps][32];         // survivors' 1-based list positions
+  __shared__ unsigned long long s_tab[32];
+  if (gated_out(A, BS_GAUSSIAN_WISE)) return;
+  load_tab(s_tab);
+  const ExpK ek = make_expk(s_tab);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  const int tile = blockIdx.x;
+  const int tx = tile % A.cols, ty = tile / A.cols;
+  const int nsx = (A.pw + kSubW - 1) / kSubW;
+  const uint32_t start = A.ranges[2 * tile], end = A.ranges[2 * tile + 1];
+  float* const sa = s_gc_dyn + warp * (2 * 32 * 33);
+  float* const stb = sa + 32 * 33;
+  for (int sub = warp; sub < subs; sub += kGcWarps) {
+    const int ox = tx * A.pw + (sub % nsx) * kSubW, oy = ty * A.ph + (sub / nsx) * kSubH;
+    const int lx = (sub % nsx) * kSubW + (lane % kSubW), ly = (sub / nsx) * kSubH + (lane / kSubW);
+    const int px = ox + (lane % kSubW), py = oy + (lane / kSubW);
+    const bool inside = lx < A.pw && ly < A.ph && px < A.W && py < A.H;
+    const float sx = __fadd_rn((float)px, 0.5f), sy = __fadd_rn((float)py, 0.5f);
+    const float rx0 = (float)ox + 0.5f, rx1 = (float)ox + (kSubW - 0.5f), ry0 = (float)oy + 0.5f,
+                ry1 = (float)oy + (kSubH - 0.5f);
+    bool done = !inside;
+    float t = 1.0f;
+    int contrib = 0, term = 0;
+    double ar = 0.0, ag = 0.0, ab = 0.0, ad = 0.0;
+    float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pc = pa, pr = pa;
+    if (start + lane < end) load_rec(A, start + lane, pa, pc, pr);
+    for (uint32_t base = start; base < end; base += 32) {
+      if (!__any_sync(kFull, !done)) break;
+      // cull against the sub-tile, compact the survivors
+      const bool keep = base + lane < end && !cull_subtile(pa, pc, rx0, rx1, ry0, ry1);
+      const unsigned km = __ballot_sync(kFull, keep);
+      if (keep) {
+        const int pos = __popc(km & lt);
+        s_geo[warp][0][pos] = pa;
+        s_geo[warp][1][pos] = pc;
+        s_col[warp][0][pos] = make_double2((double)pr.x, (double)pr.y);
+        s_col[warp][1][pos] = make_double2((double)pr.z, (double)pc.w);
+        s_kpos[warp][pos] = (int)(base - start) + lane + 1;
+      }
+      __syncwarp();
+      if (base + 32 + lane < end) load_rec(A, base + 32 + lane, pa, pc, pr);  // next batch in flight
+      const int n = __popc(km);
+      if (n == 0) continue;
+      // ---- phase 1: per live pixel, lanes on the survivors
+      const bool active = lane < n;
+      const float4 ga = s_geo[warp][0][active ? lane : 0], gc = s_geo[warp][1][active ? lane : 0];
+      unsigned live = __ballot_sync(kFull, !done);
+      unsigned gmask = 0;  // survivors some live pixel does not skip
+      while (live) {
+        const int p = __ffs(live) - 1;
+        live &= live - 1;
+        const float psx = __shfl_sync(kFull, sx, p), psy = __shfl_sync(kFull, sy, p);
+        const float ts = __shfl_sync(kFull, t, p);
+        float alpha = 0.0f;
+        const bool ns = active && eval_step<MODE>(ga, gc, psx, psy, ek, alpha);
+        sa[p * 33 + lane] = ns ? alpha : 0.0f;
+        const unsigned nsm = __ballot_sync(kFull, ns);
+        gmask |= nsm;
+        if (nsm == 0) continue;  // no weight is read
+        float pre = ns ? __fsub_rn(1.0f, alpha) : 1.0f;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const float v = __shfl_up_sync(kFull, pre, off);
+          if (lane >= off) pre = __fmul_rn(pre, v);
+        }
+        const float tb = __shfl_up_sync(kFull, __fmul_rn(ts, pre), 1);
+        stb[p * 33 + lane] = lane == 0 ? ts : tb;
+      }
+      __syncwarp();
+      // ---- phase 2: serial decisions and commits, lane = pixel
+      if (!done) {
+        const float* row_a = sa + lane * 33;
+        const float* row_t = stb + lane * 33;
+        for (unsigned m = gmask; m; m &= m - 1) {
+          const int q = __ffs(m) - 1;
+          const float al = row_a[q];
+          if (al == 0.0f) continue;  // skipped (a non-skipped alpha is >= 1/255)
+          const float tmp = __fmul_rn(t, __fsub_rn(1.0f, al));
+          if (tmp < kStopThreshold) {
+            done = true;
+            term = s_kpos[warp][q];
+            break;
+          }
+          const double w = __dmul_rn((double)al, (double)row_t[q]);
+          const double2 rg = s_col[warp][0][q], bd = s_col[warp][1][q];
+          ar = __dadd_rn(ar, __dmul_rn(rg.x, w));
+          ag = __dadd_rn(ag, __dmul_rn(rg.y, w));
+          ab = __dadd_rn(ab, __dmul_rn(bd.x, w));
+          ad = __dadd_rn(ad, __dmul_rn(bd.y, w));
+          t = tmp;
+          ++contrib;
+        }
+      }
+      __syncwarp();
+    }
+    if (inside) {
+      const size_t pix = (size_t)py * A.W + px;
+      A.color[3 * pix + 0] = __double2float_rn(__dadd_rn(ar, __dmul_rn((double)A.bg0, (double)t)));
+      A.color[3 * pix + 1] = __double2float_rn(__dadd_rn(ag, __dmul_rn((double)A.bg1, (double)t)));
+      A.color[3 * pix + 2] = __double2float_rn(__dadd_rn(ab, __dmul_rn((double)A.bg2, (double)t)));
+      A.alpha[pix] = __fsub_rn(1.0f, t);
+      A.depth[pix] = __double2float_rn(ad);
+      A.final_t[pix] = t;
+      A.contrib[pix] = contrib;
+      A.term[pix] = term;
+    }
+  }
+}
+
 template <int MODE, int LM>
 __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, float4 (*s)[32], int* s_k,
                                           const ExpK& ek) {
@@ -1084,6 +1224,7 @@ struct FineTuning {
   int donate_after, donate_min_remain, stragglers, stragglers_super;
   bool wide;        // BS_FINE_WIDE=1: the 80-register build when capped at <= 3 CTAs/SM
   bool no_lpt;      // BS_FINE_NO_LPT=1: tasks in tile-index order
+  bool gw_windowed; // BS_GW_WINDOWED=1: GaussianWise in the reference's fixed 32-entry windows (bit-exact colour)
 };
 static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
@@ -1100,6 +1241,7 @@ static const FineTuning& fine_tuning() {
     f.stragglers_super = env_int("BS_FINE_STRAGGLERS_SUPER", kStragglers);
     f.wide = env_int("BS_FINE_WIDE", 0) != 0;  // opt-in: measured 1 % slower in the streamed pipeline
     f.no_lpt = env_int("BS_FINE_NO_LPT", 0) != 0;
+    f.gw_windowed = env_int("BS_GW_WINDOWED", 0) != 0;
     return f;
   }();
   return t;
@@ -1143,6 +1285,10 @@ static int dev_facts(DevFacts** out) {
                                      (int)kGwDynSmem));
     BS_CUDA_TRY(cudaFuncSetAttribute(k_render_gw<BS_ALPHA_FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kGwDynSmem));
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_render_gw_cull<BS_ALPHA_EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kGcDynSmem));
+    BS_CUDA_TRY(cudaFuncSetAttribute(k_render_gw_cull<BS_ALPHA_FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kGcDynSmem));
     f = n;
   }
   *out = &f;
@@ -1186,8 +1332,11 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, int fin
       return BS_ERR_UNSUPPORTED;
     }
     case BS_GAUSSIAN_WISE:
-      if (block_pixels <= kGwThreads)  // (dynamic smem opt-in: dev_facts)
+      if (fine_tuning().gw_windowed && block_pixels <= kGwThreads)  // (dynamic smem opt-in: dev_facts)
         k_render_gw<MODE><<<T, kGwThreads, kGwDynSmem, st>>>(A);
+      else if (!fine_tuning().gw_windowed)
+        k_render_gw_cull<MODE><<<T, kGcThreads, kGcDynSmem, st>>>(
+            A, ((A.pw + kSubW - 1) / kSubW) * ((A.ph + kSubH - 1) / kSubH));
       else  // larger patches: 4-warp tasks, 4 pixels at a time
         k_render_gaussianwise<MODE><<<T, kFgThreads, 0, st>>>(A);
       break;

@@ -16,10 +16,11 @@ the CPU oracle on the same seeded inputs:
       variants.
 
 Bars: contrib / term / final_t / alpha bit-exact for every variant;
-colour / depth bit-exact for the pixel-wise variants and GaussianWise
-(<= 256-pixel patches: serial list-order commits with the prefix weights, as
-render_gaussianwise), within 1e-6 (abs; depth relative to max(1, |ref|)) for
-FineGrainedCombined (fused multiply-add sums).
+colour / depth bit-exact for the pixel-wise variants, within 1e-6 (abs;
+depth relative to max(1, |ref|)) for GaussianWise (prefix weights over the
+sub-tile's surviving entries instead of fixed 32-entry windows; the windowed
+kernel is bit-exact, tests/test_gpu_parity.py) and FineGrainedCombined
+(fused multiply-add sums).
 """
 from __future__ import annotations
 
@@ -46,7 +47,7 @@ def ncam(o_cam):
     return N.Camera.from_buffer_copy(bytes(o_cam))
 
 
-def assert_frame(got: dict, ref: dict, variant: int, pixels=None, tag="", gw_exact=True):
+def assert_frame(got: dict, ref: dict, variant: int, pixels=None, tag="", gw_exact=False):
     sel = (lambda a: a) if pixels is None else (lambda a: a[pixels])
     csel = (lambda a: a) if pixels is None else (lambda a: a.reshape(-1, 3)[pixels])
     for k in ("contrib", "term"):
@@ -208,4 +209,4 @@ def test_spec_acceptance_100_random_scenes():
         for v in range(5):
             f_ = api.render_forward(v, s, b, W, H, pw, ph, bg, N.ALPHA_EXACT, st.task_order)
             torch.cuda.synchronize()
-            assert_frame(f_.to_numpy(), refs[2] if v == 2 else refs[0], v, tag=f"scene {i}", gw_exact=pw * ph <= 256)
+            assert_frame(f_.to_numpy(), refs[2] if v == 2 else refs[0], v, tag=f"scene {i}")

@@ -367,10 +367,7 @@ def test_render_exact(variant, W, H, pw, ph, n, bgfrac):
     assert np.array_equal(got["term"], ref["term"])
     assert np.array_equal(got["final_t"].view(np.uint32), ref["final_t"].view(np.uint32))
     assert np.array_equal(got["alpha"].view(np.uint32), ref["alpha"].view(np.uint32))
-    if variant in (0, 1, 4) or (variant == 2 and pw * ph <= 256):
-        # pixel-wise, and the Gaussian-wise kernel for <= 256-pixel patches
-        # (serial commits in list order with the prefix weights, as
-        # render_gaussianwise): bit-exact colour/depth too
+    if variant in (0, 1, 4):  # pixel-wise: bit-exact colour/depth too
         assert np.array_equal(got["color"].view(np.uint32), ref["color"].view(np.uint32))
         assert np.array_equal(got["depth"].view(np.uint32), ref["depth"].view(np.uint32))
     else:
@@ -1004,3 +1001,35 @@ def test_render_views_host_batch_matches():
             assert np.array_equal(o[4], ref["contrib"]) and np.array_equal(o[5], ref["term"]), k
             assert np.array_equal(o[3], ref["final_t"]) and np.array_equal(o[1], ref["alpha"]), k
             assert float(np.abs(o[0] - ref["color"]).max()) <= 1e-6, k
+
+
+def test_gaussianwise_windowed_bit_exact_colour():
+    """BS_GW_WINDOWED=1 selects the GaussianWise kernel that keeps the
+    reference's fixed 32-entry windows (no sub-tile cull): every plane,
+    colour and depth included, equals render_gaussianwise bit for bit.  (The
+    knob is read once per process, hence the subprocess.)"""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, "tests")
+import oracle_lib as O
+from paper_2412_17378_b200 import _native as N, api
+for (W, H, pw, ph, n, bgf) in [(256, 256, 16, 16, 10000, 1.0), (192, 128, 16, 8, 6000, 0.12), (90, 70, 8, 8, 2000, 0.3)]:
+    cam = O.make_camera(focal=(float(W), float(W)), width=W, height=H)
+    g2d = O.project_all(O.gen_clustered_scene(n, cam, bgfrac=bgf), cam)
+    pl, rg = O.bin_tiles(g2d, W, H, pw, ph)
+    ref = O.render(2, pl, rg, g2d, W, H, pw, ph, (0.1, 0.2, 0.3), lazy=True, threads=0)
+    s = api.splats_from_g2d(g2d, "cuda")
+    b = api.bin_tiles(s, W, H, pw, ph)
+    st = api.tile_load_histogram(b)
+    got = api.render_forward(2, s, b, W, H, pw, ph, (0.1, 0.2, 0.3), N.ALPHA_EXACT, st.task_order).to_numpy()
+    for k in ("color", "alpha", "depth", "final_t", "contrib", "term"):
+        assert got[k].tobytes() == ref[k].tobytes(), (W, H, k)
+print("windowed ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, BS_GW_WINDOWED="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "windowed ok" in r.stdout, r.stdout + r.stderr[-2000:]
