@@ -103,6 +103,10 @@ __device__ __forceinline__ ExpK make_expk(const unsigned long long* s_tab) {
 }
 
 // glibc_expf_inrange with constant-bank operands (same operations, same bits).
+// SPECIAL = false drops glibc's one special-cased input; callers use it only
+// for x > kExpSpecialCut (x = -0x1.f8cbb2p+5 ~ -63.09 cannot occur).
+constexpr float kExpSpecialCut = -63.0f;
+template <bool SPECIAL = true>
 __device__ __forceinline__ float glibc_expf_fast(float x, const ExpK& k) {
   const double kShift = 0x1.8p+52;
   const double z = __dmul_rn(c_expf_k[0], (double)x);
@@ -118,6 +122,7 @@ __device__ __forceinline__ float glibc_expf_fast(float x, const ExpK& k) {
   y = __fma_rn(zz, r2, y);
   y = __dmul_rn(y, s);
   const float out = __double2float_rn(y);
+  if (!SPECIAL) return out;
   return __float_as_uint(x) == 0xC27C65D9u ? __uint_as_float(0x11FA2993u) : out;
 }
 
