@@ -633,6 +633,31 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     res["frame_work"] = {"evaluated_pairs_E": E, "committed_pairs_C": Cc, "tile_instances_K": K, "pixels": P,
                          "tile_stats": summ, "variant": api.variant_name(vsel)}
     res["render_ms_by_variant"] = per_variant
+    # SURVEY 8f(4) backward render (the training step's next kernel): per-splat
+    # gradients of this frame (exact mode, FineGrainedCombined schedule) for a
+    # synthetic dL/d(colour, alpha, depth); kernel time, warm, grads zeroed
+    # outside the events
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(0)
+    dl = [torch.randn(k * P_, device=dev, generator=gen) for k, P_ in ((3, W * H), (1, W * H), (1, W * H))]
+    api.render_forward(3, s, b, W, H, pw, ph, (0, 0, 0), N.ALPHA_EXACT, st.task_order, frame, pipe.render_ws)
+    grads = api.SplatGrads.zeros(s.n_cap, dev)
+    bt = []
+    for _ in range(6):
+        for t_ in (grads.xyab, grads.cop, grads.rgbr):
+            t_.zero_()
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        api.render_backward(s, b, frame, W, H, pw, ph, dl[0], dl[1], dl[2], (0, 0, 0), N.ALPHA_EXACT, st.task_order,
+                            grads, pipe.render_ws)
+        e.record(stream)
+        torch.cuda.synchronize()
+        bt.append(a.elapsed_time(e))
+    res["bwd_render_ms_per_frame"] = round(float(np.median(bt[1:])), 4)
+    res["bwd_def"] = ("bs_render_backward on the C2 identity view's 16x16 lists: dL/d(x, y, conic, opacity, rgb, "
+                      "depth) per splat for random dL/d(colour, alpha, depth); the forward's decisions replayed "
+                      "(exact alpha), 10 gradient terms per committed pair warp-reduced, float atomics")
+    del grads, dl
     naive = per_variant[mname]["Naive"]
     res["speedup_vs_naive"] = {k: round(naive / v, 3) for k, v in per_variant[mname].items()}
     # list entries any pixel of a tile still reads under the serial semantics:

@@ -117,6 +117,23 @@ typedef struct bs_frame_out {
   int32_t* term;    /* i32[P] 1-based termination index, 0 = none */
 } bs_frame_out;
 
+/* Backward render inputs: dL/d(outputs) of one frame (device pointers). */
+typedef struct bs_frame_grad_in {
+  const float* dl_dcolor; /* f32[3P] */
+  const float* dl_dalpha; /* f32[P] or NULL (zero) */
+  const float* dl_ddepth; /* f32[P] or NULL (zero) */
+} bs_frame_grad_in;
+
+/* Per-splat gradients, the bs_splats layout (f32x4 per splat), accumulated:
+ *   xyab: d/dx, d/dy, d/dconic_a, d/dconic_b
+ *   cop:  d/dconic_c, d/dopacity, 0, d/ddepth
+ *   rgbr: d/dr, d/dg, d/db, 0 */
+typedef struct bs_splat_grads {
+  float* xyab;
+  float* cop;
+  float* rgbr;
+} bs_splat_grads;
+
 /* TileHistogram summary — include/splatsim/preprocess.hpp:38-45. */
 typedef struct bs_tile_histogram {
   uint32_t min;
@@ -414,6 +431,20 @@ int bs_render_forward_super(int variant, const int32_t* variant_dev, int alpha_m
                             bs_frame_out out, void* ws, size_t ws_bytes, void* stream);
 int bs_super_tile_ranges(const uint32_t* super_ranges, int32_t width, int32_t height, int32_t pw, int32_t ph,
                          uint32_t* tile_ranges, void* stream);
+/* Backward render (the reference has no backward pass): the
+ * per-splat gradients of a frame's colour / alpha / depth under
+ * render_reference semantics (src/blend.cpp:8-42), the forward's skip /
+ * stop decisions held fixed; no gradient through a clamped alpha (0.99).
+ * fwd: the forward's outputs for the same inputs (colour, depth, final_t
+ * read).  gout accumulates (caller zeroes).  super_lists = 1: the frame
+ * pipeline's super-tile lists (as bs_render_forward_super).  ws: a render
+ * workspace (>= 256 bytes; its queue counters).  Checked against the CPU
+ * oracle's analytic gradient, which finite differences of the reference
+ * forward pin (tests/test_backward_oracle.py). */
+int bs_render_backward(int alpha_mode, bs_splats g, const uint32_t* point_list, const uint32_t* tile_ranges,
+                       const uint32_t* task_order, int32_t width, int32_t height, int32_t pw, int32_t ph,
+                       const float bg[3], bs_frame_out fwd, bs_frame_grad_in gin, bs_splat_grads gout,
+                       int super_lists, void* ws, size_t ws_bytes, void* stream);
 /* 1 if the context's last frame was binned into super-tile lists (frames
  * >= 1 Mpixel with power-of-two patches and a FineGrainedCombined /
  * SharedMemOpt / device-selected variant; BS_NO_SUPER=1 disables), else 0. */

@@ -391,6 +391,81 @@ RenderOutput render(Variant v, const TileBinning& b, const Gaussian2D* gs, size_
 }
 
 // ---------------------------------------------------------------------------
+// Backward render.  Per pixel, the forward of blend_pixel
+// (src/blend.cpp:16-42) is replayed to find the committed entries k with
+// their alpha_k, transmittance T_k and weight w_k = alpha_k T_k; then, with
+// colour = sum_k c_k w_k + bg t_final, depth = sum_k d_k w_k, out_alpha =
+// 1 - t_final:
+//   d colour / d alpha_k = c_k T_k - S_k / (1 - alpha_k),
+//     S_k = sum_{j>k} c_j w_j + bg t_final          (same for depth, no bg)
+//   d out_alpha / d alpha_k = t_final / (1 - alpha_k)
+//   alpha = min(0.99, o G), G = exp(power): zero gradient when clamped;
+//   power = -0.5 (a dx^2 + c dy^2) - b dx dy, dx = px + 0.5 - x.
+void render_backward(const TileBinning& b, const Gaussian2D* gs, size_t n, int width, int height, int pw, int ph,
+                     const float bg[3], const float* dl_dcolor, const float* dl_dalpha, const float* dl_ddepth,
+                     SplatGrad* out) {
+  (void)n;
+  const int cols = (width + pw - 1) / pw, rows = (height + ph - 1) / ph;
+  if (cols != b.tile_cols || rows != b.tile_rows)
+    throw std::invalid_argument("render_backward: binning grid does not match image dims");
+  struct Commit { uint32_t id; double alpha, T, G, a0, dx, dy; };
+  std::vector<Commit> cm;
+  for (int t = 0; t < b.tile_count(); ++t) {
+    const uint32_t start = b.tile_ranges[2 * size_t(t)], end = b.tile_ranges[2 * size_t(t) + 1];
+    const int tx = t % cols, ty = t / cols;
+    const int x0 = tx * pw, y0 = ty * ph, x1 = std::min(width, x0 + pw), y1 = std::min(height, y0 + ph);
+    for (int py = y0; py < y1; ++py)
+      for (int px = x0; px < x1; ++px) {
+        const float sx = float(px) + 0.5f, sy = float(py) + 0.5f;
+        cm.clear();
+        float tt = 1.0f;
+        double C[3] = {0, 0, 0}, D = 0;
+        for (uint32_t k = start; k < end; ++k) {
+          const Gaussian2D& g = gs[b.point_list[k]];
+          const AlphaEval e = eval_alpha(g, sx, sy);
+          const float alpha = e.power > 0.0f ? 0.0f : e.alpha;
+          if (alpha < kAlphaSkip) continue;
+          const float tmp = tt * (1.0f - alpha);
+          if (tmp < kStopThreshold) break;
+          const double w = double(alpha) * double(tt);
+          for (int c = 0; c < 3; ++c) C[c] += g.color[c] * w;
+          D += g.depth * w;
+          const double G = std::exp(double(e.power));
+          cm.push_back({b.point_list[k], double(alpha), double(tt), G, double(g.opacity) * G,
+                        double(sx) - double(g.x), double(sy) - double(g.y)});
+          tt = tmp;
+        }
+        const size_t p = size_t(py) * size_t(width) + size_t(px);
+        const double tf = tt;
+        double S[3], SD = D;
+        for (int c = 0; c < 3; ++c) S[c] = C[c] + double(bg[c]) * tf;
+        const double gC[3] = {dl_dcolor[3 * p], dl_dcolor[3 * p + 1], dl_dcolor[3 * p + 2]};
+        const double gA = dl_dalpha[p], gD = dl_ddepth[p];
+        for (const Commit& q : cm) {
+          const Gaussian2D& g = gs[q.id];
+          SplatGrad& o = out[q.id];
+          const double w = q.alpha * q.T;
+          for (int c = 0; c < 3; ++c) S[c] -= g.color[c] * w;
+          SD -= g.depth * w;
+          const double inv = 1.0 / (1.0 - q.alpha);
+          double dla = gA * tf * inv + gD * (g.depth * q.T - SD * inv);
+          for (int c = 0; c < 3; ++c) dla += gC[c] * (g.color[c] * q.T - S[c] * inv);
+          for (int c = 0; c < 3; ++c) o.color[c] += gC[c] * w;
+          o.depth += gD * w;
+          if (q.a0 > double(kAlphaClamp)) continue;  // alpha clamped at 0.99
+          o.opacity += dla * q.G;
+          const double dlp = dla * double(g.opacity) * q.G;
+          o.conic[0] += dlp * (-0.5 * q.dx * q.dx);
+          o.conic[1] += dlp * (-q.dx * q.dy);
+          o.conic[2] += dlp * (-0.5 * q.dy * q.dy);
+          o.xy[0] += dlp * (double(g.conic_a) * q.dx + double(g.conic_b) * q.dy);
+          o.xy[1] += dlp * (double(g.conic_c) * q.dy + double(g.conic_b) * q.dx);
+        }
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // R10 — src/kernels.cpp:27-38
 int64_t warp_steps_pixelwise(const std::vector<int64_t>& term_or_zero, int64_t list_len) {
   int64_t steps = 0;

@@ -132,6 +132,22 @@ struct RenderOutput {
   void init(int w, int h);
 };
 
+// ---- Backward render (not in the reference: the analytic
+// gradient of render_reference's serial semantics, src/blend.cpp:8-42, with
+// the forward's skip / stop decisions held fixed).  Per splat, accumulated
+// over every pixel: d/d(x, y, conic_a, conic_b, conic_c, opacity, r, g, b,
+// depth).  Double precision; pinned by finite differences of render().
+struct SplatGrad {
+  double xy[2] = {0, 0};
+  double conic[3] = {0, 0, 0};
+  double opacity = 0;
+  double color[3] = {0, 0, 0};
+  double depth = 0;
+};
+void render_backward(const TileBinning& b, const Gaussian2D* gs, size_t n, int width, int height, int pw, int ph,
+                     const float bg[3], const float* dl_dcolor, const float* dl_dalpha, const float* dl_ddepth,
+                     SplatGrad* out);
+
 enum class Variant : int { Naive = 0, DynamicBlocks = 1, GaussianWise = 2, FineGrainedCombined = 3, SharedMemOpt = 4 };
 std::string_view variant_name(Variant v);
 std::optional<Variant> variant_from_name(std::string_view s);

@@ -305,4 +305,29 @@ int64_t orc_expf_compare_batch(const float* x, const float* y, int64_t n) {
   return bad;
 }
 
+// Backward render: grads = n x 10 doubles (x, y, conic a, b, c, opacity, r,
+// g, b, depth), accumulated (caller zeroes).  0 = ok, -1 = grid mismatch.
+int orc_render_backward(const uint32_t* ranges, const uint32_t* point_list, int64_t k, const Gaussian2D* g, int64_t n,
+                        int W, int H, int pw, int ph, const float bg[3], const float* dl_dcolor, const float* dl_dalpha,
+                        const float* dl_ddepth, double* grads) {
+  TileBinning b;
+  b.tile_cols = (W + pw - 1) / pw;
+  b.tile_rows = (H + ph - 1) / ph;
+  b.point_list.assign(point_list, point_list + k);
+  b.tile_ranges.assign(ranges, ranges + 2 * size_t(b.tile_count()));
+  std::vector<SplatGrad> out(static_cast<size_t>(n));
+  try {
+    render_backward(b, g, size_t(n), W, H, pw, ph, bg, dl_dcolor, dl_dalpha, dl_ddepth, out.data());
+  } catch (...) {
+    return -1;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    const SplatGrad& o = out[size_t(i)];
+    const double v[10] = {o.xy[0], o.xy[1], o.conic[0], o.conic[1], o.conic[2], o.opacity,
+                          o.color[0], o.color[1], o.color[2], o.depth};
+    for (int j = 0; j < 10; ++j) grads[10 * i + j] += v[j];
+  }
+  return 0;
+}
+
 }  // extern "C"

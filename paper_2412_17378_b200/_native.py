@@ -30,6 +30,14 @@ class FrameOut(C.Structure):
                 ("contrib", C.c_void_p), ("term", C.c_void_p)]
 
 
+class FrameGradIn(C.Structure):
+    _fields_ = [("dl_dcolor", C.c_void_p), ("dl_dalpha", C.c_void_p), ("dl_ddepth", C.c_void_p)]
+
+
+class SplatGrads(C.Structure):
+    _fields_ = [("xyab", C.c_void_p), ("cop", C.c_void_p), ("rgbr", C.c_void_p)]
+
+
 class TileHistogram(C.Structure):
     _fields_ = [("min", C.c_uint32), ("max", C.c_uint32), ("p50", C.c_uint32), ("p99", C.c_uint32),
                 ("mean", C.c_double), ("total", C.c_uint64), ("tiles", C.c_int32), ("nonempty", C.c_int32)]
@@ -104,6 +112,8 @@ SIGNATURES = {
     "bs_super_aux_bytes": (_sz, [_i32, _i32, _i32, _i32]),
     "bs_preprocess_bin_count_super": (C.c_int, [_vp, _i64, C.POINTER(Camera), _vp, Splats, _vp, _i32, _i32, _i32,
                                                 _i32, _vp, _vp, _sz, _vp, _vp, _sz, _vp]),
+    "bs_render_backward": (C.c_int, [C.c_int, Splats, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _f32p, FrameOut,
+                                     FrameGradIn, SplatGrads, C.c_int, _vp, _sz, _vp]),
     "bs_render_forward_super": (C.c_int, [C.c_int, _vp, C.c_int, Splats, _vp, _vp, _vp, _i32, _i32, _i32, _i32,
                                           _f32p, FrameOut, _vp, _sz, _vp]),
     "bs_super_tile_ranges": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),

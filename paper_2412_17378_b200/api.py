@@ -273,6 +273,56 @@ def render_forward(variant: int, s: DeviceSplats, b: DeviceBinning, width: int, 
     return out
 
 
+GRAD_FIELDS = ("x", "y", "conic_a", "conic_b", "conic_c", "opacity", "r", "g", "b", "depth")
+
+
+@dataclass
+class SplatGrads:
+    """Per-splat gradients in the DeviceSplats layout (bs_splat_grads)."""
+    xyab: torch.Tensor  # [n, 4]: d/dx, d/dy, d/dconic_a, d/dconic_b
+    cop: torch.Tensor   # [n, 4]: d/dconic_c, d/dopacity, 0, d/ddepth
+    rgbr: torch.Tensor  # [n, 4]: d/dr, d/dg, d/db, 0
+
+    @staticmethod
+    def zeros(n: int, device) -> "SplatGrads":
+        f = lambda: torch.zeros((max(int(n), 1), 4), dtype=torch.float32, device=device)  # noqa: E731
+        return SplatGrads(f(), f(), f())
+
+    def c(self) -> N.SplatGrads:
+        return N.SplatGrads(_ptr(self.xyab), _ptr(self.cop), _ptr(self.rgbr))
+
+    def as_fields(self) -> torch.Tensor:
+        """[n, 10] in GRAD_FIELDS order (the oracle's layout)."""
+        x, c, r = self.xyab, self.cop, self.rgbr
+        return torch.stack([x[:, 0], x[:, 1], x[:, 2], x[:, 3], c[:, 0], c[:, 1], r[:, 0], r[:, 1], r[:, 2],
+                            c[:, 3]], dim=1)
+
+
+def render_backward(s: DeviceSplats, b: DeviceBinning, fwd: DeviceFrame, width: int, height: int, pw: int, ph: int,
+                    dl_dcolor: torch.Tensor, dl_dalpha: torch.Tensor | None = None,
+                    dl_ddepth: torch.Tensor | None = None, bg=(0.0, 0.0, 0.0), alpha_mode: int = ALPHA_EXACT,
+                    task_order: torch.Tensor | None = None, grads: SplatGrads | None = None,
+                    ws: torch.Tensor | None = None, super_lists: bool = False) -> SplatGrads:
+    """Backward render: per-splat gradients of the frame
+    ``fwd`` (the forward's outputs on the same splats and binning) for the
+    given dL/d(colour, alpha, depth); accumulated into ``grads``."""
+    dev = s.xyab.device
+    if b.tile_cols != (width + pw - 1) // pw or b.tile_rows != (height + ph - 1) // ph:
+        raise ValueError("render_backward: binning grid does not match image dims")
+    grads = grads or SplatGrads.zeros(s.n_cap, dev)
+    if ws is None:
+        ws = _ws(256, dev)
+    bgc = (C.c_float * 3)(*[float(x) for x in bg])
+    dc = dl_dcolor.contiguous()
+    da = None if dl_dalpha is None else dl_dalpha.contiguous()
+    dd = None if dl_ddepth is None else dl_ddepth.contiguous()
+    gin = N.FrameGradIn(_ptr(dc), _ptr(da), _ptr(dd))
+    N.call("bs_render_backward", int(alpha_mode), s.c(), _ptr(b.point_list) if b.k else None, _ptr(b.tile_ranges),
+           _ptr(task_order), width, height, pw, ph, bgc, fwd.c(), gin, grads.c(), int(super_lists), _ptr(ws),
+           ws.numel(), _stream(dev))
+    return grads
+
+
 def frame_work(f: DeviceFrame, b: DeviceBinning, pw: int, ph: int) -> tuple[int, int]:
     """(evaluated, committed) pair counts: E = sum consumed, C = sum contrib."""
     dev = f.color.device

@@ -1221,6 +1221,213 @@ __global__ void __launch_bounds__(kFineThreads) k_render_donated(RArgs A) {
 }
 
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Backward render (not in the reference): per-splat gradients
+// of the forward's colour / alpha / depth under render_reference semantics
+// (src/blend.cpp:8-42), the forward's skip / stop decisions held fixed —
+// the math of oracle/oracle.cpp render_backward:
+//   d colour / d alpha_k = c_k T_k - S_k / (1 - alpha_k),  S_k = colour -
+//     sum_{j<=k} c_j w_j (= later commits + background);  depth alike;
+//   d out_alpha / d alpha_k = t_final / (1 - alpha_k);
+//   alpha = min(0.99, o G): no gradient through a clamped alpha; G = exp(power).
+// Same schedule as FineGrainedCombined (persistent warps, 8x4-pixel
+// sub-tiles from the LPT queue, the sub-tile cull, pixel-wise serial steps
+// with the forward's exact decisions); per committed step the 10 gradient
+// terms are summed over the warp's 32 pixels by a transposing butterfly (16
+// shuffles: lane pair 2i ends holding term i) and added to the splat's
+// gradient with one red.global.add per term.
+struct BwdArgs {
+  const float* dcolor;  // f32[3P]
+  const float* dalpha;  // f32[P] or null
+  const float* ddepth;  // f32[P] or null
+  float* gxyab;         // f32x4[n] (d/dx, d/dy, d/dconic_a, d/dconic_b)
+  float* gcop;          // f32x4[n] (d/dconic_c, d/dopacity, 0, d/ddepth)
+  float* grgbr;         // f32x4[n] (d/dr, d/dg, d/db, 0)
+};
+
+// gradient term i (oracle GRAD_FIELDS order: x, y, conic a, b, c, opacity,
+// r, g, b, depth) -> its (array + component); the splat adds 4 * id
+__device__ __forceinline__ float* bwd_target(const BwdArgs& G, int i) {
+  float* base = i < 4 ? G.gxyab : (i == 4 || i == 5 || i == 9) ? G.gcop : G.grgbr;
+  const int comp = i < 4 ? i : i == 4 ? 0 : i == 5 ? 1 : i == 9 ? 3 : i - 6;
+  return base + comp;
+}
+
+template <int MODE, int LM>
+__device__ __forceinline__ void warp_task_bwd(const RArgs& A, const BwdArgs& G, int tile, int sub, float4 (*s)[32],
+                                              uint32_t* s_id, const ExpK& ek) {
+  const int lane = threadIdx.x & 31;
+  const int tx = tile % A.cols, ty = tile / A.cols;
+  const int nsx = (A.pw + kSubW - 1) / kSubW;
+  const int ox = tx * A.pw + (sub % nsx) * kSubW, oy = ty * A.ph + (sub / nsx) * kSubH;
+  const int lx = (sub % nsx) * kSubW + (lane % kSubW), ly = (sub / nsx) * kSubH + (lane / kSubW);
+  const int px = ox + (lane % kSubW), py = oy + (lane / kSubW);
+  const bool inside = lx < A.pw && ly < A.ph && px < A.W && py < A.H;
+  const float sx = __fadd_rn((float)px, 0.5f), sy = __fadd_rn((float)py, 0.5f);
+  const float rx0 = (float)ox + 0.5f, rx1 = (float)ox + (kSubW - 0.5f), ry0 = (float)oy + 0.5f,
+              ry1 = (float)oy + (kSubH - 0.5f);
+  const uint32_t start = A.ranges[2 * tile], end = A.ranges[2 * tile + 1];
+  float gr = 0.f, gg = 0.f, gb = 0.f, ga = 0.f, gd = 0.f, Sr = 0.f, Sg = 0.f, Sb = 0.f, SD = 0.f, tf = 1.f;
+  bool done = !inside;
+  if (inside) {
+    const size_t p = (size_t)py * A.W + px;
+    gr = G.dcolor[3 * p];
+    gg = G.dcolor[3 * p + 1];
+    gb = G.dcolor[3 * p + 2];
+    ga = G.dalpha ? G.dalpha[p] : 0.f;
+    gd = G.ddepth ? G.ddepth[p] : 0.f;
+    Sr = A.color[3 * p];  // the forward's outputs (colour includes bg * t_final)
+    Sg = A.color[3 * p + 1];
+    Sb = A.color[3 * p + 2];
+    SD = A.depth[p];
+    tf = A.final_t[p];
+  }
+  float t = 1.0f;
+  const int slot = (lane >> 1) & 15;  // the gradient term this lane pair ends holding
+  float* const tgt = bwd_target(G, slot < 10 ? slot : 0);
+  const bool adder = !(lane & 1) && slot < 10;
+  uint32_t base = start;
+  float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pc = pa, pr = pa;
+  uint32_t pid = 0;
+  if (base + lane < end) {
+    pid = __ldg(A.point_list + base + lane);
+    pa = __ldg(A.xyab + pid);
+    pc = __ldg(A.cop + pid);
+    pr = __ldg(A.rgbr + pid);
+  }
+  while (base < end) {
+    if (!__any_sync(kFull, !done)) break;
+    const bool member = base + lane < end && is_member<LM>(A, pa, pr, tx, ty);
+    const bool keep = member && !cull_subtile(pa, pc, rx0, rx1, ry0, ry1);
+    const unsigned km = __ballot_sync(kFull, keep);
+    const bool special = __any_sync(kFull, keep && pc.z < kExpSpecialCut);
+    if (keep) {
+      const int pos = __popc(km & lanemask_lt());
+      s[0][pos] = pa;
+      s[1][pos] = pc;
+      s[2][pos] = pr;
+      s_id[pos] = pid;
+    }
+    __syncwarp();
+    const uint32_t nb = base + 32;
+    if (nb + lane < end) {
+      pid = __ldg(A.point_list + nb + lane);
+      pa = __ldg(A.xyab + pid);
+      pc = __ldg(A.cop + pid);
+      pr = __ldg(A.rgbr + pid);
+    }
+    const int cnt = __popc(km);
+    for (int j = 0; j < cnt; ++j) {
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      bool com = false;
+      if (!done) {
+        const float4 a = s[0][j], c = s[1][j];
+        const float dx = __fsub_rn(sx, a.x), dy = __fsub_rn(sy, a.y);
+        const float q = __fadd_rn(__fmul_rn(__fmul_rn(a.z, dx), dx), __fmul_rn(__fmul_rn(c.x, dy), dy));
+        const float power = __fsub_rn(__fmul_rn(-0.5f, q), __fmul_rn(__fmul_rn(a.w, dx), dy));
+        if (!(power < c.z) && !(power > 0.0f)) {
+          float e;
+          if (MODE == BS_ALPHA_EXACT) {
+            // power >= power_cut: glibc's special-cased input only in batches
+            // holding a power_cut below kExpSpecialCut (warp-uniform branch)
+            if (special) e = glibc_expf_fast<true>(power, ek);
+            else e = glibc_expf_fast<false>(power, ek);
+          } else {
+            const float p2 = power * 1.4426950408889634f;
+            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(p2));
+          }
+          const float a0 = __fmul_rn(c.y, e);
+          const float alpha = a0 < kAlphaClamp ? a0 : kAlphaClamp;
+          if (!(alpha < kAlphaSkip)) {
+            const float om = __fsub_rn(1.0f, alpha);
+            const float tmp = __fmul_rn(t, om);
+            if (tmp < kStopThreshold) {
+              done = true;
+            } else {
+              const float4 r = s[2][j];
+              const float w = alpha * t;
+              Sr -= r.x * w;
+              Sg -= r.y * w;
+              Sb -= r.z * w;
+              SD -= c.w * w;
+              const float inv = approx_rcp(om);  // om >= 0.01
+              const float dla = gr * (r.x * t - Sr * inv) + gg * (r.y * t - Sg * inv) + gb * (r.z * t - Sb * inv) +
+                                gd * (c.w * t - SD * inv) + ga * tf * inv;
+              v[6] = gr * w;
+              v[7] = gg * w;
+              v[8] = gb * w;
+              v[9] = gd * w;
+              if (!(a0 > kAlphaClamp)) {
+                const float dlp = dla * c.y * e;
+                v[5] = dla * e;
+                v[2] = dlp * (-0.5f * dx * dx);
+                v[3] = dlp * (-dx * dy);
+                v[4] = dlp * (-0.5f * dy * dy);
+                v[0] = dlp * (a.z * dx + a.w * dy);
+                v[1] = dlp * (c.x * dy + a.w * dx);
+              }
+              t = tmp;
+              com = true;
+            }
+          }
+        }
+      }
+      if (!__any_sync(kFull, com)) continue;
+      // transposing butterfly: after the offset-16 .. offset-2 levels lane l
+      // holds a partial of term (l >> 1) & 15; offset 1 completes it
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const bool hi = lane & 16;
+        const float send = hi ? v[i] : v[i + 8];
+        v[i] = (hi ? v[i + 8] : v[i]) + __shfl_xor_sync(kFull, send, 16);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool hi = lane & 8;
+        const float send = hi ? v[i] : v[i + 4];
+        v[i] = (hi ? v[i + 4] : v[i]) + __shfl_xor_sync(kFull, send, 8);
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const bool hi = lane & 4;
+        const float send = hi ? v[i] : v[i + 2];
+        v[i] = (hi ? v[i + 2] : v[i]) + __shfl_xor_sync(kFull, send, 4);
+      }
+      {
+        const bool hi = lane & 2;
+        const float send = hi ? v[0] : v[1];
+        v[0] = (hi ? v[1] : v[0]) + __shfl_xor_sync(kFull, send, 2);
+      }
+      v[0] += __shfl_xor_sync(kFull, v[0], 1);
+      if (adder && v[0] != 0.0f) atomicAdd(tgt + 4 * (size_t)s_id[j], v[0]);
+    }
+    __syncwarp();
+    base = nb;
+  }
+}
+
+template <int MODE, int LM>
+__global__ void __launch_bounds__(kFineThreads) k_render_backward(RArgs A, BwdArgs G, int subs) {
+  __shared__ float4 s_rec[kFineWarps][3][32];
+  __shared__ uint32_t s_id[kFineWarps][32];
+  __shared__ unsigned long long s_tab[32];
+  load_tab(s_tab);
+  const ExpK ek = make_expk(s_tab);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (;;) {
+    int task = 0;
+    if (lane == 0) task = (int)atomicAdd(A.queue, 1u);
+    task = __shfl_sync(kFull, task, 0);
+    if (task >= A.total_tasks) return;
+    const int q = task / subs;
+    const int tile = A.task_order ? (int)A.task_order[q] : q;
+    warp_task_bwd<MODE, LM>(A, G, tile, task - q * subs, s_rec[warp], s_id[warp], ek);
+  }
+}
+
 __global__ void k_frame_work(const int32_t* __restrict__ term, const int32_t* __restrict__ contrib,
                              const uint32_t* __restrict__ ranges, int W, int H, int pw, int ph, int cols,
                              unsigned long long* __restrict__ out) {
@@ -1506,6 +1713,63 @@ extern "C" int bs_render_forward_super(int variant, const int32_t* variant_dev, 
   if (variant < 0 && !variant_dev) return BS_ERR_INVALID_ARGUMENT;
   return render_impl(variant < 0 ? -1 : variant, variant < 0 ? variant_dev : nullptr, alpha_mode, g, point_list,
                      tile_ranges, task_order, width, height, pw, ph, bg, out, ws, ws_bytes, stream, true);
+}
+
+// Backward render.  fwd: the forward's outputs for the same
+// inputs (colour, depth and final_t are read); grads accumulate (caller
+// zeroes).  super_lists: point_list / tile_ranges are the frame pipeline's
+// 2pw x 2ph lists (as bs_render_forward_super).  Workspace: the render
+// workspace (its queue counters).
+extern "C" int bs_render_backward(int alpha_mode, bs_splats g, const uint32_t* point_list, const uint32_t* tile_ranges,
+                                  const uint32_t* task_order, int32_t width, int32_t height, int32_t pw, int32_t ph,
+                                  const float bg[3], bs_frame_out fwd, bs_frame_grad_in gin, bs_splat_grads gout,
+                                  int super_lists, void* ws, size_t ws_bytes, void* stream) {
+  if (width <= 0 || height <= 0 || pw <= 0 || ph <= 0 || !bg || !tile_ranges) return BS_ERR_INVALID_ARGUMENT;
+  if (alpha_mode != BS_ALPHA_EXACT && alpha_mode != BS_ALPHA_FAST) return BS_ERR_INVALID_ARGUMENT;
+  if (!fwd.color || !fwd.depth || !fwd.final_t || !gin.dl_dcolor || !gout.xyab || !gout.cop || !gout.rgbr)
+    return BS_ERR_INVALID_ARGUMENT;
+  if ((int64_t)pw * ph > 1024) return BS_ERR_UNSUPPORTED;
+  if (super_lists && (!pow2(pw) || !pow2(ph))) return BS_ERR_UNSUPPORTED;
+  if (!ws || ws_bytes < 256) return BS_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  RArgs A{};
+  A.xyab = reinterpret_cast<const float4*>(g.xyab);
+  A.cop = reinterpret_cast<const float4*>(g.cop);
+  A.rgbr = reinterpret_cast<const float4*>(g.rgbr);
+  A.point_list = point_list;
+  A.ranges = tile_ranges;
+  A.task_order = task_order;
+  A.W = width; A.H = height; A.pw = pw; A.ph = ph;
+  A.cols = (width + pw - 1) / pw;
+  A.rows = (height + ph - 1) / ph;
+  const int64_t T = (int64_t)A.cols * A.rows;
+  const int subs = ((pw + kSubW - 1) / kSubW) * ((ph + kSubH - 1) / kSubH);
+  if (T * subs > 0x7fffffff) return BS_ERR_UNSUPPORTED;
+  A.T = (int)T;
+  A.bg0 = bg[0]; A.bg1 = bg[1]; A.bg2 = bg[2];
+  A.color = fwd.color; A.depth = fwd.depth; A.final_t = fwd.final_t;
+  A.queue = reinterpret_cast<unsigned int*>(ws);
+  A.total_tasks = (int)(T * subs);
+  A.sup = super_lists ? 1 : 0;
+  A.ipw = 1.0f / (float)pw;
+  A.iph = 1.0f / (float)ph;
+  BwdArgs G{gin.dl_dcolor, gin.dl_dalpha, gin.dl_ddepth, gout.xyab, gout.cop, gout.rgbr};
+  BS_CUDA_TRY(cudaMemsetAsync(ws, 0, 8 * sizeof(unsigned int), st));
+  if (T == 0) return BS_OK;
+  DevFacts* df = nullptr;
+  TRY_BS(dev_facts(&df));
+  const int grid = (int)max((int64_t)1, min((T * subs + kFineWarps - 1) / kFineWarps, (int64_t)df->sms * 4));
+#define BS_BWD(M, L) k_render_backward<M, L><<<grid, kFineThreads, 0, st>>>(A, G, subs)
+  if (alpha_mode == BS_ALPHA_EXACT) {
+    if (super_lists) BS_BWD(BS_ALPHA_EXACT, kListSuper);
+    else BS_BWD(BS_ALPHA_EXACT, kListTile);
+  } else {
+    if (super_lists) BS_BWD(BS_ALPHA_FAST, kListSuper);
+    else BS_BWD(BS_ALPHA_FAST, kListTile);
+  }
+#undef BS_BWD
+  BS_LAUNCH_CHECK();
+  return BS_OK;
 }
 
 namespace bs {

@@ -78,6 +78,8 @@ def lib() -> C.CDLL:
         L.orc_expf_compare_batch.restype = i64
         L.orc_expf_compare_range.argtypes = [C.c_uint32, i64, vp]
         L.orc_expf_compare_range.restype = i64
+        L.orc_render_backward.argtypes = [vp, vp, i64, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp,
+                                          vp]
         _lib = L
     return _lib
 
@@ -154,3 +156,23 @@ def blend_pixel(alphas, colors=None, depths=None, bg=(0, 0, 0), gaussianwise=Fal
 def fnv1a64(arr: np.ndarray, h: int = 0xCBF29CE484222325) -> int:
     b = np.ascontiguousarray(arr)
     return int(lib().orc_fnv1a64(p(b), b.nbytes, h))
+
+
+GRAD_FIELDS = ("x", "y", "conic_a", "conic_b", "conic_c", "opacity", "r", "g", "b", "depth")
+
+
+def render_backward(pl, ranges, g2d, W, H, pw, ph, bg, dl_dcolor, dl_dalpha, dl_ddepth) -> np.ndarray:
+    """Per-splat gradients (n x 10, GRAD_FIELDS order, float64) of render_reference's outputs."""
+    n = len(g2d)
+    out = np.zeros((max(n, 1), 10), np.float64)
+    pl = np.ascontiguousarray(pl, dtype=np.uint32)
+    if len(pl) == 0:
+        pl = np.zeros(1, np.uint32)
+    bgc = np.asarray(bg, dtype=np.float32)
+    dc = np.ascontiguousarray(dl_dcolor, dtype=np.float32)
+    da = np.ascontiguousarray(dl_dalpha, dtype=np.float32)
+    dd = np.ascontiguousarray(dl_ddepth, dtype=np.float32)
+    rc = lib().orc_render_backward(p(np.ascontiguousarray(ranges, dtype=np.uint32)), p(pl), len(pl),
+                                   p(g2d) if n else None, n, W, H, pw, ph, p(bgc), p(dc), p(da), p(dd), p(out))
+    assert rc == 0, rc
+    return out[:n]

@@ -1,0 +1,117 @@
+"""SURVEY 8f(4) backward render on the GPU (bs_render_backward, through the
+C-ABI) against the CPU oracle's analytic gradient (oracle/oracle.cpp
+render_backward, itself pinned by finite differences of the reference
+forward in tests/test_backward_oracle.py).
+
+Bar: per gradient field, max |gpu - oracle| <= 2e-4 * max(1, max |oracle|)
+(float32 accumulation and float atomics on the GPU vs double in the
+oracle; the forward's exact skip / stop decisions are reproduced, so no
+pixel changes its committed set)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from paper_2412_17378_b200 import _native as N  # noqa: E402
+from paper_2412_17378_b200 import api  # noqa: E402
+
+DEV = "cuda"
+TOL = 2e-4
+
+
+def _case(W, H, pw, ph, n, bgfrac, seed, f=None):
+    cam = O.make_camera(focal=(f or float(W), f or float(W)), width=W, height=H)
+    g3d = O.gen_clustered_scene(n, cam, seed=seed, sigma=0.035, bgfrac=bgfrac)
+    g2d = O.project_all(g3d, cam)
+    pl, rg = O.bin_tiles(g2d, W, H, pw, ph)
+    rng = np.random.default_rng(seed)
+    P = W * H
+    dc = rng.normal(size=3 * P).astype(np.float32)
+    da = rng.normal(size=P).astype(np.float32)
+    dd = (0.1 * rng.normal(size=P)).astype(np.float32)
+    return g2d, pl, rg, dc, da, dd
+
+
+def _compare(got: np.ndarray, ref: np.ndarray):
+    assert got.shape == ref.shape
+    for j, name in enumerate(O.GRAD_FIELDS):
+        scale = max(1.0, float(np.abs(ref[:, j]).max(initial=0.0)))
+        err = float(np.abs(got[:, j] - ref[:, j]).max(initial=0.0))
+        assert err <= TOL * scale, (name, err, scale)
+
+
+@pytest.mark.parametrize("W,H,pw,ph,n,bgfrac", [(256, 256, 16, 16, 10000, 1.0), (200, 120, 16, 16, 3000, 0.12),
+                                                (300, 170, 16, 8, 6000, 0.3), (130, 90, 8, 8, 2000, 0.5)])
+def test_backward_matches_oracle(W, H, pw, ph, n, bgfrac):
+    bg = (0.1, 0.2, 0.3)
+    g2d, pl, rg, dc, da, dd = _case(W, H, pw, ph, n, bgfrac, seed=7)
+    ref = O.render_backward(pl, rg, g2d, W, H, pw, ph, bg, dc, da, dd)
+    s = api.splats_from_g2d(g2d, DEV)
+    b = api.bin_tiles(s, W, H, pw, ph)
+    fwd = api.render_forward(3, s, b, W, H, pw, ph, bg)
+    g = api.render_backward(s, b, fwd, W, H, pw, ph, torch.from_numpy(dc).to(DEV), torch.from_numpy(da).to(DEV),
+                            torch.from_numpy(dd).to(DEV), bg)
+    torch.cuda.synchronize()
+    _compare(g.as_fields()[: len(g2d)].double().cpu().numpy(), ref)
+
+
+def test_backward_super_lists_match_tile_lists():
+    """The frame pipeline's 2pw x 2ph super-tile lists (membership-filtered)
+    give the tile lists' gradients."""
+    W, H, pw, ph = 512, 288, 16, 16
+    bg = (0.0, 0.0, 0.0)
+    g2d, pl, rg, dc, da, dd = _case(W, H, pw, ph, 20000, 0.12, seed=3, f=600.0)
+    ref = O.render_backward(pl, rg, g2d, W, H, pw, ph, bg, dc, da, dd)
+    s = api.splats_from_g2d(g2d, DEV)
+    b = api.bin_tiles(s, W, H, pw, ph)
+    fwd = api.render_forward(3, s, b, W, H, pw, ph, bg)
+    sb = api.bin_tiles(s, W, H, 2 * pw, 2 * ph)
+    T = b.tile_count
+    rt = torch.empty(2 * T, dtype=torch.int32, device=DEV)
+    N.call("bs_super_tile_ranges", sb.tile_ranges.data_ptr(), W, H, pw, ph, rt.data_ptr(), api._stream(DEV))
+    sup = api.DeviceBinning(b.tile_cols, b.tile_rows, sb.point_list, rt, sb.k)
+    args = (torch.from_numpy(dc).to(DEV), torch.from_numpy(da).to(DEV), torch.from_numpy(dd).to(DEV), bg)
+    g = api.render_backward(s, sup, fwd, W, H, pw, ph, *args, super_lists=True)
+    torch.cuda.synchronize()
+    _compare(g.as_fields()[: len(g2d)].double().cpu().numpy(), ref)
+
+
+def test_backward_colour_only_and_lpt_order():
+    """dL/dalpha, dL/ddepth omitted (NULL = zero) and an LPT task order: the
+    colour gradients alone."""
+    W, H, pw, ph = 192, 160, 16, 16
+    bg = (0.2, 0.2, 0.2)
+    g2d, pl, rg, dc, _, _ = _case(W, H, pw, ph, 4000, 0.2, seed=11)
+    P = W * H
+    ref = O.render_backward(pl, rg, g2d, W, H, pw, ph, bg, dc, np.zeros(P, np.float32), np.zeros(P, np.float32))
+    s = api.splats_from_g2d(g2d, DEV)
+    b = api.bin_tiles(s, W, H, pw, ph)
+    st = api.tile_load_histogram(b)
+    fwd = api.render_forward(3, s, b, W, H, pw, ph, bg, task_order=st.task_order)
+    g = api.render_backward(s, b, fwd, W, H, pw, ph, torch.from_numpy(dc).to(DEV), bg=bg, task_order=st.task_order)
+    torch.cuda.synchronize()
+    _compare(g.as_fields()[: len(g2d)].double().cpu().numpy(), ref)
+
+
+def test_backward_errors_and_empty():
+    W, H = 64, 64
+    s = api.DeviceSplats.empty(1, DEV)
+    b = api.DeviceBinning(4, 4, torch.zeros(1, dtype=torch.int32, device=DEV),
+                          torch.zeros(32, dtype=torch.int32, device=DEV), 0)
+    fwd = api.DeviceFrame.empty(W, H, DEV)
+    dc = torch.ones(3 * W * H, device=DEV)
+    g = api.render_backward(s, b, fwd, W, H, 16, 16, dc)  # empty lists: nothing accumulates
+    torch.cuda.synchronize()
+    assert not g.as_fields().any()
+    with pytest.raises(N.BsError):
+        N.call("bs_render_backward", 7, s.c(), None, b.tile_ranges.data_ptr(), None, W, H, 16, 16,
+               (C.c_float * 3)(0, 0, 0), fwd.c(), N.FrameGradIn(dc.data_ptr(), None, None), g.c(), 0, None, 0,
+               api._stream(DEV))

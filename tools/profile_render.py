@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--config", default=None, help="c1/c2/c4: bench.py's scene and first view (overrides n/W/H/f/sigma)")
     ap.add_argument("--frame-pipeline", action="store_true",
                     help="render through the frame pipeline (super-tile lists on >= 1 Mpixel frames)")
+    ap.add_argument("--backward", action="store_true",
+                    help="after the forward, run bs_render_backward (random dL) --reps times")
     ap.add_argument("--fine-ctas", type=int, default=0,
                     help="FineGrainedCombined CTAs per SM (bs_render_set_fine_occupancy; the bench's timed frames use 3)")
     a = ap.parse_args()
@@ -54,8 +56,14 @@ def main():
         fp.sync()
     else:
         pipe = api.Pipeline(a.W, a.H, 16, 16, "cuda", mode)
-        for _ in range(a.reps):
-            pipe.forward(d, a.n, cam, variant=v)
+        for _ in range(1 if a.backward else a.reps):
+            frame, _ = pipe.forward(d, a.n, cam, variant=v)
+        if a.backward:
+            P = a.W * a.H
+            dl = [torch.randn(k * P, device="cuda") for k in (3, 1, 1)]
+            for _ in range(a.reps):
+                api.render_backward(pipe.splats, pipe.last_binning, frame, a.W, a.H, 16, 16, dl[0], dl[1], dl[2],
+                                    alpha_mode=mode, task_order=pipe.last_stats.task_order, ws=pipe.render_ws)
     torch.cuda.synchronize()
 
 
