@@ -716,6 +716,10 @@ __device__ __forceinline__ bool is_member(const RArgs& A, const float4& a, const
   return LM == kListTile || tile_member_fast(A, tile_side(tx, ty), a.x, a.y, r.w, tx, ty);
 }
 
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+
 __device__ __forceinline__ float approx_rcp(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -843,9 +847,9 @@ constexpr size_t kGcDynSmem = sizeof(float) * kGcWarps * 2 * 32 * 33;  // phase 
 template <int MODE>
 __global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs) {
   extern __shared__ float s_gc_dyn[];
-  __shared__ float4 s_geo[kGcWarps][2][32];    // survivors' xyab, cop
-  __shared__ double2 s_col[kGcWarps][2][32];   // survivors' (r, g), (b, depth) widened once
-  __shared__ int s_kpos[kGcWarps][32];         // survivors' 1-based list positions
+  __shared__ float4 s_geo[kGcWarps][2][64];    // survivors' xyab, cop (a 2-batch queue)
+  __shared__ double2 s_col[kGcWarps][2][64];   // survivors' (r, g), (b, depth) widened once
+  __shared__ int s_kpos[kGcWarps][64];         // survivors' 1-based list positions
   __shared__ unsigned long long s_tab[32];
   if (gated_out(A, BS_GAUSSIAN_WISE)) return;
   load_tab(s_tab);
@@ -859,6 +863,10 @@ __global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs
   const uint32_t start = A.ranges[2 * tile], end = A.ranges[2 * tile + 1];
   float* const sa = s_gc_dyn + warp * (2 * 32 * 33);
   float* const stb = sa + 32 * 33;
+  // this lane's column of the warp's alpha scratch as a 32-bit shared
+  // address in a register (see ExpK)
+  uint32_t sa_s;
+  asm volatile("mov.u32 %0, %1;" : "=r"(sa_s) : "r"((uint32_t)__cvta_generic_to_shared(sa + lane)));
   for (int sub = warp; sub < subs; sub += kGcWarps) {
     const int ox = tx * A.pw + (sub % nsx) * kSubW, oy = ty * A.ph + (sub / nsx) * kSubH;
     const int lx = (sub % nsx) * kSubW + (lane % kSubW), ly = (sub / nsx) * kSubH + (lane / kSubW);
@@ -873,13 +881,16 @@ __global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs
     double ar = 0.0, ag = 0.0, ab = 0.0, ad = 0.0;
     float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pc = pa, pr = pa;
     if (start + lane < end) load_rec(A, start + lane, pa, pc, pr);
+    int qn = 0;            // queued survivors (warp-uniform)
+    bool special = false;  // a queued power_cut below kExpSpecialCut (sticky per sub-tile)
     for (uint32_t base = start; base < end; base += 32) {
       if (!__any_sync(kFull, !done)) break;
-      // cull against the sub-tile, compact the survivors
+      // cull against the sub-tile, append the survivors to the queue
       const bool keep = base + lane < end && !cull_subtile(pa, pc, rx0, rx1, ry0, ry1);
       const unsigned km = __ballot_sync(kFull, keep);
+      special |= __any_sync(kFull, keep && pc.z < kExpSpecialCut);  // (see warp_task)
       if (keep) {
-        const int pos = __popc(km & lt);
+        const int pos = qn + __popc(km & lt);
         s_geo[warp][0][pos] = pa;
         s_geo[warp][1][pos] = pc;
         s_col[warp][0][pos] = make_double2((double)pr.x, (double)pr.y);
@@ -888,8 +899,12 @@ __global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs
       }
       __syncwarp();
       if (base + 32 + lane < end) load_rec(A, base + 32 + lane, pa, pc, pr);  // next batch in flight
-      const int n = __popc(km);
-      if (n == 0) continue;
+      qn += __popc(km);
+      // groups of 32 survivors (and the list's last ones): survivor groups
+      // span batches, so the Gaussian-wise phase keeps all 32 lanes busy
+      const bool last = base + 32 >= end;
+      while (qn >= 32 || (last && qn > 0)) {
+      const int n = min(qn, 32);
       // ---- phase 1: per live pixel, lanes on the survivors
       const bool active = lane < n;
       const float4 ga = s_geo[warp][0][active ? lane : 0], gc = s_geo[warp][1][active ? lane : 0];
@@ -901,8 +916,9 @@ __global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs
         const float psx = __shfl_sync(kFull, sx, p), psy = __shfl_sync(kFull, sy, p);
         const float ts = __shfl_sync(kFull, t, p);
         float alpha = 0.0f;
-        const bool ns = active && eval_step<MODE>(ga, gc, psx, psy, ek, alpha);
-        sa[p * 33 + lane] = ns ? alpha : 0.0f;
+        const bool ns = active && (special ? eval_step<MODE, true>(ga, gc, psx, psy, ek, alpha)
+                                           : eval_step<MODE, false>(ga, gc, psx, psy, ek, alpha));
+        sts_f32(sa_s + 4u * (uint32_t)(p * 33), ns ? alpha : 0.0f);
         const unsigned nsm = __ballot_sync(kFull, ns);
         gmask |= nsm;
         if (nsm == 0) continue;  // no weight is read
@@ -913,7 +929,7 @@ __global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs
           if (lane >= off) pre = __fmul_rn(pre, v);
         }
         const float tb = __shfl_up_sync(kFull, __fmul_rn(ts, pre), 1);
-        stb[p * 33 + lane] = lane == 0 ? ts : tb;
+        sts_f32(sa_s + 4u * (uint32_t)(32 * 33 + p * 33), lane == 0 ? ts : tb);
       }
       __syncwarp();
       // ---- phase 2: serial decisions and commits, lane = pixel
@@ -930,17 +946,31 @@ __global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs
             term = s_kpos[warp][q];
             break;
           }
+          // exact weight (24 x 24-bit product), one fused multiply-add per
+          // channel (the variant's colour bar is 1e-6, as FineGrainedCombined)
           const double w = __dmul_rn((double)al, (double)row_t[q]);
           const double2 rg = s_col[warp][0][q], bd = s_col[warp][1][q];
-          ar = __dadd_rn(ar, __dmul_rn(rg.x, w));
-          ag = __dadd_rn(ag, __dmul_rn(rg.y, w));
-          ab = __dadd_rn(ab, __dmul_rn(bd.x, w));
-          ad = __dadd_rn(ad, __dmul_rn(bd.y, w));
+          ar = __fma_rn(rg.x, w, ar);
+          ag = __fma_rn(rg.y, w, ag);
+          ab = __fma_rn(bd.x, w, ab);
+          ad = __fma_rn(bd.y, w, ad);
           t = tmp;
           ++contrib;
         }
       }
       __syncwarp();
+      // move the queue's remainder (< 32 survivors, n == 32) to the front
+      qn -= n;
+      if (lane < qn) {
+        s_geo[warp][0][lane] = s_geo[warp][0][n + lane];
+        s_geo[warp][1][lane] = s_geo[warp][1][n + lane];
+        s_col[warp][0][lane] = s_col[warp][0][n + lane];
+        s_col[warp][1][lane] = s_col[warp][1][n + lane];
+        s_kpos[warp][lane] = s_kpos[warp][n + lane];
+      }
+      __syncwarp();
+      if (!__any_sync(kFull, !done)) break;
+      }
     }
     if (inside) {
       const size_t pix = (size_t)py * A.W + px;
