@@ -191,6 +191,23 @@ __global__ void __launch_bounds__(256) k_project_write(const bs_gaussian3d* __re
 // binning grid g is the 2pw x 2ph super-tile grid): its list lengths feed the
 // tile statistics, the LPT order and the selector.  SMEM2: that grid too in
 // shared memory (after the first), else global atomics.
+// cp.async staging of the Gaussian chunks (k_project_bin)
+constexpr int kStageBytes = 256 * (int)sizeof(bs_gaussian3d);  // 14,336
+__host__ __device__ constexpr size_t kStageOff(int cells) { return ((size_t)cells * sizeof(int) + 15) & ~(size_t)15; }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <bool SMEM_DIFF, bool DIFF2, bool SMEM2>
 __global__ void __launch_bounds__(256, 3) k_project_bin(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam_,
                                                      const bs_camera* __restrict__ camd, Grid g,
@@ -213,41 +230,90 @@ __global__ void __launch_bounds__(256, 3) k_project_bin(const bs_gaussian3d* __r
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = (int32_t)n;
   int vis_n = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    bs_gaussian3d gs;
-    load_g3d(g3d, i, gs);
-    Projected o;
-    uint32_t cnt = 0;
-    uint2 pk = make_uint2(0u, 0u);
-    if (project_one(gs, cam, o)) {
-      ++vis_n;
-      xyab[i] = make_float4(o.x, o.y, o.ca, o.cb);
-      cop[i] = make_float4(o.cc, gs.opacity, power_cut_of(gs.opacity), o.depth);
-      rgbr[i] = make_float4(gs.color[0], gs.color[1], gs.color[2], o.radius);
-      Rect r;
-      if (tile_rect(o.x, o.y, o.radius, g, r)) {
-        const uint32_t w = (uint32_t)(r.tx1 - r.tx0 + 1), h = (uint32_t)(r.ty1 - r.ty0 + 1);
-        cnt = w * h;
-        pk = make_uint2((uint32_t)r.tx0 | ((uint32_t)r.ty0 << 16), w | (h << 16));
-        atomicAdd(&dd[r.ty0 * stride + r.tx0], 1);
-        atomicAdd(&dd[r.ty0 * stride + r.tx1 + 1], -1);
-        atomicAdd(&dd[(r.ty1 + 1) * stride + r.tx0], -1);
-        atomicAdd(&dd[(r.ty1 + 1) * stride + r.tx1 + 1], 1);
-      }
-      if (DIFF2) {
-        Rect r2;
-        if (tile_rect(o.x, o.y, o.radius, g2, r2)) {
-          atomicAdd(&dd2[r2.ty0 * stride2 + r2.tx0], 1);
-          atomicAdd(&dd2[r2.ty0 * stride2 + r2.tx1 + 1], -1);
-          atomicAdd(&dd2[(r2.ty1 + 1) * stride2 + r2.tx0], -1);
-          atomicAdd(&dd2[(r2.ty1 + 1) * stride2 + r2.tx1 + 1], 1);
+  auto project = [&](int64_t i, const bs_gaussian3d& gs) {
+      Projected o;
+      uint32_t cnt = 0;
+      uint2 pk = make_uint2(0u, 0u);
+      if (project_one(gs, cam, o)) {
+        ++vis_n;
+        xyab[i] = make_float4(o.x, o.y, o.ca, o.cb);
+        cop[i] = make_float4(o.cc, gs.opacity, power_cut_of(gs.opacity), o.depth);
+        rgbr[i] = make_float4(gs.color[0], gs.color[1], gs.color[2], o.radius);
+        Rect r;
+        if (tile_rect(o.x, o.y, o.radius, g, r)) {
+          const uint32_t w = (uint32_t)(r.tx1 - r.tx0 + 1), h = (uint32_t)(r.ty1 - r.ty0 + 1);
+          cnt = w * h;
+          pk = make_uint2((uint32_t)r.tx0 | ((uint32_t)r.ty0 << 16), w | (h << 16));
+          atomicAdd(&dd[r.ty0 * stride + r.tx0], 1);
+          atomicAdd(&dd[r.ty0 * stride + r.tx1 + 1], -1);
+          atomicAdd(&dd[(r.ty1 + 1) * stride + r.tx0], -1);
+          atomicAdd(&dd[(r.ty1 + 1) * stride + r.tx1 + 1], 1);
+        }
+        if (DIFF2) {
+          Rect r2;
+          if (tile_rect(o.x, o.y, o.radius, g2, r2)) {
+            atomicAdd(&dd2[r2.ty0 * stride2 + r2.tx0], 1);
+            atomicAdd(&dd2[r2.ty0 * stride2 + r2.tx1 + 1], -1);
+            atomicAdd(&dd2[(r2.ty1 + 1) * stride2 + r2.tx0], -1);
+            atomicAdd(&dd2[(r2.ty1 + 1) * stride2 + r2.tx1 + 1], 1);
+          }
         }
       }
+      touched[i] = cnt;
+      rects[i] = pk;
+      dkeys[i] = cnt ? float_sort_key(o.depth) : 0xffffffffu;
+      dvals[i] = (uint32_t)i;
+  };
+  if constexpr (SMEM_DIFF) {
+    // grid-stride over 256-Gaussian chunks staged through shared memory:
+    // the chunk's 14 KB arrive by coalesced 16-byte cp.async copies, double
+    // buffered (the next chunk in flight while this one is projected), and
+    // each thread reads its Gaussian from smem (stride 56 B: conflict-free
+    // 8-byte loads) instead of 14 scattered 4-byte global loads
+    char* const stage = reinterpret_cast<char*>(s_diff) + kStageOff(cells + (SMEM2 ? cells2 : 0));
+    const int64_t chunks = (n + 255) / 256;
+    auto issue = [&](int64_t ch, int buf) {
+      const char* src = reinterpret_cast<const char*>(g3d + ch * 256);
+      const int bytes = (int)(min((int64_t)256, n - ch * 256) * (int64_t)sizeof(bs_gaussian3d));
+      char* dst = stage + buf * kStageBytes;
+      for (int q = threadIdx.x; q * 16 < bytes; q += blockDim.x) {
+        if (q * 16 + 16 <= bytes) cp_async16(dst + q * 16, src + q * 16);
+        else cp_async8(dst + q * 16, src + q * 16);  // (bytes is a multiple of 8)
+      }
+      cp_async_commit();
+    };
+    int buf = 0;
+    int64_t ch = blockIdx.x;
+    if (ch < chunks) issue(ch, 0);
+    for (; ch < chunks; ch += gridDim.x) {
+      const int64_t nx = ch + gridDim.x;
+      if (nx < chunks) {
+        issue(nx, buf ^ 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const int64_t i = ch * 256 + threadIdx.x;
+      if (i < n) {
+        const float2* sp =
+            reinterpret_cast<const float2*>(stage + buf * kStageBytes + threadIdx.x * sizeof(bs_gaussian3d));
+        float2 v[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) v[k] = sp[k];
+        bs_gaussian3d gs;
+        memcpy(&gs, v, sizeof(gs));
+        project(i, gs);
+      }
+      __syncthreads();  // the buffer is refilled two chunks later
+      buf ^= 1;
     }
-    touched[i] = cnt;
-    rects[i] = pk;
-    dkeys[i] = cnt ? float_sort_key(o.depth) : 0xffffffffu;
-    dvals[i] = (uint32_t)i;
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      bs_gaussian3d gs;
+      load_g3d(g3d, i, gs);
+      project(i, gs);
+    }
   }
   const int tot = block_reduce_sum<int>(vis_n);
   if (threadIdx.x == 0 && tot) atomicAdd(&counts[1], tot);
@@ -283,7 +349,7 @@ cudaError_t launch_project_bin(const bs_gaussian3d* g3d, int64_t n, const bs_cam
   const size_t diff2_bytes = g2 ? sizeof(int) * (size_t)(g2->cols + 1) * (g2->rows + 1) : 0;
   const bool smem2 = g2 && smem_diff && diff_bytes + diff2_bytes <= (size_t)64 * 1024;
   if (smem_diff) {
-    const size_t sm = diff_bytes + (smem2 ? diff2_bytes : 0);
+    const size_t sm = kStageOff((int)((diff_bytes + (smem2 ? diff2_bytes : 0)) / sizeof(int))) + 2 * (size_t)kStageBytes;
     // one kernel per combination; per-combination occupancy cached
     auto go = [&](auto kern) -> cudaError_t {
       static size_t attr_bytes[4] = {0, 0, 0, 0};

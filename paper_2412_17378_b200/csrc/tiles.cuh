@@ -24,16 +24,24 @@ struct Rect {
   int tx0, tx1, ty0, ty1;
 };
 
+// x / p for the patch size p: a multiply by 1/p when p is a power of two
+// (both round the same exact value x * 2^-k, so the bits are identical), an
+// IEEE division otherwise.
+__device__ __forceinline__ float div_patch(float x, int p) {
+  if ((p & (p - 1)) == 0) return __fmul_rn(x, __uint_as_float((uint32_t)(127 - (31 - __clz(p))) << 23));
+  return __fdiv_rn(x, (float)p);
+}
+
 // src/preprocess.cpp:81-92.  Returns false when rejected / empty.
 __device__ __forceinline__ bool tile_rect(float x, float y, float radius, const Grid& g, Rect& r) {
   const float rr = ceilf(radius);
   const float x0 = __fsub_rn(x, rr), x1 = __fadd_rn(x, rr);
   const float y0 = __fsub_rn(y, rr), y1 = __fadd_rn(y, rr);
   if (x1 < 0.0f || y1 < 0.0f || x0 >= (float)g.W || y0 >= (float)g.H) return false;
-  r.tx0 = max(0, x86_f2i(floorf(__fdiv_rn(x0, (float)g.pw))));
-  r.tx1 = min(g.cols - 1, x86_f2i(floorf(__fdiv_rn(x1, (float)g.pw))));
-  r.ty0 = max(0, x86_f2i(floorf(__fdiv_rn(y0, (float)g.ph))));
-  r.ty1 = min(g.rows - 1, x86_f2i(floorf(__fdiv_rn(y1, (float)g.ph))));
+  r.tx0 = max(0, x86_f2i(floorf(div_patch(x0, g.pw))));
+  r.tx1 = min(g.cols - 1, x86_f2i(floorf(div_patch(x1, g.pw))));
+  r.ty0 = max(0, x86_f2i(floorf(div_patch(y0, g.ph))));
+  r.ty1 = min(g.rows - 1, x86_f2i(floorf(div_patch(y1, g.ph))));
   return r.tx0 <= r.tx1 && r.ty0 <= r.ty1;
 }
 

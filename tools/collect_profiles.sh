@@ -1,27 +1,15 @@
 #!/usr/bin/env bash
-# Copy a gpu_round.sh run's evidence into profiles/ (tracked).
+# Copy a gpu_evidence.sh run's evidence into profiles/ (tracked), prefixed <tag>_.
 #   bash tools/collect_profiles.sh <tag>
 set -eu
-IN=gpurun_out/$1
+TAG=$1
+IN=gpurun_out/$TAG
 P=profiles
-cp "$IN/bench.json" $P/r1_bench_c2.json
-cp "$IN/bench_c1.json" $P/r1_bench_c1.json
-cp "$IN/bench_c4.json" $P/r1_bench_c4.json
-cp "$IN/bench_reference.json" $P/r1_bench_reference.json
-python tools/launches.py "$IN/launches.csv" > $P/r1_launches_c2.txt
-python tools/ncu_summary.py "$IN/render_fine_full.ncu-rep" > $P/r1_ncu_full_render_fine_exact.txt
-for c in c1 c4; do
-  [ -f "$IN/render_fine_full_$c.ncu-rep" ] && \
-    python tools/ncu_summary.py "$IN/render_fine_full_$c.ncu-rep" > $P/r1_ncu_full_render_fine_exact_$c.txt
+for c in c1 c2 c4 reference; do cp "$IN/bench_$c.json" "$P/${TAG}_bench_$c.json"; done
+{ echo "# ncu --metrics gpu__time_duration.sum --clock-control none over bench.py --steps 1 --warmup 3 --no-extras --batch 4 (C2 frame pipeline; per-kernel totals, serialised / cold), run $TAG"
+  python tools/launches.py "$IN/launches.csv"; } > "$P/${TAG}_launches_c2.txt"
+for f in fine_api_c2 fine_super_c2 fine_api_c4 fine_super_c4 gw_c2 bwd_c2 scatter_c2; do
+  [ -f "$IN/$f.ncu-rep" ] && python tools/ncu_summary.py "$IN/$f.ncu-rep" > "$P/${TAG}_ncu_$f.txt"
 done
-for c in c2 c4; do
-  [ -f "$IN/render_fine_super_$c.ncu-rep" ] && \
-    python tools/ncu_summary.py "$IN/render_fine_super_$c.ncu-rep" > $P/r1_ncu_full_render_fine_super_$c.txt
-done
-python tools/ncu_traffic.py $P > $P/ncu_traffic.json
-python tools/ncu_summary.py "$IN/chunk_scatter_full.ncu-rep" > $P/r1_ncu_chunk_scatter.txt
-cp "$IN/c3_sweep.jsonl" $P/r1_c3_sweep.jsonl
-cp "$IN/training_run.csv" $P/r1_training_run.csv
-{ tail -3 "$IN/pytest_gpu.log"; cat "$IN/smoke.log"; } > $P/r1_pytest_gpu.txt
-grep -m1 "Model name" "$IN/nproc.txt" > $P/r1_host.txt || true
-head -1 "$IN/nproc.txt" >> $P/r1_host.txt
+cp "$IN/ncu_counters.json" "$P/ncu_counters.json"
+{ tail -3 "$IN/pytest_gpu.log"; cat "$IN/smoke.log"; } > "$P/${TAG}_pytest_gpu.txt"

@@ -1,9 +1,9 @@
 #!/usr/bin/env bash
-# Full r2 (second session) evidence pass on one B200: GPU tests, smoke, the C2 bench line
+# Full evidence pass on one B200: GPU tests, smoke, the C2 bench line
 # (defaults: batch step, extras incl. C3 sweep / e2e / cpu_baseline), C1 and
 # C4 lines, the reference arm (complete frames), a launch list, ncu counters
 # of the render kernels.  Outputs in gpurun_out/<tag>/.
-#   gpurun --timeout 3600 -- 'bash tools/gpu_round2.sh r2g'
+#   gpurun --timeout 3600 -- 'bash tools/gpu_evidence.sh <tag>'
 set -u
 TAG=${1:-r2}
 OUT=gpurun_out/$TAG

@@ -49,6 +49,23 @@ def main():
             if mode == N.ALPHA_EXACT:
                 check(f.to_numpy(), refs[2 if v == 2 else 0], v in (0, 1, 4))
     print("C1 API path: 5 variants x 2 modes ok", flush=True)
+    # backward render on C1, both alpha modes; exact vs the oracle
+    rng = np.random.default_rng(0)
+    P = W * H
+    dl = [rng.normal(size=k * P).astype(np.float32) for k in (3, 1, 1)]
+    gref = O.render_backward(pl, rg, g2d, W, H, 16, 16, bg, *dl)
+    s = api.splats_from_g2d(g2d, "cuda")
+    b = api.bin_tiles(s, W, H, 16, 16)
+    for mode in (N.ALPHA_EXACT, N.ALPHA_FAST):
+        f = api.render_forward(3, s, b, W, H, 16, 16, bg, mode)
+        g = api.render_backward(s, b, f, W, H, 16, 16, *[torch.from_numpy(x).cuda() for x in dl], bg=bg,
+                                alpha_mode=mode)
+        torch.cuda.synchronize()
+        if mode == N.ALPHA_EXACT:
+            got = g.as_fields()[: len(g2d)].double().cpu().numpy()
+            scale = np.maximum(1.0, np.abs(gref).max(axis=0))
+            assert (np.abs(got - gref).max(axis=0) <= 2e-4 * scale).all()
+    print("C1 backward render: 2 modes ok", flush=True)
     # frame pipeline at 1 Mpixel (super-tile lists), async + graphs
     W = H = 1024
     cam = O.make_camera(focal=(1024.0, 1024.0), width=W, height=H)
