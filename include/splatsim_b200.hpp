@@ -209,6 +209,24 @@ KernelRun run_kernel(KernelVariant variant, const TileBinning& binning, const st
 double time_kernel_ms(KernelVariant variant, const TileBinning& binning, const std::vector<Gaussian2D>& gaussians,
                       int width, int height, int patch_width, int patch_height, int repeats = 3);
 
+// ---- backward render (the reference has no backward pass) ----
+// d/d(Gaussian2D field) of sum(dl_dcolor * colour + dl_dalpha * alpha +
+// dl_ddepth * depth) over the frame `forward` (render_reference's output on
+// the same inputs), the forward's skip / stop decisions held fixed, no
+// gradient through a clamped alpha; bs_render_backward on the device.
+struct SplatGrad {
+  std::array<float, 2> xy{};
+  std::array<float, 3> conic{};  // a, b, c
+  float opacity = 0.0f;
+  std::array<float, 3> color{};
+  float depth = 0.0f;
+};
+std::vector<SplatGrad> render_backward(const TileBinning& binning, const std::vector<Gaussian2D>& gaussians,
+                                       int width, int height, int patch_width, int patch_height,
+                                       const std::array<float, 3>& background, const RenderOutput& forward,
+                                       const std::vector<float>& dl_dcolor, const std::vector<float>& dl_dalpha,
+                                       const std::vector<float>& dl_ddepth);
+
 // ---- selector (adaptive.hpp), with measured B200 kernel times ----
 struct SelectionState {
   KernelVariant current = KernelVariant::FineGrainedCombined;

@@ -64,6 +64,7 @@ struct DBuf {
 struct Ctx {
   cudaStream_t st = nullptr;
   DBuf g3d, xyab, cop, rgbr, nvis, kdev, pre_ws, bin_ws, pl, ranges, stats_ws, order, hist, render_ws, g2d;
+  DBuf dl, grads;  // render_backward: dL planes, per-splat gradients
   DBuf planes[6];
   DBuf flush;  // L2 flush buffer for time_kernel_ms (larger than the 126 MB L2)
   Ctx() { cu("cudaStreamCreate", cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)); }
@@ -337,6 +338,61 @@ KernelRun run_kernel(KernelVariant variant, const TileBinning& binning, const st
   }
   run.trace = trace_from_work(variant, tiles);
   return run;
+}
+
+std::vector<SplatGrad> render_backward(const TileBinning& binning, const std::vector<Gaussian2D>& gaussians,
+                                       int width, int height, int patch_width, int patch_height,
+                                       const std::array<float, 3>& background, const RenderOutput& forward,
+                                       const std::vector<float>& dl_dcolor, const std::vector<float>& dl_dalpha,
+                                       const std::vector<float>& dl_ddepth) {
+  check_grid("render_backward", binning, width, height, patch_width, patch_height);
+  const size_t P = size_t(width) * size_t(height);
+  if (forward.width != width || forward.height != height || forward.color.size() != 3 * P ||
+      forward.depth.size() != P || forward.final_t.size() != P)
+    throw std::invalid_argument("render_backward: forward output does not match image dims");
+  if (dl_dcolor.size() != 3 * P || (!dl_dalpha.empty() && dl_dalpha.size() != P) ||
+      (!dl_ddepth.empty() && dl_ddepth.size() != P))
+    throw std::invalid_argument("render_backward: gradient planes do not match image dims");
+  Ctx& c = ctx();
+  bs_splats s = upload_g2d(c, gaussians);
+  DeviceBinning d = upload_binning(c, binning);
+  bs_frame_out fo = device_frame(c, int64_t(P));
+  cu("H2D fwd", cudaMemcpyAsync(fo.color, forward.color.data(), P * 12, cudaMemcpyHostToDevice, c.st));
+  cu("H2D fwd", cudaMemcpyAsync(fo.depth, forward.depth.data(), P * 4, cudaMemcpyHostToDevice, c.st));
+  cu("H2D fwd", cudaMemcpyAsync(fo.final_t, forward.final_t.data(), P * 4, cudaMemcpyHostToDevice, c.st));
+  // dL planes (colour, alpha, depth) and the zeroed gradients, one buffer each
+  float* dl = static_cast<float*>(c.dl.get(P * 20));
+  cu("H2D dl", cudaMemcpyAsync(dl, dl_dcolor.data(), P * 12, cudaMemcpyHostToDevice, c.st));
+  if (!dl_dalpha.empty())
+    cu("H2D dl", cudaMemcpyAsync(dl + 3 * P, dl_dalpha.data(), P * 4, cudaMemcpyHostToDevice, c.st));
+  if (!dl_ddepth.empty())
+    cu("H2D dl", cudaMemcpyAsync(dl + 4 * P, dl_ddepth.data(), P * 4, cudaMemcpyHostToDevice, c.st));
+  const size_t n = gaussians.size();
+  const size_t gb = std::max<size_t>(n, 1) * 48;
+  float* g = static_cast<float*>(c.grads.get(gb));
+  cu("grads", cudaMemsetAsync(g, 0, gb, c.st));
+  const size_t n4 = std::max<size_t>(n, 1) * 4;
+  const bs_frame_grad_in gin{dl, dl_dalpha.empty() ? nullptr : dl + 3 * P, dl_ddepth.empty() ? nullptr : dl + 4 * P};
+  const bs_splat_grads gout{g, g + n4, g + 2 * n4};
+  const size_t rwb = bs_render_workspace_bytes(width, height);
+  ck("render_backward", bs_render_backward(mode_c(), s, binning.point_list.empty() ? nullptr : d.pl, d.ranges,
+                                           nullptr, width, height, patch_width, patch_height, background.data(), fo,
+                                           gin, gout, 0, c.render_ws.get(rwb), rwb, c.st));
+  std::vector<float> h(3 * n4);
+  cu("D2H grads", cudaMemcpyAsync(h.data(), g, h.size() * 4, cudaMemcpyDeviceToHost, c.st));
+  c.sync();
+  std::vector<SplatGrad> out(n);
+  for (size_t i = 0; i < n; ++i) {
+    const float* x = &h[4 * i];
+    const float* o = &h[n4 + 4 * i];
+    const float* r = &h[2 * n4 + 4 * i];
+    out[i].xy = {x[0], x[1]};
+    out[i].conic = {x[2], x[3], o[0]};
+    out[i].opacity = o[1];
+    out[i].color = {r[0], r[1], r[2]};
+    out[i].depth = o[3];
+  }
+  return out;
 }
 
 double time_kernel_ms(KernelVariant variant, const TileBinning& binning, const std::vector<Gaussian2D>& gaussians,

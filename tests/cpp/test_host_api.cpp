@@ -1,6 +1,7 @@
 // test_host_api.cpp — the C++ drop-in API (splatsim_b200.hpp) against the CPU
 // oracle (test infrastructure), the way the reference's own C++ tests would
 // call it.  Exit code 0 = all checks passed.  Run by tests/test_cpp_api.py.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -92,6 +93,45 @@ int main() {
     const size_t expect_tasks = size_t(b.tile_count()) * (v == splatsim::KernelVariant::FineGrainedCombined ? 32 : 1);
     CHECK(run.trace.tasks.size() == expect_tasks);
     CHECK(splatsim::make_task_specs(v, W, H, pw, ph).size() == expect_tasks);
+  }
+
+  // backward render against the oracle's analytic gradient
+  {
+    const size_t P = size_t(W) * H;
+    std::vector<float> dc(3 * P), da(P), dd(P);
+    uint64_t st = 12345;
+    auto uni = [&]() {
+      st = st * 6364136223846793005ull + 1442695040888963407ull;
+      return float(double(st >> 11) * 0x1.0p-53) - 0.5f;
+    };
+    for (auto& x : dc) x = uni();
+    for (auto& x : da) x = uni();
+    for (auto& x : dd) x = 0.1f * uni();
+    const auto grads = splatsim::render_backward(b, g2d, W, H, pw, ph, bg, rr, dc, da, dd);
+    std::vector<oracle::SplatGrad> og(og2d.size());
+    oracle::render_backward(ob, og2d.data(), og2d.size(), W, H, pw, ph, obg, dc.data(), da.data(), dd.data(),
+                            og.data());
+    CHECK(grads.size() == og.size());
+    double scale[10] = {}, err[10] = {};
+    for (size_t i = 0; i < og.size() && i < grads.size(); ++i) {
+      const double r[10] = {og[i].xy[0], og[i].xy[1], og[i].conic[0], og[i].conic[1], og[i].conic[2],
+                            og[i].opacity, og[i].color[0], og[i].color[1], og[i].color[2], og[i].depth};
+      const auto& gg = grads[i];
+      const double g[10] = {gg.xy[0], gg.xy[1], gg.conic[0], gg.conic[1], gg.conic[2],
+                            gg.opacity, gg.color[0], gg.color[1], gg.color[2], gg.depth};
+      for (int j = 0; j < 10; ++j) {
+        scale[j] = std::max(scale[j], std::abs(r[j]));
+        err[j] = std::max(err[j], std::abs(g[j] - r[j]));
+      }
+    }
+    for (int j = 0; j < 10; ++j) CHECK(err[j] <= 2e-4 * std::max(1.0, scale[j]));
+    bool bthrew = false;
+    try {
+      splatsim::render_backward(b, g2d, W, H, pw, ph, bg, rr, std::vector<float>(5), da, dd);
+    } catch (const std::invalid_argument&) {
+      bthrew = true;
+    }
+    CHECK(bthrew);
   }
 
   // exceptions as the reference throws them
