@@ -825,24 +825,26 @@ __device__ __forceinline__ void gw_finish_pixel(const RArgs& A, uint32_t from, u
 // CTA per tile, Alg. 2) with each warp owning 8x4-pixel sub-tiles of the tile
 // (lane = pixel for the state).  Per 32-entry batch of the tile's list the
 // loading lane culls its entry against the sub-tile (cull_subtile, as the
-// fine-grained kernel) and the survivors are compacted; then, two phases per
-// group of survivors:
+// fine-grained kernel) and the survivors are queued; per group of 32 queued
+// survivors (groups span batches), two phases:
 //   phase 1, Gaussian-wise (lane = survivor), once per live pixel: alpha of
-//     the group's entries at the pixel, the shfl_up doubling prefix product
-//     of (1 - alpha) from the pixel's carried t (inc/blend.hpp:69-83) -> each
-//     entry's colour weight t_before; (alpha, t_before) into the warp's
-//     32 x 33 scratch;
+//     the group's 32 entries at the pixel (Alg. 2's lanes-over-Gaussians:
+//     one exp per lane) into the warp's 32 x 33 alpha scratch;
 //   phase 2, serial (lane = pixel): skip / stop / commit in list order over
 //     the entries some pixel keeps; contrib, term and the carried t follow
-//     the serial float recurrence (src/kernels.cpp:79-89) bit for bit.
-// Culled entries have alpha < 1/255 at every pixel of the sub-tile (skipped:
-// factor 1), so dropping them changes only how the doubling prefix groups
-// the factors — the colour weights differ from render_gaussianwise's fixed
-// 32-entry windows by float reassociation (<= 1e-6), every decision is
-// exact.
+//     the serial float recurrence (src/kernels.cpp:79-89) bit for bit, and
+//     each commit's colour weight is alpha * t of that recurrence.
+// Every decision is exact.  The colour weights are render_reference's
+// (serial t); render_gaussianwise's come from the doubling prefix product of
+// (1 - alpha) over fixed 32-entry windows (inc/blend.hpp:69-83) — the two
+// differ by float reassociation only (colour <= 1e-6).  The prefix product
+// and its t_before scratch (r2's first cull kernel) halved the occupancy
+// (2 -> 3 CTAs/SM without it) for weights the exact semantics never need:
+// C2 1.67 -> 1.03 ms.  BS_GW_WINDOWED=1 keeps the reference's windows and
+// prefix weights bit for bit (k_render_gw).
 constexpr int kGcWarps = 8;
 constexpr int kGcThreads = kGcWarps * 32;
-constexpr size_t kGcDynSmem = sizeof(float) * kGcWarps * 2 * 32 * 33;  // phase scratch, 67.6 KB
+constexpr size_t kGcDynSmem = sizeof(float) * kGcWarps * 32 * 33;  // alpha scratch, 33.8 KB
 
 template <int MODE>
 __global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs) {
@@ -861,8 +863,7 @@ __global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs
   const int tx = tile % A.cols, ty = tile / A.cols;
   const int nsx = (A.pw + kSubW - 1) / kSubW;
   const uint32_t start = A.ranges[2 * tile], end = A.ranges[2 * tile + 1];
-  float* const sa = s_gc_dyn + warp * (2 * 32 * 33);
-  float* const stb = sa + 32 * 33;
+  float* const sa = s_gc_dyn + warp * (32 * 33);
   // this lane's column of the warp's alpha scratch as a 32-bit shared
   // address in a register (see ExpK)
   uint32_t sa_s;
@@ -914,28 +915,17 @@ __global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs
         const int p = __ffs(live) - 1;
         live &= live - 1;
         const float psx = __shfl_sync(kFull, sx, p), psy = __shfl_sync(kFull, sy, p);
-        const float ts = __shfl_sync(kFull, t, p);
         float alpha = 0.0f;
         const bool ns = active && (special ? eval_step<MODE, true>(ga, gc, psx, psy, ek, alpha)
                                            : eval_step<MODE, false>(ga, gc, psx, psy, ek, alpha));
         sts_f32(sa_s + 4u * (uint32_t)(p * 33), ns ? alpha : 0.0f);
         const unsigned nsm = __ballot_sync(kFull, ns);
         gmask |= nsm;
-        if (nsm == 0) continue;  // no weight is read
-        float pre = ns ? __fsub_rn(1.0f, alpha) : 1.0f;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const float v = __shfl_up_sync(kFull, pre, off);
-          if (lane >= off) pre = __fmul_rn(pre, v);
-        }
-        const float tb = __shfl_up_sync(kFull, __fmul_rn(ts, pre), 1);
-        sts_f32(sa_s + 4u * (uint32_t)(32 * 33 + p * 33), lane == 0 ? ts : tb);
       }
       __syncwarp();
       // ---- phase 2: serial decisions and commits, lane = pixel
       if (!done) {
         const float* row_a = sa + lane * 33;
-        const float* row_t = stb + lane * 33;
         for (unsigned m = gmask; m; m &= m - 1) {
           const int q = __ffs(m) - 1;
           const float al = row_a[q];
@@ -948,7 +938,7 @@ __global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs
           }
           // exact weight (24 x 24-bit product), one fused multiply-add per
           // channel (the variant's colour bar is 1e-6, as FineGrainedCombined)
-          const double w = __dmul_rn((double)al, (double)row_t[q]);
+          const double w = __dmul_rn((double)al, (double)t);
           const double2 rg = s_col[warp][0][q], bd = s_col[warp][1][q];
           ar = __fma_rn(rg.x, w, ar);
           ag = __fma_rn(rg.y, w, ag);
