@@ -445,6 +445,13 @@ int bs_render_backward(int alpha_mode, bs_splats g, const uint32_t* point_list, 
                        const uint32_t* task_order, int32_t width, int32_t height, int32_t pw, int32_t ph,
                        const float bg[3], bs_frame_out fwd, bs_frame_grad_in gin, bs_splat_grads gout,
                        int super_lists, void* ws, size_t ws_bytes, void* stream);
+/* Backward render of a frame context's last frame (bs_render_frame_device,
+ * bs_render_views...; the frame pipeline's training step): per-Gaussian
+ * gradients at the INPUT index i of that frame's g3d array (culled Gaussians
+ * receive none), accumulated into caller-zeroed gout holding >= n entries
+ * per array.  Verifies pending async frames first.  BS_ERR_UNSUPPORTED when
+ * the frame ran the compacting projection (BS_NO_FUSED_PRE=1). */
+int bs_context_render_backward(bs_context* ctx, bs_frame_grad_in gin, bs_splat_grads gout);
 /* 1 if the context's last frame was binned into super-tile lists (frames
  * >= 1 Mpixel with power-of-two patches and a FineGrainedCombined /
  * SharedMemOpt / device-selected variant; BS_NO_SUPER=1 disables), else 0. */

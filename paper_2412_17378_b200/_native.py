@@ -114,6 +114,7 @@ SIGNATURES = {
                                                 _i32, _vp, _vp, _sz, _vp, _vp, _sz, _vp]),
     "bs_render_backward": (C.c_int, [C.c_int, Splats, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _f32p, FrameOut,
                                      FrameGradIn, SplatGrads, C.c_int, _vp, _sz, _vp]),
+    "bs_context_render_backward": (C.c_int, [_vp, FrameGradIn, SplatGrads]),
     "bs_render_forward_super": (C.c_int, [C.c_int, _vp, C.c_int, Splats, _vp, _vp, _vp, _i32, _i32, _i32, _i32,
                                           _f32p, FrameOut, _vp, _sz, _vp]),
     "bs_super_tile_ranges": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),

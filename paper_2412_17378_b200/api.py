@@ -442,6 +442,18 @@ class FramePipeline:
                self.frame.c(), C.byref(fi) if info else None)
         return self.frame, fi
 
+    def backward(self, n: int, dl_dcolor: torch.Tensor, dl_dalpha: torch.Tensor | None = None,
+                 dl_ddepth: torch.Tensor | None = None, grads: "SplatGrads | None" = None) -> "SplatGrads":
+        """Backward render of the last frame (bs_context_render_backward):
+        per-Gaussian gradients at the input index (n = the frame's Gaussian
+        count), accumulated into ``grads``."""
+        grads = grads or SplatGrads.zeros(n, self.device)
+        dc = dl_dcolor.contiguous()
+        da = None if dl_dalpha is None else dl_dalpha.contiguous()
+        dd = None if dl_ddepth is None else dl_ddepth.contiguous()
+        N.call("bs_context_render_backward", self.ctx, N.FrameGradIn(_ptr(dc), _ptr(da), _ptr(dd)), grads.c())
+        return grads
+
     def sync(self) -> int:
         """Finish every pending frame (re-rendering any whose K overflowed the
         point_list capacity); returns the number of such re-renders so far."""

@@ -80,6 +80,8 @@ struct bs_context {
   int32_t last_variant = -1;  // host-known variant, -1 = device-selected
   int64_t last_k = 0;
   int last_W = 0, last_H = 0, last_pw = 0, last_ph = 0;
+  int64_t last_n = 0;
+  float last_bg[3] = {0, 0, 0};
   // per-stage timing (bs_context_enable_timing)
   bs_frame_out last_out{};
   bool timing = false;
@@ -513,6 +515,8 @@ int frame_device(bs_context* c, const bs_gaussian3d* g3d_dev, int64_t n, const b
                             c->render_ws_bytes, st));
   mark(6);
   c->last_variant = variant;
+  c->last_n = n;
+  for (int i = 0; i < 3; ++i) c->last_bg[i] = bg[i];
   c->last_W = W;
   c->last_H = H;
   c->last_pw = pw;
@@ -785,6 +789,25 @@ extern "C" int bs_context_capacity(bs_context* c, int64_t* point_list_cap, int64
   if (point_list_cap) *point_list_cap = c->pl_cap;
   if (grows) *grows = c->pl_grows;
   return BS_OK;
+}
+
+// Backward render of the context's last frame: its splats
+// (at the input Gaussian index — the fused projection does not compact),
+// lists (super-tile or pw x ph, as the frame used), LPT order and output
+// planes.  Pending frames are verified first, so an overflowed frame has
+// been rendered again and the lists are final.
+extern "C" int bs_context_render_backward(bs_context* c, bs_frame_grad_in gin, bs_splat_grads gout) {
+  if (!c || !gin.dl_dcolor || !gout.xyab || !gout.cop || !gout.rgbr) return BS_ERR_INVALID_ARGUMENT;
+  if (c->last_W <= 0 || !c->last_out.color) return BS_ERR_INVALID_ARGUMENT;  // no frame yet
+  if (!c->last_fused) return BS_ERR_UNSUPPORTED;  // compacted splats (BS_NO_FUSED_PRE=1)
+  cudaStream_t st = static_cast<cudaStream_t>(bs_context_stream(c));
+  TRY(verify_pending(c, st, 0));
+  const bs_splats sp{reinterpret_cast<float*>(c->splat[0]), reinterpret_cast<float*>(c->splat[1]),
+                     reinterpret_cast<float*>(c->splat[2])};
+  return bs_render_backward(c->alpha_mode, sp, c->last_k > 0 ? c->point_list : nullptr,
+                            c->last_super ? c->ranges_t : c->ranges, c->order, c->last_W, c->last_H, c->last_pw,
+                            c->last_ph, c->last_bg, c->last_out, gin, gout, c->last_super ? 1 : 0, c->render_ws,
+                            c->render_ws_bytes, st);
 }
 
 extern "C" int bs_context_last_info(bs_context* c, bs_frame_info* info) {

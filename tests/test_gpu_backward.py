@@ -115,3 +115,39 @@ def test_backward_errors_and_empty():
         N.call("bs_render_backward", 7, s.c(), None, b.tile_ranges.data_ptr(), None, W, H, 16, 16,
                (C.c_float * 3)(0, 0, 0), fwd.c(), N.FrameGradIn(dc.data_ptr(), None, None), g.c(), 0, None, 0,
                api._stream(DEV))
+
+
+@pytest.mark.parametrize("W,H,async_mode,graphs", [(1024, 1024, True, True), (512, 384, False, False),
+                                                   (1024, 1024, False, False)])
+def test_frame_pipeline_backward_matches_oracle(W, H, async_mode, graphs):
+    """bs_context_render_backward on the frame pipeline's last frame (fused
+    projection: gradients at the input Gaussian index; super-tile lists at
+    >= 1 Mpixel, async K checks and CUDA-graph replays) == the oracle's
+    gradient of the same frame, mapped through the visible splats."""
+    pw = ph = 16
+    n = 20000
+    bg = (0.1, 0.2, 0.3)
+    cam = O.make_camera(focal=(float(W), float(W)), width=W, height=H)
+    g3d = O.gen_clustered_scene(n, cam, seed=5, sigma=0.035, bgfrac=0.2)
+    vis = np.array([O.lib().orc_project_gaussian(g3d[i:i + 1].ctypes.data, C.byref(cam),
+                                                 np.zeros(1, O.G2D_DTYPE).ctypes.data) for i in range(n)], bool)
+    g2d = O.project_all(g3d, cam)
+    assert vis.sum() == len(g2d)
+    pl, rg = O.bin_tiles(g2d, W, H, pw, ph)
+    rng = np.random.default_rng(1)
+    P = W * H
+    dc = rng.normal(size=3 * P).astype(np.float32)
+    da = rng.normal(size=P).astype(np.float32)
+    dd = (0.1 * rng.normal(size=P)).astype(np.float32)
+    ref = O.render_backward(pl, rg, g2d, W, H, pw, ph, bg, dc, da, dd)
+    fp = api.FramePipeline(W, H, pw, ph, DEV, N.ALPHA_EXACT, async_mode=async_mode, graphs=graphs)
+    d = api.g3d_to_device(g3d, DEV)
+    ncam = N.Camera.from_buffer_copy(bytes(cam))
+    for _ in range(3):
+        fp.forward(d, n, ncam, variant=3, bg=bg)
+    g = fp.backward(n, torch.from_numpy(dc).to(DEV), torch.from_numpy(da).to(DEV), torch.from_numpy(dd).to(DEV))
+    torch.cuda.synchronize()
+    got = g.as_fields()[:n].double().cpu().numpy()
+    assert not got[~vis].any()  # culled Gaussians receive nothing
+    _compare(got[vis], ref)
+    fp.close()
