@@ -752,26 +752,27 @@ __device__ __forceinline__ bool cull_subtile(const float4 a, const float4 c, flo
   if ((a.x + ex < rx0) || (a.x - ex > rx1) || (a.y + ey < ry0) || (a.y - ey > ry1)) return true;
   // the box test passed: exact ellipse-rectangle test.  q(d) = a dx^2 +
   // 2b dx dy + c dy^2 is convex, so with the centre outside the rectangle its
-  // minimum over the rectangle lies on an edge, where it is a 1-D quadratic
-  // minimised at the clamped stationary point.  The 1 % margin in r2 covers
-  // the float rounding here and in the exact power.
+  // minimum over the rectangle lies on an edge FACING the centre (from a
+  // point of any other edge, the segment toward the centre stays inside and
+  // q decreases along it): at most one vertical and one horizontal edge,
+  // where q is a 1-D quadratic minimised at the clamped stationary point.
+  // The 1 % margin in r2 covers the float rounding here and in the exact
+  // power.
   const float mx = a.x, my = a.y, qa = a.z, qb = a.w, qc = c.x;
   if (mx >= rx0 && mx <= rx1 && my >= ry0 && my <= ry1) return false;
   const float ia = approx_rcp(qa), ic = approx_rcp(qc);  // stationary points: error only 2nd order in q
   float best;
   {
-    const float dx0 = rx0 - mx, dx1 = rx1 - mx;
-    const float dy0 = fminf(fmaxf(-qb * dx0 * ic, ry0 - my), ry1 - my);
-    const float dy1 = fminf(fmaxf(-qb * dx1 * ic, ry0 - my), ry1 - my);
-    best = fminf(qa * dx0 * dx0 + 2.0f * qb * dx0 * dy0 + qc * dy0 * dy0,
-                 qa * dx1 * dx1 + 2.0f * qb * dx1 * dy1 + qc * dy1 * dy1);
+    const float dx = (mx < rx0 ? rx0 : rx1) - mx;  // the vertical edge facing the centre (if any)
+    const float dy = fminf(fmaxf(-qb * dx * ic, ry0 - my), ry1 - my);
+    const float q = qa * dx * dx + 2.0f * qb * dx * dy + qc * dy * dy;
+    best = (mx < rx0 || mx > rx1) ? q : INFINITY;
   }
   {
-    const float dy0 = ry0 - my, dy1 = ry1 - my;
-    const float dx0 = fminf(fmaxf(-qb * dy0 * ia, rx0 - mx), rx1 - mx);
-    const float dx1 = fminf(fmaxf(-qb * dy1 * ia, rx0 - mx), rx1 - mx);
-    best = fminf(best, fminf(qa * dx0 * dx0 + 2.0f * qb * dx0 * dy0 + qc * dy0 * dy0,
-                             qa * dx1 * dx1 + 2.0f * qb * dx1 * dy1 + qc * dy1 * dy1));
+    const float dy = (my < ry0 ? ry0 : ry1) - my;  // the horizontal edge facing the centre (if any)
+    const float dx = fminf(fmaxf(-qb * dy * ia, rx0 - mx), rx1 - mx);
+    const float q = qa * dx * dx + 2.0f * qb * dx * dy + qc * dy * dy;
+    best = fminf(best, (my < ry0 || my > ry1) ? q : INFINITY);
   }
   return best > r2;
 }
