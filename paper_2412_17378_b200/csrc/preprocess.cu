@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(256, 3) k_project_bin(const bs_gaussian3d* __r
                                                      float4* __restrict__ rgbr, uint32_t* __restrict__ touched,
                                                      uint2* __restrict__ rects, uint32_t* __restrict__ dkeys,
                                                      uint32_t* __restrict__ dvals, int* __restrict__ diff,
-                                                     int32_t* __restrict__ counts, Grid g2, int* __restrict__ diff2) {
+                                                     int32_t* __restrict__ counts, Grid g2, int* __restrict__ diff2,
+                                                     bool staged) {
   extern __shared__ int s_diff[];
   const CamDev cam = cam_of(camd, cam_);
   const int stride = g.cols + 1;
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(256, 3) k_project_bin(const bs_gaussian3d* __r
       dkeys[i] = cnt ? float_sort_key(o.depth) : 0xffffffffu;
       dvals[i] = (uint32_t)i;
   };
-  if constexpr (SMEM_DIFF) {
+  if (SMEM_DIFF && staged) {  // (staged: g3d 16-byte aligned, as cp.async needs)
     // grid-stride over 256-Gaussian chunks staged through shared memory:
     // the chunk's 14 KB arrive by coalesced 16-byte cp.async copies, double
     // buffered (the next chunk in flight while this one is projected), and
@@ -373,7 +374,8 @@ cudaError_t launch_project_bin(const bs_gaussian3d* g3d, int64_t n, const bs_cam
       }
       const int64_t grid = nb < (int64_t)sms * per_sm[slot] ? nb : (int64_t)sms * per_sm[slot];
       kern<<<(unsigned)(grid > 0 ? grid : 1), 256, sm, st>>>(g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects,
-                                                             dkeys, dvals, diff, counts, gg2, diff2);
+                                                             dkeys, dvals, diff, counts, gg2, diff2,
+                                                             (reinterpret_cast<uintptr_t>(g3d) & 15) == 0);
       return cudaSuccess;
     };
     cudaError_t e;
@@ -383,10 +385,10 @@ cudaError_t launch_project_bin(const bs_gaussian3d* g3d, int64_t n, const bs_cam
     if (e != cudaSuccess) return e;
   } else if (g2) {
     k_project_bin<false, true, false><<<(unsigned)(nb > 0 ? nb : 1), 256, 0, st>>>(
-        g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects, dkeys, dvals, diff, counts, gg2, diff2);
+        g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects, dkeys, dvals, diff, counts, gg2, diff2, false);
   } else {
     k_project_bin<false, false, false><<<(unsigned)(nb > 0 ? nb : 1), 256, 0, st>>>(
-        g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects, dkeys, dvals, diff, counts, gg2, diff2);
+        g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects, dkeys, dvals, diff, counts, gg2, diff2, false);
   }
   count_launches(1);
   return cudaPeekAtLastError();

@@ -151,3 +151,34 @@ def test_frame_pipeline_backward_matches_oracle(W, H, async_mode, graphs):
     assert not got[~vis].any()  # culled Gaussians receive nothing
     _compare(got[vis], ref)
     fp.close()
+
+
+def test_backward_drives_a_fit():
+    """A few gradient-descent steps on the splats' colour and opacity (forward
+    and backward on the device, the lists fixed) toward a target frame
+    rendered from different colours / opacities: the image loss falls."""
+    W, H, pw, ph = 128, 96, 16, 16
+    g2d, pl, rg, _, _, _ = _case(W, H, pw, ph, 1500, 0.3, seed=21)
+    target = g2d.copy()
+    rng = np.random.default_rng(3)
+    target["color"] = rng.uniform(0, 1, size=target["color"].shape).astype(np.float32)
+    target["opacity"] = np.clip(target["opacity"] * rng.uniform(0.6, 1.2, size=len(target)), 0.05, 0.95)
+    bg = (0.0, 0.0, 0.0)
+    st = api.splats_from_g2d(target, DEV)
+    b = api.bin_tiles(st, W, H, pw, ph)
+    tgt = api.render_forward(3, st, b, W, H, pw, ph, bg).color.clone()
+    s = api.splats_from_g2d(g2d, DEV)
+    losses = []
+    for _ in range(15):
+        fwd = api.render_forward(3, s, b, W, H, pw, ph, bg)
+        diff = fwd.color - tgt
+        losses.append(float((diff * diff).sum()))
+        g = api.render_backward(s, b, fwd, W, H, pw, ph, 2.0 * diff, bg=bg)
+        # normalised steps (the per-splat sums span orders of magnitude)
+        gc, go = g.rgbr[:, :3], g.cop[:, 1]
+        s.rgbr[:, :3] = (s.rgbr[:, :3] - 0.1 * gc / (gc.abs().max() + 1e-12)).clamp(0.0, 1.0)
+        s.cop[:, 1] = (s.cop[:, 1] - 0.05 * go / (go.abs().max() + 1e-12)).clamp(0.02, 0.99)
+        # keep power_cut consistent with the opacity: ln(1 / (255 o)) - 0.01
+        s.cop[:, 2] = torch.log(1.0 / (255.0 * s.cop[:, 1])) - 0.01
+    torch.cuda.synchronize()
+    assert losses[-1] < 0.5 * losses[0], losses

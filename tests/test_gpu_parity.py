@@ -135,12 +135,16 @@ def test_binning_bit_exact_large(W, H, f, n, bgfrac):
     assert np.array_equal(b.point_list.cpu().numpy().view(np.uint32), pl_ref)
 
 
-@pytest.mark.parametrize("W,H,f,n,bgfrac", [(960, 540, 500.0, 30000, 0.3), (1920, 1080, 1000.0, 40000, 0.12)])
-def test_fused_project_bin_matches_reference(W, H, f, n, bgfrac):
+@pytest.mark.parametrize("W,H,f,n,bgfrac,misaligned", [(960, 540, 500.0, 30000, 0.3, False),
+                                                        (1920, 1080, 1000.0, 40000, 0.12, False),
+                                                        (960, 540, 500.0, 30001, 0.3, True)])
+def test_fused_project_bin_matches_reference(W, H, f, n, bgfrac, misaligned):
     """bs_preprocess_bin_count (the frame pipeline's projection fused with the
     per-splat binning pass, splats left uncompacted) + bs_bin_sort: the
     visible splats equal project_all's, and mapping every list entry through
-    the compaction gives bin_tiles' point_list and ranges exactly."""
+    the compaction gives bin_tiles' point_list and ranges exactly.
+    misaligned: the scene pointer only 8-byte aligned (the kernel then skips
+    its 16-byte cp.async staging)."""
     g3d, cam = scene(n, W, H, f, bgfrac=bgfrac)
     g3d["mean"][::53, 2] = 0.004  # near-plane culls scattered through the input
     g2d = O.project_all(g3d, cam)
@@ -148,6 +152,11 @@ def test_fused_project_bin_matches_reference(W, H, f, n, bgfrac):
     vis = np.array([len(O.project_all(g3d[i:i + 1], cam)) == 1 for i in range(n)])
     assert vis.sum() == len(g2d) < n
     d = api.g3d_to_device(g3d)
+    if misaligned:
+        buf = torch.zeros(d.numel() + 16, dtype=torch.uint8, device=DEV)
+        buf[8:8 + d.numel()] = d
+        d = buf[8:8 + d.numel()]
+        assert d.data_ptr() % 16 == 8
     s = api.DeviceSplats.empty(n, DEV)
     counts = torch.zeros(2, dtype=torch.int32, device=DEV)
     b = api.Binner(W, H, 16, 16, DEV)
