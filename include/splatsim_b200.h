@@ -18,6 +18,9 @@
  *   bs_frame_work        TileWork.consumed / trace inputs  src/kernels.cpp:283-298
  *   bs_select_variant    (per-frame form of) checkpoint    include/splatsim/adaptive.hpp:54-55
  *   bs_variant_name/_from_name  variant_name/_from_name    include/splatsim/kernels.hpp:25-26
+ * Beyond the reference (it has no backward pass):
+ *   bs_render_backward, bs_context_render_backward — per-splat gradients of
+ *   render_reference's outputs (src/blend.cpp:8-42 differentiated).
  * The C++ host layer (splatsim_b200.hpp) restores the reference's value-typed
  * signatures and exceptions on top of this ABI.
  */
