@@ -672,6 +672,12 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     pad[:H, :W] = cons
     prefix_entries = int(pad.reshape(rows, ph, cols, pw).max(axis=(1, 3)).sum())
     bytes_prefix = 44 * prefix_entries + 32 * P
+    # the consumed-work histogram beside the list-length one
+    # (consumed(p) = term > 0 ? term : list length, src/kernels.cpp:296)
+    qs = (50, 90, 99, 99.9, 100)
+    res["frame_work"]["consumed_per_pixel"] = {f"p{q:g}": int(np.percentile(cons, q)) for q in qs}
+    res["frame_work"]["consumed_per_pixel"]["mean"] = round(float(cons.mean()), 1)
+    res["frame_work"]["list_len_per_tile"] = {f"p{q:g}": int(np.percentile(lens, q)) for q in qs}
     # the render the timed frames run: on >= 1 Mpixel frames the frame
     # pipeline bins into 2pw x 2ph super-tile lists and the render filters
     # each tile's members (bs_render_forward_super) — time that render stage

@@ -440,6 +440,7 @@ class FramePipeline:
         fi = N.FrameInfo() if info else None
         N.call("bs_render_frame_device", self.ctx, _ptr(g3d_dev), int(n), C.byref(cam), self.pw, self.ph, int(v), bgc,
                self.frame.c(), C.byref(fi) if info else None)
+        self._last_n = int(n)
         return self.frame, fi
 
     def backward(self, n: int, dl_dcolor: torch.Tensor, dl_dalpha: torch.Tensor | None = None,
@@ -447,7 +448,11 @@ class FramePipeline:
         """Backward render of the last frame (bs_context_render_backward):
         per-Gaussian gradients at the input index (n = the frame's Gaussian
         count), accumulated into ``grads``."""
+        if n < getattr(self, "_last_n", 0):
+            raise ValueError(f"backward: n={n} is below the last frame's {self._last_n} Gaussians")
         grads = grads or SplatGrads.zeros(n, self.device)
+        if grads.xyab.shape[0] < n:
+            raise ValueError("backward: grads hold fewer than n splats")
         dc = dl_dcolor.contiguous()
         da = None if dl_dalpha is None else dl_dalpha.contiguous()
         dd = None if dl_ddepth is None else dl_ddepth.contiguous()
