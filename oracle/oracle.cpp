@@ -416,6 +416,10 @@ void render_backward(const TileBinning& b, const Gaussian2D* gs, size_t n, int w
     const int x0 = tx * pw, y0 = ty * ph, x1 = std::min(width, x0 + pw), y1 = std::min(height, y0 + ph);
     for (int py = y0; py < y1; ++py)
       for (int px = x0; px < x1; ++px) {
+        const size_t pp = size_t(py) * size_t(width) + size_t(px);
+        if (dl_dcolor[3 * pp] == 0.0f && dl_dcolor[3 * pp + 1] == 0.0f && dl_dcolor[3 * pp + 2] == 0.0f &&
+            dl_dalpha[pp] == 0.0f && dl_ddepth[pp] == 0.0f)
+          continue;  // contributes nothing (lets tests sample tiles of large frames)
         const float sx = float(px) + 0.5f, sy = float(py) + 0.5f;
         cm.clear();
         float tt = 1.0f;

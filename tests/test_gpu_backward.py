@@ -182,3 +182,49 @@ def test_backward_drives_a_fit():
         s.cop[:, 2] = torch.log(1.0 / (255.0 * s.cop[:, 1])) - 0.01
     torch.cuda.synchronize()
     assert losses[-1] < 0.5 * losses[0], losses
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c4"])
+def test_backward_full_size_tile_sampled(cfg):
+    """The backward at the headline sizes (C2 1080p/1M, C4 4K/3M): dL/d(planes)
+    nonzero only on sampled tiles (the 16 longest lists + 0.3 % random, seed
+    42), so the gradients are sums over those tiles' pixels; the GPU runs the
+    whole frame on the device binning, the oracle only the sampled tiles on
+    the same lists (each checked equal to the reference rule by
+    test_gpu_parity)."""
+    import bench
+    W, H, f, n, bgf, sig = bench.CONFIGS[cfg]
+    pw = ph = 16
+    bg = (0.1, 0.2, 0.3)
+    cam = N.make_camera(None, (f, f), W, H)
+    g3d = api.gen_clustered_scene(n, cam, cluster_sigma=sig, background_fraction=bgf)
+    pipe = api.Pipeline(W, H, pw, ph, DEV, N.ALPHA_EXACT)
+    frame, _ = pipe.forward(api.g3d_to_device(g3d), n, cam, variant=3, bg=bg)
+    b, s = pipe.last_binning, pipe.splats
+    g2d = api.splats_to_g2d(s)
+    cols, rows = (W + pw - 1) // pw, (H + ph - 1) // ph
+    T = cols * rows
+    rg = b.tile_ranges.cpu().numpy().view(np.uint32)
+    lens = (rg[1::2] - rg[0::2]).astype(np.int64)
+    rng = np.random.default_rng(42)
+    tiles = np.unique(np.concatenate([np.argsort(-lens, kind="stable")[:16], rng.choice(T, T // 300, replace=False)]))
+    sub_pl, sub_rg, pos = [], np.zeros(2 * T, np.uint32), 0
+    for t in tiles.tolist():
+        lst = b.point_list[int(rg[2 * t]):int(rg[2 * t + 1])].cpu().numpy().view(np.uint32)
+        sub_rg[2 * t], sub_rg[2 * t + 1] = pos, pos + len(lst)
+        sub_pl.append(lst)
+        pos += len(lst)
+    px = np.zeros((H, W), bool)
+    for t in tiles.tolist():
+        px[(t // cols) * ph:(t // cols) * ph + ph, (t % cols) * pw:(t % cols) * pw + pw] = True
+    m = px.reshape(-1)
+    P = W * H
+    dc = (rng.normal(size=3 * P).astype(np.float32).reshape(P, 3) * m[:, None]).reshape(-1)
+    da = rng.normal(size=P).astype(np.float32) * m
+    dd = (0.1 * rng.normal(size=P)).astype(np.float32) * m
+    ref = O.render_backward(np.concatenate(sub_pl), sub_rg, g2d, W, H, pw, ph, bg, dc, da, dd)
+    assert (ref[:, 6] != 0).sum() > 1000 and (ref[:, 0] != 0).sum() > 1000  # the sample is substantial
+    g = api.render_backward(s, b, frame, W, H, pw, ph, torch.from_numpy(dc).to(DEV), torch.from_numpy(da).to(DEV),
+                            torch.from_numpy(dd).to(DEV), bg, task_order=pipe.last_stats.task_order)
+    torch.cuda.synchronize()
+    _compare(g.as_fields()[: len(g2d)].double().cpu().numpy(), ref)
