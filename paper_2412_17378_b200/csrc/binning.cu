@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256) k_bin_rect(const float4* __restrict__ xya
                                                   uint32_t* __restrict__ touched, uint2* __restrict__ rects,
                                                   uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
                                                   int* __restrict__ diff) {
+  bs::pdl_wait();
   extern __shared__ int s_diff[];
   const int stride = g.cols + 1;
   const int cells = stride * (g.rows + 1);
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(256) k_bin_rect(const float4* __restrict__ xya
 // One CTA: 2-D inclusive prefix of the difference grid in shared memory ->
 // per-tile counts.
 __global__ void __launch_bounds__(1024) k_diff_scan(const int* __restrict__ diff, Grid g, uint32_t* __restrict__ counts) {
+  bs::pdl_wait();
   extern __shared__ int s_grid[];
   const int stride = g.cols + 1, cells = stride * (g.rows + 1);
   for (int i = threadIdx.x; i < cells; i += blockDim.x) s_grid[i] = diff[i];
@@ -106,6 +108,7 @@ __global__ void __launch_bounds__(1024) k_diff_scan(const int* __restrict__ diff
 
 // Fallback for grids beyond shared memory: row CTAs, then a thread per column.
 __global__ void __launch_bounds__(256) k_diff_rows(int* __restrict__ diff, int stride) {
+  bs::pdl_wait();
   int* row = diff + (size_t)blockIdx.x * stride;
   __shared__ int carry;
   if (threadIdx.x == 0) carry = 0;
@@ -124,6 +127,7 @@ __global__ void __launch_bounds__(256) k_diff_rows(int* __restrict__ diff, int s
 }
 
 __global__ void __launch_bounds__(256) k_diff_cols(const int* __restrict__ diff, Grid g, uint32_t* __restrict__ counts) {
+  bs::pdl_wait();
   const int tx = blockIdx.x * blockDim.x + threadIdx.x;
   if (tx >= g.cols) return;
   const int stride = g.cols + 1;
@@ -150,6 +154,7 @@ constexpr int kExpandWin = kExpandItems + 1;
 // b*4096: every splat marks the expansion blocks whose first output it owns.
 __global__ void k_mark_starts(const uint64_t* __restrict__ offs, const uint32_t* __restrict__ touched_sorted,
                               int64_t n_cap, const int32_t* __restrict__ n_visible, uint32_t* __restrict__ block_j0) {
+  bs::pdl_wait();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n_cap || j >= *n_visible) return;
   const uint64_t lo = offs[j], hi = lo + touched_sorted[j];
@@ -161,6 +166,7 @@ __global__ void __launch_bounds__(256) k_expand(const uint64_t* __restrict__ off
                                                 const int32_t* __restrict__ n_visible, int64_t K, int cols,
                                                 const uint32_t* __restrict__ block_j0, uint32_t* __restrict__ keys,
                                                 uint32_t* __restrict__ vals) {
+  bs::pdl_wait();
   __shared__ uint64_t s_offs[kExpandWin + 1];
   const int tid = threadIdx.x;
   const int64_t o0 = (int64_t)blockIdx.x * kExpandItems;
@@ -258,6 +264,7 @@ constexpr size_t kMaxScatterSmem = 200 * 1024;           // offsets row (T u32) 
 __global__ void k_chunk_bounds(const uint64_t* __restrict__ offs, const uint32_t* __restrict__ touched_sorted,
                                int64_t n_cap, const int32_t* __restrict__ n_visible, const uint64_t* __restrict__ kd,
                                int64_t k_cap, int nchunks, uint32_t* __restrict__ first) {
+  bs::pdl_wait();
   const uint64_t K = *kd;
   if (K == 0 || K > (uint64_t)k_cap) return;  // nothing to do / point_list too small (bs_bin_sort_async)
   const int64_t q = (int64_t)((K + (uint64_t)nchunks - 1) / (uint64_t)nchunks);
@@ -279,6 +286,7 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_hist(const uint2* __restri
                                                            const uint32_t* __restrict__ first, Grid g,
                                                            uint32_t* __restrict__ m, uint32_t* __restrict__ rowc,
                                                            const uint64_t* __restrict__ kd, int64_t k_cap) {
+  bs::pdl_wait();
   if (*kd == 0 || *kd > (uint64_t)k_cap) return;
   extern __shared__ int s_grid[];
   const int stride = g.cols + 1, cells = stride * (g.rows + 1);
@@ -338,6 +346,7 @@ constexpr int kCsSeg = 32;
 __global__ void __launch_bounds__(kCsSeg * 32) k_chunk_scan(uint32_t* __restrict__ m,
                                                             const uint32_t* __restrict__ starts, int T, int nchunks,
                                                             const uint64_t* __restrict__ kd, int64_t k_cap) {
+  bs::pdl_wait();
   if (*kd == 0 || *kd > (uint64_t)k_cap) return;
   __shared__ uint32_t s_part[kCsSeg][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -392,6 +401,7 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
                                                               int rows, uint32_t* __restrict__ point_list,
                                                               const uint64_t* __restrict__ kd, int64_t k_cap,
                                                               int band_rows) {
+  bs::pdl_wait();
   if (*kd == 0 || *kd > (uint64_t)k_cap) return;
   extern __shared__ uint32_t s_off[];
   __shared__ ScQ s_q[kScWarps][64];
@@ -553,6 +563,7 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
 // behind it reads nothing.
 __global__ void k_ranges(const uint32_t* __restrict__ starts, const uint32_t* __restrict__ counts, int T,
                          uint32_t* __restrict__ ranges, const uint64_t* __restrict__ kd, int64_t k_cap) {
+  bs::pdl_wait();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   if (kd && *kd > (uint64_t)k_cap) {
@@ -647,6 +658,7 @@ inline void bin_ws_layout(C& c, int64_t n_cap, const Grid& g, int64_t k_cap, Bin
 // K to *k_total — device memory, or mapped pinned host memory (the frame
 // pipeline reads K there without a D2H copy); total == null stores 0
 __global__ void k_store_k(const uint64_t* __restrict__ total, int64_t* k_total) {
+  bs::pdl_wait();
   *reinterpret_cast<volatile int64_t*>(k_total) = total ? (int64_t)*total : 0;
   __threadfence_system();
 }
@@ -686,20 +698,20 @@ static int bin_count_tail(int64_t n_cap, const int32_t* n_visible, const Grid& g
     uint64_t* total = w.offs_partials + scan_num_blocks(n_cap);
     BS_CUDA_TRY((exclusive_scan<uint32_t, uint64_t>(w.touched_sorted, w.offs, n_cap, n_visible, w.offs_partials,
                                                     total, st)));
-    k_store_k<<<1, 1, 0, st>>>(total, k_total);
+    bs::launch_pdl(k_store_k, 1, 1, 0, st, total, k_total);
     BS_LAUNCH_CHECK();
   } else {
-    k_store_k<<<1, 1, 0, st>>>(nullptr, k_total);
+    bs::launch_pdl(k_store_k, 1, 1, 0, st, nullptr, k_total);
     BS_LAUNCH_CHECK();
   }
   // tile histogram from the difference grid -> counts, starts, digit counts
   if (smem_diff) {
-    k_diff_scan<<<1, 1024, diff_bytes, st>>>(w.diff, gr, w.counts);
+    bs::launch_pdl(k_diff_scan, 1, 1024, diff_bytes, st, w.diff, gr, w.counts);
     BS_LAUNCH_CHECK();
   } else {
-    k_diff_rows<<<(unsigned)(gr.rows + 1), 256, 0, st>>>(w.diff, gr.cols + 1);
+    bs::launch_pdl(k_diff_rows, (unsigned)(gr.rows + 1), 256, 0, st, w.diff, gr.cols + 1);
     BS_LAUNCH_CHECK();
-    k_diff_cols<<<(unsigned)((gr.cols + 255) / 256), 256, 0, st>>>(w.diff, gr, w.counts);
+    bs::launch_pdl(k_diff_cols, (unsigned)((gr.cols + 255) / 256), 256, 0, st, w.diff, gr, w.counts);
     BS_LAUNCH_CHECK();
   }
   BS_CUDA_TRY((exclusive_scan<uint32_t, uint32_t>(w.counts, w.starts, T, nullptr, w.cpartials, nullptr, st)));
@@ -738,10 +750,10 @@ extern "C" int bs_bin_count(bs_splats g, int64_t n_cap, const int32_t* n_visible
       BS_CUDA_TRY(cudaGetDevice(&dev));
       BS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       const unsigned grid = (unsigned)min((int64_t)nb, (int64_t)sms * 2);
-      k_bin_rect<true><<<grid, 256, diff_bytes, st>>>(xa, xc, xr, n_cap, n_visible, gr, w.touched, w.rects, w.dk0,
+      bs::launch_pdl(k_bin_rect<true>, grid, 256, diff_bytes, st, xa, xc, xr, n_cap, n_visible, gr, w.touched, w.rects, w.dk0,
                                                       w.dv0, w.diff);
     } else {
-      k_bin_rect<false><<<nb, 256, 0, st>>>(xa, xc, xr, n_cap, n_visible, gr, w.touched, w.rects, w.dk0, w.dv0,
+      bs::launch_pdl(k_bin_rect<false>, nb, 256, 0, st, xa, xc, xr, n_cap, n_visible, gr, w.touched, w.rects, w.dk0, w.dv0,
                                             w.diff);
     }
     BS_LAUNCH_CHECK();
@@ -882,16 +894,16 @@ extern "C" int bs_super_tile_lengths(void* aux, size_t aux_bytes, int32_t width,
     g_diff_attr_set = true;
   }
   if (diff2_bytes <= kMaxDiffSmem) {
-    k_diff_scan<<<1, 1024, diff2_bytes, st>>>(diff2, gt, counts2);
+    bs::launch_pdl(k_diff_scan, 1, 1024, diff2_bytes, st, diff2, gt, counts2);
     BS_LAUNCH_CHECK();
   } else {
-    k_diff_rows<<<(unsigned)(gt.rows + 1), 256, 0, st>>>(diff2, gt.cols + 1);
+    bs::launch_pdl(k_diff_rows, (unsigned)(gt.rows + 1), 256, 0, st, diff2, gt.cols + 1);
     BS_LAUNCH_CHECK();
-    k_diff_cols<<<(unsigned)((gt.cols + 255) / 256), 256, 0, st>>>(diff2, gt, counts2);
+    bs::launch_pdl(k_diff_cols, (unsigned)((gt.cols + 255) / 256), 256, 0, st, diff2, gt, counts2);
     BS_LAUNCH_CHECK();
   }
   BS_CUDA_TRY((exclusive_scan<uint32_t, uint32_t>(counts2, starts2, T, nullptr, partials2, nullptr, st)));
-  k_ranges<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(starts2, counts2, (int)T, tile_ranges, nullptr, 0);
+  bs::launch_pdl(k_ranges, (unsigned)((T + 255) / 256), 256, 0, st, starts2, counts2, (int)T, tile_ranges, nullptr, 0);
   BS_LAUNCH_CHECK();
   return BS_OK;
 }
@@ -947,32 +959,32 @@ static int bin_sort_impl(int64_t n_cap, const int32_t* n_visible, int32_t width,
     const int64_t waves = max(min_waves, (kk + slots * per_chunk - 1) / (slots * per_chunk));
     const int64_t nch = max((int64_t)1, min(max_chunks(gr), min(max((int64_t)1, slots * waves / nbands),
                                                                  (kk + 4095) / 4096)));
-    k_chunk_bounds<<<(unsigned)((n_cap + 255) / 256), 256, 0, st>>>(w.offs, w.touched_sorted, n_cap, n_visible, kd,
+    bs::launch_pdl(k_chunk_bounds, (unsigned)((n_cap + 255) / 256), 256, 0, st, w.offs, w.touched_sorted, n_cap, n_visible, kd,
                                                                    k_cap, (int)nch, w.chunk_first);
     BS_LAUNCH_CHECK();
-    k_chunk_hist<<<(unsigned)nch, kScThreads, diff_bytes + sizeof(int) * (size_t)(gr.rows + 1), st>>>(
+    bs::launch_pdl(k_chunk_hist, (unsigned)nch, kScThreads, diff_bytes + sizeof(int) * (size_t)(gr.rows + 1), st, 
         w.rects_sorted, w.chunk_first, gr, w.chunk_m, w.chunk_rowc, kd, k_cap);
     BS_LAUNCH_CHECK();
-    k_chunk_scan<<<(unsigned)((T + 31) / 32), kCsSeg * 32, 0, st>>>(w.chunk_m, w.starts, (int)T, (int)nch, kd, k_cap);
+    bs::launch_pdl(k_chunk_scan, (unsigned)((T + 31) / 32), kCsSeg * 32, 0, st, w.chunk_m, w.starts, (int)T, (int)nch, kd, k_cap);
     BS_LAUNCH_CHECK();
-    k_chunk_scatter<<<dim3((unsigned)nch, (unsigned)nbands), kScThreads, off_bytes, st>>>(
+    bs::launch_pdl(k_chunk_scatter, dim3((unsigned)nch, (unsigned)nbands), kScThreads, off_bytes, st, 
         w.chunk_m, w.chunk_rowc, w.chunk_first, w.rects_sorted, order, (int)T, gr.cols, gr.rows, point_list, kd, k_cap,
         band_rows);
     BS_LAUNCH_CHECK();
   } else if (k > 0) {
     const uint32_t* order = w.dv0;  // depth order (4 passes end in dv0)
     const int bits = bits_for(T);
-    k_mark_starts<<<(unsigned)((n_cap + 255) / 256), 256, 0, st>>>(w.offs, w.touched_sorted, n_cap, n_visible,
+    bs::launch_pdl(k_mark_starts, (unsigned)((n_cap + 255) / 256), 256, 0, st, w.offs, w.touched_sorted, n_cap, n_visible,
                                                                  w.block_j0);
     BS_LAUNCH_CHECK();
-    k_expand<<<(unsigned)((k + kExpandItems - 1) / kExpandItems), 256, 0, st>>>(
+    bs::launch_pdl(k_expand, (unsigned)((k + kExpandItems - 1) / kExpandItems), 256, 0, st, 
         w.offs, order, w.rects_sorted, n_cap, n_visible, k, gr.cols, w.block_j0, w.tk0, point_list);
     BS_LAUNCH_CHECK();
     bool alt = false;
     BS_CUDA_TRY(radix_sort_pairs(w.tk0, point_list, w.tk1, w.tv_alt, k, nullptr, bits, w.rws_k, &alt, st));
     if (alt) BS_CUDA_TRY(cudaMemcpyAsync(point_list, w.tv_alt, sizeof(uint32_t) * (size_t)k, cudaMemcpyDeviceToDevice, st));
   }
-  k_ranges<<<(unsigned)((T + 255) / 256), 256, 0, st>>>(w.starts, w.counts, (int)T, tile_ranges,
+  bs::launch_pdl(k_ranges, (unsigned)((T + 255) / 256), 256, 0, st, w.starts, w.counts, (int)T, tile_ranges,
                                                         n_cap > 0 ? kd : nullptr, k < 0 ? k_cap : k);
   BS_LAUNCH_CHECK();
   return BS_OK;

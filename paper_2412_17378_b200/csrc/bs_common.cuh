@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #include "splatsim_b200.h"
 
@@ -29,6 +32,36 @@
   } while (0)
 
 namespace bs {
+
+// Programmatic dependent launch (PDL): every kernel is launched with
+// programmatic stream serialization and waits (griddepcontrol.wait) for its
+// stream predecessor before touching memory, so a kernel's CTAs are
+// scheduled — and run up to the wait — while the previous kernel drains (in
+// streams and in the frame pipeline's CUDA graphs).  The wait is a no-op for
+// kernels launched without the attribute.  BS_PDL=0 disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("BS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Library-wide kernel launch counter (bs_kernel_launches()).
 void count_launches(unsigned long long n);

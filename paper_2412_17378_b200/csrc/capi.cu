@@ -71,6 +71,7 @@ extern "C" int bs_select_variant(const bs_tile_histogram* stats, int32_t width, 
 namespace bs {
 __global__ void k_select_variant(const bs_tile_histogram* __restrict__ stats, int pw, int ph, int sm_count,
                                  int32_t* __restrict__ variant) {
+  bs::pdl_wait();
   *variant = select_variant_formula(stats->total, stats->max, stats->tiles, pw, ph, sm_count);
 }
 }  // namespace bs
@@ -78,13 +79,14 @@ __global__ void k_select_variant(const bs_tile_histogram* __restrict__ stats, in
 extern "C" int bs_select_variant_device(const bs_tile_histogram* stats, int32_t width, int32_t height, int32_t pw,
                                         int32_t ph, int32_t sm_count, int32_t* variant, void* stream) {
   if (!stats || !variant || width <= 0 || height <= 0 || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
-  bs::k_select_variant<<<1, 1, 0, (cudaStream_t)stream>>>(stats, pw, ph, sm_count, variant);
+  bs::launch_pdl(bs::k_select_variant, 1, 1, 0, (cudaStream_t)stream, stats, pw, ph, sm_count, variant);
   BS_LAUNCH_CHECK();
   return BS_OK;
 }
 
 namespace bs {
 __global__ void k_publish_i64(const int64_t* __restrict__ src, int64_t* dst) {
+  bs::pdl_wait();
   *reinterpret_cast<volatile int64_t*>(dst) = *src;
   __threadfence_system();
 }
@@ -95,7 +97,7 @@ __global__ void k_publish_i64(const int64_t* __restrict__ src, int64_t* dst) {
 // download running on another stream (a cudaMemcpyAsync D2H would).
 extern "C" int bs_publish_i64(const int64_t* src_dev, int64_t* dst_host_mapped, void* stream) {
   if (!src_dev || !dst_host_mapped) return BS_ERR_INVALID_ARGUMENT;
-  bs::k_publish_i64<<<1, 1, 0, (cudaStream_t)stream>>>(src_dev, dst_host_mapped);
+  bs::launch_pdl(bs::k_publish_i64, 1, 1, 0, (cudaStream_t)stream, src_dev, dst_host_mapped);
   BS_LAUNCH_CHECK();
   return BS_OK;
 }

@@ -140,6 +140,7 @@ __device__ __forceinline__ CamDev cam_of(const bs_camera* __restrict__ camd, con
 __global__ void __launch_bounds__(256) k_project_flags(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam_,
                                                        const bs_camera* __restrict__ camd,
                                                        uint32_t* __restrict__ block_counts) {
+  bs::pdl_wait();
   const CamDev cam = cam_of(camd, cam_);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool vis = false;
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(256) k_project_write(const bs_gaussian3d* __re
                                                        const bs_camera* __restrict__ camd,
                                                        const uint32_t* __restrict__ block_offsets, float4* __restrict__ xyab,
                                                        float4* __restrict__ cop, float4* __restrict__ rgbr) {
+  bs::pdl_wait();
   const CamDev cam = cam_of(camd, cam_);
   __shared__ uint32_t warp_counts[8];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -217,6 +219,7 @@ __global__ void __launch_bounds__(256, 3) k_project_bin(const bs_gaussian3d* __r
                                                      uint32_t* __restrict__ dvals, int* __restrict__ diff,
                                                      int32_t* __restrict__ counts, Grid g2, int* __restrict__ diff2,
                                                      bool staged) {
+  bs::pdl_wait();
   extern __shared__ int s_diff[];
   const CamDev cam = cam_of(camd, cam_);
   const int stride = g.cols + 1;
@@ -373,7 +376,7 @@ cudaError_t launch_project_bin(const bs_gaussian3d* g3d, int64_t n, const bs_cam
         per_sm[slot] = per_sm[slot] < 1 ? 1 : (per_sm[slot] > 3 ? 3 : per_sm[slot]);  // each CTA flushes once
       }
       const int64_t grid = nb < (int64_t)sms * per_sm[slot] ? nb : (int64_t)sms * per_sm[slot];
-      kern<<<(unsigned)(grid > 0 ? grid : 1), 256, sm, st>>>(g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects,
+      bs::launch_pdl(kern, (unsigned)(grid > 0 ? grid : 1), 256, sm, st, g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects,
                                                              dkeys, dvals, diff, counts, gg2, diff2,
                                                              (reinterpret_cast<uintptr_t>(g3d) & 15) == 0);
       return cudaSuccess;
@@ -384,10 +387,10 @@ cudaError_t launch_project_bin(const bs_gaussian3d* g3d, int64_t n, const bs_cam
     else e = go(k_project_bin<true, true, false>);
     if (e != cudaSuccess) return e;
   } else if (g2) {
-    k_project_bin<false, true, false><<<(unsigned)(nb > 0 ? nb : 1), 256, 0, st>>>(
+    bs::launch_pdl(k_project_bin<false, true, false>, (unsigned)(nb > 0 ? nb : 1), 256, 0, st, 
         g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects, dkeys, dvals, diff, counts, gg2, diff2, false);
   } else {
-    k_project_bin<false, false, false><<<(unsigned)(nb > 0 ? nb : 1), 256, 0, st>>>(
+    bs::launch_pdl(k_project_bin<false, false, false>, (unsigned)(nb > 0 ? nb : 1), 256, 0, st, 
         g3d, n, c, camd, g, xyab, cop, rgbr, touched, rects, dkeys, dvals, diff, counts, gg2, diff2, false);
   }
   count_launches(1);
@@ -396,6 +399,7 @@ cudaError_t launch_project_bin(const bs_gaussian3d* g3d, int64_t n, const bs_cam
 
 __global__ void k_splats_from_g2d(const bs_gaussian2d* __restrict__ g2d, int64_t n, float4* __restrict__ xyab,
                                   float4* __restrict__ cop, float4* __restrict__ rgbr) {
+  bs::pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const bs_gaussian2d g = g2d[i];
@@ -406,6 +410,7 @@ __global__ void k_splats_from_g2d(const bs_gaussian2d* __restrict__ g2d, int64_t
 
 __global__ void k_splats_to_g2d(const float4* __restrict__ xyab, const float4* __restrict__ cop,
                                 const float4* __restrict__ rgbr, int64_t n, bs_gaussian2d* __restrict__ g2d) {
+  bs::pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float4 a = xyab[i], b = cop[i], c = rgbr[i];
@@ -452,12 +457,12 @@ static int preprocess_impl(const bs_gaussian3d* g3d, int64_t n, const bs_camera*
   uint32_t* counts = wc.take<uint32_t>((size_t)nb);
   uint32_t* partials = wc.take<uint32_t>((size_t)scan_num_blocks(nb));
   if (!wc.ok || !ws) return BS_ERR_WORKSPACE;
-  k_project_flags<<<(unsigned)nb, 256, 0, st>>>(g3d, n, c, cam ? nullptr : cam_dev, counts);
+  bs::launch_pdl(k_project_flags, (unsigned)nb, 256, 0, st, g3d, n, c, cam ? nullptr : cam_dev, counts);
   BS_LAUNCH_CHECK();
   // exclusive scan of block counts in place; grand total -> n_visible (u32 == i32 bits for n < 2^31)
   BS_CUDA_TRY((exclusive_scan<uint32_t, uint32_t>(counts, counts, nb, nullptr, partials,
                                                  reinterpret_cast<uint32_t*>(n_visible), st)));
-  k_project_write<<<(unsigned)nb, 256, 0, st>>>(g3d, n, c, cam ? nullptr : cam_dev, counts,
+  bs::launch_pdl(k_project_write, (unsigned)nb, 256, 0, st, g3d, n, c, cam ? nullptr : cam_dev, counts,
                                                 reinterpret_cast<float4*>(out.xyab), reinterpret_cast<float4*>(out.cop),
                                                 reinterpret_cast<float4*>(out.rgbr));
   BS_LAUNCH_CHECK();
@@ -479,7 +484,7 @@ extern "C" int bs_preprocess_devcam(const bs_gaussian3d* g3d, int64_t n, const b
 extern "C" int bs_splats_from_g2d(const bs_gaussian2d* g2d, int64_t n, bs_splats out, void* stream) {
   if (n < 0 || (n > 0 && (!g2d || !out.xyab || !out.cop || !out.rgbr))) return BS_ERR_INVALID_ARGUMENT;
   if (n == 0) return BS_OK;
-  k_splats_from_g2d<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+  bs::launch_pdl(k_splats_from_g2d, (unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream, 
       g2d, n, reinterpret_cast<float4*>(out.xyab), reinterpret_cast<float4*>(out.cop), reinterpret_cast<float4*>(out.rgbr));
   BS_LAUNCH_CHECK();
   return BS_OK;
@@ -488,7 +493,7 @@ extern "C" int bs_splats_from_g2d(const bs_gaussian2d* g2d, int64_t n, bs_splats
 extern "C" int bs_splats_to_g2d(bs_splats in, int64_t n, bs_gaussian2d* g2d, void* stream) {
   if (n < 0 || (n > 0 && (!g2d || !in.xyab || !in.cop || !in.rgbr))) return BS_ERR_INVALID_ARGUMENT;
   if (n == 0) return BS_OK;
-  k_splats_to_g2d<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+  bs::launch_pdl(k_splats_to_g2d, (unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream, 
       reinterpret_cast<const float4*>(in.xyab), reinterpret_cast<const float4*>(in.cop),
       reinterpret_cast<const float4*>(in.rgbr), n, g2d);
   BS_LAUNCH_CHECK();

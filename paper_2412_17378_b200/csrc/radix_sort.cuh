@@ -42,6 +42,7 @@ static __global__ void __launch_bounds__(kSortThreads) k_radix_hist(const uint32
                                                                     const int32_t* __restrict__ d_count, int shift,
                                                                     uint32_t mask, int64_t nb,
                                                                     uint32_t* __restrict__ hist) {
+  bs::pdl_wait();
   __shared__ uint32_t cnt[kSortWarps][kSortBuckets];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < kSortWarps * kSortBuckets; i += kSortThreads) (&cnt[0][0])[i] = 0;
@@ -81,6 +82,7 @@ static __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(const uin
                                                                        uint32_t mask, int64_t nb,
                                                                        const uint32_t* __restrict__ offsets,
                                                                        RadixGather gat) {
+  bs::pdl_wait();
   __shared__ uint16_t wcnt[kSortWarps][kSortBuckets];
   __shared__ uint32_t local_start[kSortBuckets];
   __shared__ uint32_t digit_base[kSortBuckets];
@@ -197,14 +199,14 @@ inline cudaError_t radix_sort_pairs(uint32_t* k0, uint32_t* v0, uint32_t* k1, ui
     const int bits = (key_bits - shift + (passes - p) - 1) / (passes - p);  // balanced split
     const uint32_t mask = (1u << bits) - 1u;
     const int64_t buckets = (int64_t)mask + 1;
-    k_radix_hist<<<(unsigned)nb, kSortThreads, 0, st>>>(ki, n_cap, d_count, shift, mask, nb, w.hist);
+    bs::launch_pdl(k_radix_hist, (unsigned)nb, kSortThreads, 0, st, ki, n_cap, d_count, shift, mask, nb, w.hist);
     cudaError_t e = exclusive_scan<uint32_t, uint32_t>(w.hist, w.hist, buckets * nb, nullptr, w.partials, nullptr, st);
     if (e != cudaSuccess) return e;
     if (gather && p == passes - 1)
-      k_radix_scatter<true><<<(unsigned)nb, kSortThreads, 0, st>>>(ki, vi, ko, vo, n_cap, d_count, shift, mask, nb,
+      bs::launch_pdl(k_radix_scatter<true>, (unsigned)nb, kSortThreads, 0, st, ki, vi, ko, vo, n_cap, d_count, shift, mask, nb,
                                                                    w.hist, *gather);
     else
-      k_radix_scatter<false><<<(unsigned)nb, kSortThreads, 0, st>>>(ki, vi, ko, vo, n_cap, d_count, shift, mask, nb,
+      bs::launch_pdl(k_radix_scatter<false>, (unsigned)nb, kSortThreads, 0, st, ki, vi, ko, vo, n_cap, d_count, shift, mask, nb,
                                                                     w.hist, RadixGather{});
     count_launches(2);
     uint32_t* t;

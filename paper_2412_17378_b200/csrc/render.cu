@@ -337,6 +337,7 @@ __device__ __forceinline__ void pixelwise_tile(const RArgs& A, int tile, float4*
 
 template <int MODE, bool STAGE_COLOR, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_render_pixelwise(RArgs A) {
+  bs::pdl_wait();
   if (gated_out(A, STAGE_COLOR ? BS_SHARED_MEM_OPT : BS_NAIVE)) return;
   constexpr int CHUNK = PwChunk<MODE, STAGE_COLOR, BLOCK>::value;
   __shared__ float4 s_xyab[CHUNK];
@@ -357,6 +358,7 @@ __global__ void __launch_bounds__(BLOCK) k_render_pixelwise(RArgs A) {
 // Paper Alg. 1 (with the exit test fixed to >=).
 template <int MODE, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_render_dynamic(RArgs A) {
+  bs::pdl_wait();
   __shared__ float4 s_xyab[BLOCK];
   __shared__ float4 s_cop[BLOCK];
   __shared__ uint32_t s_id[BLOCK];
@@ -501,6 +503,7 @@ __device__ __forceinline__ void gaussianwise_task(const RArgs& A, int tile, int 
 
 template <int MODE>
 __global__ void __launch_bounds__(kFgThreads) k_render_gaussianwise(RArgs A) {
+  bs::pdl_wait();
   __shared__ float4 s_xyab[kFgThreads];
   __shared__ float4 s_cop[kFgThreads];
   __shared__ float4 s_rgb[kFgThreads];
@@ -543,6 +546,7 @@ constexpr size_t kGwDynSmem = sizeof(float) * kGwWarps * 2 * 32 * 33;  // per-wa
 
 template <int MODE>
 __global__ void __launch_bounds__(kGwThreads) k_render_gw(RArgs A) {
+  bs::pdl_wait();
   __shared__ float4 s_xyab[kGwChunk];
   __shared__ float4 s_cop[kGwChunk];
   __shared__ double2 s_rg[kGwChunk];  // (r, g) widened once per staged entry
@@ -849,6 +853,7 @@ constexpr size_t kGcDynSmem = sizeof(float) * kGcWarps * 32 * 33;  // alpha scra
 
 template <int MODE>
 __global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs) {
+  bs::pdl_wait();
   extern __shared__ float s_gc_dyn[];
   __shared__ float4 s_geo[kGcWarps][2][64];    // survivors' xyab, cop (a 2-batch queue)
   __shared__ double2 s_col[kGcWarps][2][64];   // survivors' (r, g), (b, depth) widened once
@@ -1142,6 +1147,7 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
 // uncapped 64-register kernel is best.
 template <int MODE, int LM, int MINB>
 __global__ void __launch_bounds__(kFineThreads, MINB) k_render_fine(RArgs A, int subs) {
+  bs::pdl_wait();
   __shared__ float4 s_rec[kFineWarps][4][32];
   __shared__ int s_k[kFineWarps][32];
   __shared__ unsigned long long s_tab[32];
@@ -1169,6 +1175,7 @@ __global__ void __launch_bounds__(kFineThreads, MINB) k_render_fine(RArgs A, int
 // for all 8 warps — the tail of the heaviest tiles is spread over all SMs.
 template <int MODE>
 __global__ void __launch_bounds__(kFineThreads) k_render_donated(RArgs A) {
+  bs::pdl_wait();
   __shared__ float4 s_xyab[kFineThreads];
   __shared__ float4 s_cop[kFineThreads];
   __shared__ float4 s_rgb[kFineThreads];
@@ -1431,6 +1438,7 @@ __device__ __forceinline__ void warp_task_bwd(const RArgs& A, const BwdArgs& G, 
 
 template <int MODE, int LM>
 __global__ void __launch_bounds__(kFineThreads) k_render_backward(RArgs A, BwdArgs G, int subs) {
+  bs::pdl_wait();
   __shared__ float4 s_rec[kFineWarps][3][32];
   __shared__ uint32_t s_id[kFineWarps][32];
   __shared__ unsigned long long s_tab[32];
@@ -1452,6 +1460,7 @@ __global__ void __launch_bounds__(kFineThreads) k_render_backward(RArgs A, BwdAr
 __global__ void k_frame_work(const int32_t* __restrict__ term, const int32_t* __restrict__ contrib,
                              const uint32_t* __restrict__ ranges, int W, int H, int pw, int ph, int cols,
                              unsigned long long* __restrict__ out) {
+  bs::pdl_wait();
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long e = 0, c = 0;
   if (p < (int64_t)W * H) {
@@ -1570,8 +1579,8 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, int fin
       const int grid = A.gate ? max(1, min(T, sms * 8)) : T;
 #define BS_PW_CASE(B)                                                                   \
   if (block_pixels <= B) {                                                              \
-    if (smem) k_render_pixelwise<MODE, true, B><<<grid, B, 0, st>>>(A);                 \
-    else k_render_pixelwise<MODE, false, B><<<grid, B, 0, st>>>(A);                     \
+    if (smem) bs::launch_pdl(k_render_pixelwise<MODE, true, B>, grid, B, 0, st, A);                 \
+    else bs::launch_pdl(k_render_pixelwise<MODE, false, B>, grid, B, 0, st, A);                     \
     break;                                                                              \
   }
       BS_PW_CASE(64) BS_PW_CASE(128) BS_PW_CASE(256) BS_PW_CASE(512) BS_PW_CASE(1024)
@@ -1582,7 +1591,7 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, int fin
 #define BS_DYN_CASE(I, B)                                                      \
   if (block_pixels <= B) {                                                     \
     const int grid = max(1, min(T, sms * max(1, df->dyn_per_sm[MODE][I])));   \
-    k_render_dynamic<MODE, B><<<grid, B, 0, st>>>(A);                          \
+    bs::launch_pdl(k_render_dynamic<MODE, B>, grid, B, 0, st, A);                          \
     break;                                                                     \
   }
       BS_DYN_CASE(0, 64) BS_DYN_CASE(1, 128) BS_DYN_CASE(2, 256) BS_DYN_CASE(3, 512) BS_DYN_CASE(4, 1024)
@@ -1591,12 +1600,12 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, int fin
     }
     case BS_GAUSSIAN_WISE:
       if (fine_tuning().gw_windowed && block_pixels <= kGwThreads)  // (dynamic smem opt-in: dev_facts)
-        k_render_gw<MODE><<<T, kGwThreads, kGwDynSmem, st>>>(A);
+        bs::launch_pdl(k_render_gw<MODE>, T, kGwThreads, kGwDynSmem, st, A);
       else if (!fine_tuning().gw_windowed)
-        k_render_gw_cull<MODE><<<T, kGcThreads, kGcDynSmem, st>>>(
+        bs::launch_pdl(k_render_gw_cull<MODE>, T, kGcThreads, kGcDynSmem, st, 
             A, ((A.pw + kSubW - 1) / kSubW) * ((A.ph + kSubH - 1) / kSubH));
       else  // larger patches: 4-warp tasks, 4 pixels at a time
-        k_render_gaussianwise<MODE><<<T, kFgThreads, 0, st>>>(A);
+        bs::launch_pdl(k_render_gaussianwise<MODE>, T, kFgThreads, 0, st, A);
       break;
     case BS_FINE_GRAINED_COMBINED: {
       const FineTuning& ft = fine_tuning();
@@ -1619,15 +1628,15 @@ static int launch_variant(int variant, const RArgs& A, int block_pixels, int fin
       B.donate_min_remain = ft.donate_min_remain;
       B.stragglers = A.sup ? ft.stragglers_super : ft.stragglers;
       if (lm == kListSuper) {
-        if (wide) k_render_fine<MODE, kListSuper, 3><<<grid, kFineThreads, 0, st>>>(B, subs);
-        else k_render_fine<MODE, kListSuper, 4><<<grid, kFineThreads, 0, st>>>(B, subs);
+        if (wide) bs::launch_pdl(k_render_fine<MODE, kListSuper, 3>, grid, kFineThreads, 0, st, B, subs);
+        else bs::launch_pdl(k_render_fine<MODE, kListSuper, 4>, grid, kFineThreads, 0, st, B, subs);
       } else {
-        if (wide) k_render_fine<MODE, kListTile, 3><<<grid, kFineThreads, 0, st>>>(B, subs);
-        else k_render_fine<MODE, kListTile, 4><<<grid, kFineThreads, 0, st>>>(B, subs);
+        if (wide) bs::launch_pdl(k_render_fine<MODE, kListTile, 3>, grid, kFineThreads, 0, st, B, subs);
+        else bs::launch_pdl(k_render_fine<MODE, kListTile, 4>, grid, kFineThreads, 0, st, B, subs);
       }
       BS_LAUNCH_CHECK();
       if (!B.donate) return BS_OK;
-      k_render_donated<MODE><<<sms * max(1, df->donated_per_sm[MODE]), kFineThreads, 0, st>>>(B);
+      bs::launch_pdl(k_render_donated<MODE>, sms * max(1, df->donated_per_sm[MODE]), kFineThreads, 0, st, B);
       break;
     }
     default:
@@ -1780,7 +1789,7 @@ extern "C" int bs_render_backward(int alpha_mode, bs_splats g, const uint32_t* p
   DevFacts* df = nullptr;
   TRY_BS(dev_facts(&df));
   const int grid = (int)max((int64_t)1, min((T * subs + kFineWarps - 1) / kFineWarps, (int64_t)df->sms * 4));
-#define BS_BWD(M, L) k_render_backward<M, L><<<grid, kFineThreads, 0, st>>>(A, G, subs)
+#define BS_BWD(M, L) bs::launch_pdl(k_render_backward<M, L>, grid, kFineThreads, 0, st, A, G, subs)
   if (alpha_mode == BS_ALPHA_EXACT) {
     if (super_lists) BS_BWD(BS_ALPHA_EXACT, kListSuper);
     else BS_BWD(BS_ALPHA_EXACT, kListTile);
@@ -1796,6 +1805,7 @@ extern "C" int bs_render_backward(int alpha_mode, bs_splats g, const uint32_t* p
 namespace bs {
 __global__ void k_super_tile_ranges(const uint32_t* __restrict__ sranges, int cols, int rows, int scols,
                                     uint32_t* __restrict__ out) {
+  bs::pdl_wait();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= cols * rows) return;
   const int st = ((t / cols) >> 1) * scols + ((t % cols) >> 1);
@@ -1811,7 +1821,7 @@ extern "C" int bs_super_tile_ranges(const uint32_t* super_ranges, int32_t width,
   const int scols = (width + 2 * pw - 1) / (2 * pw);
   const int T = cols * rows;
   if (T > 0)
-    bs::k_super_tile_ranges<<<(T + 255) / 256, 256, 0, (cudaStream_t)stream>>>(super_ranges, cols, rows, scols,
+    bs::launch_pdl(bs::k_super_tile_ranges, (T + 255) / 256, 256, 0, (cudaStream_t)stream, super_ranges, cols, rows, scols,
                                                                               tile_ranges);
   BS_LAUNCH_CHECK();
   return BS_OK;
@@ -1835,6 +1845,7 @@ __device__ __forceinline__ float render_expf(float x, int mode, const ExpK& ek, 
 }
 
 __global__ void k_test_expf(const float* __restrict__ x, float* __restrict__ y, int64_t n, int mode) {
+  bs::pdl_wait();
   __shared__ unsigned long long s_tab[32];
   load_tab(s_tab);
   __syncthreads();
@@ -1845,6 +1856,7 @@ __global__ void k_test_expf(const float* __restrict__ x, float* __restrict__ y, 
 
 // y[i] = exp(float with bit pattern first_bits + i)
 __global__ void k_test_expf_range(uint32_t first_bits, float* __restrict__ y, int64_t n, int mode) {
+  bs::pdl_wait();
   __shared__ unsigned long long s_tab[32];
   load_tab(s_tab);
   __syncthreads();
@@ -1858,7 +1870,7 @@ extern "C" int bs_test_expf(const float* x, float* y, int64_t n, int alpha_mode,
   if (n < 0 || (n > 0 && (!x || !y))) return BS_ERR_INVALID_ARGUMENT;
   if (n == 0) return BS_OK;
   const int64_t blocks = min((n + 255) / 256, (int64_t)148 * 16);
-  k_test_expf<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, y, n, alpha_mode);
+  bs::launch_pdl(k_test_expf, (unsigned)blocks, 256, 0, (cudaStream_t)stream, x, y, n, alpha_mode);
   BS_LAUNCH_CHECK();
   return BS_OK;
 }
@@ -1867,7 +1879,7 @@ extern "C" int bs_test_expf_range(uint32_t first_bits, int64_t n, float* y, int 
   if (n < 0 || (n > 0 && !y) || (uint64_t)first_bits + (uint64_t)n > 0x100000000ull) return BS_ERR_INVALID_ARGUMENT;
   if (n == 0) return BS_OK;
   const int64_t blocks = min((n + 255) / 256, (int64_t)148 * 16);
-  k_test_expf_range<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(first_bits, y, n, alpha_mode);
+  bs::launch_pdl(k_test_expf_range, (unsigned)blocks, 256, 0, (cudaStream_t)stream, first_bits, y, n, alpha_mode);
   BS_LAUNCH_CHECK();
   return BS_OK;
 }
@@ -1879,7 +1891,7 @@ extern "C" int bs_frame_work(const int32_t* term, const int32_t* contrib, const 
   cudaStream_t st = (cudaStream_t)stream;
   BS_CUDA_TRY(cudaMemsetAsync(evaluated_committed, 0, 2 * sizeof(uint64_t), st));
   const int64_t P = (int64_t)width * height;
-  k_frame_work<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(term, contrib, tile_ranges, width, height, pw, ph,
+  bs::launch_pdl(k_frame_work, (unsigned)((P + 255) / 256), 256, 0, st, term, contrib, tile_ranges, width, height, pw, ph,
                                                             (width + pw - 1) / pw,
                                                             reinterpret_cast<unsigned long long*>(evaluated_committed));
   BS_LAUNCH_CHECK();

@@ -64,6 +64,7 @@ template <typename TIn, typename TOut>
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const TIn* __restrict__ in, int64_t n_cap,
                                                               const int32_t* __restrict__ d_count,
                                                               TOut* __restrict__ partials) {
+  bs::pdl_wait();
   const int64_t n = d_count ? (int64_t)*d_count : n_cap;
   const int64_t base = (int64_t)blockIdx.x * kScanTile;
   TOut s = 0;
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_downsweep(const TIn* __re
                                                                  const int32_t* __restrict__ d_count,
                                                                  const TOut* __restrict__ partials,
                                                                  TOut* __restrict__ out, TOut* __restrict__ total_out) {
+  bs::pdl_wait();
   __shared__ TOut s_prefix;
   {
     TOut p = 0;
@@ -125,6 +127,7 @@ template <typename TIn, typename TOut>
 __global__ void __launch_bounds__(1024) k_scan_single(const TIn* __restrict__ in, TOut* __restrict__ out,
                                                       int64_t n_cap, const int32_t* __restrict__ d_count,
                                                       TOut* __restrict__ total_out) {
+  bs::pdl_wait();
   const int64_t n = d_count ? min((int64_t)*d_count, n_cap) : n_cap;
   const int64_t per = (n_cap + 1023) / 1024;
   const int64_t b = (int64_t)threadIdx.x * per, e = min(b + per, n_cap);
@@ -150,12 +153,12 @@ inline cudaError_t exclusive_scan(const TIn* in, TOut* out, int64_t n_cap, const
     return cudaSuccess;
   }
   if (n_cap <= kScanSingleMax) {
-    k_scan_single<TIn, TOut><<<1, 1024, 0, st>>>(in, out, n_cap, d_count, total);
+    bs::launch_pdl(k_scan_single<TIn, TOut>, 1, 1024, 0, st, in, out, n_cap, d_count, total);
     count_launches(1);
     return cudaPeekAtLastError();
   }
-  k_scan_reduce<TIn, TOut><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_cap, d_count, partials);
-  k_scan_downsweep<TIn, TOut><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_cap, d_count, partials, out, total);
+  bs::launch_pdl(k_scan_reduce<TIn, TOut>, (unsigned)nb, kScanThreads, 0, st, in, n_cap, d_count, partials);
+  bs::launch_pdl(k_scan_downsweep<TIn, TOut>, (unsigned)nb, kScanThreads, 0, st, in, n_cap, d_count, partials, out, total);
   count_launches(2);
   return cudaPeekAtLastError();
 }

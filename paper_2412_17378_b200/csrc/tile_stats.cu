@@ -17,6 +17,7 @@ namespace bs {
 
 __global__ void k_counts(const uint32_t* __restrict__ ranges, int T, uint32_t* __restrict__ counts,
                          uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  bs::pdl_wait();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   const uint32_t c = ranges[2 * t + 1] - ranges[2 * t];
@@ -28,6 +29,7 @@ __global__ void k_counts(const uint32_t* __restrict__ ranges, int T, uint32_t* _
 __global__ void __launch_bounds__(1024) k_stats_finish(const uint32_t* __restrict__ counts,
                                                        const uint32_t* __restrict__ desc_order, int T,
                                                        bs_tile_histogram* __restrict__ out) {
+  bs::pdl_wait();
   unsigned long long sum = 0, nonempty = 0;
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     const uint32_t c = counts[t];
@@ -83,6 +85,7 @@ struct SelectOut {  // optional: the per-frame variant choice from the same stat
 __global__ void __launch_bounds__(1024) k_tile_order(const uint32_t* __restrict__ ranges, int T,
                                                      uint32_t* __restrict__ order_out,
                                                      bs_tile_histogram* __restrict__ out, SelectOut sel) {
+  bs::pdl_wait();
   __shared__ uint32_t s_cnt[32][kOrderBuckets];  // (warp, bucket) counts, then bases
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < 32 * kOrderBuckets; i += 1024) (&s_cnt[0][0])[i] = 0;
@@ -189,16 +192,16 @@ extern "C" int bs_tile_stats(const uint32_t* tile_ranges, int32_t tiles, bs_tile
   RadixWs rw;
   stats_ws_layout(c, tiles, &k0, &v0, &k1, &v1, &cnt, &rw);
   if (tiles > 0) {
-    k_counts<<<(tiles + 255) / 256, 256, 0, st>>>(tile_ranges, tiles, cnt, k0, v0);
+    bs::launch_pdl(k_counts, (tiles + 255) / 256, 256, 0, st, tile_ranges, tiles, cnt, k0, v0);
     BS_LAUNCH_CHECK();
     bool alt = false;
     BS_CUDA_TRY(radix_sort_pairs(k0, v0, k1, v1, tiles, nullptr, 32, rw, &alt, st));
     const uint32_t* order = alt ? v1 : v0;
     if (counts) BS_CUDA_TRY(cudaMemcpyAsync(counts, cnt, sizeof(uint32_t) * tiles, cudaMemcpyDeviceToDevice, st));
     if (task_order) BS_CUDA_TRY(cudaMemcpyAsync(task_order, order, sizeof(uint32_t) * tiles, cudaMemcpyDeviceToDevice, st));
-    k_stats_finish<<<1, 1024, 0, st>>>(cnt, order, tiles, stats);
+    bs::launch_pdl(k_stats_finish, 1, 1024, 0, st, cnt, order, tiles, stats);
   } else {
-    k_stats_finish<<<1, 1024, 0, st>>>(cnt, nullptr, 0, stats);
+    bs::launch_pdl(k_stats_finish, 1, 1024, 0, st, cnt, nullptr, 0, stats);
   }
   BS_LAUNCH_CHECK();
   return BS_OK;
@@ -208,7 +211,7 @@ extern "C" int bs_tile_order(const uint32_t* tile_ranges, int32_t tiles, bs_tile
                              uint32_t* task_order, void* stream) {
   if (tiles < 0 || !stats || !task_order || (tiles > 0 && !tile_ranges)) return BS_ERR_INVALID_ARGUMENT;
   if (tiles > kOrderMaxTiles) return BS_ERR_UNSUPPORTED;
-  k_tile_order<<<1, 1024, 0, (cudaStream_t)stream>>>(tile_ranges, tiles, task_order, stats,
+  bs::launch_pdl(k_tile_order, 1, 1024, 0, (cudaStream_t)stream, tile_ranges, tiles, task_order, stats,
                                                      SelectOut{nullptr, 0, 0, 0});
   BS_LAUNCH_CHECK();
   return BS_OK;
@@ -222,7 +225,7 @@ extern "C" int bs_tile_order_select(const uint32_t* tile_ranges, int32_t tiles, 
   if (tiles < 0 || !stats || !task_order || !variant || (tiles > 0 && !tile_ranges)) return BS_ERR_INVALID_ARGUMENT;
   if (width <= 0 || height <= 0 || pw <= 0 || ph <= 0) return BS_ERR_INVALID_ARGUMENT;
   if (tiles > kOrderMaxTiles) return BS_ERR_UNSUPPORTED;
-  k_tile_order<<<1, 1024, 0, (cudaStream_t)stream>>>(tile_ranges, tiles, task_order, stats,
+  bs::launch_pdl(k_tile_order, 1, 1024, 0, (cudaStream_t)stream, tile_ranges, tiles, task_order, stats,
                                                      SelectOut{variant, pw, ph, sm_count});
   BS_LAUNCH_CHECK();
   return BS_OK;
