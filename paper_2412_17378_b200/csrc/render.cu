@@ -865,7 +865,9 @@ __global__ void __launch_bounds__(kGcThreads) k_render_gw_cull(RArgs A, int subs
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lt = lanemask_lt();
-  const int tile = blockIdx.x;
+  // the static grid in LPT order when the caller passes one (the longest
+  // lists start first; the heavy tiles' CTAs no longer form the tail)
+  const int tile = A.task_order ? (int)A.task_order[blockIdx.x] : (int)blockIdx.x;
   const int tx = tile % A.cols, ty = tile / A.cols;
   const int nsx = (A.pw + kSubW - 1) / kSubW;
   const uint32_t start = A.ranges[2 * tile], end = A.ranges[2 * tile + 1];
