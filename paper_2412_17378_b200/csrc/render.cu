@@ -351,8 +351,13 @@ __global__ void __launch_bounds__(BLOCK) k_render_pixelwise(RArgs A) {
   // one tile per CTA, or (a gated auto-mode candidate, launched with fewer
   // CTAs so that not being selected costs little) tiles in grid stride —
   // the next tile's first chunk barrier orders the shared-memory reuse
-  for (int tile = blockIdx.x; tile < A.T; tile += gridDim.x)
+  // SharedMemOpt (the selector's fallback) takes the LPT tile order when
+  // given (heavy tiles first); Naive keeps the plain grid — the paper's
+  // baseline kernel
+  for (int i = blockIdx.x; i < A.T; i += gridDim.x) {
+    const int tile = (STAGE_COLOR && A.task_order) ? (int)A.task_order[i] : i;
     pixelwise_tile<MODE, STAGE_COLOR, BLOCK>(A, tile, s_xyab, s_cop, s_rgb, s_id, s_mem, make_expk(s_tab));
+  }
 }
 
 // Paper Alg. 1 (with the exit test fixed to >=).
