@@ -376,8 +376,11 @@ __global__ void __launch_bounds__(BLOCK) k_render_dynamic(RArgs A) {
     __syncthreads();
     if (threadIdx.x == 0) s_tile = (int)atomicAdd(A.queue, 1u);
     __syncthreads();
-    const int tile = s_tile;
-    if (tile >= A.T) return;
+    const int ticket = s_tile;
+    if (ticket >= A.T) return;
+    // the queue hands tiles out in LPT order when given (paper Alg. 1 uses
+    // index order; longest lists first keeps the heavy tiles off the tail)
+    const int tile = A.task_order ? (int)A.task_order[ticket] : ticket;
     pixelwise_tile<MODE, false, BLOCK>(A, tile, s_xyab, s_cop, nullptr, s_id, nullptr, ek);
   }
 }
