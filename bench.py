@@ -319,6 +319,13 @@ def run_reference(args) -> None:
     print(json.dumps(out), flush=True)
 
 
+def auto_streams(W: int, H: int) -> int:
+    """Frame contexts for --streams 0: small frames are launch-latency-bound
+    (more frames in flight fill the GPU), large ones are render-bound (a
+    fifth+ context only adds contention)."""
+    return 8 if W * H < (1 << 20) else 4
+
+
 def metric_name(cfg: str) -> str:
     return "fwd render views/s (1080p, 1M Gaussians; full forward per view)" if cfg == "c2" else \
         f"fwd render views/s ({cfg})"
@@ -345,7 +352,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sync-frames", action="store_true", help="wait for K inside each frame (no async mode)")
     ap.add_argument("--no-graphs", action="store_true", help="launch every kernel instead of replaying a CUDA graph")
-    ap.add_argument("--streams", type=int, default=4, help="frame contexts on separate streams (views round-robin)")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="frame contexts on separate streams (views round-robin); 0 = auto: 8 for frames below "
+                         "1 Mpixel (launch-latency-bound: C1 12.1k -> 14.5k views/s), else 4 (C2: 8 measured "
+                         "7 %% slower)")
     ap.add_argument("--fine-ctas", type=int, default=0,
                     help="FineGrainedCombined CTAs per SM per context when streams > 1 (0 = as many as fit; "
                          "tools/sweep_occupancy.sh: uncapped is best with the r2 kernels)")
@@ -396,7 +406,8 @@ def main():
     # re-rendered), CUDA-graph replay; --streams contexts on their own streams
     # take the views round-robin, so view i+1's preprocess / binning overlaps
     # view i's render
-    ns = max(1, args.streams)
+    ns = max(1, args.streams) if args.streams > 0 else auto_streams(W, H)
+    args.streams = ns
     fine_ctas = args.fine_ctas if ns > 1 else 0  # leave SM room for the other contexts' kernels during a render
     streams = [torch.cuda.Stream(device=dev) for _ in range(ns)]
     fps = []
@@ -772,12 +783,13 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     # copies inside the timed region.  Batch mode (the timed steps' shape):
     # each step is one bs_render_views_host call — the scene uploaded once
     # from pinned host memory, the step's 64 views rendered round-robin over
-    # --streams contexts (async frame bodies), every view's six output planes
+    # min(--streams, 4) contexts (async frame bodies; C1 with 8 host-buffer
+    # contexts measured 10.2k vs 11.3k views/s with 4), every view's six output planes
     # downloaded into its own pinned host buffers; --batch 0: one
     # bs_render_frame_host_async call (scene upload + frame + download) per
     # view.  Wall clock from the first enqueue to bs_context_sync on every
     # context.
-    nctx = max(1, args.streams)
+    nctx = max(1, min(args.streams, 4))
     ctxs = []
     for _ in range(nctx):
         cx = C.c_void_p()
