@@ -1006,6 +1006,9 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
   const float sx = __fadd_rn((float)px, 0.5f), sy = __fadd_rn((float)py, 0.5f);
   const float rx0 = (float)ox + 0.5f, rx1 = (float)ox + (kSubW - 0.5f), ry0 = (float)oy + 0.5f,
               ry1 = (float)oy + (kSubH - 0.5f);
+  // the pixel index replaces (px, py) from here on: with them dead, sx / sy
+  // are held instead of being re-derived (I2F + add) at every step
+  const uint32_t pix = (uint32_t)py * (uint32_t)A.W + (uint32_t)px;
   const uint32_t start = A.ranges[2 * tile], end = A.ranges[2 * tile + 1];
 
   bool done = !inside, donated = false, donate_now = false;
@@ -1062,7 +1065,7 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
       slot0 = __shfl_sync(kFull, slot0, 0);
       if (!done) {
         Donation& d = A.donate[slot0 + __popc(live & lanemask_lt())];
-        d.pixel = (uint32_t)py * (uint32_t)A.W + (uint32_t)px;
+        d.pixel = pix;
         d.start = start;
         d.from = base;
         d.end = end;
@@ -1146,7 +1149,7 @@ __device__ __forceinline__ void warp_task(const RArgs& A, int tile, int sub, flo
     if (LM != kListTile) mpos += (uint32_t)__popc(mm);
     base = nb;
   }
-  if (inside && !donated) acc.finish(A, (size_t)py * A.W + px, t, contrib, term);
+  if (inside && !donated) acc.finish(A, (size_t)pix, t, contrib, term);
 }
 
 // MINB: resident CTAs per SM the register budget is sized for — 4 (64
