@@ -210,8 +210,10 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// (256, 2): 124 registers, no spills, 2 CTAs/SM — the 3-CTA budget (80
+// registers) spilled 12-36 bytes and measured ~1 us slower per C2 frame
 template <bool SMEM_DIFF, bool DIFF2, bool SMEM2>
-__global__ void __launch_bounds__(256, 3) k_project_bin(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam_,
+__global__ void __launch_bounds__(256, 2) k_project_bin(const bs_gaussian3d* __restrict__ g3d, int64_t n, CamDev cam_,
                                                      const bs_camera* __restrict__ camd, Grid g,
                                                      float4* __restrict__ xyab, float4* __restrict__ cop,
                                                      float4* __restrict__ rgbr, uint32_t* __restrict__ touched,
