@@ -44,3 +44,26 @@ for _ in range(20):
 e.record(stream)
 torch.cuda.synchronize()
 print(f"per-call events (synced): median {np.median(per):.4f} ms; 20 back-to-back: {a.elapsed_time(e) / 20:.4f} ms/call")
+
+# backward render on the same frame (random dL; grads accumulate, zeroed once)
+if os.environ.get("DIAG_BWD", "1") == "1":
+    g = torch.Generator(device="cuda").manual_seed(3)
+    P = W * H
+    dl = (torch.rand(3 * P, device="cuda", generator=g) - 0.5, torch.rand(P, device="cuda", generator=g) - 0.5,
+          torch.rand(P, device="cuda", generator=g) - 0.5)
+    grads = api.SplatGrads.zeros(s.n_cap, "cuda")
+
+    def bcall():
+        api.render_backward(s, b, frame, W, H, 16, 16, dl[0], dl[1], dl[2], (0, 0, 0), N.ALPHA_EXACT, st.task_order,
+                            grads, pipe.render_ws)
+
+    for _ in range(3):
+        bcall()
+    torch.cuda.synchronize()
+    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(10):
+        bcall()
+    e.record(stream)
+    torch.cuda.synchronize()
+    print(f"backward: {a.elapsed_time(e) / 10:.4f} ms/call")

@@ -9,7 +9,7 @@ OUT=gpurun_out/$TAG; mkdir -p $OUT
 LIB=paper_2412_17378_b200/lib/libsplatsim_b200.so
 for r in 1 2; do for v in $NAMES; do
   cp ab_libs/$v.so $LIB
-  echo "$v render: $(timeout 300 python tools/diag_render_time.py 2>> $OUT/err.log | tail -1)" >> $OUT/ab.txt
+  echo "$v render: $(timeout 300 python tools/diag_render_time.py 2>> $OUT/err.log | tail -2 | tr "\n" " ")" >> $OUT/ab.txt
   timeout 600 python bench.py --steps 10 --warmup 3 --no-extras --no-cpu-baseline > $OUT/b_${v}_$r.json 2>> $OUT/err.log
   python - "$OUT/b_${v}_$r.json" "$v" >> $OUT/ab.txt <<'PY'
 import json, sys
