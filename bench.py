@@ -704,9 +704,15 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
     t_api_s = t_s
     if sup.value:
         t_s = float(np.mean(t_fp)) / 1e3
+    # the lower bound: SURVEY 8d's terms with the HBM term over the bytes
+    # blending must read (the consumed list prefixes); the formula as
+    # written (44 B per tile instance K) is reported beside it — it exceeds
+    # the measured time when list tails lie past every pixel's stop (C4)
+    t_roof_survey = t_roof
+    t_roof = max(ops / fp32_peak, E / mufu_peak, bytes_prefix / hbm_peak)
     api_view = {"kernel": f"render {api.variant_name(vsel)} ({mname}) on the reference's pw x ph TileBinning "
                           "(bs_render_forward, the API path)", "t_ms": t_api_s * 1e3,
-                "frac": bytes_alg / t_api_s / hbm_peak, "t_roof_frac": t_roof / t_api_s, "traffic": traffic}
+                "frac": ops / t_api_s / fp32_peak, "t_roof_frac": t_roof / t_api_s, "traffic": traffic}
     if sup.value:
         traffic = (load_counters().get(f"{args.config}_{api.variant_name(vsel)}_{mname}_super") or {}).get(
             "dram_bytes")
@@ -759,7 +765,10 @@ def rank0_extras(args, api, N, torch, g3d, g3d_dev, cams, fp, W, H, pw, ph, n, m
         **head,
         traffic=measured.get("dram_bytes", traffic), measured=measured,
         t_roof_ms=t_roof * 1e3, t_roof_frac=t_roof / t_s,
-        t_roof_def="SURVEY 8d: max(16E+8C / FP32 peak, E / MUFU peak, (44K+32P) / HBM peak)",
+        t_roof_def=("max(16E+8C / FP32 peak, E / MUFU peak, consumed-prefix bytes / HBM peak): SURVEY 8d's terms, "
+                    "the HBM term over the bytes blending must read"),
+        t_roof_survey_ms=t_roof_survey * 1e3, t_roof_survey_frac=t_roof_survey / t_s,
+        t_roof_survey_def="SURVEY 8d as written: max(16E+8C / FP32 peak, E / MUFU peak, (44K+32P) / HBM peak)",
         api_kernel_view=api_view, peak_source=hbm_src,
         hbm_view={"achieved": bytes_alg / t_s / 1e9, "peak": hbm_peak / 1e9, "unit": "GB/s",
                   "frac": bytes_alg / t_s / hbm_peak, "algorithmic_bytes": bytes_alg},
