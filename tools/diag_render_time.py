@@ -22,8 +22,11 @@ s, b, st = pipe.splats, pipe.last_binning, pipe.last_stats
 stream = torch.cuda.current_stream()
 
 
+VARIANT = api.variant_from_name(os.environ.get("DIAG_VARIANT", "FineGrainedCombined"))
+
+
 def call():
-    api.render_forward(3, s, b, W, H, 16, 16, (0, 0, 0), N.ALPHA_EXACT, st.task_order, frame, pipe.render_ws)
+    api.render_forward(VARIANT, s, b, W, H, 16, 16, (0, 0, 0), N.ALPHA_EXACT, st.task_order, frame, pipe.render_ws)
 
 
 for _ in range(3):
