@@ -430,9 +430,13 @@ __global__ void __launch_bounds__(kScThreads) k_chunk_scatter(const uint32_t* __
   const int rows_b = nbr;
   const uint64_t total = s_rowp[rows_b];
   if (total == 0) return;
+  // (a multiply by a per-CTA reciprocal instead of a 64-bit division: any
+  // monotone owner function gives contiguous bands, and every warp of the
+  // CTA evaluates the same one)
+  const double own_scale = (double)kScWarps / (2.0 * (double)total);
   auto owner = [&](int r) -> int {
-    const uint64_t mid2 = (uint64_t)s_rowp[r] + s_rowp[r + 1];  // 2 * middle
-    return (int)min((uint64_t)(kScWarps - 1), (mid2 * kScWarps) / (2 * total));
+    const double mid2 = (double)s_rowp[r] + (double)s_rowp[r + 1];  // 2 * middle
+    return min(kScWarps - 1, (int)(mid2 * own_scale));
   };
   auto band_start = [&](int w) -> int {  // first row whose owner >= w
     int lo = 0, hi = rows_b;
