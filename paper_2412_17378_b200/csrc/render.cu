@@ -1688,6 +1688,8 @@ static int render_impl(int variant, const int32_t* gate, int alpha_mode, bs_spla
   if (alpha_mode != BS_ALPHA_EXACT && alpha_mode != BS_ALPHA_FAST) return BS_ERR_INVALID_ARGUMENT;
   if (!out.color || !out.alpha || !out.depth || !out.final_t || !out.contrib || !out.term) return BS_ERR_INVALID_ARGUMENT;
   if ((int64_t)pw * ph > 1024) return BS_ERR_UNSUPPORTED;
+  // pixel indices are 32-bit in the kernels and the tail hand-off records
+  if ((int64_t)width * height > (int64_t)0xffffffff) return BS_ERR_UNSUPPORTED;
   if (!ws || ws_bytes < bs_render_workspace_bytes(width, height)) return BS_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   RArgs A;
@@ -1780,6 +1782,7 @@ extern "C" int bs_render_backward(int alpha_mode, bs_splats g, const uint32_t* p
   if (!fwd.color || !fwd.depth || !fwd.final_t || !gin.dl_dcolor || !gout.xyab || !gout.cop || !gout.rgbr)
     return BS_ERR_INVALID_ARGUMENT;
   if ((int64_t)pw * ph > 1024) return BS_ERR_UNSUPPORTED;
+  if ((int64_t)width * height > (int64_t)0xffffffff) return BS_ERR_UNSUPPORTED;  // (32-bit pixel indices)
   if (super_lists && (!pow2(pw) || !pow2(ph))) return BS_ERR_UNSUPPORTED;
   if (!ws || ws_bytes < 256) return BS_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;

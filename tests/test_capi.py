@@ -76,6 +76,10 @@ def test_argument_validation_without_device():
     fo = N.FrameOut(None, None, None, None, None, None)
     assert L.bs_render_forward(9, 0, s, None, None, None, 64, 64, 16, 16, bg, fo, None, 0, None) == -1
     assert L.bs_render_forward(0, 5, s, None, None, None, 64, 64, 16, 16, bg, fo, None, 0, None) == -1
+    # frames past 2^32 pixels (32-bit pixel indices in the kernels): BS_ERR_UNSUPPORTED before any device work
+    one = C.c_void_p(16)
+    fo1 = N.FrameOut(one, one, one, one, one, one)
+    assert L.bs_render_forward(0, 0, s, None, one, None, 70000, 70000, 32, 32, bg, fo1, None, 0, None) == -6
 
 
 def test_selector_rule():
