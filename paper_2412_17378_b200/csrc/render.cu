@@ -1332,9 +1332,12 @@ __device__ __forceinline__ void warp_task_bwd(const RArgs& A, const BwdArgs& G, 
     tf = A.final_t[p];
   }
   float t = 1.0f;
-  const int slot = (lane >> 1) & 15;  // the gradient term this lane pair ends holding
-  float* const tgt = bwd_target(G, slot < 10 ? slot : 0);
-  const bool adder = !(lane & 1) && slot < 10;
+  // the gradient term this lane ends holding after the 10-term reduction
+  // below: bit 4 picks terms 0-4 / 5-9; bits 3, 2, 1 the term inside them
+  const bool h3 = lane & 8, h2 = lane & 4, h1 = lane & 2;
+  const int slot = ((lane & 16) ? 5 : 0) + (h3 ? (h2 ? 4 : 3) : (h2 ? 2 : (h1 ? 1 : 0)));
+  float* const tgt = bwd_target(G, slot);
+  const bool adder = !(lane & 1) && ((!h3 && !h2) || !h1);  // one lane per term
   uint32_t base = start;
   float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pc = pa, pr = pa;
   uint32_t pid = 0;
@@ -1367,9 +1370,9 @@ __device__ __forceinline__ void warp_task_bwd(const RArgs& A, const BwdArgs& G, 
     }
     const int cnt = __popc(km);
     for (int j = 0; j < cnt; ++j) {
-      float v[16];
+      float v[10];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      for (int i = 0; i < 10; ++i) v[i] = 0.f;
       bool com = false;
       if (!done) {
         const float4 a = s[0][j], c = s[1][j];
@@ -1424,30 +1427,39 @@ __device__ __forceinline__ void warp_task_bwd(const RArgs& A, const BwdArgs& G, 
         }
       }
       if (!__any_sync(kFull, com)) continue;
-      // transposing butterfly: after the offset-16 .. offset-2 levels lane l
-      // holds a partial of term (l >> 1) & 15; offset 1 completes it
+      // transposing reduction of the 10 terms over the 32 lanes, 12 shuffles:
+      // xor 16 halves the terms (5 each), xor 8 splits them 3 / 2, xor 4
+      // 2 / 1 and 1 / 1, xor 2 splits the last pair (or adds the duplicate
+      // single term), xor 1 completes every sum
+      {
+        const bool h4 = lane & 16;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const bool hi = lane & 16;
-        const float send = hi ? v[i] : v[i + 8];
-        v[i] = (hi ? v[i + 8] : v[i]) + __shfl_xor_sync(kFull, send, 16);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const bool hi = lane & 8;
-        const float send = hi ? v[i] : v[i + 4];
-        v[i] = (hi ? v[i + 4] : v[i]) + __shfl_xor_sync(kFull, send, 8);
-      }
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const bool hi = lane & 4;
-        const float send = hi ? v[i] : v[i + 2];
-        v[i] = (hi ? v[i + 2] : v[i]) + __shfl_xor_sync(kFull, send, 4);
+        for (int i = 0; i < 5; ++i) {
+          const float send = h4 ? v[i] : v[i + 5];
+          v[i] = (h4 ? v[i + 5] : v[i]) + __shfl_xor_sync(kFull, send, 16);
+        }
       }
       {
-        const bool hi = lane & 2;
-        const float send = hi ? v[0] : v[1];
-        v[0] = (hi ? v[1] : v[0]) + __shfl_xor_sync(kFull, send, 2);
+        const float s0 = h3 ? v[0] : v[3], s1 = h3 ? v[1] : v[4], s2 = h3 ? v[2] : 0.0f;
+        const float k0 = h3 ? v[3] : v[0], k1 = h3 ? v[4] : v[1], k2 = h3 ? 0.0f : v[2];
+        v[0] = k0 + __shfl_xor_sync(kFull, s0, 8);
+        v[1] = k1 + __shfl_xor_sync(kFull, s1, 8);
+        v[2] = k2 + __shfl_xor_sync(kFull, s2, 8);
+      }
+      {
+        // lanes with bit 3 clear hold 3 terms (p0, p1, p2), the others 2
+        const float s0 = h2 ? v[0] : (h3 ? v[1] : v[2]);
+        const float k0 = h2 ? (h3 ? v[1] : v[2]) : v[0];
+        const float s1 = (!h3 && h2) ? v[1] : 0.0f;
+        const float k1 = (!h3 && !h2) ? v[1] : 0.0f;
+        v[0] = k0 + __shfl_xor_sync(kFull, s0, 4);
+        v[1] = k1 + __shfl_xor_sync(kFull, s1, 4);
+      }
+      {
+        const bool two = !h3 && !h2;  // still two terms
+        const float s0 = two ? (h1 ? v[0] : v[1]) : v[0];
+        const float k0 = two ? (h1 ? v[1] : v[0]) : v[0];
+        v[0] = k0 + __shfl_xor_sync(kFull, s0, 2);
       }
       v[0] += __shfl_xor_sync(kFull, v[0], 1);
       if (adder && v[0] != 0.0f) atomicAdd(tgt + 4 * (size_t)s_id[j], v[0]);
