@@ -1204,10 +1204,11 @@ __global__ void __launch_bounds__(kFineThreads) k_render_donated(RArgs A) {
   __shared__ unsigned long long s_tab[32];
   __shared__ unsigned s_task;
   if (gated_out(A, BS_FINE_GRAINED_COMBINED)) return;
+  const unsigned ntasks = *(volatile unsigned*)(A.queue + 3);
+  if (ntasks == 0) return;  // nothing parked (most frames): no ticket, no barriers
   load_tab(s_tab);
   const ExpK ek = make_expk(s_tab);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned ntasks = *(volatile unsigned*)(A.queue + 3);
   for (;;) {
     __syncthreads();
     if (tid == 0) s_task = atomicAdd(A.queue + 2, 1u);
